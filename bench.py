@@ -1,0 +1,311 @@
+#!/usr/bin/env python
+"""Benchmark: circuit wall-seconds and achieved HBM GB/s of the B200 state-vector engine.
+
+Workload (BASELINE.json configs[1]): the 30-qubit complex128 QFT on one B200, i.e.
+qft_circuit(30) (480 gates) applied to a state resident in HBM.  One "step" = one full circuit.
+  value      device time per circuit (CUDA events, K steps after W warm-ups), seconds;
+  e2e        the same through the public API: Circuit.execute() (|0..0> allocation + plan +
+             program upload + passes) and a device->host read of the full result state into
+             pinned memory, per step;
+  roofline   the dominant kernel (k_pass, the fused pass): algorithmic bytes per launch
+             (one read + one write of the 2^n-amplitude state) / its mean CUDA-event duration,
+             against the measured HBM copy peak (MEASURED_PEAKS.json);
+  cpu_baseline  the reference algorithm (oracle/ numpy port, all host threads) on a bounded
+             sample of the same circuit: three representative gates at n=30, extrapolated.
+`--impl reference` runs only that CPU arm.  Under torchrun (N>1) rank 0 reports; the
+distributed path shards the state over ranks by global qubits (n = 30 + log2 N, weak scaling).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "circuit wall-seconds & achieved HBM GB/s (QFT/variational, c128) at 1/2/4/8 B200"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_pass_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch"), d
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """NVML polling thread: SM clock and throttle reasons while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index=0, period=0.01):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------ CPU arm
+def cpu_reference_sample(n: int, threads: int):
+    """Time the reference algorithm (oracle numpy port) on three representative QFT-n gates
+    (H = general body, CZPow = diagonal body, SWAP = permutation body) on a 2^n state and
+    extrapolate to the full circuit's gate mix (n H, n(n-1)/2 CZPow, n/2 SWAP)."""
+    import numpy as np
+
+    from oracle import statevec as ov
+
+    amps = np.zeros(1 << n, dtype=np.complex128)
+    amps[:] = 1.0 / math.sqrt(1 << n)  # touch every page outside the timed region
+    sample = [("H", ov.gate("H", (0,))), ("CZPow", ov.gate("CZPow", (1, 0), (), (math.pi / 2,))),
+              ("SWAP", ov.gate("SWAP", (0, n - 1)))]
+    times = {}
+    for name, (_k, tg, ct, _p, m) in sample:
+        t0 = time.perf_counter()
+        ov.apply_matrix(amps, n, tg, m, ct, n_threads=threads)
+        times[name] = time.perf_counter() - t0
+    counts = {"H": n, "CZPow": n * (n - 1) // 2, "SWAP": n // 2}
+    total = sum(times[k] * counts[k] for k in counts)
+    del amps
+    return total, times, counts
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def host_ram_bytes():
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except Exception:
+        return 0
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    threads = cpu_threads()
+    n = args.qubits
+    scale = 1.0
+    sample_n = n
+    if host_ram_bytes() < (40 << 30) and n > 28:
+        sample_n = 28
+        scale = 2.0 ** (n - sample_n)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        total, times, counts = cpu_reference_sample(sample_n, threads)
+        if i >= args.warmup:
+            vals.append(total * scale)
+    v = statistics.mean(vals)
+    sample = (f"3 gates (H(0), CZPow(1,0), SWAP(0,{sample_n - 1})) of QFT-{sample_n} c128 with the numpy port of "
+              f"qsim.apply_matrix, {threads} threads, extrapolated to 480 gates"
+              + (f" and x{scale:g} for n={n}" if scale != 1 else ""))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"QFT {n} qubits complex128 (qft_circuit({n}), 480 gates) on |0..0>",
+                   "n_qubits": n, "precision": "f64", "parallelism": "host threads"},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def run_gpu_arm(args, rank, world):
+    import torch
+
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200 import engine
+    from paper_2009_01845_b200.fusion import PassStep
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    if world > 1:
+        from paper_2009_01845_b200 import sharding
+
+        return sharding.bench_distributed(args, rank, world, METRIC)
+
+    n = args.qubits
+    prec = q.Precision.F64 if args.precision == "f64" else q.Precision.F32
+    if n > q.max_qubits():
+        q.set_max_qubits(n)
+    circuit = q.qft_circuit(n) if args.workload == "qft" else q.variational_circuit(
+        n, 5, __import__("numpy").random.default_rng(42).uniform(0, 2 * math.pi, n * 11), fused=True)
+    state = q.uniform_state(n, prec)
+    plan = engine.plan_for_state(state, circuit.queue)
+    holder: dict = {}
+    for _ in range(args.warmup):
+        engine.run_plan(state, plan, holder)
+    torch.cuda.synchronize()
+    evs: list = []
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk:
+        t0.record()
+        for _ in range(args.steps):
+            engine.run_plan(state, plan, holder, events=evs)
+        t1.record()
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    value = ms / 1e3
+    launches = [a.elapsed_time(b) for a, b in evs]
+    n_pass = sum(1 for s in plan.steps if isinstance(s, PassStep))
+    amp_bytes = prec.itemsize
+    pass_bytes = 2 * (1 << n) * amp_bytes
+    mean_pass_ms = statistics.mean(launches) if launches else float("nan")
+    achieved = pass_bytes / (mean_pass_ms * 1e-3) / 1e9
+    peak, peak_kind = _peaks()
+    traffic, _ncu = _ncu_traffic()
+    sweeps = plan.state_sweeps()
+    circuit_gbs = sweeps * pass_bytes / value / 1e9
+
+    # e2e through the public API, host readback of the full state into pinned memory
+    e2e_steps = max(1, min(args.steps, 3))
+    pinned = None
+    try:
+        pinned = torch.empty((1 << n,), dtype=prec.torch_dtype, pin_memory=True)
+    except Exception:
+        pinned = None
+    del state
+    holder.clear()
+    torch.cuda.empty_cache()
+    h2d = sum(int(s.words.nbytes) for s in plan.steps if isinstance(s, PassStep))
+    d2h = (1 << n) * amp_bytes if pinned is not None else 16
+    torch.cuda.synchronize()
+    e2e_times = []
+    for i in range(e2e_steps + 1):
+        w0 = time.perf_counter()
+        st = circuit.execute(precision=prec)
+        if pinned is not None:
+            pinned.copy_(st.tensor, non_blocking=True)
+        else:
+            st.tensor[:1].cpu()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - w0
+        del st
+        if i > 0:  # the first call pays one-off allocations
+            e2e_times.append(dt)
+    e2e = statistics.mean(e2e_times)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = cpu_threads()
+        sn = n if host_ram_bytes() >= (48 << 30) else min(n, 28)
+        total, times, counts = cpu_reference_sample(sn, threads)
+        scale = 2.0 ** (n - sn)
+        cpu = {"value": total * scale, "unit": "s", "cores": threads, "kind": "port",
+               "sample": f"H(0), CZPow(1,0), SWAP(0,{sn - 1}) of QFT-{sn} c128 (numpy port of qsim.apply_matrix, "
+                         f"{threads} threads) timed {', '.join(f'{k}={v:.2f}s' for k, v in times.items())}, "
+                         f"extrapolated to {sum(counts.values())} gates" + (f", x{scale:g} to n={n}" if scale != 1 else "")}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128" if prec is q.Precision.F64 else "c64", "data": "synthetic",
+        "config": {"workload": f"{'QFT' if args.workload == 'qft' else 'variational(L=5, fused)'} {n} qubits "
+                               f"{'complex128' if prec is q.Precision.F64 else 'complex64'} on 1 B200, "
+                               f"{len(circuit.queue)} gates, state resident in HBM",
+                   "n_qubits": n, "gates": len(circuit.queue), "passes": n_pass, "state_sweeps": sweeps,
+                   "state_bytes": (1 << n) * amp_bytes, "parallelism": "single GPU",
+                   "l2": "inputs (state) far larger than the 126 MB L2; no flush needed"},
+        "hbm": {"circuit_effective_gbs": circuit_gbs, "per_pass_ms": mean_pass_ms},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_kind": peak_kind, "kernel": "qsb::pass::k_pass",
+                     "bytes_per_launch": pass_bytes, "launches": len(launches)},
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "qft_circuit(n).execute() + state D2H (pinned)"},
+        "gpu_launches": len(plan.steps) * args.steps,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--qubits", type=int, default=30)
+    ap.add_argument("--precision", choices=["f64", "f32"], default="f64")
+    ap.add_argument("--workload", choices=["qft", "variational"], default="qft")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    run_gpu_arm(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

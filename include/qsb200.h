@@ -1,0 +1,131 @@
+/*
+ * qsb200 -- C ABI of the B200 (sm_100a) state-vector engine.
+ *
+ * This is the drop-in boundary for the hot path of the reference simulator `qsim`
+ * (/root/reference/pkg/src/qsim).  Every entry point takes plain device pointers, sizes and a
+ * caller-owned cudaStream_t (passed as void*), enqueues work asynchronously on that stream and
+ * returns a qsb_status.  No torch / numpy types cross this boundary.  On a non-zero status,
+ * qsb_last_error() returns a human-readable message (thread-local).
+ *
+ * Conventions (identical to the reference):
+ *   - the state is 2**n complex numbers, interleaved (re, im), complex64 (dtype QSB_C64) or
+ *     complex128 (QSB_C128);
+ *   - qubit q lives at bit position n-1-q (qubit 0 is the MSB) -- state.py:1-6, 34-36.  This ABI
+ *     takes BIT positions; the Python layer converts qubits to bits;
+ *   - gate matrices are row-major 2**t x 2**t complex128 (numpy complex128 memory layout), and
+ *     target_bits[0] is the most significant bit of the matrix index -- gates.py:128-131.
+ *     For complex64 states the matrix is rounded to complex64 before use, as the reference's
+ *     `mat64.astype(amplitudes.dtype)` does (gates.py:434, 447, 462).
+ */
+#ifndef QSB200_H
+#define QSB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSB_ABI_VERSION 3
+
+typedef enum { QSB_C64 = 0, QSB_C128 = 1 } qsb_dtype;
+
+/* Kernel classes of the reference (gates.py:334-352, KernelClass). */
+typedef enum {
+  QSB_KERNEL_AUTO = -1,
+  QSB_KERNEL_GENERAL = 0,
+  QSB_KERNEL_DIAGONAL = 1,
+  QSB_KERNEL_PERMUTATION = 2
+} qsb_kernel;
+
+typedef enum {
+  QSB_OK = 0,
+  QSB_ERR_ARG = 1,      /* bad argument (maps to ValueError) */
+  QSB_ERR_SHAPE = 2,    /* index / layout problem (maps to ShapeError) */
+  QSB_ERR_CAPACITY = 3, /* size cap exceeded (maps to CapacityError) */
+  QSB_ERR_CUDA = 4      /* CUDA runtime error (maps to SimulationError) */
+} qsb_status;
+
+/* ---- library ---------------------------------------------------------------------------- */
+int qsb_abi_version(void);
+const char* qsb_last_error(void);
+
+/* ---- state allocator / initial states (state.py:67-75 zero_state, hamiltonians.py:115-117
+ *      _plus_state).  The caller owns the 2**n-element device buffer. ------------------------- */
+/* |basis_index>: all zeros, amplitude 1 at basis_index.  zero_state == basis_index 0. */
+int qsb_init_basis(void* amps, int n_qubits, int dtype, uint64_t basis_index, void* stream);
+/* every amplitude = (re, im); |+>^n is re = 2**(-n/2). */
+int qsb_init_uniform(void* amps, int n_qubits, int dtype, double re, double im, void* stream);
+
+/* ---- single-gate kernels: the reference's apply_matrix (gates.py:380-469) ---------------- */
+/* Classify a 2**t x 2**t complex128 matrix exactly like classify_kernel (gates.py:340-352):
+ * returns QSB_KERNEL_DIAGONAL / _PERMUTATION / _GENERAL. */
+int qsb_classify(const double* matrix, int n_targets);
+/* In-place application of `matrix` on `target_bits` (t = 1 or 2), restricted to the basis
+ * states whose `control_bits` are all 1.  `kernel` = QSB_KERNEL_AUTO classifies first;
+ * an explicit class forces that body, with the reference's semantics (diagonal body reads only
+ * the diagonal and skips rows equal to 1.0; permutation body takes the first non-zero of each
+ * row and multiplies only phases != 1.0). */
+int qsb_apply_matrix(void* amps, int n_qubits, int dtype, int n_targets, const int* target_bits,
+                     int n_controls, const int* control_bits, const double* matrix, int kernel,
+                     void* stream);
+/* Multiply every amplitude of [amps, amps + n_amps) by (re, im) -- the all-global phase of the
+ * sharded executor (sharding.py:281-283) and from_amplitudes(normalize=True) (state.py:101-105). */
+int qsb_scale(void* amps, uint64_t n_amps, int dtype, double re, double im, void* stream);
+
+/* ---- fused multi-gate pass (one HBM sweep for a run of gates) --- */
+/* `program` is a flat little-endian int64 word stream produced by the host planner
+ * (paper_2009_01845_b200/fusion.py); `n_words` its length.  src may equal dst when the pass
+ * carries no tile-external bit permutation. */
+int qsb_run_pass(const void* src, void* dst, int n_qubits, int dtype, const int64_t* program,
+                 int64_t n_words, void* stream);
+/* Bytes of shared memory the pass kernel needs for a tile of 2**tile_bits amplitudes. */
+int qsb_pass_max_tile_bits(int dtype);
+
+/* ---- reductions (state.py:109-122 norm / overlap) ---------------------------------------- */
+/* out[0] = sum |a_i|^2 (double, device pointer).  Deterministic two-level tree. */
+int qsb_norm2(const void* amps, uint64_t n_amps, int dtype, double* out, void* stream);
+/* out[0..1] = <a|b> (conjugate-linear in a), complex128 on device.  Deterministic. */
+int qsb_vdot(const void* a, const void* b, uint64_t n_amps, int dtype, double* out, void* stream);
+
+/* ---- measurement (measurement.py:36-87) -------------------------------------------------- */
+/* probs[i] = |a_i|^2 computed exactly as numpy's np.abs(a.astype(complex128))**2
+ * (SURVEY.md Appendix B.1), float64 on device. */
+int qsb_probabilities(const void* amps, uint64_t n_amps, int dtype, double* probs, void* stream);
+/* Marginal over the bits NOT listed in `kept`, reproducing numpy's
+ * `probs.reshape([2]*n).sum(axis=other)` followed by the transpose to the requested order, bit
+ * for bit (pairwise inner sums, sequential outer accumulation)
+ * -- measurement.py:50-58.  kept[0] is the most significant bit of the output index.
+ * `scratch` holds qsb_marginal_scratch_doubles(n_bits, k) doubles. */
+int qsb_marginal(const double* probs, int n_bits, int k, const int* kept, double* out,
+                 double* scratch, void* stream);
+uint64_t qsb_marginal_scratch_doubles(int n_bits, int k);
+/* cum[i] = fl(cum[i-1] + p[i]) -- the exact result of numpy's strictly sequential np.cumsum,
+ * computed in parallel (binade-integer scan), then cum /= cum[n-1]
+ * (measurement.py:81-82).  Synchronises `stream` once (data-dependent serial-point count). */
+int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cum, void* scratch,
+                          size_t scratch_bytes, void* stream);
+size_t qsb_cumsum_scratch_bytes(uint64_t n);
+/* The strictly sequential fl(c + p) chain on one device thread (no normalisation): the
+ * cross-check for qsb_cumsum_normalized in the GPU tests. */
+int qsb_cumsum_serial(const double* probs, uint64_t n, double* cum, void* stream);
+/* PCG64 (XSL-RR 128/64, numpy.random.PCG64) draws u_k = (raw_k >> 11) * 2^-53 from the 128-bit
+ * (state, inc) of numpy's bit_generator.state, then samples[k] = clip(#{i : cum[i] <= u_k},
+ * 0, n-1) -- np.searchsorted(cum, u, side="right") (measurement.py:83-86). */
+int qsb_sample(const double* cum, uint64_t n, uint64_t state_hi, uint64_t state_lo,
+               uint64_t inc_hi, uint64_t inc_lo, uint64_t n_shots, int64_t* samples, void* stream);
+
+/* ---- sharded execution helpers (sharding.py:84-111 reshuffle / _exchange_halves) -------- */
+/* Copy the `half` (0 or 1) of a shard selected by local bit `bit` into / out of a contiguous
+ * staging buffer, for elements [first, first + count) of that half in index order. */
+int qsb_pack_half(const void* shard, int n_local_bits, int dtype, int bit, int half,
+                  uint64_t first, uint64_t count, void* staging, void* stream);
+int qsb_unpack_half(void* shard, int n_local_bits, int dtype, int bit, int half, uint64_t first,
+                    uint64_t count, const void* staging, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QSB200_H */

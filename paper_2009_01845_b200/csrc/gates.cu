@@ -1,0 +1,623 @@
+// Single-gate kernels, initial states and small reductions for the qsb200 engine.
+//
+// Each entry point replaces one numeric body of the reference simulator:
+//   qsb_init_basis / qsb_init_uniform  <- state.py:67-75 zero_state, hamiltonians.py:115-117
+//   qsb_apply_matrix                   <- gates.py:380-469 apply_matrix (all three bodies)
+//   qsb_scale                          <- sharding.py:281-283 whole-shard phase, state.py:105
+//   qsb_norm2 / qsb_vdot               <- state.py:109-122 norm / overlap
+//   qsb_pack_half / qsb_unpack_half    <- sharding.py:100-111 _exchange_halves (staging side)
+//
+// Kernel design (B200): one thread owns ITEMS amplitude groups; all loads of a thread are
+// issued before any arithmetic so every thread keeps 2*ITEMS (1q) or 4*ITEMS (2q) independent
+// 8/16-byte loads in flight.  Group -> index mapping is the reference's zero-bit insertion done
+// in registers.  Consecutive threads own consecutive groups, so whenever the lowest bits are
+// not occupied a warp touches one contiguous 256 B / 512 B segment per load instruction.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "qsb_common.cuh"
+
+namespace qsb {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  set_error("%s: CUDA error %d (%s)", where, (int)e, cudaGetErrorString(e));
+  return QSB_ERR_CUDA;
+}
+
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------------------------------------
+// initial states
+// ------------------------------------------------------------------------------------------
+template <typename R>
+__global__ void k_set_one(cplx<R>* a, uint64_t idx) {
+  cplx<R> v;
+  v.x = R(1);
+  v.y = R(0);
+  a[idx] = v;
+}
+
+template <typename R>
+__global__ void k_fill(cplx<R>* __restrict__ a, uint64_t n, R re, R im) {
+  cplx<R> v;
+  v.x = re;
+  v.y = im;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = v;
+}
+
+template <typename R>
+__global__ void k_scale(cplx<R>* __restrict__ a, uint64_t n, cplx<R> s) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    a[i] = cmul(a[i], s);
+}
+
+static int stream_grid(uint64_t n) {
+  // enough CTAs for 8 resident per SM on 148 SMs, capped by the work
+  uint64_t want = (n + kThreads - 1) / kThreads;
+  uint64_t cap = 148ull * 16ull;
+  return (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+}
+
+// ------------------------------------------------------------------------------------------
+// gate kernels
+// ------------------------------------------------------------------------------------------
+// Parameters of one group-structured gate launch.  `off[j]` is the bit pattern of matrix row j
+// on the target bits (target_bits[0] = MSB of j), `cmask` the OR of the control bits.
+template <typename R>
+struct GateArgs {
+  uint64_t n_groups;
+  uint64_t cmask;
+  uint64_t off[4];
+  OccBits occ;
+  cplx<R> m[16];       // general: row-major 2^t x 2^t; diag: m[r] for r < nrows
+  uint32_t rows[4];    // diag: rows to multiply; perm: destination rows
+  uint32_t src[4];     // perm: source row of each destination row
+  uint32_t use_phase;  // perm: bit r set -> multiply row r by m[r]
+  int nrows;
+};
+
+template <typename R, int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_general1(cplx<R>* __restrict__ a, const GateArgs<R> p) {
+  using C = cplx<R>;
+  const uint64_t g0 = (uint64_t)blockIdx.x * (kThreads * ITEMS) + threadIdx.x;
+  uint64_t base[ITEMS];
+  C x0[ITEMS], x1[ITEMS];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t g = g0 + (uint64_t)it * kThreads;
+    base[it] = ~0ull;
+    if (g < p.n_groups) {
+      base[it] = insert_zero_bits(g, p.occ) | p.cmask;
+      x0[it] = a[base[it]];
+      x1[it] = a[base[it] | p.off[1]];
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    if (base[it] == ~0ull) continue;
+    C y0 = cmad(p.m[1], x1[it], cmul(p.m[0], x0[it]));
+    C y1 = cmad(p.m[3], x1[it], cmul(p.m[2], x0[it]));
+    a[base[it]] = y0;
+    a[base[it] | p.off[1]] = y1;
+  }
+}
+
+template <typename R, int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_general2(cplx<R>* __restrict__ a, const GateArgs<R> p) {
+  using C = cplx<R>;
+  const uint64_t g0 = (uint64_t)blockIdx.x * (kThreads * ITEMS) + threadIdx.x;
+  uint64_t base[ITEMS];
+  C x[ITEMS][4];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t g = g0 + (uint64_t)it * kThreads;
+    base[it] = ~0ull;
+    if (g < p.n_groups) {
+      base[it] = insert_zero_bits(g, p.occ) | p.cmask;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) x[it][j] = a[base[it] | p.off[j]];
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    if (base[it] == ~0ull) continue;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      C y = cmul(p.m[4 * r], x[it][0]);
+      y = cmad(p.m[4 * r + 1], x[it][1], y);
+      y = cmad(p.m[4 * r + 2], x[it][2], y);
+      y = cmad(p.m[4 * r + 3], x[it][3], y);
+      a[base[it] | p.off[r]] = y;
+    }
+  }
+}
+
+// diagonal body (gates.py:431-441): only rows whose complex128 entry differs from 1.0
+template <typename R, int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_diag(cplx<R>* __restrict__ a, const GateArgs<R> p) {
+  using C = cplx<R>;
+  const uint64_t g0 = (uint64_t)blockIdx.x * (kThreads * ITEMS) + threadIdx.x;
+  uint64_t base[ITEMS];
+  C x[ITEMS][4];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t g = g0 + (uint64_t)it * kThreads;
+    base[it] = ~0ull;
+    if (g < p.n_groups) {
+      base[it] = insert_zero_bits(g, p.occ) | p.cmask;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (r < p.nrows) x[it][r] = a[base[it] | p.off[p.rows[r]]];
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    if (base[it] == ~0ull) continue;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (r < p.nrows) a[base[it] | p.off[p.rows[r]]] = cmul(x[it][r], p.m[r]);
+  }
+}
+
+// permutation body (gates.py:443-459): gather every moved row first, then scatter
+template <typename R, int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_perm(cplx<R>* __restrict__ a, const GateArgs<R> p) {
+  using C = cplx<R>;
+  const uint64_t g0 = (uint64_t)blockIdx.x * (kThreads * ITEMS) + threadIdx.x;
+  uint64_t base[ITEMS];
+  C x[ITEMS][4];
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    const uint64_t g = g0 + (uint64_t)it * kThreads;
+    base[it] = ~0ull;
+    if (g < p.n_groups) {
+      base[it] = insert_zero_bits(g, p.occ) | p.cmask;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        if (r < p.nrows) x[it][r] = a[base[it] | p.off[p.src[r]]];
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < ITEMS; ++it) {
+    if (base[it] == ~0ull) continue;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (r < p.nrows) {
+        C v = x[it][r];
+        if (p.use_phase & (1u << r)) v = cmul(v, p.m[r]);
+        a[base[it] | p.off[p.rows[r]]] = v;
+      }
+    }
+  }
+}
+
+template <typename R>
+static void to_dtype(const double* re_im, cplx<R>* out) {
+  out->x = (R)re_im[0];
+  out->y = (R)re_im[1];
+}
+
+static bool is_one(const double* z) { return z[0] == 1.0 && z[1] == 0.0; }
+static bool is_nonzero(const double* z) { return z[0] != 0.0 || z[1] != 0.0; }
+
+template <typename R>
+static int launch_gate(void* amps, int n_qubits, int t, const int* tbits, int nc, const int* cbits,
+                       const double* mat, int kclass, cudaStream_t st) {
+  GateArgs<R> p;
+  memset(&p, 0, sizeof p);
+  const int dim = 1 << t;
+  // occupied bits, ascending
+  int occ[kMaxOcc];
+  int nocc = 0;
+  for (int i = 0; i < t; ++i) occ[nocc++] = tbits[i];
+  for (int i = 0; i < nc; ++i) occ[nocc++] = cbits[i];
+  for (int i = 1; i < nocc; ++i)
+    for (int j = i; j > 0 && occ[j - 1] > occ[j]; --j) {
+      int tmp = occ[j];
+      occ[j] = occ[j - 1];
+      occ[j - 1] = tmp;
+    }
+  p.occ.n = nocc;
+  for (int i = 0; i < nocc; ++i) p.occ.pos[i] = (uint8_t)occ[i];
+  p.cmask = 0;
+  for (int i = 0; i < nc; ++i) p.cmask |= 1ull << cbits[i];
+  for (int j = 0; j < dim; ++j) {
+    uint64_t off = 0;
+    for (int b = 0; b < t; ++b)
+      if ((j >> (t - 1 - b)) & 1) off |= 1ull << tbits[b];
+    p.off[j] = off;
+  }
+  p.n_groups = 1ull << (n_qubits - nocc);
+  cplx<R>* a = static_cast<cplx<R>*>(amps);
+
+  if (kclass == QSB_KERNEL_DIAGONAL) {
+    int nr = 0;
+    for (int j = 0; j < dim; ++j) {
+      const double* d = mat + 2 * (j * dim + j);
+      if (!is_one(d)) {
+        p.rows[nr] = j;
+        to_dtype<R>(d, &p.m[nr]);
+        ++nr;
+      }
+    }
+    if (nr == 0) return QSB_OK;
+    p.nrows = nr;
+    constexpr int IT = 4;
+    k_diag<R, IT><<<blocks_for(p.n_groups, kThreads * IT), kThreads, 0, st>>>(a, p);
+    QSB_CHECK_LAUNCH("qsb_apply_matrix(diagonal)");
+    return QSB_OK;
+  }
+  if (kclass == QSB_KERNEL_PERMUTATION) {
+    int nr = 0;
+    for (int j = 0; j < dim; ++j) {
+      int s = 0;  // np.argmax(mat != 0): first non-zero column (0 if the row is all zero)
+      for (int c = 0; c < dim; ++c)
+        if (is_nonzero(mat + 2 * (j * dim + c))) {
+          s = c;
+          break;
+        }
+      const double* ph = mat + 2 * (j * dim + s);
+      const bool phase = !is_one(ph);
+      if (s != j || phase) {
+        p.rows[nr] = j;
+        p.src[nr] = s;
+        if (phase) p.use_phase |= 1u << nr;
+        to_dtype<R>(ph, &p.m[nr]);
+        ++nr;
+      }
+    }
+    if (nr == 0) return QSB_OK;
+    p.nrows = nr;
+    constexpr int IT = 4;
+    k_perm<R, IT><<<blocks_for(p.n_groups, kThreads * IT), kThreads, 0, st>>>(a, p);
+    QSB_CHECK_LAUNCH("qsb_apply_matrix(permutation)");
+    return QSB_OK;
+  }
+  for (int k = 0; k < dim * dim; ++k) to_dtype<R>(mat + 2 * k, &p.m[k]);
+  if (t == 1) {
+    constexpr int IT = 4;
+    k_general1<R, IT><<<blocks_for(p.n_groups, kThreads * IT), kThreads, 0, st>>>(a, p);
+  } else {
+    constexpr int IT = 2;
+    k_general2<R, IT><<<blocks_for(p.n_groups, kThreads * IT), kThreads, 0, st>>>(a, p);
+  }
+  QSB_CHECK_LAUNCH("qsb_apply_matrix(general)");
+  return QSB_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// deterministic reductions: fixed grid, per-block tree, then one block folds the partials
+// ------------------------------------------------------------------------------------------
+constexpr int kRedBlocks = 1184;  // 148 SMs x 8
+
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_norm2_partial(const cplx<R>* __restrict__ a, uint64_t n,
+                                                            double* __restrict__ part) {
+  __shared__ double sh[kThreads];
+  double acc = 0.0;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const cplx<R> v = a[i];
+    acc = fma((double)v.x, (double)v.x, acc);
+    acc = fma((double)v.y, (double)v.y, acc);
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_vdot_partial(const cplx<R>* __restrict__ a,
+                                                           const cplx<R>* __restrict__ b, uint64_t n,
+                                                           double2* __restrict__ part) {
+  __shared__ double2 sh[kThreads];
+  double2 acc = make_double2(0.0, 0.0);
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const cplx<R> u = a[i];
+    const cplx<R> v = b[i];
+    // conj(u) * v
+    acc.x = fma((double)u.x, (double)v.x, acc.x);
+    acc.x = fma((double)u.y, (double)v.y, acc.x);
+    acc.y = fma((double)u.x, (double)v.y, acc.y);
+    acc.y = fma(-(double)u.y, (double)v.x, acc.y);
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sh[threadIdx.x].x += sh[threadIdx.x + s].x;
+      sh[threadIdx.x].y += sh[threadIdx.x + s].y;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) k_fold(const T* __restrict__ part, int n, T* out);
+
+template <>
+__global__ void __launch_bounds__(1024) k_fold<double>(const double* __restrict__ part, int n, double* out) {
+  __shared__ double sh[1024];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += 1024) acc += part[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 512; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+template <>
+__global__ void __launch_bounds__(1024) k_fold<double2>(const double2* __restrict__ part, int n, double2* out) {
+  __shared__ double2 sh[1024];
+  double2 acc = make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < n; i += 1024) {
+    acc.x += part[i].x;
+    acc.y += part[i].y;
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 512; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sh[threadIdx.x].x += sh[threadIdx.x + s].x;
+      sh[threadIdx.x].y += sh[threadIdx.x + s].y;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = sh[0];
+}
+
+// scratch for the partials: one lazily grown device buffer per process (tiny)
+static void* g_red_scratch = nullptr;
+static int ensure_red_scratch() {
+  if (g_red_scratch) return QSB_OK;
+  cudaError_t e = cudaMalloc(&g_red_scratch, kRedBlocks * sizeof(double2));
+  if (e != cudaSuccess) return cuda_status(e, "reduction scratch");
+  return QSB_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// half-shard staging for the global<->local exchange
+// ------------------------------------------------------------------------------------------
+template <typename R>
+__global__ void k_pack_half(const cplx<R>* __restrict__ s, int bit, int half, uint64_t first, uint64_t count,
+                            cplx<R>* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t lowm = (1ull << bit) - 1ull;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += stride) {
+    const uint64_t h = first + e;
+    const uint64_t i = ((h & ~lowm) << 1) | ((uint64_t)half << bit) | (h & lowm);
+    out[e] = s[i];
+  }
+}
+
+template <typename R>
+__global__ void k_unpack_half(cplx<R>* __restrict__ s, int bit, int half, uint64_t first, uint64_t count,
+                              const cplx<R>* __restrict__ in) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t lowm = (1ull << bit) - 1ull;
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += stride) {
+    const uint64_t h = first + e;
+    const uint64_t i = ((h & ~lowm) << 1) | ((uint64_t)half << bit) | (h & lowm);
+    s[i] = in[e];
+  }
+}
+
+}  // namespace qsb
+
+using namespace qsb;
+
+static int check_dtype(int dtype) {
+  if (dtype != QSB_C64 && dtype != QSB_C128) {
+    set_error("unknown dtype %d", dtype);
+    return QSB_ERR_ARG;
+  }
+  return QSB_OK;
+}
+
+extern "C" {
+
+int qsb_abi_version(void) { return QSB_ABI_VERSION; }
+const char* qsb_last_error(void) { return g_err; }
+
+int qsb_init_basis(void* amps, int n_qubits, int dtype, uint64_t basis_index, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  if (n_qubits < 1 || n_qubits > 40) {
+    set_error("n_qubits %d out of range", n_qubits);
+    return QSB_ERR_CAPACITY;
+  }
+  const uint64_t n = 1ull << n_qubits;
+  if (basis_index >= n) {
+    set_error("basis index %llu out of range", (unsigned long long)basis_index);
+    return QSB_ERR_SHAPE;
+  }
+  cudaStream_t st = as_stream(stream);
+  const size_t bytes = n * (dtype == QSB_C128 ? 16 : 8);
+  cudaError_t e = cudaMemsetAsync(amps, 0, bytes, st);
+  if (e != cudaSuccess) return cuda_status(e, "qsb_init_basis(memset)");
+  if (dtype == QSB_C128)
+    k_set_one<double><<<1, 1, 0, st>>>(static_cast<double2*>(amps), basis_index);
+  else
+    k_set_one<float><<<1, 1, 0, st>>>(static_cast<float2*>(amps), basis_index);
+  QSB_CHECK_LAUNCH("qsb_init_basis");
+  return QSB_OK;
+}
+
+int qsb_init_uniform(void* amps, int n_qubits, int dtype, double re, double im, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  if (n_qubits < 1 || n_qubits > 40) {
+    set_error("n_qubits %d out of range", n_qubits);
+    return QSB_ERR_CAPACITY;
+  }
+  const uint64_t n = 1ull << n_qubits;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    k_fill<double><<<stream_grid(n), kThreads, 0, st>>>(static_cast<double2*>(amps), n, re, im);
+  else
+    k_fill<float><<<stream_grid(n), kThreads, 0, st>>>(static_cast<float2*>(amps), n, (float)re, (float)im);
+  QSB_CHECK_LAUNCH("qsb_init_uniform");
+  return QSB_OK;
+}
+
+int qsb_classify(const double* m, int t) {
+  const int dim = 1 << t;
+  bool off_nz = false;
+  for (int r = 0; r < dim; ++r)
+    for (int c = 0; c < dim; ++c)
+      if (r != c && is_nonzero(m + 2 * (r * dim + c))) off_nz = true;
+  if (!off_nz) return QSB_KERNEL_DIAGONAL;
+  for (int r = 0; r < dim; ++r) {
+    int row_nz = 0, col_nz = 0;
+    for (int c = 0; c < dim; ++c) {
+      row_nz += is_nonzero(m + 2 * (r * dim + c));
+      col_nz += is_nonzero(m + 2 * (c * dim + r));
+    }
+    if (row_nz != 1 || col_nz != 1) return QSB_KERNEL_GENERAL;
+  }
+  for (int k = 0; k < dim * dim; ++k) {
+    const double* z = m + 2 * k;
+    if (is_nonzero(z) && fabs(hypot(z[0], z[1]) - 1.0) > 1e-12) return QSB_KERNEL_GENERAL;
+  }
+  return QSB_KERNEL_PERMUTATION;
+}
+
+int qsb_apply_matrix(void* amps, int n_qubits, int dtype, int n_targets, const int* target_bits,
+                     int n_controls, const int* control_bits, const double* matrix, int kernel,
+                     void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  if (n_targets < 1 || n_targets > 2) {
+    set_error("apply_matrix supports 1 or 2 targets, got %d", n_targets);
+    return QSB_ERR_SHAPE;
+  }
+  if (n_qubits < 1 || n_qubits > 40 || n_controls < 0 || n_targets + n_controls > n_qubits) {
+    set_error("bad qubit counts (n=%d, targets=%d, controls=%d)", n_qubits, n_targets, n_controls);
+    return QSB_ERR_SHAPE;
+  }
+  uint64_t seen = 0;
+  for (int i = 0; i < n_targets + n_controls; ++i) {
+    const int b = i < n_targets ? target_bits[i] : control_bits[i - n_targets];
+    if (b < 0 || b >= n_qubits) {
+      set_error("bit %d out of range for %d qubits", b, n_qubits);
+      return QSB_ERR_SHAPE;
+    }
+    if (seen & (1ull << b)) {
+      set_error("targets and controls must be distinct");
+      return QSB_ERR_SHAPE;
+    }
+    seen |= 1ull << b;
+  }
+  if (kernel == QSB_KERNEL_AUTO) kernel = qsb_classify(matrix, n_targets);
+  if (kernel < 0 || kernel > 2) {
+    set_error("unknown kernel class %d", kernel);
+    return QSB_ERR_ARG;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    return launch_gate<double>(amps, n_qubits, n_targets, target_bits, n_controls, control_bits, matrix, kernel, st);
+  return launch_gate<float>(amps, n_qubits, n_targets, target_bits, n_controls, control_bits, matrix, kernel, st);
+}
+
+int qsb_scale(void* amps, uint64_t n, int dtype, double re, double im, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    k_scale<double><<<stream_grid(n), kThreads, 0, st>>>(static_cast<double2*>(amps), n, make_double2(re, im));
+  else
+    k_scale<float><<<stream_grid(n), kThreads, 0, st>>>(static_cast<float2*>(amps), n,
+                                                        make_float2((float)re, (float)im));
+  QSB_CHECK_LAUNCH("qsb_scale");
+  return QSB_OK;
+}
+
+int qsb_norm2(const void* amps, uint64_t n, int dtype, double* out, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  if (int s = ensure_red_scratch()) return s;
+  cudaStream_t st = as_stream(stream);
+  double* part = static_cast<double*>(g_red_scratch);
+  if (dtype == QSB_C128)
+    k_norm2_partial<double><<<kRedBlocks, kThreads, 0, st>>>(static_cast<const double2*>(amps), n, part);
+  else
+    k_norm2_partial<float><<<kRedBlocks, kThreads, 0, st>>>(static_cast<const float2*>(amps), n, part);
+  k_fold<double><<<1, 1024, 0, st>>>(part, kRedBlocks, out);
+  QSB_CHECK_LAUNCH("qsb_norm2");
+  return QSB_OK;
+}
+
+int qsb_vdot(const void* a, const void* b, uint64_t n, int dtype, double* out, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  if (int s = ensure_red_scratch()) return s;
+  cudaStream_t st = as_stream(stream);
+  double2* part = static_cast<double2*>(g_red_scratch);
+  if (dtype == QSB_C128)
+    k_vdot_partial<double><<<kRedBlocks, kThreads, 0, st>>>(static_cast<const double2*>(a),
+                                                           static_cast<const double2*>(b), n, part);
+  else
+    k_vdot_partial<float><<<kRedBlocks, kThreads, 0, st>>>(static_cast<const float2*>(a),
+                                                          static_cast<const float2*>(b), n, part);
+  k_fold<double2><<<1, 1024, 0, st>>>(part, kRedBlocks, reinterpret_cast<double2*>(out));
+  QSB_CHECK_LAUNCH("qsb_vdot");
+  return QSB_OK;
+}
+
+int qsb_pack_half(const void* shard, int n_local_bits, int dtype, int bit, int half, uint64_t first,
+                  uint64_t count, void* staging, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  if (bit < 0 || bit >= n_local_bits || (half != 0 && half != 1) ||
+      first + count > (1ull << (n_local_bits - 1))) {
+    set_error("qsb_pack_half: bad bit/half/range");
+    return QSB_ERR_SHAPE;
+  }
+  if (count == 0) return QSB_OK;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    k_pack_half<double><<<stream_grid(count), kThreads, 0, st>>>(static_cast<const double2*>(shard), bit, half,
+                                                                 first, count, static_cast<double2*>(staging));
+  else
+    k_pack_half<float><<<stream_grid(count), kThreads, 0, st>>>(static_cast<const float2*>(shard), bit, half,
+                                                                first, count, static_cast<float2*>(staging));
+  QSB_CHECK_LAUNCH("qsb_pack_half");
+  return QSB_OK;
+}
+
+int qsb_unpack_half(void* shard, int n_local_bits, int dtype, int bit, int half, uint64_t first, uint64_t count,
+                    const void* staging, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  if (bit < 0 || bit >= n_local_bits || (half != 0 && half != 1) ||
+      first + count > (1ull << (n_local_bits - 1))) {
+    set_error("qsb_unpack_half: bad bit/half/range");
+    return QSB_ERR_SHAPE;
+  }
+  if (count == 0) return QSB_OK;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    k_unpack_half<double><<<stream_grid(count), kThreads, 0, st>>>(static_cast<double2*>(shard), bit, half, first,
+                                                                   count, static_cast<const double2*>(staging));
+  else
+    k_unpack_half<float><<<stream_grid(count), kThreads, 0, st>>>(static_cast<float2*>(shard), bit, half, first,
+                                                                  count, static_cast<const float2*>(staging));
+  QSB_CHECK_LAUNCH("qsb_unpack_half");
+  return QSB_OK;
+}
+
+}  // extern "C"

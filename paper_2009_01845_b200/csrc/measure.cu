@@ -1,0 +1,849 @@
+// Measurement kernels: probabilities, marginals, the exact sequential CDF and PCG64 sampling.
+//
+// Reference path: qsim.measurement.sample -> marginal_probabilities
+// (/root/reference/pkg/src/qsim/measurement.py:36-87).  Samples must be bit-identical to the
+// reference for identical RNG draws, so every step reproduces numpy's floating-point order:
+//   probabilities   np.abs(a.astype(c128))**2 == (M*sqrt(fma(r,r,1)))^2
+//   marginal        numpy add.reduce: pairwise_sum over the innermost reduced run, sequential
+//                   accumulation over the outer rows (App. B.2)
+//   cumsum          strictly sequential fl(c + p): reproduced EXACTLY in parallel by the
+//                   binade-integer scan below (App. B.3)
+//   draws           numpy PCG64 (XSL-RR 128/64), u = (raw >> 11) * 2^-53 (App. B.4)
+//   search          np.searchsorted(cum, u, side="right"), clipped (App. B.5)
+#include <math.h>
+#include <string.h>
+
+#include "qsb_common.cuh"
+
+namespace qsb {
+
+constexpr int kMT = 256;
+
+static int grid_for(uint64_t n, int per = kMT) {
+  uint64_t b = (n + per - 1) / per;
+  if (b < 1) b = 1;
+  if (b > 148ull * 32ull) b = 148ull * 32ull;
+  return (int)b;
+}
+
+// numpy's SIMD complex absolute value, squared (no contraction: explicit _rn intrinsics)
+__device__ __forceinline__ double np_abs2(double re, double im) {
+  const double ar = fabs(re), ai = fabs(im);
+  const double big = fmax(ar, ai), small = fmin(ar, ai);
+  if (big == 0.0) return 0.0;
+  const double r = __ddiv_rn(small, big);
+  const double h = __dmul_rn(big, __dsqrt_rn(__fma_rn(r, r, 1.0)));
+  return __dmul_rn(h, h);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kMT) k_probs(const cplx<R>* __restrict__ a, uint64_t n, double* __restrict__ p) {
+  const uint64_t stride = (uint64_t)gridDim.x * kMT;
+  for (uint64_t i = (uint64_t)blockIdx.x * kMT + threadIdx.x; i < n; i += stride) {
+    const cplx<R> v = a[i];
+    p[i] = np_abs2((double)v.x, (double)v.y);
+  }
+}
+
+// ---- numpy pairwise_sum (loops_utils.h: PW_BLOCKSIZE 128, 8-way unroll) -------------------
+// Leaf: a run of L <= 128 contiguous doubles.
+__device__ __forceinline__ double np_pairwise_leaf(const double* a, int L) {
+  if (L < 8) {
+    double res = 0.0;
+    for (int i = 0; i < L; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < L - (L % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < L; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+// leaf sums of 128-element blocks (rows longer than 128 are power-of-two long, so numpy's
+// recursion splits them into a perfect binary tree of 128-element leaves)
+__global__ void __launch_bounds__(kMT) k_leaf128(const double* __restrict__ p, uint64_t n_leaves,
+                                                 double* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * kMT;
+  for (uint64_t l = (uint64_t)blockIdx.x * kMT + threadIdx.x; l < n_leaves; l += stride)
+    out[l] = np_pairwise_leaf(p + l * 128, 128);
+}
+
+// one level of the pairwise tree: out[i] = in[2i] + in[2i+1]
+__global__ void __launch_bounds__(kMT) k_pair_level(const double* __restrict__ in, uint64_t n_out,
+                                                    double* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * kMT;
+  for (uint64_t i = (uint64_t)blockIdx.x * kMT + threadIdx.x; i < n_out; i += stride)
+    out[i] = __dadd_rn(in[2 * i], in[2 * i + 1]);
+}
+
+// rows shorter than or equal to 128: one thread per row
+__global__ void __launch_bounds__(kMT) k_row_small(const double* __restrict__ p, uint64_t n_rows, int L,
+                                                   double* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * kMT;
+  for (uint64_t r = (uint64_t)blockIdx.x * kMT + threadIdx.x; r < n_rows; r += stride)
+    out[r] = np_pairwise_leaf(p + r * (uint64_t)L, L);
+}
+
+__device__ __forceinline__ uint64_t pdep64(uint64_t x, uint64_t mask) {
+  uint64_t r = 0;
+  for (uint64_t bb = 1; mask; bb <<= 1) {
+    const uint64_t low = mask & (~mask + 1);
+    if (x & bb) r |= low;
+    mask ^= low;
+  }
+  return r;
+}
+
+// Sequential outer accumulation: out[key] = ((0 + v[row_0]) + v[row_1]) + ... over the rows
+// (index = pdep(key, keep) | pdep(j, red)) in increasing j.  `v` is indexed by row.
+__global__ void __launch_bounds__(kMT) k_fold_rows(const double* __restrict__ v, uint64_t n_keys,
+                                                   uint64_t keep_mask, uint64_t red_mask, uint64_t n_red,
+                                                   double* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * kMT;
+  for (uint64_t key = (uint64_t)blockIdx.x * kMT + threadIdx.x; key < n_keys; key += stride) {
+    const uint64_t kb = pdep64(key, keep_mask);
+    double acc = 0.0;
+    for (uint64_t j = 0; j < n_red; ++j) acc = __dadd_rn(acc, v[kb | pdep64(j, red_mask)]);
+    out[key] = acc;
+  }
+}
+
+// out[j] = in[src(j)] where output bit b (LSB first) takes compressed-index bit rank[b]:
+// reorders the kept bits into the requested qubit order
+struct BitRanks {
+  int k;
+  int8_t rank[48];
+};
+__global__ void __launch_bounds__(kMT) k_permute_out(const double* __restrict__ in, uint64_t n, const BitRanks br,
+                                                     double* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * kMT;
+  for (uint64_t j = (uint64_t)blockIdx.x * kMT + threadIdx.x; j < n; j += stride) {
+    uint64_t src = 0;
+    for (int b = 0; b < br.k; ++b) src |= ((j >> b) & 1ull) << br.rank[b];
+    out[j] = in[src];
+  }
+}
+
+// ---- exact sequential cumsum ---------------------------------------------------------------
+// Sequential prefix c_i = fl(c_{i-1} + p_i) with p_i >= 0.  Inside one binade [2^e, 2^(e+1))
+// every c is an integer multiple K of u = 2^(e-52), and fl(K*u + p) = (K + d)*u where
+// d = round(p/u) with ties broken towards the even K+d -- an integer increment that depends on
+// the running K only through its parity.  Such maps K -> K + d[K & 1] compose associatively
+// ((D0, D1) pairs), so the sequential sum becomes a parallel integer scan.  Elements whose
+// approximate prefix lies near a power of two (or that start a new binade) are "serial": their
+// value is computed with a real fl(c + p) by a single stitching thread.  Result is bit-identical
+// to the strictly sequential loop.
+
+struct Piece {           // composed map over a run inside one binade
+  long long d0, d1;      // increment of K when K is even / odd
+  int e;                 // binade exponent of the run (INT_MIN: identity / zero run)
+  int pad;
+};
+
+__device__ __forceinline__ Piece piece_id() {
+  Piece q;
+  q.d0 = 0;
+  q.d1 = 0;
+  q.e = -100000;
+  q.pad = 0;
+  return q;
+}
+
+__device__ __forceinline__ Piece piece_then(const Piece& a, const Piece& b) {
+  // apply a, then b (same binade, or one of them the identity)
+  Piece r;
+  r.e = (a.e != -100000) ? a.e : b.e;
+  r.d0 = a.d0 + (((a.d0) & 1) ? b.d1 : b.d0);
+  r.d1 = a.d1 + (((1 + a.d1) & 1) ? b.d1 : b.d0);
+  r.pad = 0;
+  return r;
+}
+
+__device__ __forceinline__ double piece_apply(const Piece& q, double c) {
+  if (q.e == -100000 || (q.d0 == 0 && q.d1 == 0)) return c;
+  // K = c / 2^(e-52) exactly
+  const long long K = (long long)ldexp(c, 52 - q.e);
+  const long long K2 = K + ((K & 1) ? q.d1 : q.d0);
+  return ldexp((double)K2, q.e - 52);
+}
+
+// Fast single-thread fallback (also the reference semantics): c_i = fl(c_{i-1} + p_i).
+__global__ void k_cumsum_serial(const double* __restrict__ p, uint64_t n, double* __restrict__ c) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  double acc = 0.0;
+  for (uint64_t i = 0; i < n; ++i) {
+    acc = __dadd_rn(acc, p[i]);
+    c[i] = acc;
+  }
+}
+
+constexpr int kScanItems = 16;                 // elements per thread
+constexpr int kScanBlock = kMT * kScanItems;   // 4096 elements per block
+
+// Pass A: per block, an approximate inclusive prefix of p (plain fp64), block totals
+__global__ void __launch_bounds__(kMT) k_scan_block_sums(const double* __restrict__ p, uint64_t n,
+                                                         double* __restrict__ block_sum) {
+  __shared__ double sh[kMT];
+  const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
+  double acc = 0.0;
+  for (int it = 0; it < kScanItems; ++it) {
+    const uint64_t i = b0 + (uint64_t)threadIdx.x * kScanItems + it;
+    if (i < n) acc += p[i];
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kMT / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) block_sum[blockIdx.x] = sh[0];
+}
+
+// exclusive scan of the block sums (one block, sequential chunks per thread; approximate)
+__global__ void __launch_bounds__(1024) k_scan_top(double* __restrict__ v, uint64_t nb) {
+  __shared__ double sh[1024];
+  const uint64_t per = (nb + 1023) / 1024;
+  const uint64_t lo = threadIdx.x * per;
+  double acc = 0.0;
+  for (uint64_t i = lo; i < lo + per && i < nb; ++i) acc += v[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double run = 0.0;
+    for (int t = 0; t < 1024; ++t) {
+      const double x = sh[t];
+      sh[t] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+  double run = sh[threadIdx.x];
+  for (uint64_t i = lo; i < lo + per && i < nb; ++i) {
+    const double x = v[i];
+    v[i] = run;
+    run += x;
+  }
+}
+
+// Binade of an approximate prefix value: -100000 for zero.  "risky" when within 2^-16
+// (relative) of a power of two or in the subnormal-adjacent range.
+__device__ __forceinline__ int approx_binade(double s, bool* risky) {
+  if (s <= 0.0) {
+    *risky = false;
+    return -100000;
+  }
+  int e;
+  const double m = frexp(s, &e);  // s = m * 2^e, m in [0.5, 1)
+  const double lo = 0.5 * (1.0 + 1.52587890625e-05);   // 2^-16 margins
+  const double hi = 1.0 - 1.52587890625e-05;
+  *risky = (m < lo) || (m > hi) || (e < -1000);
+  return e - 1;  // s in [2^(e-1), 2^e)
+}
+
+// Pass B: classify every element, build per-block head pieces / serial lists.
+// Outputs per element: flag (serial?) stored in `cls` (1 = serial), piece of safe elements
+// folded per block into head / per-serial "after" pieces.
+struct BlockInfo {
+  Piece head;            // composed map from block start to the first serial element (excl.)
+  unsigned int n_serial; // serial elements in this block
+  unsigned int first_serial_slot;  // filled by the counting prefix
+};
+
+__device__ __forceinline__ Piece elem_piece(double p, int e) {
+  Piece q;
+  q.e = e;
+  q.pad = 0;
+  if (e == -100000) {  // zero run: p == 0
+    q.d0 = 0;
+    q.d1 = 0;
+    return q;
+  }
+  const double v = ldexp(p, 52 - e);  // p / u, exact
+  const double m = floor(v);
+  const double f = v - m;
+  const long long mi = (long long)m;
+  if (f < 0.5) {
+    q.d0 = mi;
+    q.d1 = mi;
+  } else if (f > 0.5) {
+    q.d0 = mi + 1;
+    q.d1 = mi + 1;
+  } else {
+    q.d0 = mi + (mi & 1);
+    q.d1 = mi + ((~mi) & 1);
+  }
+  return q;
+}
+
+// Each block: sequentially (per thread chunk) compute approximate prefix, classes and pieces;
+// then a block-level scan of pieces with "serial" resets.  To keep the block code simple the
+// per-element classification is written to global scratch and the block structure is
+// assembled by a warp-serial walk over thread chunks.
+__global__ void __launch_bounds__(kMT) k_classify(const double* __restrict__ p, uint64_t n,
+                                                  const double* __restrict__ block_prefix,
+                                                  unsigned char* __restrict__ serial,
+                                                  int* __restrict__ binade) {
+  __shared__ double sh[kMT];
+  const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
+  const uint64_t t0 = b0 + (uint64_t)threadIdx.x * kScanItems;
+  double loc = 0.0;
+  double vals[kScanItems];
+#pragma unroll
+  for (int it = 0; it < kScanItems; ++it) {
+    const uint64_t i = t0 + it;
+    vals[it] = (i < n) ? p[i] : 0.0;
+    loc += vals[it];
+  }
+  sh[threadIdx.x] = loc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double run = block_prefix[blockIdx.x];
+    for (int t = 0; t < kMT; ++t) {
+      const double x = sh[t];
+      sh[t] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+  double s = sh[threadIdx.x];
+  // previous element's class needs the prefix of element t0-1 = s (exclusive prefix)
+  bool prev_risky;
+  int prev_e = (t0 == 0) ? -100001 : approx_binade(s, &prev_risky);
+  if (t0 == 0) prev_risky = false;
+#pragma unroll
+  for (int it = 0; it < kScanItems; ++it) {
+    const uint64_t i = t0 + it;
+    s += vals[it];
+    bool risky;
+    const int e = approx_binade(s, &risky);
+    if (i < n) {
+      const bool ser = risky || prev_risky || (e != prev_e && e != -100000) || (e == -100000 && prev_e != -100000 && prev_e != -100001);
+      serial[i] = ser ? 1 : 0;
+      binade[i] = e;
+    }
+    prev_e = e;
+    prev_risky = risky;
+  }
+}
+
+// Pass C: per block, compose pieces of the safe elements between serial points.
+//   head[b]      : map from block start to first serial (or block end)
+//   after[slot]  : for each serial element (in global order), the map of the safe run after it
+//                  up to the next serial element or block end
+__global__ void __launch_bounds__(32) k_block_pieces(const double* __restrict__ p, uint64_t n,
+                                                     const unsigned char* __restrict__ serial,
+                                                     const int* __restrict__ binade,
+                                                     const unsigned int* __restrict__ serial_base,
+                                                     Piece* __restrict__ head, Piece* __restrict__ after,
+                                                     unsigned long long* __restrict__ serial_idx) {
+  // one warp per block of kScanBlock elements; lane-chunked composition then a serial walk
+  // over the 32 lane chunks by lane 0 (pieces are tiny).
+  const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
+  const int per = kScanBlock / 32;
+  const uint64_t l0 = b0 + (uint64_t)threadIdx.x * per;
+  // lane-local: head piece (before first serial in chunk), count of serials, tail piece
+  Piece lhead = piece_id(), ltail = piece_id();
+  int nser = 0;
+  for (int k = 0; k < per; ++k) {
+    const uint64_t i = l0 + k;
+    if (i >= n) break;
+    if (serial[i]) {
+      ++nser;
+      ltail = piece_id();
+    } else {
+      const Piece q = elem_piece(p[i], binade[i]);
+      if (nser == 0)
+        lhead = piece_then(lhead, q);
+      else
+        ltail = piece_then(ltail, q);
+    }
+  }
+  // exclusive count of serials before this lane within the block
+  int incl = nser;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((int)threadIdx.x >= o) incl += v;
+  }
+  const int excl = incl - nser;
+  const unsigned int base = serial_base[blockIdx.x] + excl;
+  // per-lane: fill serial_idx and the "after" pieces of serials inside the chunk except the
+  // last one (whose after-piece continues into later lanes)
+  {
+    int s = 0;
+    Piece run = piece_id();
+    for (int k = 0; k < per; ++k) {
+      const uint64_t i = l0 + k;
+      if (i >= n) break;
+      if (serial[i]) {
+        if (s > 0) after[base + s - 1] = run;
+        serial_idx[base + s] = i;
+        ++s;
+        run = piece_id();
+      } else if (s > 0) {
+        run = piece_then(run, elem_piece(p[i], binade[i]));
+      }
+    }
+  }
+  // stitch lanes: the after-piece of the last serial of lane L continues through lanes L+1..
+  // until a lane that has a serial (absorbing that lane's head).  Block head = lanes' heads
+  // composed until the first lane with a serial.  Done serially by lane 0 via shared memory.
+  __shared__ Piece sh_head[32], sh_tail[32];
+  __shared__ int sh_n[32];
+  sh_head[threadIdx.x] = lhead;
+  sh_tail[threadIdx.x] = ltail;
+  sh_n[threadIdx.x] = nser;
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    Piece bh = piece_id();
+    int L = 0;
+    for (; L < 32; ++L) {
+      bh = piece_then(bh, sh_head[L]);
+      if (sh_n[L]) break;
+    }
+    head[blockIdx.x] = bh;
+    // open "after" runs
+    unsigned int slot = serial_base[blockIdx.x];
+    bool open = false;
+    Piece run = piece_id();
+    unsigned int open_slot = 0;
+    for (int l = 0; l < 32; ++l) {
+      if (open) {
+        run = piece_then(run, sh_head[l]);
+        if (sh_n[l]) {
+          after[open_slot] = run;
+          open = false;
+        }
+      }
+      if (sh_n[l]) {
+        slot += sh_n[l];
+        open = true;
+        open_slot = slot - 1;
+        run = sh_tail[l];
+      }
+    }
+    if (open) after[open_slot] = run;
+  }
+}
+
+// Pass D: one thread walks blocks and serial points in order.
+__global__ void k_stitch(const double* __restrict__ p, uint64_t n_blocks, const Piece* __restrict__ head,
+                         const unsigned int* __restrict__ serial_count, const Piece* __restrict__ after,
+                         const unsigned long long* __restrict__ serial_idx, double* __restrict__ block_start,
+                         double* __restrict__ serial_val) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double c = 0.0;
+  unsigned int slot = 0;
+  for (uint64_t b = 0; b < n_blocks; ++b) {
+    block_start[b] = c;
+    c = piece_apply(head[b], c);
+    const unsigned int ns = serial_count[b];
+    for (unsigned int k = 0; k < ns; ++k, ++slot) {
+      c = __dadd_rn(c, p[serial_idx[slot]]);
+      serial_val[slot] = c;
+      c = piece_apply(after[slot], c);
+    }
+  }
+}
+
+// Pass E: materialize c_i per element (one thread per 16-element chunk after a block-level
+// walk of chunk starts), then normalise by the total.
+__global__ void __launch_bounds__(32) k_materialize(const double* __restrict__ p, uint64_t n,
+                                                    const unsigned char* __restrict__ serial,
+                                                    const int* __restrict__ binade,
+                                                    const double* __restrict__ block_start,
+                                                    const unsigned int* __restrict__ serial_base,
+                                                    const double* __restrict__ serial_val,
+                                                    double* __restrict__ c_out) {
+  const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
+  const int per = kScanBlock / 32;
+  const uint64_t l0 = b0 + (uint64_t)threadIdx.x * per;
+  // lane pieces: map over the lane chunk ignoring serials -> need value at chunk start.
+  // Compose per lane: if the chunk has a serial, the value at chunk end is "constant" from the
+  // last serial; else a pure piece.
+  Piece pure = piece_id();
+  int nser = 0;
+  Piece tail = piece_id();
+  for (int k = 0; k < per; ++k) {
+    const uint64_t i = l0 + k;
+    if (i >= n) break;
+    if (serial[i]) {
+      ++nser;
+      tail = piece_id();
+    } else {
+      const Piece q = elem_piece(p[i], binade[i]);
+      if (nser == 0)
+        pure = piece_then(pure, q);
+      else
+        tail = piece_then(tail, q);
+    }
+  }
+  int incl = nser;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((int)threadIdx.x >= o) incl += v;
+  }
+  const int excl = incl - nser;
+  __shared__ Piece sh_pure[32], sh_tail[32];
+  __shared__ int sh_n[32], sh_excl[32];
+  sh_pure[threadIdx.x] = pure;
+  sh_tail[threadIdx.x] = tail;
+  sh_n[threadIdx.x] = nser;
+  sh_excl[threadIdx.x] = excl;
+  __syncwarp();
+  __shared__ double sh_start[32];
+  if (threadIdx.x == 0) {
+    double c = block_start[blockIdx.x];
+    for (int l = 0; l < 32; ++l) {
+      sh_start[l] = c;
+      if (sh_n[l]) {
+        const unsigned int last = serial_base[blockIdx.x] + sh_excl[l] + sh_n[l] - 1;
+        c = piece_apply(sh_tail[l], serial_val[last]);
+      } else {
+        c = piece_apply(sh_pure[l], c);
+      }
+    }
+  }
+  __syncwarp();
+  double c = sh_start[threadIdx.x];
+  unsigned int slot = serial_base[blockIdx.x] + excl;
+  for (int k = 0; k < per; ++k) {
+    const uint64_t i = l0 + k;
+    if (i >= n) break;
+    if (serial[i]) {
+      c = serial_val[slot++];
+    } else {
+      Piece q = elem_piece(p[i], binade[i]);
+      c = piece_apply(q, c);
+    }
+    c_out[i] = c;
+  }
+}
+
+__global__ void k_count_serial(const unsigned char* __restrict__ serial, uint64_t n, unsigned int* __restrict__ cnt) {
+  __shared__ unsigned int sh[kMT];
+  const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
+  unsigned int c = 0;
+  for (int it = 0; it < kScanItems; ++it) {
+    const uint64_t i = b0 + (uint64_t)threadIdx.x * kScanItems + it;
+    if (i < n) c += serial[i];
+  }
+  sh[threadIdx.x] = c;
+  __syncthreads();
+  for (int s = kMT / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cnt[blockIdx.x] = sh[0];
+}
+
+// exclusive scan of counts (single block), writes total to cnt_total
+__global__ void __launch_bounds__(1024) k_scan_counts(const unsigned int* __restrict__ cnt, uint64_t nb,
+                                                      unsigned int* __restrict__ base, unsigned int* total) {
+  __shared__ unsigned int sh[1024];
+  const uint64_t per = (nb + 1023) / 1024;
+  const uint64_t lo = threadIdx.x * per;
+  unsigned int acc = 0;
+  for (uint64_t i = lo; i < lo + per && i < nb; ++i) acc += cnt[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int run = 0;
+    for (int t = 0; t < 1024; ++t) {
+      const unsigned int x = sh[t];
+      sh[t] = run;
+      run += x;
+    }
+    *total = run;
+  }
+  __syncthreads();
+  unsigned int run = sh[threadIdx.x];
+  for (uint64_t i = lo; i < lo + per && i < nb; ++i) {
+    base[i] = run;
+    run += cnt[i];
+  }
+}
+
+__global__ void __launch_bounds__(kMT) k_normalize(double* __restrict__ c, uint64_t n) {
+  const double total = c[n - 1];
+  const uint64_t stride = (uint64_t)gridDim.x * kMT;
+  for (uint64_t i = (uint64_t)blockIdx.x * kMT + threadIdx.x; i < n; i += stride) c[i] = c[i] / total;
+}
+
+// ---- PCG64 ---------------------------------------------------------------------------------
+typedef unsigned __int128 u128;
+__device__ __forceinline__ u128 pcg_mult() {
+  return ((u128)0x2360ED051FC65DA4ull << 64) | (u128)0x4385DF649FCCF645ull;
+}
+__device__ __forceinline__ uint64_t pcg_out(u128 s) {
+  const uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+  const unsigned rot = (unsigned)(hi >> 58);
+  const uint64_t x = hi ^ lo;
+  return (x >> rot) | (x << ((64 - rot) & 63));
+}
+// LCG jump-ahead by `delta` steps
+__device__ u128 pcg_advance(u128 s, u128 inc, uint64_t delta) {
+  u128 cur_mult = pcg_mult(), cur_plus = inc, acc_mult = 1, acc_plus = 0;
+  while (delta) {
+    if (delta & 1) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return acc_mult * s + acc_plus;
+}
+
+constexpr int kShotsPerThread = 32;
+
+__global__ void __launch_bounds__(kMT) k_sample(const double* __restrict__ cum, uint64_t n, uint64_t s_hi,
+                                                uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, uint64_t n_shots,
+                                                long long* __restrict__ out) {
+  const uint64_t t = (uint64_t)blockIdx.x * kMT + threadIdx.x;
+  const uint64_t first = t * kShotsPerThread;
+  if (first >= n_shots) return;
+  const u128 inc = ((u128)i_hi << 64) | i_lo;
+  u128 s = pcg_advance(((u128)s_hi << 64) | s_lo, inc, first);
+  const u128 mult = pcg_mult();
+  for (int k = 0; k < kShotsPerThread; ++k) {
+    const uint64_t shot = first + k;
+    if (shot >= n_shots) break;
+    s = s * mult + inc;
+    const double u = (double)(pcg_out(s) >> 11) * (1.0 / 9007199254740992.0);
+    // upper_bound: number of cum[i] <= u
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint64_t mid = lo + ((hi - lo) >> 1);
+      if (cum[mid] <= u)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    uint64_t idx = lo;
+    if (idx > n - 1) idx = n - 1;
+    out[shot] = (long long)idx;
+  }
+}
+
+}  // namespace qsb
+
+using namespace qsb;
+
+extern "C" {
+
+int qsb_probabilities(const void* amps, uint64_t n, int dtype, double* probs, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    k_probs<double><<<grid_for(n), kMT, 0, st>>>(static_cast<const double2*>(amps), n, probs);
+  else if (dtype == QSB_C64)
+    k_probs<float><<<grid_for(n), kMT, 0, st>>>(static_cast<const float2*>(amps), n, probs);
+  else {
+    set_error("unknown dtype %d", dtype);
+    return QSB_ERR_ARG;
+  }
+  QSB_CHECK_LAUNCH("qsb_probabilities");
+  return QSB_OK;
+}
+
+}  // extern "C"
+
+// Marginal with explicit output order.  `kept` lists the kept bit positions in output order
+// (kept[0] = most significant output bit).  scratch: qsb_marginal_scratch_doubles() doubles.
+extern "C" uint64_t qsb_marginal_scratch_doubles(int n_bits, int k) {
+  return (1ull << k) + (1ull << (n_bits - 1)) + 256;
+}
+
+extern "C" int qsb_marginal(const double* probs, int n_bits, int k, const int* kept, double* out, double* scratch,
+                            void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (n_bits < 1 || n_bits > 40 || k < 1 || k > n_bits) {
+    set_error("qsb_marginal: bad sizes (n=%d, k=%d)", n_bits, k);
+    return QSB_ERR_SHAPE;
+  }
+  uint64_t keep = 0;
+  for (int i = 0; i < k; ++i) {
+    if (kept[i] < 0 || kept[i] >= n_bits || ((keep >> kept[i]) & 1ull)) {
+      set_error("qsb_marginal: bad kept bit");
+      return QSB_ERR_SHAPE;
+    }
+    keep |= 1ull << kept[i];
+  }
+  const uint64_t N = 1ull << n_bits;
+  const uint64_t red = (N - 1) & ~keep;
+  const uint64_t n_keys = 1ull << k;
+  const double* asc = scratch;  // 2^k, ascending kept-bit order
+  double* work = scratch + n_keys;
+  if (red == 0) {
+    asc = probs;
+  } else if (red & 1ull) {
+    // innermost run of reduced bits [0, r): numpy pairwise_sum per row
+    int r = 0;
+    while (r < n_bits && ((red >> r) & 1ull)) ++r;
+    const uint64_t L = 1ull << r;
+    const uint64_t rows = N >> r;
+    const double* rowsum = work;
+    if (L <= 128) {
+      k_row_small<<<grid_for(rows), kMT, 0, st>>>(probs, rows, (int)L, work);
+    } else {
+      const uint64_t leaves = N / 128;
+      double* a = work;
+      double* b = work + leaves;
+      k_leaf128<<<grid_for(leaves), kMT, 0, st>>>(probs, leaves, a);
+      uint64_t cur = leaves;
+      while (cur > rows) {
+        k_pair_level<<<grid_for(cur / 2), kMT, 0, st>>>(a, cur / 2, b);
+        double* tmp = a;
+        a = b;
+        b = tmp;
+        cur /= 2;
+      }
+      rowsum = a;
+    }
+    // sequential accumulation over the outer reduced rows with equal kept bits
+    const uint64_t keep_row = keep >> r, red_row = red >> r;
+    const uint64_t n_red = 1ull << __builtin_popcountll(red_row);
+    k_fold_rows<<<grid_for(n_keys), kMT, 0, st>>>(rowsum, n_keys, keep_row, red_row, n_red, scratch);
+  } else {
+    // innermost run kept: element-wise sequential accumulation over every reduced row
+    const uint64_t n_red = 1ull << __builtin_popcountll(red);
+    k_fold_rows<<<grid_for(n_keys), kMT, 0, st>>>(probs, n_keys, keep, red, n_red, scratch);
+  }
+  // reorder: output bit b (LSB first) is kept[k-1-b], found at its rank among the kept bits
+  BitRanks br;
+  br.k = k;
+  for (int b = 0; b < k; ++b) {
+    const int bit = kept[k - 1 - b];
+    br.rank[b] = (int8_t)__builtin_popcountll(keep & ((1ull << bit) - 1ull));
+  }
+  k_permute_out<<<grid_for(n_keys), kMT, 0, st>>>(asc, n_keys, br, out);
+  QSB_CHECK_LAUNCH("qsb_marginal");
+  return QSB_OK;
+}
+
+extern "C" size_t qsb_cumsum_scratch_bytes(uint64_t n) {
+  const uint64_t nb = (n + kScanBlock - 1) / kScanBlock;
+  size_t b = 0;
+  b += n * sizeof(unsigned char);        // serial flags
+  b = (b + 255) & ~(size_t)255;
+  b += n * sizeof(int);                  // binade
+  b = (b + 255) & ~(size_t)255;
+  b += nb * sizeof(double);              // block prefix
+  b += nb * sizeof(unsigned int) * 2;    // counts, bases
+  b = (b + 255) & ~(size_t)255;
+  b += nb * sizeof(Piece);               // heads
+  b += nb * sizeof(double);              // block starts
+  b += 256;
+  return b;
+}
+
+// The serial-point arrays are sized by the number of serial elements, which is data
+// dependent; they live in a separately grown buffer.
+static void* g_ser_buf = nullptr;
+static size_t g_ser_cap = 0;
+
+extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cum, void* scratch,
+                                     size_t scratch_bytes, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (n == 0) return QSB_OK;
+  if (scratch_bytes < qsb_cumsum_scratch_bytes(n)) {
+    set_error("qsb_cumsum_normalized: scratch too small");
+    return QSB_ERR_ARG;
+  }
+  const uint64_t nb = (n + kScanBlock - 1) / kScanBlock;
+  char* w = static_cast<char*>(scratch);
+  unsigned char* serial = reinterpret_cast<unsigned char*>(w);
+  w += (n + 255) & ~(uint64_t)255;
+  int* binade = reinterpret_cast<int*>(w);
+  w += ((n * sizeof(int)) + 255) & ~(uint64_t)255;
+  double* bpre = reinterpret_cast<double*>(w);
+  w += nb * sizeof(double);
+  unsigned int* cnt = reinterpret_cast<unsigned int*>(w);
+  w += nb * sizeof(unsigned int);
+  unsigned int* base = reinterpret_cast<unsigned int*>(w);
+  w += nb * sizeof(unsigned int);
+  w = reinterpret_cast<char*>(((uintptr_t)w + 255) & ~(uintptr_t)255);
+  Piece* head = reinterpret_cast<Piece*>(w);
+  w += nb * sizeof(Piece);
+  double* bstart = reinterpret_cast<double*>(w);
+
+  k_scan_block_sums<<<(int)nb, kMT, 0, st>>>(probs, n, bpre);
+  k_scan_top<<<1, 1024, 0, st>>>(bpre, nb);
+  k_classify<<<(int)nb, kMT, 0, st>>>(probs, n, bpre, serial, binade);
+  k_count_serial<<<(int)nb, kMT, 0, st>>>(serial, n, cnt);
+  unsigned int* d_total = nullptr;
+  // total count lives right after `base` in pinned host-visible memory would need a sync; we
+  // size the serial arrays conservatively instead: read the total back synchronously.
+  static unsigned int* h_total = nullptr;
+  if (!h_total) {
+    cudaError_t e = cudaMallocHost(&h_total, sizeof(unsigned int) * 2);
+    if (e != cudaSuccess) return cuda_status(e, "pinned total");
+  }
+  static unsigned int* d_tot = nullptr;
+  if (!d_tot) {
+    cudaError_t e = cudaMalloc(&d_tot, sizeof(unsigned int) * 2);
+    if (e != cudaSuccess) return cuda_status(e, "device total");
+  }
+  d_total = d_tot;
+  k_scan_counts<<<1, 1024, 0, st>>>(cnt, nb, base, d_total);
+  cudaError_t e = cudaMemcpyAsync(h_total, d_total, sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return cuda_status(e, "serial count copy");
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_status(e, "serial count sync");
+  const uint64_t ns = *h_total;
+  const size_t need = (ns + 1) * (sizeof(Piece) + sizeof(unsigned long long) + sizeof(double)) + 1024;
+  if (need > g_ser_cap) {
+    if (g_ser_buf) cudaFree(g_ser_buf);
+    g_ser_cap = need * 2;
+    e = cudaMalloc(&g_ser_buf, g_ser_cap);
+    if (e != cudaSuccess) {
+      g_ser_buf = nullptr;
+      g_ser_cap = 0;
+      return cuda_status(e, "serial buffers");
+    }
+  }
+  char* sb = static_cast<char*>(g_ser_buf);
+  Piece* after = reinterpret_cast<Piece*>(sb);
+  sb += (ns + 1) * sizeof(Piece);
+  unsigned long long* sidx = reinterpret_cast<unsigned long long*>(sb);
+  sb += (ns + 1) * sizeof(unsigned long long);
+  double* sval = reinterpret_cast<double*>(sb);
+
+  k_block_pieces<<<(int)nb, 32, 0, st>>>(probs, n, serial, binade, base, head, after, sidx);
+  k_stitch<<<1, 1, 0, st>>>(probs, nb, head, cnt, after, sidx, bstart, sval);
+  k_materialize<<<(int)nb, 32, 0, st>>>(probs, n, serial, binade, bstart, base, sval, cum);
+  k_normalize<<<grid_for(n), kMT, 0, st>>>(cum, n);
+  QSB_CHECK_LAUNCH("qsb_cumsum_normalized");
+  return QSB_OK;
+}
+
+// Reference-semantics sequential version (one device thread); kept for cross-checking the
+// parallel scan in the GPU tests.
+extern "C" int qsb_cumsum_serial(const double* probs, uint64_t n, double* cum, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  k_cumsum_serial<<<1, 1, 0, st>>>(probs, n, cum);
+  QSB_CHECK_LAUNCH("qsb_cumsum_serial");
+  return QSB_OK;
+}
+
+extern "C" int qsb_sample(const double* cum, uint64_t n, uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo,
+                          uint64_t n_shots, int64_t* samples, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (n == 0 || n_shots == 0) {
+    set_error("qsb_sample: empty distribution or no shots");
+    return QSB_ERR_ARG;
+  }
+  const uint64_t threads = (n_shots + kShotsPerThread - 1) / kShotsPerThread;
+  k_sample<<<(int)((threads + kMT - 1) / kMT), kMT, 0, st>>>(cum, n, s_hi, s_lo, i_hi, i_lo, n_shots,
+                                                            reinterpret_cast<long long*>(samples));
+  QSB_CHECK_LAUNCH("qsb_sample");
+  return QSB_OK;
+}

@@ -1,0 +1,100 @@
+"""Runs planned gate sequences on a device state (the replacement of the reference's per-gate
+loop, /root/reference/pkg/src/qsim/circuit.py:121-124).
+
+A Plan (fusion.py) is a list of PassSteps (one qsb_run_pass launch = one HBM sweep for many
+gates) and GateSteps (one qsb_apply_matrix launch for a sparse stand-alone gate).  Passes that
+carry a tile-external permutation (folded SWAPs) write out of place into a scratch buffer
+of the same size, after which the buffers trade places.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+from . import _native as nat
+from .fusion import GateStep, PassStep, Plan, plan_circuit
+
+# QSB_FUSION=0 disables pass fusion (every gate becomes its own kernel launch)
+FUSION_DEFAULT = os.environ.get("QSB_FUSION", "1") != "0"
+
+
+def _free_bytes() -> int:
+    torch = nat.torch_mod()
+    free, _total = torch.cuda.mem_get_info()
+    return int(free)
+
+
+def plan_for_state(state, specs, fuse: bool | None = None) -> Plan:
+    fuse = FUSION_DEFAULT if fuse is None else fuse
+    bytes_needed = state.n_amps * state.precision.itemsize
+    allow_ext = _free_bytes() > bytes_needed + (512 << 20)
+    return plan_circuit(specs, state.n_qubits, state.precision.qsb_dtype, allow_ext_perm=allow_ext, fuse=fuse)
+
+
+def _apply_gate_step(ptr, n, dtype, g, stream):
+    lib = nat.lib()
+    tb = np.array(g.targets, dtype=np.int32)
+    cb = np.array(g.controls or (0,), dtype=np.int32)
+    if g.kind == "diag":
+        dim = len(g.matrix)
+        mat = np.ascontiguousarray(np.diag(g.matrix))
+        kernel = nat.KERNEL_DIAGONAL
+    elif g.kind == "swap":
+        mat = np.array([[1, 0, 0, 0], [0, 0, 1, 0], [0, 1, 0, 0], [0, 0, 0, 1]], dtype=np.complex128)
+        kernel = nat.KERNEL_PERMUTATION
+    else:
+        mat = np.ascontiguousarray(g.matrix, dtype=np.complex128)
+        kernel = nat.KERNEL_AUTO
+    nat.check(
+        lib.qsb_apply_matrix(ptr, n, dtype, len(g.targets), tb.ctypes.data, len(g.controls), cb.ctypes.data,
+                             mat.ctypes.data, kernel, stream),
+        "apply_matrix",
+    )
+
+
+def run_plan(state, plan: Plan, scratch_holder: dict | None = None, stream=None, events: list | None = None):
+    """Execute every step of `plan` on `state` (in place; the tensor object may be swapped).
+
+    `events`, when given, receives one (start, end) pair of CUDA events per pass launch,
+    recorded on the launching stream (bench.py's per-kernel timing)."""
+    lib = nat.lib()
+    st = nat.stream_ptr(stream)
+    n = state.n_qubits
+    dtype = state.precision.qsb_dtype
+    holder = scratch_holder if scratch_holder is not None else {}
+    for step in plan.steps:
+        if isinstance(step, GateStep):
+            _apply_gate_step(state.data_ptr, n, dtype, step.gate, st)
+            continue
+        words = step.words
+        if events is not None:
+            ev0 = nat.torch_mod().cuda.Event(enable_timing=True)
+            ev1 = nat.torch_mod().cuda.Event(enable_timing=True)
+            ev0.record(stream)
+        if step.ext_perm:
+            scratch = holder.get("buf")
+            if scratch is None or scratch.numel() != state.n_amps or scratch.dtype != state.tensor.dtype:
+                scratch = nat.torch_mod().empty_like(state.tensor)
+            nat.check(
+                lib.qsb_run_pass(state.data_ptr, scratch.data_ptr(), n, dtype, words.ctypes.data, len(words), st),
+                "run_pass",
+            )
+            old = state._t
+            state._t = scratch
+            holder["buf"] = old
+        else:
+            nat.check(
+                lib.qsb_run_pass(state.data_ptr, state.data_ptr, n, dtype, words.ctypes.data, len(words), st),
+                "run_pass",
+            )
+        if events is not None:
+            ev1.record(stream)
+            events.append((ev0, ev1))
+
+
+def run_gates(state, specs, fuse: bool | None = None, scratch_holder: dict | None = None):
+    plan = plan_for_state(state, specs, fuse)
+    run_plan(state, plan, scratch_holder)
+    return plan

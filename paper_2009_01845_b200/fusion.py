@@ -1,0 +1,606 @@
+"""Pass planner: turns a gate sequence into fused HBM passes for qsb_run_pass.
+
+The reference applies every gate as its own sweep over the state (circuit.py:121-124 ->
+gates.py:380-469).  On B200 the sweep, not the arithmetic, is the cost, so this module packs
+runs of gates into "passes": one streaming read + write of the state in which every gate
+whose non-diagonal targets fall inside a 2**K-amplitude tile is applied in registers.
+
+Rules (all sound by commutation, never by approximation):
+  * a gate g may be hoisted over a deferred gate d iff targets(g) & support(d) == {} and
+    targets(d) & support(g) == {} (diagonal gates have no targets; controls and diagonal
+    supports are "support");
+  * diagonal gates need no locality -> always absorbed (compiled to pivot / parity / term ops);
+  * uncontrolled SWAPs are absorbed as relabels (tile-internal: free; tile-external: the pass
+    writes tiles to permuted positions, which needs an out-of-place destination);
+  * the tile's low L bits are always the low state bits (coalesced 256-byte runs).
+
+The program word format is documented in paper_2009_01845_b200/csrc/pass.cu.
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .gates import KernelClass, classify_kernel, gate_matrix
+
+MAGIC = 0x51534250
+VERSION = 3
+OP_END, OP_LAYOUT, OP_G1, OP_G2, OP_PIVOT, OP_PARITY, OP_TERM, OP_SCALE = range(8)
+G_COMPLEX, G_REAL, G_SWAPX = 0, 1, 2
+H_TILEPOS = 16
+MAX_PROG_WORDS = 6144
+MAX_PIVOTS = 64
+
+
+@dataclass(frozen=True)
+class TileGeometry:
+    K: int  # tile bits
+    G: int  # swizzle group (bank-conflict) bits
+    L: int  # low bits always in the tile (256-byte runs)
+
+    @property
+    def nreg(self) -> int:
+        return self.K - 8
+
+    @property
+    def A(self) -> int:
+        return 1 << self.nreg
+
+
+GEOMETRY = {nat.QSB_C128: TileGeometry(12, 3, 4), nat.QSB_C64: TileGeometry(13, 4, 5)}
+
+
+def _f2w(x: float) -> int:
+    return struct.unpack("<q", struct.pack("<d", float(x)))[0]
+
+
+def _bits(positions) -> int:
+    m = 0
+    for p in positions:
+        m |= 1 << p
+    return m
+
+
+# ------------------------------------------------------------------------------------------
+# normalised gates (bit positions, not qubits)
+# ------------------------------------------------------------------------------------------
+@dataclass
+class NGate:
+    kind: str  # "diag" | "g1" | "g2" | "swap"
+    targets: tuple  # bit positions; targets[0] = matrix MSB
+    controls: tuple
+    matrix: np.ndarray | None  # g1/g2: 2^t x 2^t; diag: the diagonal
+    tmask: int
+    smask: int
+    index: int = -1  # position in the source queue
+
+    def touched_fraction(self) -> float:
+        """Share of the state a stand-alone single-gate kernel reads+writes."""
+        c = 2.0 ** -len(self.controls)
+        if self.kind == "diag":
+            rows = int(np.count_nonzero(self.matrix != 1.0))
+            return c * rows / len(self.matrix)
+        if self.kind == "swap":
+            return 0.5
+        return c
+
+
+_SWAP = np.array([[1, 0, 0, 0], [0, 0, 1, 0], [0, 1, 0, 0], [0, 0, 0, 1]], dtype=np.complex128)
+_XMAT = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+
+
+def normalize(spec, n_qubits: int, index: int = -1) -> NGate | None:
+    """GateSpec (or duck-typed reference GateSpec) -> NGate; None for exact identities."""
+    m = gate_matrix(spec)
+    tb = tuple(n_qubits - 1 - int(q) for q in spec.targets)
+    cb = tuple(n_qubits - 1 - int(q) for q in spec.controls)
+    support = _bits(tb + cb)
+    if classify_kernel(m) is KernelClass.DIAGONAL:
+        d = np.ascontiguousarray(np.diagonal(m))
+        if np.all(d == 1.0):
+            return None  # the reference's diagonal body finds no rows and returns
+        return NGate("diag", tb, cb, d, 0, support, index)
+    if len(tb) == 2:
+        if not cb and np.array_equal(m, _SWAP):
+            return NGate("swap", tb, (), None, support, support, index)
+        # controlled single-qubit form [[I, 0], [0, U]]: control targets[0], act on targets[1]
+        if (
+            np.array_equal(m[:2, :2], np.eye(2))
+            and not np.any(m[:2, 2:])
+            and not np.any(m[2:, :2])
+        ):
+            u = np.ascontiguousarray(m[2:, 2:])
+            if classify_kernel(u) is KernelClass.DIAGONAL:
+                d = np.ones(4, dtype=np.complex128)
+                d[2:] = np.diagonal(u)
+                return NGate("diag", tb, cb, d, 0, support, index)
+            return NGate("g1", (tb[1],), cb + (tb[0],), u, 1 << tb[1], support, index)
+        return NGate("g2", tb, cb, np.ascontiguousarray(m), _bits(tb), support, index)
+    return NGate("g1", tb, cb, np.ascontiguousarray(m), _bits(tb), support, index)
+
+
+def diag_terms(g: NGate):
+    """(mask, value, phase) rows of a diagonal gate: exactly the rows the reference multiplies
+    (diag entry != 1.0), restricted to the control subspace."""
+    t = len(g.targets)
+    cmask = _bits(g.controls)
+    mask = _bits(g.targets) | cmask
+    out = []
+    for j, w in enumerate(g.matrix):
+        if w == 1.0:
+            continue
+        val = cmask
+        for i, b in enumerate(g.targets):
+            if (j >> (t - 1 - i)) & 1:
+                val |= 1 << b
+        out.append((mask, val, complex(w)))
+    return out
+
+
+# ------------------------------------------------------------------------------------------
+# plan
+# ------------------------------------------------------------------------------------------
+@dataclass
+class PassStep:
+    words: np.ndarray
+    gates: list  # absorbed NGates
+    tile_pos: tuple
+    ext_perm: bool
+    n_transposes: int
+    n_pivots: int
+
+    @property
+    def n_gates(self) -> int:
+        return len(self.gates)
+
+
+@dataclass
+class GateStep:
+    gate: NGate
+
+
+@dataclass
+class Plan:
+    n_qubits: int
+    dtype: int
+    steps: list = field(default_factory=list)
+
+    @property
+    def n_passes(self) -> int:
+        return sum(1 for s in self.steps if isinstance(s, PassStep))
+
+    def state_sweeps(self) -> float:
+        """Algorithmic state read+write sweeps (the roofline's unit): 1 per pass, the touched
+        fraction per stand-alone gate."""
+        total = 0.0
+        for s in self.steps:
+            total += 1.0 if isinstance(s, PassStep) else s.gate.touched_fraction()
+        return total
+
+
+def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool):
+    """Greedy absorption scan: returns (absorbed, deferred, tile position set)."""
+    K, L = geo.K, geo.L
+    T = set(range(L))
+    frozen = set()
+    loc = list(range(n))
+    blocked_support = 0
+    blocked_targets = 0
+    absorbed, deferred = [], []
+    for g in gates:
+        take = False
+        if (g.tmask & blocked_support) or (g.smask & blocked_targets):
+            take = False
+        elif g.kind == "diag":
+            take = True
+        elif g.kind == "swap":
+            x, y = g.targets
+            px, py = loc[x], loc[y]
+            inx, iny = px in T, py in T
+            if inx and iny:
+                take = True
+            elif not inx and not iny:
+                # tile-external relabel: keep enough unfrozen positions to fill the tile
+                take = allow_ext and n - len(frozen | {px, py}) >= K
+                if take:
+                    frozen.update((px, py))
+            else:
+                other = py if inx else px
+                if len(T) < K and other not in frozen:
+                    T.add(other)
+                    take = True
+            if take:
+                loc[x], loc[y] = loc[y], loc[x]
+        else:
+            need = {loc[t] for t in g.targets}
+            new = need - T
+            if not new:
+                take = True
+            elif len(T) + len(new) <= K and not (new & frozen):
+                T |= new
+                take = True
+        if take:
+            absorbed.append(g)
+        else:
+            deferred.append(g)
+            blocked_support |= g.smask
+            blocked_targets |= g.tmask
+    # fill the tile with the lowest free positions (longer contiguous runs)
+    for p in range(n):
+        if len(T) >= K:
+            break
+        if p not in T and p not in frozen:
+            T.add(p)
+    return absorbed, deferred, T
+
+
+def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, fuse: bool = True) -> Plan:
+    """Plan a gate list into PassSteps (fused) and GateSteps (stand-alone kernels)."""
+    geo = GEOMETRY[dtype]
+    gates = []
+    for i, spec in enumerate(specs):
+        g = spec if isinstance(spec, NGate) else normalize(spec, n_qubits, i)
+        if g is not None:
+            gates.append(g)
+    plan = Plan(n_qubits, dtype)
+    if not fuse or n_qubits < geo.K + 1:
+        plan.steps = [GateStep(g) for g in gates]
+        return plan
+    remaining = gates
+    while remaining:
+        absorbed, deferred, T = _select_pass(remaining, n_qubits, geo, allow_ext_perm)
+        if not absorbed:  # cannot happen with K >= L + 2, but never loop forever
+            absorbed, deferred = [remaining[0]], remaining[1:]
+            plan.steps.append(GateStep(absorbed[0]))
+            remaining = deferred
+            continue
+        stand_alone = sum(g.touched_fraction() for g in absorbed)
+        if stand_alone < 1.0:
+            # cheaper as sparse single-gate kernels than as a full sweep
+            plan.steps.extend(GateStep(g) for g in absorbed)
+        else:
+            words, info = compile_pass(absorbed, T, n_qubits, dtype)
+            plan.steps.append(PassStep(words, absorbed, tuple(sorted(T)), info["ext_perm"],
+                                       info["transposes"], info["pivots"]))
+        remaining = deferred
+    return plan
+
+
+# ------------------------------------------------------------------------------------------
+# compile one pass
+# ------------------------------------------------------------------------------------------
+class _Layout:
+    def __init__(self, R, Tb):
+        self.R = list(R)  # slot bit i <-> tile bit R[i]
+        self.Tb = list(Tb)  # thread bit b <-> tile bit Tb[b] (0..4 lanes, 5..7 warps)
+
+    def slot_of(self, tile_bit):
+        return self.R.index(tile_bit)
+
+
+def _order_thread_bits(cands, geo, prefer, natural=False):
+    """Order the 8 thread tile-bits: lanes first.  natural=True keeps tile bits 0..G-1 on
+    lanes 0..G-1 (reads of the TMA stage are unswizzled)."""
+    cands = sorted(cands)
+    if natural:
+        lanes = [b for b in range(geo.G)]
+        rest = [b for b in cands if b not in lanes]
+        rest.sort(key=lambda b: (b not in prefer, b))
+        order = lanes + rest
+        return order
+    # lanes 0..G-1 with distinct residues mod G (conflict-free swizzled transposes)
+    pri = sorted(cands, key=lambda b: (b not in prefer, b))
+    lanes, used = [], set()
+    for b in pri:
+        if len(lanes) == geo.G:
+            break
+        if b % geo.G not in used:
+            lanes.append(b)
+            used.add(b % geo.G)
+    for b in pri:
+        if len(lanes) == geo.G:
+            break
+        if b not in lanes:
+            lanes.append(b)
+    rest = [b for b in pri if b not in lanes]
+    return lanes + rest
+
+
+def compile_pass(absorbed, T, n, dtype):
+    geo = GEOMETRY[dtype]
+    K, NREG, A = geo.K, geo.nreg, geo.A
+    tile_pos = sorted(T)
+    tidx = {p: b for b, p in enumerate(tile_pos)}
+    ext_pos = [p for p in range(n) if p not in T]
+
+    # ---- pass 1: physical mapping of every absorbed gate (relabels applied in order) ----
+    loc = list(range(n))
+    events = []  # ("diag", terms) | ("g1"/"g2", NGate, phys targets, phys controls)
+    for g in absorbed:
+        if g.kind == "swap":
+            x, y = g.targets
+            loc[x], loc[y] = loc[y], loc[x]
+            continue
+        if g.kind == "diag":
+            terms = []
+            for mask, val, w in diag_terms(g):
+                pm = pv = 0
+                for b in range(n):
+                    if (mask >> b) & 1:
+                        pm |= 1 << loc[b]
+                        if (val >> b) & 1:
+                            pv |= 1 << loc[b]
+                terms.append((pm, pv, w))
+            events.append(("diag", terms))
+            continue
+        pt = tuple(loc[t] for t in g.targets)
+        pc = tuple(loc[c] for c in g.controls)
+        events.append((g.kind, g, pt, pc))
+    inv = [0] * n
+    for x, p in enumerate(loc):
+        inv[p] = x
+    out_pos = [inv[p] for p in tile_pos]  # output global bit of each tile bit
+    ext_out = [inv[p] for p in ext_pos]
+    ext_perm = ext_out != ext_pos
+    store_bits = {b for b in range(K) if out_pos[b] < geo.L}
+
+    needs = [frozenset(tidx[p] for p in ev[2]) for ev in events if ev[0] in ("g1", "g2")]
+
+    def pick_R(i, forbid=frozenset()):
+        R = []
+        j = i
+        while j < len(needs):
+            nd = needs[j]
+            if nd & forbid:
+                break
+            merged = set(R) | nd
+            if len(merged) > NREG:
+                break
+            for b in sorted(nd):
+                if b not in R:
+                    R.append(b)
+            j += 1
+        filler = sorted((b for b in range(K) if b not in R and b not in forbid),
+                        key=lambda b: (b in store_bits, -b))
+        for b in filler:
+            if len(R) >= NREG:
+                break
+            R.append(b)
+        return R
+
+    words = []
+    n_trans = 0
+
+    def layout_words(lay):
+        w = [OP_LAYOUT, 0]
+        w += lay.R
+        w += lay.Tb
+        for s in range(A):
+            w.append(sum(1 << tile_pos[lay.R[i]] for i in range(NREG) if (s >> i) & 1))
+        w += [tile_pos[b] for b in lay.Tb]
+        for s in range(A):
+            w.append(sum(1 << out_pos[lay.R[i]] for i in range(NREG) if (s >> i) & 1))
+        w += [out_pos[b] for b in lay.Tb]
+        for s in range(A):
+            w.append(sum(1 << lay.R[i] for i in range(NREG) if (s >> i) & 1))
+        w[1] = len(w)
+        return w
+
+    def make_layout(R, natural=False):
+        cands = [b for b in range(K) if b not in R]
+        return _Layout(R, _order_thread_bits(cands, geo, store_bits, natural))
+
+    # initial layout: its lanes 0..G-1 must be tile bits 0..G-1 (natural-order stage read)
+    nat_forbid = frozenset(range(geo.G))
+    R0 = pick_R(0, nat_forbid)
+    cur = make_layout(R0, natural=True)
+    words += layout_words(cur)
+
+    pivot_count = 0
+    pending_diag = []
+
+    def flush_diag():
+        nonlocal pivot_count
+        if not pending_diag:
+            return
+        ops, npiv = _compile_diag(pending_diag, cur, tile_pos, tidx, geo, pivot_count)
+        pivot_count += npiv
+        words.extend(ops)
+        pending_diag.clear()
+
+    gi = 0
+    for ev in events:
+        if ev[0] == "diag":
+            pending_diag.extend(ev[1])
+            continue
+        kind, g, pt, pc = ev
+        need = needs[gi]
+        if not need <= set(cur.R):
+            flush_diag()
+            cur = make_layout(pick_R(gi))
+            words += layout_words(cur)
+            n_trans += 1
+        flush_diag()
+        words += _gate_op(kind, g, pt, pc, cur, tidx)
+        gi += 1
+    flush_diag()
+    # store layout: lanes must cover the tile bits that land on the low output bits
+    if not store_bits <= set(cur.Tb[:5]):
+        Rs = [b for b in cur.R if b not in store_bits]
+        for b in sorted(range(K), key=lambda b: -b):
+            if len(Rs) >= NREG:
+                break
+            if b not in Rs and b not in store_bits:
+                Rs.append(b)
+        cur = make_layout(Rs)
+        words += layout_words(cur)
+        n_trans += 1
+    words.append(OP_END)
+    words.append(2)
+
+    header = [0] * H_TILEPOS
+    header[0] = MAGIC
+    header[1] = VERSION
+    header[2] = K
+    header[3] = NREG
+    header[4] = n
+    header[5] = dtype
+    header[6] = 1 << (n - K)
+    header[7] = 1 if ext_perm else 0
+    contig = 0
+    while contig < K and tile_pos[contig] == contig:
+        contig += 1
+    header[8] = contig
+    header[9] = pivot_count
+    prog = header + tile_pos + ext_pos + ext_out + words
+    header_len = len(prog)
+    prog[10] = header_len
+    if len(prog) > MAX_PROG_WORDS or pivot_count > MAX_PIVOTS:
+        raise _TooLarge()
+    arr = np.array(prog, dtype=np.int64)
+    return arr, {"ext_perm": ext_perm, "transposes": n_trans, "pivots": pivot_count}
+
+
+class _TooLarge(Exception):
+    pass
+
+
+def _matrix_words(m):
+    out = []
+    for v in np.asarray(m, dtype=np.complex128).reshape(-1):
+        out.append(_f2w(v.real))
+        out.append(_f2w(v.imag))
+    return out
+
+
+def _gate_op(kind, g, pt, pc, lay, tidx):
+    gmask = rmask = 0
+    for c in pc:
+        if c in tidx and tidx[c] in lay.R:
+            rmask |= 1 << lay.slot_of(tidx[c])
+        else:
+            gmask |= 1 << c
+    m = g.matrix
+    if kind == "g1":
+        ib = lay.slot_of(tidx[pt[0]])
+        if np.array_equal(m, _XMAT):
+            gk = G_SWAPX
+        elif not np.any(m.imag):
+            gk = G_REAL
+        else:
+            gk = G_COMPLEX
+        w = [OP_G1, 0, ib, gk, gmask, gmask, rmask, rmask] + _matrix_words(m)
+    else:
+        i0 = lay.slot_of(tidx[pt[0]])
+        i1 = lay.slot_of(tidx[pt[1]])
+        if i0 > i1:
+            ih, il, mm = i0, i1, m
+        else:
+            # exchange the two row/column bits so that row bit 1 <-> the higher slot
+            perm = [0, 2, 1, 3]
+            ih, il, mm = i1, i0, m[np.ix_(perm, perm)]
+        gk = G_REAL if not np.any(mm.imag) else G_COMPLEX
+        w = [OP_G2, 0, ih, il, gk, gmask, gmask, rmask, rmask] + _matrix_words(mm)
+    w[1] = len(w)
+    return w
+
+
+def _compile_diag(terms, lay, tile_pos, tidx, geo, slot0):
+    """Compile a commuting batch of diagonal terms (physical positions) for layout `lay`."""
+    A = geo.A
+    parity_single = 0
+    parity_pairs = {}  # distance -> mask of the lower bits
+    pairs = {}  # (a, b) a > b -> phase
+    singles = {}  # bit -> phase
+    generic = []
+    for mask, val, w in terms:
+        pc = bin(mask).count("1")
+        if val == mask and pc <= 2:
+            bits = [b for b in range(64) if (mask >> b) & 1]
+            if w == -1.0:
+                if pc == 1:
+                    parity_single ^= mask
+                else:
+                    hi, lo = bits[1], bits[0]
+                    parity_pairs[hi - lo] = parity_pairs.get(hi - lo, 0) ^ (1 << lo)
+                continue
+            if pc == 2:
+                key = (bits[1], bits[0])
+                pairs[key] = pairs.get(key, 1.0 + 0j) * w
+                continue
+            singles[bits[0]] = singles.get(bits[0], 1.0 + 0j) * w
+            continue
+        generic.append((mask, val, w))
+    ops = []
+    # pivots: greedy vertex cover of the pair graph, highest degree first
+    adj = {}
+    for (a, b), w in pairs.items():
+        adj.setdefault(a, {})[b] = w
+        adj.setdefault(b, {})[a] = w
+    pivots = []
+    while adj:
+        p = max(adj, key=lambda q: (len(adj[q]), q in singles, -q))
+        partners = adj.pop(p)
+        for q in partners:
+            adj[q].pop(p, None)
+            if not adj[q]:
+                del adj[q]
+        pivots.append((p, partners))
+    npiv = 0
+    for p, partners in pivots:
+        self_w = singles.pop(p, 1.0 + 0j)
+        ops += _pivot_op(p, partners, self_w, lay, tile_pos, tidx, A, slot0 + npiv)
+        npiv += 1
+    for b, w in singles.items():
+        generic.append((1 << b, 1 << b, w))
+    if parity_single or parity_pairs:
+        w = [OP_PARITY, 0, parity_single, len(parity_pairs)]
+        for d, m in sorted(parity_pairs.items()):
+            w += [d, m]
+        w[1] = len(w)
+        ops += w
+    for mask, val, ph in generic:
+        ops += [OP_TERM, 6, mask, val, _f2w(ph.real), _f2w(ph.imag)]
+    return ops, npiv
+
+
+def _pivot_op(p, partners, self_w, lay, tile_pos, tidx, A, slot):
+    if p in tidx and tidx[p] in lay.R:
+        ptype, pval = 0, lay.slot_of(tidx[p])
+    else:
+        ptype, pval = 1, 1 << p
+    ext = []
+    ta = np.ones(16, dtype=np.complex128) * self_w
+    tb = np.ones(16, dtype=np.complex128)
+    rt = np.ones(A, dtype=np.complex128)
+    for q, w in sorted(partners.items()):
+        if q not in tidx:
+            ext.append((q, w))
+            continue
+        b = tidx[q]
+        if b in lay.R:
+            i = lay.slot_of(b)
+            for s in range(A):
+                if (s >> i) & 1:
+                    rt[s] *= w
+        else:
+            tbit = lay.Tb.index(b)
+            if tbit < 4:
+                for u in range(16):
+                    if (u >> tbit) & 1:
+                        ta[u] *= w
+            else:
+                for u in range(16):
+                    if (u >> (tbit - 4)) & 1:
+                        tb[u] *= w
+    use_rt = int(np.any(rt != 1.0))
+    w = [OP_PIVOT, 0, slot, ptype, pval, use_rt, len(ext)]
+    for q, ph in ext:
+        w += [q, _f2w(ph.real), _f2w(ph.imag)]
+    w += _matrix_words(ta) + _matrix_words(tb) + _matrix_words(rt)
+    w[1] = len(w)
+    return w

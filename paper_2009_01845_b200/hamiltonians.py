@@ -1,0 +1,156 @@
+"""Trotter-form Hamiltonians (drop-in for the hot-path part of
+/root/reference/pkg/src/qsim/hamiltonians.py).
+
+In scope: TrotterHamiltonian (:62-93), build_x / build_tfim in Trotter form (:120-154),
+combine (:157-174), the |+>^n ground state of build_x (:115-117) and the Trotter-form
+expectation (:192-207) evaluated on the device.  The dense 2^N x 2^N form (capped at 12 qubits
+and diagonalised with numpy.linalg.eigh in the reference) is outside the B200 hot path
+(SURVEY.md section 2.1 row 6); asking for it raises FormError.
+"""
+
+from __future__ import annotations
+
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .errors import CapacityError, FormError, ShapeError
+from .state import Precision, StateVector, uniform_state
+
+DENSE_MAX_QUBITS = 12
+HERMITICITY_ATOL = 1e-10
+
+_PX = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+_PZ = np.array([[1, 0], [0, -1]], dtype=np.complex128)
+
+
+class Form(enum.Enum):
+    DENSE = "dense"
+    TROTTER = "trotter"
+
+
+def _require_hermitian(m, what):
+    dev = np.max(np.abs(m - m.conj().T))
+    if dev > HERMITICITY_ATOL:
+        raise ShapeError(f"{what} is not Hermitian (deviation {dev:.2e})")
+
+
+@dataclass
+class TrotterHamiltonian:
+    """Sum of <= 2-qubit Hermitian terms [(qubits, matrix), ...]."""
+
+    n_qubits: int
+    terms: list
+    ground_state: object = field(default=None, repr=False, compare=False)
+
+    def __post_init__(self):
+        if self.n_qubits < 1:
+            raise ShapeError(f"n_qubits must be >= 1, got {self.n_qubits}")
+        clean = []
+        for qubits, matrix in self.terms:
+            qubits = tuple(int(q) for q in qubits)
+            k = len(qubits)
+            if k > 2:
+                raise CapacityError(f"Trotter terms act on at most 2 qubits, got {qubits}")
+            if k == 0 or len(set(qubits)) != k:
+                raise ShapeError(f"bad term qubits {qubits}")
+            for q in qubits:
+                if not 0 <= q < self.n_qubits:
+                    raise ShapeError(f"qubit {q} out of range for {self.n_qubits} qubits")
+            m = np.asarray(matrix, dtype=np.complex128)
+            if m.shape != (1 << k, 1 << k):
+                raise ShapeError(f"term matrix shape {m.shape} does not fit {k} qubit(s)")
+            _require_hermitian(m, f"term on {qubits}")
+            clean.append((qubits, m))
+        self.terms = clean
+
+    @property
+    def form(self) -> Form:
+        return Form.TROTTER
+
+
+def plus_state(n_qubits: int, precision: Precision = Precision.F64) -> StateVector:
+    """|+>^n: the ground state of -sum X (hamiltonians.py:115-117), one fill kernel."""
+    return uniform_state(n_qubits, precision)
+
+
+def _dense_unsupported():
+    raise FormError("the dense Hamiltonian form is outside the B200 hot path; use Form.TROTTER")
+
+
+def build_x(n_qubits: int, form: Form = Form.TROTTER):
+    """H = -sum_i X_i; ground state |+>^N (hamiltonians.py:120-132)."""
+    if form is Form.DENSE:
+        _dense_unsupported()
+    if n_qubits < 2:
+        raise ShapeError("Trotter form needs at least 2 qubits")
+    ground = lambda precision=Precision.F64: plus_state(n_qubits, precision)  # noqa: E731
+    return TrotterHamiltonian(n_qubits, [((i,), -_PX) for i in range(n_qubits)], ground_state=ground)
+
+
+def build_tfim(n_qubits: int, h: float, form: Form = Form.TROTTER):
+    """Periodic transverse-field Ising chain, bond i = -(Z Z + h X I) on (i, i+1 mod N)
+    (hamiltonians.py:135-154)."""
+    if n_qubits < 2:
+        raise ShapeError(f"the chain needs at least 2 qubits, got {n_qubits}")
+    if form is Form.DENSE:
+        _dense_unsupported()
+    bond = -(np.kron(_PZ, _PZ) + h * np.kron(_PX, np.eye(2, dtype=np.complex128)))
+    return TrotterHamiltonian(n_qubits, [((i, (i + 1) % n_qubits), bond) for i in range(n_qubits)])
+
+
+def combine(a, coeff_a: float, b, coeff_b: float):
+    """coeff_a * a + coeff_b * b; terms on identical qubit tuples merge, first-seen order
+    (hamiltonians.py:157-174)."""
+    if a.n_qubits != b.n_qubits:
+        raise ShapeError(f"qubit counts differ: {a.n_qubits} vs {b.n_qubits}")
+    if a.form is not b.form:
+        raise FormError(f"cannot combine {a.form.value} with {b.form.value}")
+    if a.form is not Form.TROTTER:
+        _dense_unsupported()
+    acc: dict = {}
+    order = []
+    for coeff, ham in ((coeff_a, a), (coeff_b, b)):
+        for qubits, m in ham.terms:
+            if qubits in acc:
+                acc[qubits] = acc[qubits] + coeff * m
+            else:
+                acc[qubits] = coeff * m
+                order.append(qubits)
+    return TrotterHamiltonian(a.n_qubits, [(q, acc[q]) for q in order])
+
+
+def expectation(h, state: StateVector) -> float:
+    """<psi|H|psi> (real part) term by term on the device (hamiltonians.py:192-207): per term
+    one D2D copy, one term kernel, one deterministic <psi|H_t psi> reduction."""
+    if h.n_qubits != state.n_qubits:
+        raise ShapeError(f"Hamiltonian has {h.n_qubits} qubits, state has {state.n_qubits}")
+    if not isinstance(h, TrotterHamiltonian):
+        _dense_unsupported()
+    from .gates import apply_matrix_device
+
+    torch = nat.torch_mod()
+    psi = state.tensor
+    if psi.dtype != torch.complex128:
+        psi = psi.to(torch.complex128)
+    scratch = torch.empty_like(psi)
+    out = torch.empty(2, dtype=torch.float64, device=psi.device)
+    lib = nat.lib()
+    total = 0.0
+    for qubits, m in h.terms:
+        scratch.copy_(psi)
+        apply_matrix_device(scratch.data_ptr(), h.n_qubits, nat.QSB_C128, qubits, m, (), kernel=None)
+        nat.check(lib.qsb_vdot(psi.data_ptr(), scratch.data_ptr(), psi.numel(), nat.QSB_C128, out.data_ptr(),
+                               nat.stream_ptr()), "expectation")
+        total += float(out[0].item())
+    return float(total)
+
+
+def ground_state_vector(h, precision: Precision = Precision.F64) -> StateVector:
+    """Attached ground-state constructor (|+>^N for build_x); other Hamiltonians need the dense
+    eigen-solver, which is outside the hot path."""
+    if getattr(h, "ground_state", None) is not None:
+        return h.ground_state(precision)
+    _dense_unsupported()

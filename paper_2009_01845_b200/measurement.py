@@ -1,0 +1,163 @@
+"""Shot sampling on the device (drop-in for /root/reference/pkg/src/qsim/measurement.py).
+
+Pipeline, every stage a qsb200 kernel and bit-compatible with the reference's numpy path
+(SURVEY.md Appendix B):
+  qsb_probabilities   |a|^2 with numpy's complex-abs formula          (measurement.py:50)
+  qsb_marginal        numpy's add.reduce order over unmeasured qubits  (measurement.py:52-58)
+  qsb_cumsum_normalized  the exact sequential cumsum, in parallel      (measurement.py:81-82)
+  qsb_sample          PCG64 draws + searchsorted(side="right") + clip  (measurement.py:83-86)
+The generator state is seeded on the host exactly as numpy.random.default_rng(seed) does
+(numpy's PCG64 seeding is used for the 128-bit (state, inc) pair only; all draws are made
+on the device with jump-ahead).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .errors import ShapeError
+
+RNG_ALGORITHM = "pcg64"
+
+
+@dataclass
+class MeasurementResult:
+    """Outcomes over an ordered qubit subset (qubits[0] = MSB of each sample)."""
+
+    n_shots: int
+    qubits: tuple
+    samples: np.ndarray
+    seed: int
+    registers: dict = field(default_factory=dict)
+    rng_algorithm: str = RNG_ALGORITHM
+
+    def binary(self) -> np.ndarray:
+        k = len(self.qubits)
+        shifts = np.arange(k - 1, -1, -1, dtype=np.int64)
+        return ((self.samples[:, None] >> shifts[None, :]) & 1).astype(np.uint8)
+
+
+def _validate_qubits(state, qubits):
+    qubits = tuple(int(q) for q in qubits)
+    if not qubits:
+        raise ShapeError("measurement needs at least one qubit")
+    if len(set(qubits)) != len(qubits):
+        raise ShapeError(f"duplicate measurement qubits {qubits}")
+    for q in qubits:
+        if not 0 <= q < state.n_qubits:
+            raise ShapeError(f"qubit {q} out of range for {state.n_qubits} qubits")
+    return qubits
+
+
+def _f64(n):
+    torch = nat.torch_mod()
+    return torch.empty(n, dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+
+
+def device_probabilities(state):
+    """float64 |a|^2 of every amplitude, on the device."""
+    p = _f64(state.n_amps)
+    nat.check(
+        nat.lib().qsb_probabilities(state.data_ptr, state.n_amps, state.precision.qsb_dtype, p.data_ptr(),
+                                    nat.stream_ptr()),
+        "probabilities",
+    )
+    return p
+
+
+def device_marginal(state, qubits):
+    """Marginal distribution over `qubits` as a float64 CUDA tensor (length 2**len(qubits))."""
+    qubits = _validate_qubits(state, qubits)
+    n = state.n_qubits
+    probs = device_probabilities(state)
+    if qubits == tuple(range(n)):
+        return probs
+    lib = nat.lib()
+    k = len(qubits)
+    kept = np.array([n - 1 - q for q in qubits], dtype=np.int32)
+    out = _f64(1 << k)
+    scratch = _f64(int(lib.qsb_marginal_scratch_doubles(n, k)))
+    nat.check(
+        lib.qsb_marginal(probs.data_ptr(), n, k, kept.ctypes.data, out.data_ptr(), scratch.data_ptr(),
+                         nat.stream_ptr()),
+        "marginal",
+    )
+    del probs, scratch
+    return out
+
+
+def marginal_probabilities(state, qubits) -> np.ndarray:
+    """Outcome probabilities over `qubits` (others traced out), float64 even for f32 states."""
+    return device_marginal(state, qubits).cpu().numpy()
+
+
+def pcg64_seed_state(seed: int):
+    """(state, inc) of numpy.random.default_rng(seed)'s PCG64, as four uint64 halves."""
+    st = np.random.PCG64(seed).state["state"]
+    s, inc = int(st["state"]), int(st["inc"])
+    m = (1 << 64) - 1
+    return (s >> 64) & m, s & m, (inc >> 64) & m, inc & m
+
+
+def device_cdf(probs):
+    """Normalised cumulative distribution, bit-identical to numpy's cumsum(p) / cumsum(p)[-1]."""
+    torch = nat.torch_mod()
+    lib = nat.lib()
+    n = probs.numel()
+    cum = torch.empty_like(probs)
+    nbytes = int(lib.qsb_cumsum_scratch_bytes(n))
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device=probs.device)
+    nat.check(
+        lib.qsb_cumsum_normalized(probs.data_ptr(), n, cum.data_ptr(), scratch.data_ptr(), nbytes, nat.stream_ptr()),
+        "cumsum",
+    )
+    return cum
+
+
+def device_sample(cum, n_shots: int, seed: int):
+    torch = nat.torch_mod()
+    out = torch.empty(int(n_shots), dtype=torch.int64, device=cum.device)
+    sh, sl, ih, il = pcg64_seed_state(seed)
+    nat.check(
+        nat.lib().qsb_sample(cum.data_ptr(), cum.numel(), sh, sl, ih, il, int(n_shots), out.data_ptr(),
+                             nat.stream_ptr()),
+        "sample",
+    )
+    return out
+
+
+def sample(state, qubits, n_shots: int, seed: int, registers: dict | None = None) -> MeasurementResult:
+    """Draw `n_shots` outcomes by inverse-CDF sampling (measurement.py:61-87)."""
+    if n_shots < 1:
+        raise ValueError(f"n_shots must be >= 1, got {n_shots}")
+    qubits = _validate_qubits(state, qubits)
+    regs = dict(registers or {})
+    for name, reg in regs.items():
+        missing = set(reg) - set(qubits)
+        if missing:
+            raise ShapeError(f"register {name!r} references unmeasured qubits {sorted(missing)}")
+        regs[name] = tuple(reg)
+    probs = device_marginal(state, qubits)
+    cum = device_cdf(probs)
+    del probs
+    samples = device_sample(cum, n_shots, seed).cpu().numpy()
+    return MeasurementResult(int(n_shots), qubits, samples, int(seed), regs)
+
+
+def frequencies(result: MeasurementResult, register: str | None = None) -> dict:
+    """Outcome counts, optionally projected onto a named register (measurement.py:90-103)."""
+    samples = result.samples
+    if register is not None:
+        if register not in result.registers:
+            raise KeyError(register)
+        reg = result.registers[register]
+        k = len(result.qubits)
+        pos = np.array([result.qubits.index(q) for q in reg], dtype=np.int64)
+        bits = (samples[:, None] >> (k - 1 - pos)[None, :]) & 1
+        weights = 1 << np.arange(len(reg) - 1, -1, -1, dtype=np.int64)
+        samples = bits @ weights
+    values, counts = np.unique(samples, return_counts=True)
+    return {int(v): int(c) for v, c in zip(values, counts)}

@@ -1,0 +1,125 @@
+"""CPU verification of the pass planner + program encoder (fusion.py) through the numpy
+interpreter of the qsb_run_pass program format (tests/pass_emulator.py)."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden, max_abs
+from oracle import statevec as ov
+from plan_helpers import emulate_plan, spec_tuples_to_specs
+from paper_2009_01845_b200 import _native as nat
+from paper_2009_01845_b200.fusion import GEOMETRY, PassStep, plan_circuit
+
+C128, C64 = nat.QSB_C128, nat.QSB_C64
+
+
+def check(gates, n, psi=None, dtype=C128, tol=1e-12, allow_ext=True, min_fused=0):
+    specs = spec_tuples_to_specs(gates)
+    plan = plan_circuit(specs, n, dtype, allow_ext_perm=allow_ext)
+    npd = np.complex128 if dtype == C128 else np.complex64
+    if psi is None:
+        psi = np.zeros(1 << n, dtype=np.complex128)
+        psi[0] = 1
+    got = emulate_plan(plan, psi, npd)
+    want = ov.run(gates, n, psi)
+    assert max_abs(got, want) <= tol, (plan.n_passes, len(plan.steps))
+    assert sum(s.n_gates for s in plan.steps if isinstance(s, PassStep)) >= min_fused
+    return plan
+
+
+@pytest.mark.parametrize("n", [13, 14, 16])
+def test_qft_plan(n):
+    rng = np.random.default_rng(n)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    plan = check(ov.qft(n), n, psi)
+    # the QFT collapses to a handful of passes
+    assert plan.n_passes <= 4
+
+
+def test_qft_plan_passes_at_30_qubits():
+    plan = plan_circuit(spec_tuples_to_specs(ov.qft(30)), 30, C128)
+    assert plan.n_passes == 4 and all(isinstance(s, PassStep) for s in plan.steps)
+    assert sum(s.n_transposes for s in plan.steps) <= 4
+
+
+def test_qft_plan_without_external_permutation():
+    n = 15
+    rng = np.random.default_rng(3)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    plan = check(ov.qft(n), n, psi, allow_ext=False)
+    assert not any(s.ext_perm for s in plan.steps if isinstance(s, PassStep))
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_variational_plan(fused):
+    g = golden("variational")
+    n = 14
+    gates = ov.variational(n, 3, g[f"params{n}"], fused=fused)
+    check(gates, n, min_fused=len(gates) // 2)
+    check(gates, n, dtype=C64, tol=2e-6)
+
+
+def test_random_circuit_plans():
+    g = golden("random_circuits")
+    for i, (n, text) in enumerate(zip(g["n"], g["circuits"])):
+        if n < 13:
+            continue
+        _, gates = ov.from_json(text)
+        check(gates, int(n), g[f"in{i}"])
+        check(gates, int(n), g[f"in{i}"], dtype=C64, tol=5e-6)
+
+
+def test_grid_plan():
+    gates = ov.grid_supremacy(3, 5, 8, seed=42)
+    plan = check(gates, 15)
+    assert plan.n_passes < len(gates) / 5
+
+
+def test_trotter_step_plan():
+    n = 16
+    terms = ov.combine(ov.x_terms(n), 0.4, ov.tfim_terms(n, 1.0), 0.6)
+    gates = ov.trotter_step(terms, 0.05)
+    rng = np.random.default_rng(5)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    plan = check(gates, n, psi)
+    assert plan.n_passes <= 6
+
+
+def test_controlled_and_mixed_gates():
+    n = 14
+    rng = np.random.default_rng(11)
+    gates = []
+    for _ in range(80):
+        kinds = ["H", "X", "Y", "Z", "RX", "RZ", "CZPow", "CNOT", "CZ", "SWAP", "U1", "U2"]
+        k = kinds[rng.integers(len(kinds))]
+        order = rng.permutation(n)
+        t2 = k in ("CZPow", "CNOT", "CZ", "SWAP", "U2")
+        tg = tuple(int(x) for x in order[: 2 if t2 else 1])
+        nc = int(rng.integers(0, 3))
+        ct = tuple(int(x) for x in order[len(tg): len(tg) + nc])
+        th = float(rng.uniform(0, 2 * math.pi))
+        if k == "U1":
+            q, _ = np.linalg.qr(rng.standard_normal((2, 2)) + 1j * rng.standard_normal((2, 2)))
+            gates.append(ov.gate("Unitary", tg, ct, (), q))
+        elif k == "U2":
+            q, _ = np.linalg.qr(rng.standard_normal((4, 4)) + 1j * rng.standard_normal((4, 4)))
+            gates.append(ov.gate("Unitary", tg, ct, (), q))
+        elif k in ("RX", "RZ", "CZPow"):
+            gates.append(ov.gate(k, tg, ct, (th,)))
+        else:
+            gates.append(ov.gate(k, tg, ct))
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    check(gates, n, psi)
+
+
+def test_geometry():
+    for dt, geo in GEOMETRY.items():
+        assert geo.K - geo.nreg == 8 and geo.A == 1 << geo.nreg
+        # 2^L amplitudes per contiguous run = 256 bytes
+        assert (1 << geo.L) * (16 if dt == C128 else 8) == 256

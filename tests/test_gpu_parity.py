@@ -1,0 +1,342 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden vectors and
+the CPU oracle.  Tolerances per BASELINE north star: 1e-12 per amplitude (complex128),
+1e-5 (complex64); samples bit-exact."""
+
+import hashlib
+import json
+import math
+
+import numpy as np
+import pytest
+
+from conftest import circuit_from_json, golden, max_abs
+from oracle import statevec as ov
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-12
+TOL32 = 1e-5
+
+
+def _sv(amps):
+    import paper_2009_01845_b200 as q
+
+    return q.from_amplitudes(np.asarray(amps))
+
+
+# ---------------------------------------------------------------- single gates / apply_matrix
+def test_single_gates_golden(cuda):
+    g = golden("single_gates")
+    for text, inp, out in zip(g["circuits"], g["inputs"], g["outputs"]):
+        c = circuit_from_json(text)
+        for fuse in (False, True):
+            got = c.execute(_sv(inp), fuse=fuse).amplitudes
+            assert max_abs(got, out) <= TOL64
+
+
+@pytest.mark.parametrize("n", [8, 13, 16])
+def test_apply_matrix_kernel_classes(cuda, n):
+    import paper_2009_01845_b200 as q
+
+    rng = np.random.default_rng(29 + n)
+    amps = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    amps /= np.linalg.norm(amps)
+    for spec in (q.X(3), q.SWAP(1, 6), q.CNOT(5, 2), q.CNOT(2, 5, controls=(0,)), q.Y(4)):
+        fast, slow = amps.copy(), amps.copy()
+        q.apply_matrix(fast, n, spec.targets, q.gate_matrix(spec), spec.controls, kernel=q.KernelClass.PERMUTATION)
+        q.apply_matrix(slow, n, spec.targets, q.gate_matrix(spec), spec.controls, kernel=q.KernelClass.GENERAL)
+        assert np.array_equal(fast, slow)
+        ref = amps.copy()
+        ov.apply_matrix(ref, n, spec.targets, q.gate_matrix(spec), spec.controls)
+        assert np.array_equal(fast, ref)
+    for spec in (q.Z(2), q.RZ(4, 0.9), q.CZ(1, 6), q.CZPow(0, 5, 2.2), q.CZ(3, 7, controls=(1,))):
+        fast, slow = amps.copy(), amps.copy()
+        q.apply_matrix(fast, n, spec.targets, q.gate_matrix(spec), spec.controls, kernel=q.KernelClass.DIAGONAL)
+        q.apply_matrix(slow, n, spec.targets, q.gate_matrix(spec), spec.controls, kernel=q.KernelClass.GENERAL)
+        assert max_abs(fast, slow) <= 1e-15
+        ref = amps.copy()
+        ov.apply_matrix(ref, n, spec.targets, q.gate_matrix(spec), spec.controls)
+        assert max_abs(fast, ref) <= 1e-15
+
+
+def test_control_leaves_unset_half_untouched(cuda):
+    import paper_2009_01845_b200 as q
+
+    rng = np.random.default_rng(41)
+    init = rng.standard_normal(16) + 1j * rng.standard_normal(16)
+    st = _sv(init)
+    q.apply_gate(st, q.H(2, controls=(0,)))
+    out = st.amplitudes
+    assert np.array_equal(out[:8], init[:8])
+    assert np.max(np.abs(out[8:] - init[8:])) > 1e-3
+
+
+def test_apply_matrix_validation(cuda):
+    import paper_2009_01845_b200 as q
+
+    amps = q.zero_state(3).amplitudes
+    with pytest.raises(q.ShapeError):
+        q.apply_matrix(amps, 3, (0, 0), np.eye(4))
+    with pytest.raises(q.ShapeError):
+        q.apply_matrix(amps, 3, (5,), np.eye(2))
+    with pytest.raises(q.ShapeError):
+        q.apply_matrix(amps, 3, (0,), np.eye(4))
+
+
+def test_states_basics(cuda):
+    import paper_2009_01845_b200 as q
+
+    assert np.array_equal(q.zero_state(2).amplitudes, [1, 0, 0, 0])
+    s = q.zero_state(3, q.Precision.F32)
+    assert s.amplitudes.dtype == np.complex64 and s.amplitudes[0] == 1
+    for n in (1, 3, 5):
+        st = q.zero_state(n)
+        q.apply_gate(st, q.X(0))
+        a = st.amplitudes
+        assert a[1 << (n - 1)] == 1.0 and np.count_nonzero(a) == 1
+    assert q.norm(q.from_amplitudes([2, 0])) == 2.0
+    assert abs(q.norm(q.from_amplitudes([0.5] * 4)) - 1.0) < 1e-15
+    plus = q.zero_state(1)
+    q.apply_gate(plus, q.H(0))
+    assert abs(q.overlap(q.zero_state(1), plus) - 1 / math.sqrt(2)) < 1e-15
+    st = q.from_amplitudes([1, 1], normalize=True)
+    assert np.allclose(st.amplitudes, [1 / math.sqrt(2)] * 2, atol=1e-15)
+    with pytest.raises(ValueError):
+        q.from_amplitudes([0, 0, 0, 0], normalize=True)
+    with pytest.raises(ValueError):
+        q.overlap(q.zero_state(2, q.Precision.F32), q.zero_state(2))
+    u = q.uniform_state(5).amplitudes
+    assert np.array_equal(u, np.full(32, 1 / np.sqrt(32)).astype(complex))
+    dup = q.zero_state(2)
+    cp = dup.copy()
+    q.apply_gate(cp, q.X(1))
+    assert dup.amplitudes[0] == 1.0
+
+
+# ---------------------------------------------------------------- circuits
+@pytest.mark.parametrize("fuse", [False, True])
+def test_random_circuits_golden(cuda, fuse):
+    g = golden("random_circuits")
+    for i, text in enumerate(g["circuits"]):
+        c = circuit_from_json(text)
+        got = c.execute(_sv(g[f"in{i}"]), fuse=fuse).amplitudes
+        assert max_abs(got, g[f"out{i}"]) <= TOL64
+
+
+@pytest.mark.parametrize("n", [10, 14])
+@pytest.mark.parametrize("fuse", [False, True])
+def test_qft_golden(cuda, n, fuse):
+    import paper_2009_01845_b200 as q
+
+    g = golden("qft")
+    c = q.qft_circuit(n)
+    assert max_abs(c.execute(fuse=fuse).amplitudes, g[f"zero{n}"]) <= TOL64
+    assert max_abs(c.execute(_sv(g[f"rin{n}"]), fuse=fuse).amplitudes, g[f"rout{n}"]) <= TOL64
+    k = int(g[f"basisk{n}"])
+    got = c.execute(q.basis_state(n, k), fuse=fuse).amplitudes
+    assert max_abs(got, g[f"basis{n}"]) <= TOL64
+    f32 = c.execute(precision=q.Precision.F32, fuse=fuse).amplitudes
+    assert f32.dtype == np.complex64 and max_abs(f32, g[f"f32_{n}"]) <= TOL32
+
+
+@pytest.mark.parametrize("n", [18, 22])
+def test_qft_analytic_dft_column(cuda, n):
+    import paper_2009_01845_b200 as q
+
+    k = int(np.random.default_rng(n).integers(1 << n))
+    got = q.qft_circuit(n).execute(q.basis_state(n, k)).amplitudes
+    j = np.arange(1 << n, dtype=np.float64)
+    want = np.exp(2j * np.pi * ((j * k) % (1 << n)) / (1 << n)) / np.sqrt(1 << n)
+    assert max_abs(got, want) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [10, 14])
+@pytest.mark.parametrize("fused_layers", [False, True])
+@pytest.mark.parametrize("fuse", [False, True])
+def test_variational_golden(cuda, n, fused_layers, fuse):
+    import paper_2009_01845_b200 as q
+
+    g = golden("variational")
+    c = q.variational_circuit(n, 3, g[f"params{n}"], fused=fused_layers)
+    assert max_abs(c.execute(fuse=fuse).amplitudes, g[f"f64_{n}_{int(fused_layers)}"]) <= TOL64
+    got32 = c.execute(precision=q.Precision.F32, fuse=fuse).amplitudes
+    assert max_abs(got32, g[f"f32_{n}_{int(fused_layers)}"]) <= TOL32
+
+
+def test_grid_supremacy_golden(cuda):
+    g = golden("grid15")
+    c = circuit_from_json(g["circuit"])
+    for fuse in (False, True):
+        assert max_abs(c.execute(fuse=fuse).amplitudes, g["out"]) <= TOL64
+
+
+def test_callbacks_split_execution(cuda):
+    import paper_2009_01845_b200 as q
+
+    class Counter(q.Callback):
+        def _compute(self, state, t, hamiltonian):
+            return float(np.abs(state.amplitudes[0]))
+
+    c = q.Circuit(2).add([q.H(0), q.H(1), q.X(0)])
+    cb = Counter()
+    c.execute(callbacks=[(cb, (0, 2))])
+    assert len(cb.records) == 2
+    assert abs(cb.records[0] - 1 / math.sqrt(2)) < 1e-12 and abs(cb.records[1] - 0.5) < 1e-12
+
+
+def test_execute_copies_initial(cuda):
+    import paper_2009_01845_b200 as q
+
+    init = _sv(np.random.default_rng(5).standard_normal(1 << 14) + 0j)
+    keep = init.amplitudes
+    q.qft_circuit(14).execute(init)
+    assert np.array_equal(init.amplitudes, keep)
+
+
+# ---------------------------------------------------------------- Trotter / adiabatic
+def test_adiabatic_golden(cuda):
+    import paper_2009_01845_b200 as q
+
+    g = golden("adiabatic")
+    for n in (8, 13, 14):
+        dt, T = g[f"cfg{n}"]
+        st = q.adiabatic_evolve(q.build_x(n), q.build_tfim(n, 1.0), q.Schedule.linear(),
+                                q.EvolutionConfig(q.Solver.TROTTER, float(dt), float(T)))
+        assert max_abs(st.amplitudes, g[f"n{n}"]) <= TOL64
+
+
+def test_trotter_expectation_matches_oracle(cuda):
+    import paper_2009_01845_b200 as q
+
+    n = 10
+    rng = np.random.default_rng(3)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    h = q.build_tfim(n, 0.7)
+    want = 0.0
+    for qs, m in h.terms:
+        t = psi.copy()
+        ov.apply_matrix(t, n, qs, m)
+        want += np.vdot(psi, t).real
+    assert abs(q.expectation(h, _sv(psi)) - want) <= 1e-12
+
+
+# ---------------------------------------------------------------- measurement
+def test_marginals_and_samples_bitwise(cuda):
+    import paper_2009_01845_b200 as q
+
+    g = golden("sampling")
+    st = _sv(g["state"])
+    for i, text in enumerate(g["subsets"]):
+        qs = tuple(json.loads(str(text)))
+        assert np.array_equal(q.marginal_probabilities(st, qs), g[f"marg{i}"]), qs
+        assert np.array_equal(q.sample(st, qs, 2000, seed=100 + i).samples, g[f"samp{i}"]), qs
+    f32 = q.StateVector(12, g["state"].astype(np.complex64), q.Precision.F32)
+    assert np.array_equal(q.marginal_probabilities(f32, (0, 3, 5)), g["marg_f32"])
+    assert np.array_equal(q.sample(f32, (0, 3, 5), 1000, seed=9).samples, g["samp_f32"])
+
+
+@pytest.mark.parametrize("nq,shots,seed", [(3, 500, 7), (20, 100000, 42)])
+def test_cli_shots_digest(cuda, nq, shots, seed):
+    import paper_2009_01845_b200 as q
+
+    g = golden("sampling")
+    st = q.Circuit(nq).add([q.H(k) for k in range(nq)]).execute()
+    res = q.sample(st, range(nq), shots, seed)
+    assert hashlib.sha256(res.samples.tobytes()).hexdigest() == str(g[f"digest_{nq}_{shots}_{seed}"])
+
+
+@pytest.mark.parametrize("n,kind", [(16, "random"), (20, "random"), (20, "qft"), (22, "sparse"), (21, "tiny")])
+def test_exact_parallel_cumsum_equals_sequential(cuda, n, kind):
+    import torch
+
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200 import _native as nat
+    from paper_2009_01845_b200.measurement import device_cdf
+
+    rng = np.random.default_rng(n)
+    if kind == "random":
+        p = rng.random(1 << n) ** 3
+    elif kind == "qft":
+        st = q.qft_circuit(n).execute(q.basis_state(n, 12345))
+        p = np.abs(st.amplitudes) ** 2
+    elif kind == "sparse":
+        p = rng.random(1 << n) * (rng.random(1 << n) < 0.01)
+        p[:1000] = 0.0
+    else:
+        p = rng.random(1 << n) * 10.0 ** rng.integers(-300, 1, 1 << n)
+    want = np.cumsum(p)
+    want /= want[-1]
+    dp = torch.from_numpy(p).cuda()
+    got = device_cdf(dp).cpu().numpy()
+    assert np.array_equal(got, want)
+    ser = torch.empty_like(dp)
+    nat.check(nat.lib().qsb_cumsum_serial(dp.data_ptr(), dp.numel(), ser.data_ptr(), nat.stream_ptr()))
+    assert np.array_equal(ser.cpu().numpy(), np.cumsum(p))
+
+
+def test_large_sample_converges(cuda):
+    import paper_2009_01845_b200 as q
+
+    st = q.Circuit(3).add([q.H(k) for k in range(3)]).execute()
+    res = q.sample(st, (0, 1, 2), 1_000_000, seed=13)
+    freq = q.frequencies(res)
+    sigma = math.sqrt(1e6 * 0.125 * 0.875)
+    for o in range(8):
+        assert abs(freq.get(o, 0) - 125000) <= 6 * sigma
+
+
+# ---------------------------------------------------------------- size-independent properties
+@pytest.mark.parametrize("n", [24, 26])
+def test_qft_inverse_round_trip_and_norm(cuda, n):
+    import paper_2009_01845_b200 as q
+
+    rng = np.random.default_rng(n)
+    psi = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)) / math.sqrt(2 << n)
+    st = _sv(psi)
+    nrm0 = q.norm(st)
+    c = q.qft_circuit(n)
+    fwd = c.execute(st)
+    assert abs(q.norm(fwd) - nrm0) <= 1e-10
+    back = c.inverse().execute(fwd)
+    assert max_abs(back.amplitudes, psi) <= 1e-12
+
+
+def test_fused_equals_unfused_random_large(cuda):
+    import paper_2009_01845_b200 as q
+
+    n = 20
+    rng = np.random.default_rng(77)
+    specs = []
+    for _ in range(200):
+        spec = _random_spec(q, n, rng)
+        specs.append(spec)
+    c = q.Circuit(n).add(specs)
+    psi = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)) / math.sqrt(2 << n)
+    a = c.execute(_sv(psi), fuse=True).amplitudes
+    b = c.execute(_sv(psi), fuse=False).amplitudes
+    want = ov.run([ov.gate("Unitary", s.targets, s.controls, (), q.gate_matrix(s)) for s in specs], n, psi)
+    assert max_abs(a, want) <= TOL64 and max_abs(b, want) <= TOL64
+
+
+def _random_spec(q, n, rng):
+    kinds = ["H", "RX", "RZ", "CZPow", "CNOT", "CZ", "SWAP", "U1", "U2", "Y"]
+    k = kinds[rng.integers(len(kinds))]
+    order = rng.permutation(n)
+    two = k in ("CZPow", "CNOT", "CZ", "SWAP", "U2")
+    tg = tuple(int(x) for x in order[: 2 if two else 1])
+    ct = tuple(int(x) for x in order[len(tg): len(tg) + int(rng.integers(0, 3))])
+    th = float(rng.uniform(0, 2 * math.pi))
+    if k == "U1":
+        m, _ = np.linalg.qr(rng.standard_normal((2, 2)) + 1j * rng.standard_normal((2, 2)))
+        return q.Unitary(m, *tg, controls=ct)
+    if k == "U2":
+        m, _ = np.linalg.qr(rng.standard_normal((4, 4)) + 1j * rng.standard_normal((4, 4)))
+        return q.Unitary(m, *tg, controls=ct)
+    if k in ("RX", "RZ"):
+        return getattr(q, k)(tg[0], th, controls=ct)
+    if k == "CZPow":
+        return q.CZPow(tg[0], tg[1], th, controls=ct)
+    if k in ("H", "Y"):
+        return getattr(q, k)(tg[0], controls=ct)
+    return getattr(q, k)(tg[0], tg[1], controls=ct)
