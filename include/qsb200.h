@@ -83,6 +83,19 @@ int qsb_run_pass(const void* src, void* dst, int n_qubits, int dtype, const int6
 /* Bytes of shared memory the pass kernel needs for a tile of 2**tile_bits amplitudes. */
 int qsb_pass_max_tile_bits(int dtype);
 
+/* ---- pass specialisation (NVRTC): a straight-line kernel per pass structure -------------- */
+/* 1 when NVRTC (dlopen'ed from `nvrtc_path` or the default search path) and the driver API
+ * entry points are usable. */
+int qsb_jit_available(const char* nvrtc_path);
+/* Compile CUDA C++ `source` for sm_100a and return the CUfunction `name` in *func_out. */
+int qsb_jit_compile(const char* source, const char* name, const char* nvrtc_path, void** func_out,
+                    char* log_out, size_t log_cap);
+/* Launch a specialised pass kernel on the tile geometry of `program` (same word stream as
+ * qsb_run_pass) with the per-launch gate coefficients `coeffs`. */
+int qsb_jit_run_pass(void* func, const void* src, void* dst, int n_qubits, int dtype,
+                     const int64_t* program, int64_t n_words, const double* coeffs, int64_t n_coeffs,
+                     int threads, int smem_bytes, void* stream);
+
 /* ---- reductions (state.py:109-122 norm / overlap) ---------------------------------------- */
 /* out[0] = sum |a_i|^2 (double, device pointer).  Deterministic two-level tree. */
 int qsb_norm2(const void* amps, uint64_t n_amps, int dtype, double* out, void* stream);

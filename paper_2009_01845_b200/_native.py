@@ -53,6 +53,12 @@ SIGNATURES = {
     "qsb_cumsum_scratch_bytes": (_c_size_t, [_c_u64]),
     "qsb_cumsum_serial": (_c_int, [_c_void_p, _c_u64, _c_void_p, _c_void_p]),
     "qsb_sample": (_c_int, [_c_void_p, _c_u64, _c_u64, _c_u64, _c_u64, _c_u64, _c_u64, _c_void_p, _c_void_p]),
+    "qsb_jit_available": (_c_int, [ctypes.c_char_p]),
+    "qsb_jit_compile": (_c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _c_void_p, _c_void_p, _c_size_t]),
+    "qsb_jit_run_pass": (
+        _c_int,
+        [_c_void_p, _c_void_p, _c_void_p, _c_int, _c_int, _c_void_p, _c_i64, _c_void_p, _c_i64, _c_int, _c_int, _c_void_p],
+    ),
     "qsb_pack_half": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_u64, _c_u64, _c_void_p, _c_void_p]),
     "qsb_unpack_half": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_u64, _c_u64, _c_void_p, _c_void_p]),
 }

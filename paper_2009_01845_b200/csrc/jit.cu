@@ -1,0 +1,210 @@
+// Runtime specialisation of fused passes: NVRTC compiles the straight-line consumer body that
+// paper_2009_01845_b200/jit.py generates for one pass *structure* (bit positions, layouts, op
+// kinds; matrix / phase values stay runtime coefficients), for sm_100a, and the driver API
+// loads and launches it.  Same TMA producer, mbarrier ring and tile addressing as the
+// interpreted kernel in pass.cu; no dispatch loop, every amplitude stays in a named register.
+#include <dlfcn.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "pass_host.h"
+#include "qsb_common.cuh"
+
+namespace qsb {
+namespace jit {
+
+// --- NVRTC (dlopen'ed: the library does not hard-link it) ----------------------------------
+typedef int nvrtcResult_t;
+typedef void* nvrtcProgram_t;
+struct Nvrtc {
+  nvrtcResult_t (*create)(nvrtcProgram_t*, const char*, const char*, int, const char* const*, const char* const*);
+  nvrtcResult_t (*compile)(nvrtcProgram_t, int, const char* const*);
+  nvrtcResult_t (*cubin_size)(nvrtcProgram_t, size_t*);
+  nvrtcResult_t (*cubin)(nvrtcProgram_t, char*);
+  nvrtcResult_t (*log_size)(nvrtcProgram_t, size_t*);
+  nvrtcResult_t (*log)(nvrtcProgram_t, char*);
+  nvrtcResult_t (*destroy)(nvrtcProgram_t*);
+  bool ok = false;
+};
+
+static Nvrtc* nvrtc(const char* path_hint) {
+  static Nvrtc n;
+  static bool tried = false;
+  if (tried) return n.ok ? &n : nullptr;
+  tried = true;
+  const char* cands[] = {path_hint, "libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"};
+  void* h = nullptr;
+  for (const char* c : cands) {
+    if (!c || !*c) continue;
+    h = dlopen(c, RTLD_NOW | RTLD_LOCAL);
+    if (h) break;
+  }
+  if (!h) return nullptr;
+#define QSB_SYM(field, name)                                              \
+  n.field = reinterpret_cast<decltype(n.field)>(dlsym(h, name));          \
+  if (!n.field) return nullptr;
+  QSB_SYM(create, "nvrtcCreateProgram")
+  QSB_SYM(compile, "nvrtcCompileProgram")
+  QSB_SYM(cubin_size, "nvrtcGetCUBINSize")
+  QSB_SYM(cubin, "nvrtcGetCUBIN")
+  QSB_SYM(log_size, "nvrtcGetProgramLogSize")
+  QSB_SYM(log, "nvrtcGetProgramLog")
+  QSB_SYM(destroy, "nvrtcDestroyProgram")
+#undef QSB_SYM
+  n.ok = true;
+  return &n;
+}
+
+// --- driver API through the runtime's entry-point query (no -lcuda) -------------------------
+struct Driver {
+  CUresult (*load)(CUmodule*, const void*);
+  CUresult (*get_fn)(CUfunction*, CUmodule, const char*);
+  CUresult (*set_attr)(CUfunction, CUfunction_attribute, int);
+  CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
+                     void**, void**);
+  bool ok = false;
+};
+
+static Driver* driver() {
+  static Driver d;
+  static bool tried = false;
+  if (tried) return d.ok ? &d : nullptr;
+  tried = true;
+  cudaDriverEntryPointQueryResult q;
+  void* p = nullptr;
+#define QSB_DRV(field, name)                                                                    \
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) \
+    return nullptr;                                                                             \
+  d.field = reinterpret_cast<decltype(d.field)>(p);
+  QSB_DRV(load, "cuModuleLoadData")
+  QSB_DRV(get_fn, "cuModuleGetFunction")
+  QSB_DRV(set_attr, "cuFuncSetAttribute")
+  QSB_DRV(launch, "cuLaunchKernel")
+#undef QSB_DRV
+  d.ok = true;
+  return &d;
+}
+
+}  // namespace jit
+}  // namespace qsb
+
+using namespace qsb;
+
+extern "C" int qsb_jit_available(const char* nvrtc_path) {
+  return (jit::nvrtc(nvrtc_path) && jit::driver()) ? 1 : 0;
+}
+
+// Compile `source` (CUDA C++) with NVRTC for sm_100a and return the CUfunction `name`.
+extern "C" int qsb_jit_compile(const char* source, const char* name, const char* nvrtc_path, void** func_out,
+                               char* log_out, size_t log_cap) {
+  jit::Nvrtc* nv = jit::nvrtc(nvrtc_path);
+  jit::Driver* dr = jit::driver();
+  if (!nv || !dr) {
+    set_error("qsb_jit_compile: NVRTC or the CUDA driver API is unavailable");
+    return QSB_ERR_CUDA;
+  }
+  // NVRTC needs a current context for nothing, but module loading does: make sure the runtime
+  // has initialised the primary context on this thread.
+  cudaFree(nullptr);
+  jit::nvrtcProgram_t prog = nullptr;
+  if (nv->create(&prog, source, "qsb_pass.cu", 0, nullptr, nullptr) != 0) {
+    set_error("nvrtcCreateProgram failed");
+    return QSB_ERR_CUDA;
+  }
+  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo", "--use_fast_math=false"};
+  const int rc = nv->compile(prog, 4, opts);
+  size_t ls = 0;
+  nv->log_size(prog, &ls);
+  if (log_out && log_cap) {
+    log_out[0] = 0;
+    if (ls > 1) {
+      char* buf = new char[ls];
+      nv->log(prog, buf);
+      snprintf(log_out, log_cap, "%s", buf);
+      delete[] buf;
+    }
+  }
+  if (rc != 0) {
+    nv->destroy(&prog);
+    set_error("NVRTC compilation failed (see log)");
+    return QSB_ERR_ARG;
+  }
+  size_t cs = 0;
+  nv->cubin_size(prog, &cs);
+  char* cubin = new char[cs];
+  nv->cubin(prog, cubin);
+  nv->destroy(&prog);
+  CUmodule mod = nullptr;
+  CUresult r = dr->load(&mod, cubin);
+  delete[] cubin;
+  if (r != CUDA_SUCCESS) {
+    set_error("cuModuleLoadData failed (%d)", (int)r);
+    return QSB_ERR_CUDA;
+  }
+  CUfunction fn = nullptr;
+  r = dr->get_fn(&fn, mod, name);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuModuleGetFunction(%s) failed (%d)", name, (int)r);
+    return QSB_ERR_CUDA;
+  }
+  *func_out = reinterpret_cast<void*>(fn);
+  return QSB_OK;
+}
+
+// Launch a JIT pass kernel: params (src, dst, tmap, tma plan, coefficients).  `program` is the
+// same word stream the interpreter takes (its header gives the tile geometry for the TMA plan).
+extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, int n_qubits, int dtype,
+                                const int64_t* program, int64_t n_words, const double* coeffs, int64_t n_coeffs,
+                                int threads, int smem_bytes, void* stream) {
+  jit::Driver* dr = jit::driver();
+  if (!dr || !func) {
+    set_error("qsb_jit_run_pass: no driver / function");
+    return QSB_ERR_CUDA;
+  }
+  if (program[4] != n_qubits || program[5] != dtype) {
+    set_error("qsb_jit_run_pass: program built for another state");
+    return QSB_ERR_ARG;
+  }
+  cudaStream_t st = as_stream(stream);
+  const int K = (int)program[2];
+  void* dcoef = nullptr;
+  if (n_coeffs > 0) {
+    if (int rc = pass::stage_words(coeffs, sizeof(double) * n_coeffs, &dcoef, st)) return rc;
+  }
+  alignas(64) CUtensorMap map;
+  memset(&map, 0, sizeof map);
+  pass::TmaPlan tp;
+  pass::plan_tma(src, n_qubits, K, program + 16, dtype == QSB_C128 ? 16 : 8, &map, &tp);
+  if (tp.mode != 1) {
+    set_error("qsb_jit_run_pass: tile needs the bulk-copy fallback (use the interpreter)");
+    return QSB_ERR_ARG;
+  }
+  CUfunction fn = reinterpret_cast<CUfunction>(func);
+  static CUfunction attr_done[64];
+  static int n_attr = 0;
+  bool seen = false;
+  for (int i = 0; i < n_attr; ++i) seen |= attr_done[i] == fn;
+  if (!seen) {
+    CUresult r = dr->set_attr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem_bytes);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuFuncSetAttribute failed (%d)", (int)r);
+      return QSB_ERR_CUDA;
+    }
+    if (n_attr < 64) attr_done[n_attr++] = fn;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t n_tiles = 1ull << (n_qubits - K);
+  const unsigned grid = (unsigned)(n_tiles < (uint64_t)sms ? n_tiles : (uint64_t)sms);
+  const void* a_src = src;
+  void* a_dst = dst;
+  const double* a_cf = static_cast<const double*>(dcoef);
+  void* args[] = {(void*)&a_src, (void*)&a_dst, (void*)&map, (void*)&tp, (void*)&a_cf};
+  CUresult r = dr->launch(fn, grid, 1, 1, (unsigned)threads, 1, 1, (unsigned)smem_bytes, (CUstream)st, args, nullptr);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuLaunchKernel failed (%d)", (int)r);
+    return QSB_ERR_CUDA;
+  }
+  return QSB_OK;
+}

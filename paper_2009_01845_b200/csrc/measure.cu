@@ -571,8 +571,11 @@ __global__ void __launch_bounds__(1024) k_scan_counts(const unsigned int* __rest
   }
 }
 
-__global__ void __launch_bounds__(kMT) k_normalize(double* __restrict__ c, uint64_t n) {
-  const double total = c[n - 1];
+// total is read from a separate copy: c[n-1] itself is overwritten by the normalisation
+__global__ void k_copy_last(const double* __restrict__ c, uint64_t n, double* __restrict__ total) { *total = c[n - 1]; }
+
+__global__ void __launch_bounds__(kMT) k_normalize(double* __restrict__ c, uint64_t n, const double* __restrict__ tot) {
+  const double total = *tot;
   const uint64_t stride = (uint64_t)gridDim.x * kMT;
   for (uint64_t i = (uint64_t)blockIdx.x * kMT + threadIdx.x; i < n; i += stride) c[i] = c[i] / total;
 }
@@ -789,7 +792,7 @@ extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cu
   }
   static unsigned int* d_tot = nullptr;
   if (!d_tot) {
-    cudaError_t e = cudaMalloc(&d_tot, sizeof(unsigned int) * 2);
+    cudaError_t e = cudaMalloc(&d_tot, sizeof(double) * 2);
     if (e != cudaSuccess) return cuda_status(e, "device total");
   }
   d_total = d_tot;
@@ -820,7 +823,8 @@ extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cu
   k_block_pieces<<<(int)nb, 32, 0, st>>>(probs, n, serial, binade, base, head, after, sidx);
   k_stitch<<<1, 1, 0, st>>>(probs, nb, head, cnt, after, sidx, bstart, sval);
   k_materialize<<<(int)nb, 32, 0, st>>>(probs, n, serial, binade, bstart, base, sval, cum);
-  k_normalize<<<grid_for(n), kMT, 0, st>>>(cum, n);
+  k_copy_last<<<1, 1, 0, st>>>(cum, n, reinterpret_cast<double*>(d_tot) + 1);
+  k_normalize<<<grid_for(n), kMT, 0, st>>>(cum, n, reinterpret_cast<const double*>(d_tot) + 1);
   QSB_CHECK_LAUNCH("qsb_cumsum_normalized");
   return QSB_OK;
 }

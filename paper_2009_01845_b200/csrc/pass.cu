@@ -21,10 +21,13 @@
 //   * the result is written straight from registers to HBM (coalesced: the store layout puts
 //     lane bits on the low output bits), optionally to permuted positions (SWAP gates folded
 //     into the pass as relabels, tile-external swaps as an output tile permutation).
+#include <cuda.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "qsb_common.cuh"
+#include "pass_host.h"
 
 namespace qsb {
 namespace pass {
@@ -47,7 +50,8 @@ enum Op : int64_t {
 
 enum GKind : int64_t { G_COMPLEX = 0, G_REAL = 1, G_SWAPX = 2 };
 
-constexpr int kConsumers = 256;
+constexpr int kConsumers = 512;
+constexpr int kThrBits = 9;  // 5 lane bits + 4 warp bits
 constexpr int kThreads = kConsumers + 32;
 constexpr int kStages = 2;
 constexpr int kMaxProgWords = 6144;  // 48 KB of program in shared memory
@@ -88,6 +92,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// one multi-dimensional TMA tensor load (always rank 5; unused dims have extent 1)
+__device__ __forceinline__ void tma_load_5d(void* dst_smem, const CUtensorMap* map, const int32_t* c, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
+      "[%7];" ::"r"(smem_u32(dst_smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -120,8 +133,9 @@ struct Layout {
 template <int NREG>
 struct LW {
   static constexpr int A = 1 << NREG;
-  static constexpr int REG_TB = 0, THR_TB = NREG, REG_GOFF = NREG + 8, THR_GPOS = REG_GOFF + A, REG_OOFF = THR_GPOS + 8,
-                       THR_OPOS = REG_OOFF + A, REG_JT = THR_OPOS + 8, SIZE = REG_JT + A;
+  static constexpr int T = kThrBits;
+  static constexpr int REG_TB = 0, THR_TB = NREG, REG_GOFF = NREG + T, THR_GPOS = REG_GOFF + A, REG_OOFF = THR_GPOS + T,
+                       THR_OPOS = REG_OOFF + A, REG_JT = THR_OPOS + T, SIZE = REG_JT + A;
 };
 
 template <int NREG>
@@ -133,7 +147,7 @@ __device__ __forceinline__ Layout make_layout(const int64_t* w, int tid) {
   l.gthr = 0;
   l.othr = 0;
 #pragma unroll
-  for (int b = 0; b < 8; ++b) {
+  for (int b = 0; b < kThrBits; ++b) {
     if ((tid >> b) & 1) {
       l.jt |= 1u << (int)w[L::THR_TB + b];
       l.gthr |= 1ull << (int)w[L::THR_GPOS + b];
@@ -144,7 +158,7 @@ __device__ __forceinline__ Layout make_layout(const int64_t* w, int tid) {
 }
 
 // --- gate bodies (register bit indices are template parameters -> fully static indexing) -----
-template <typename C, int A, int IB>
+template <typename C, int A, int IB, bool CT>
 __device__ __forceinline__ void g1_complex(C (&v)[A], const int64_t* m, uint32_t rmask, uint32_t rval) {
   C a00, a01, a10, a11;
   a00.x = w2d(m[0]); a00.y = w2d(m[1]);
@@ -154,7 +168,7 @@ __device__ __forceinline__ void g1_complex(C (&v)[A], const int64_t* m, uint32_t
 #pragma unroll
   for (int s = 0; s < A; ++s) {
     if (s & (1 << IB)) continue;
-    if ((s & rmask) != rval) continue;
+    if (CT && (s & rmask) != rval) continue;
     const int s1 = s | (1 << IB);
     const C x0 = v[s], x1 = v[s1];
     v[s] = cmad(a01, x1, cmul(a00, x0));
@@ -162,14 +176,14 @@ __device__ __forceinline__ void g1_complex(C (&v)[A], const int64_t* m, uint32_t
   }
 }
 
-template <typename C, int A, int IB>
+template <typename C, int A, int IB, bool CT>
 __device__ __forceinline__ void g1_real(C (&v)[A], const int64_t* m, uint32_t rmask, uint32_t rval) {
   using R = decltype(C().x);
   const R a00 = (R)w2d(m[0]), a01 = (R)w2d(m[2]), a10 = (R)w2d(m[4]), a11 = (R)w2d(m[6]);
 #pragma unroll
   for (int s = 0; s < A; ++s) {
     if (s & (1 << IB)) continue;
-    if ((s & rmask) != rval) continue;
+    if (CT && (s & rmask) != rval) continue;
     const int s1 = s | (1 << IB);
     const C x0 = v[s], x1 = v[s1];
     C y0, y1;
@@ -182,12 +196,12 @@ __device__ __forceinline__ void g1_real(C (&v)[A], const int64_t* m, uint32_t rm
   }
 }
 
-template <typename C, int A, int IB>
+template <typename C, int A, int IB, bool CT>
 __device__ __forceinline__ void g1_swap(C (&v)[A], uint32_t rmask, uint32_t rval) {
 #pragma unroll
   for (int s = 0; s < A; ++s) {
     if (s & (1 << IB)) continue;
-    if ((s & rmask) != rval) continue;
+    if (CT && (s & rmask) != rval) continue;
     const int s1 = s | (1 << IB);
     const C t = v[s];
     v[s] = v[s1];
@@ -197,12 +211,21 @@ __device__ __forceinline__ void g1_swap(C (&v)[A], uint32_t rmask, uint32_t rval
 
 template <typename C, int A, int IB>
 __device__ __forceinline__ void g1_dispatch(C (&v)[A], int64_t kind, const int64_t* m, uint32_t rmask, uint32_t rval) {
-  if (kind == G_REAL)
-    g1_real<C, A, IB>(v, m, rmask, rval);
-  else if (kind == G_SWAPX)
-    g1_swap<C, A, IB>(v, rmask, rval);
-  else
-    g1_complex<C, A, IB>(v, m, rmask, rval);
+  if (rmask) {
+    if (kind == G_REAL)
+      g1_real<C, A, IB, true>(v, m, rmask, rval);
+    else if (kind == G_SWAPX)
+      g1_swap<C, A, IB, true>(v, rmask, rval);
+    else
+      g1_complex<C, A, IB, true>(v, m, rmask, rval);
+  } else {
+    if (kind == G_REAL)
+      g1_real<C, A, IB, false>(v, m, 0, 0);
+    else if (kind == G_SWAPX)
+      g1_swap<C, A, IB, false>(v, 0, 0);
+    else
+      g1_complex<C, A, IB, false>(v, m, 0, 0);
+  }
 }
 
 template <typename C, int A, int NREG>
@@ -220,13 +243,13 @@ __device__ __forceinline__ void apply_g1(C (&v)[A], int ib, int64_t kind, const 
 
 // two-target gate on register bits IH (row bit 1 = targets[0]) and IL (row bit 0); IH > IL is
 // canonicalised by the host (it transposes the matrix when needed).
-template <typename C, int A, int IH, int IL>
+template <typename C, int A, int IH, int IL, bool CT>
 __device__ __forceinline__ void g2_body(C (&v)[A], int64_t kind, const int64_t* m, uint32_t rmask, uint32_t rval) {
   using R = decltype(C().x);
 #pragma unroll
   for (int s = 0; s < A; ++s) {
     if (s & ((1 << IH) | (1 << IL))) continue;
-    if ((s & rmask) != rval) continue;
+    if (CT && (s & rmask) != rval) continue;
     const int sidx[4] = {s, s | (1 << IL), s | (1 << IH), s | (1 << IH) | (1 << IL)};
     C x[4];
 #pragma unroll
@@ -268,10 +291,15 @@ template <typename C, int A, int NREG>
 __device__ __forceinline__ void apply_g2(C (&v)[A], int ih, int il, int64_t kind, const int64_t* m, uint32_t rmask,
                                          uint32_t rval) {
   // ih > il
-#define QSB_G2(H, L)                                                   \
-  if (ih == H && il == L) {                                            \
-    if (H < NREG) g2_body<C, A, (H < NREG ? H : 1), L>(v, kind, m, rmask, rval); \
-    return;                                                            \
+#define QSB_G2(H, L)                                                                  \
+  if (ih == H && il == L) {                                                           \
+    if (H < NREG) {                                                                   \
+      if (rmask)                                                                      \
+        g2_body<C, A, (H < NREG ? H : 1), L, true>(v, kind, m, rmask, rval);          \
+      else                                                                            \
+        g2_body<C, A, (H < NREG ? H : 1), L, false>(v, kind, m, 0, 0);                \
+    }                                                                                 \
+    return;                                                                           \
   }
   QSB_G2(1, 0)
   QSB_G2(2, 0)
@@ -329,6 +357,7 @@ struct Smem {
   cplx<double> ep[2][kMaxPivots];  // per-tile external pivot factors, double-buffered by tile parity
   uint64_t full[kStages];
   uint64_t empty[kStages];
+  uint64_t base[kStages][2];  // input / output tile base of the tile in each stage (producer-written)
 };
 
 // Program header word offsets
@@ -339,11 +368,11 @@ enum : int {
 template <typename R>
 __global__ void __launch_bounds__(kThreads, 1)
     k_pass(const cplx<R>* __restrict__ src, cplx<R>* __restrict__ dst, const int64_t* __restrict__ gprog,
-           int n_words) {
+           int n_words, const __grid_constant__ CUtensorMap tmap, const TmaPlan tp) {
   using C = cplx<R>;
   constexpr int K = Tile<R>::K;
   constexpr int G = Tile<R>::G;
-  constexpr int NREG = K - 8;
+  constexpr int NREG = K - kThrBits;
   constexpr int A = 1 << NREG;
   using LWN = LW<NREG>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -396,6 +425,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ph = (it / kStages) & 1;
       if (it >= kStages) mbar_wait(&sm.empty[s], ph ^ 1);
       const uint64_t base = tile_base(c);
+      if (lane == 0) {
+        sm.base[s][0] = base;
+        sm.base[s][1] = (flags & 1) ? tile_out(c) : base;
+      }
+      if (tp.mode == 1) {
+        if (lane == 0) {
+          mbar_expect_tx(&sm.full[s], (uint32_t)((1u << K) * sizeof(C)));
+          int32_t co[5] = {0, 0, 0, 0, 0};
+          for (int g = 0; g < tp.n_gap; ++g)
+            co[tp.gap_dim[g]] = (int32_t)((base >> tp.gap_lo[g]) & ((1ull << tp.gap_nb[g]) - 1ull));
+          const int32_t top0 = tp.top_dim >= 0 ? (int32_t)(base >> tp.top_lo) : 0;
+          char* dstb = reinterpret_cast<char*>(&sm.stage[s][0]);
+          for (int k = 0; k < tp.n_calls; ++k) {
+            if (tp.top_dim >= 0) co[tp.top_dim] = top0 + (int32_t)tp.call_coord[k];
+            tma_load_5d(dstb + (size_t)k * tp.call_bytes, &tmap, co, &sm.full[s]);
+          }
+        }
+        __syncwarp();
+        continue;
+      }
       if (lane == 0) mbar_expect_tx(&sm.full[s], (uint32_t)((1u << K) * sizeof(C)));
       __syncwarp();
       for (int r = lane; r < n_runs; r += 32) {
@@ -414,8 +463,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (uint64_t c = blockIdx.x; c < n_tiles; c += gridDim.x, ++it) {
     const int s = it % kStages;
     const uint32_t ph = (it / kStages) & 1;
-    const uint64_t base = tile_base(c);
-    const uint64_t obase = (flags & 1) ? tile_out(c) : base;
+    mbar_wait(&sm.full[s], ph);
+    const uint64_t base = sm.base[s][0];
+    const uint64_t obase = sm.base[s][1];
 
     // external pivot factors for this tile: one thread per pivot op
     {
@@ -449,7 +499,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
 
-    mbar_wait(&sm.full[s], ph);
     cplx<R>* buf = sm.stage[s];
 
     // initial layout: read registers from the natural-order stage
@@ -496,11 +545,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           break;
         }
         case OP_PIVOT: {
-          // a: [slot, ptype, pval, use_rt, n_ext, ext(3*n_ext), TA(32), TB(32), RT(2A)]
+          // a: [slot, ptype, pval, use_rt, n_ext, ext(3*n_ext), TA(2*16), TB(2*32), RT(2A)]
           const int ne = (int)a[4];
           const int64_t* ta = a + 5 + 3 * ne;
           const int64_t* tb = ta + 32;
-          const int64_t* rt = tb + 32;
+          const int64_t* rt = tb + 64;
           const bool use_rt = a[3] != 0;
           const int ptype = (int)a[1];
           bool active = true;
@@ -580,6 +629,153 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// Describe the state as a rank-5 tensor of 8-byte elements whose box is one tile.
+void plan_tma(const void* src, int n, int K, const int64_t* tile_pos, int amp_bytes, CUtensorMap* map,
+              TmaPlan* tp) {
+  memset(tp, 0, sizeof *tp);
+  tp->mode = 0;
+  tp->top_dim = -1;
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return;
+  const int epa = amp_bytes / 8;  // 8-byte elements per amplitude
+  uint64_t tmask = 0;
+  for (int b = 0; b < K; ++b) tmask |= 1ull << tile_pos[b];
+  struct D { int lo, nb; bool tile; };
+  D dims[64];
+  int nd = 0;
+  int b = 0;
+  while (b < n) {
+    const bool t = (tmask >> b) & 1ull;
+    int e = b;
+    while (e < n && (((tmask >> e) & 1ull) != 0) == t) ++e;
+    if (t) {
+      int p = b;
+      while (p < e) {
+        const int lim = (nd == 0 && epa == 2) ? 7 : 8;  // box extent <= 256 elements
+        const int w = (e - p) < lim ? (e - p) : lim;
+        dims[nd++] = {p, w, true};
+        p += w;
+      }
+    } else {
+      dims[nd++] = {b, e - b, false};
+    }
+    b = e;
+  }
+  int use = nd;
+  uint64_t iter_mask = 0;
+  int top_lo = n;
+  if (nd > 5) {
+    use = 5;
+    top_lo = dims[4].lo;
+    iter_mask = (tmask >> top_lo);  // tile bits inside the merged top dim are iterated
+    dims[4] = {top_lo, n - top_lo, false};
+  }
+  const int iter_bits = __builtin_popcountll(iter_mask);
+  if (iter_bits > 5) return;  // > 32 calls: bulk-copy fallback
+  for (int d = 0; d < use; ++d)
+    if (!dims[d].tile && dims[d].nb > 31) return;
+  cuuint64_t gdim[5], gstride[4];
+  cuuint32_t box[5], estride[5];
+  uint64_t extent_bytes = 8;
+  for (int d = 0; d < 5; ++d) {
+    if (d < use) {
+      gdim[d] = (1ull << dims[d].nb) * (d == 0 ? epa : 1);
+      box[d] = dims[d].tile ? (cuuint32_t)gdim[d] : 1u;
+      if (d > 0) gstride[d - 1] = (1ull << dims[d].lo) * amp_bytes;
+    } else {
+      gdim[d] = 1;
+      box[d] = 1;
+      if (d > 0) gstride[d - 1] = (1ull << n) * amp_bytes;
+    }
+    estride[d] = 1;
+  }
+  (void)extent_bytes;
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<void*>(src), gdim, gstride, box, estride,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return;
+  tp->n_gap = 0;
+  for (int d = 0; d < use; ++d) {
+    if (dims[d].tile) continue;
+    if (nd > 5 && d == 4) continue;
+    tp->gap_dim[tp->n_gap] = d;
+    tp->gap_lo[tp->n_gap] = dims[d].lo;
+    tp->gap_nb[tp->n_gap] = dims[d].nb;
+    ++tp->n_gap;
+  }
+  uint64_t box_elems = 1;
+  for (int d = 0; d < 5; ++d) box_elems *= box[d];
+  tp->call_bytes = (uint32_t)(box_elems * 8);
+  if (nd > 5) {
+    tp->top_dim = 4;
+    tp->top_lo = top_lo;
+    tp->n_calls = 1 << iter_bits;
+    for (int k = 0; k < tp->n_calls; ++k) {
+      // deposit the bits of k onto the tile bits of the top dim (ascending)
+      uint32_t off = 0;
+      int j = 0;
+      for (int q = 0; q < 64 && (iter_mask >> q); ++q)
+        if ((iter_mask >> q) & 1ull) {
+          if ((k >> j) & 1) off |= 1u << q;
+          ++j;
+        }
+      tp->call_coord[k] = off;
+    }
+  } else {
+    tp->n_calls = 1;
+    tp->call_coord[0] = 0;
+  }
+  tp->mode = 1;
+}
+
+// Device ring for per-launch program / coefficient words.  Copies are stream-ordered; when the
+// ring wraps, the stream is synchronised once so no in-flight launch can see overwritten words.
+int stage_words(const void* host, size_t bytes, void** device_out, cudaStream_t st) {
+  static char* ring = nullptr;
+  static size_t cursor = 0;
+  constexpr size_t kRing = 16u << 20;
+  if (bytes > kRing / 4) {
+    set_error("stage_words: %zu bytes too large", bytes);
+    return QSB_ERR_ARG;
+  }
+  if (!ring) {
+    cudaError_t e = cudaMalloc(&ring, kRing);
+    if (e != cudaSuccess) {
+      ring = nullptr;
+      return cuda_status(e, "program ring");
+    }
+  }
+  size_t off = (cursor + 255) & ~(size_t)255;
+  if (off + bytes > kRing) {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_status(e, "program ring wrap");
+    off = 0;
+  }
+  cursor = off + bytes;
+  cudaError_t e = cudaMemcpyAsync(ring + off, host, bytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_status(e, "program upload");
+  *device_out = ring + off;
+  return QSB_OK;
+}
+
 template <typename R>
 static int launch(const void* src, void* dst, const int64_t* hprog, int64_t n_words, cudaStream_t st) {
   constexpr int K = Tile<R>::K;
@@ -587,7 +783,7 @@ static int launch(const void* src, void* dst, const int64_t* hprog, int64_t n_wo
     set_error("qsb_run_pass: program of %lld words exceeds %d", (long long)n_words, kMaxProgWords);
     return QSB_ERR_ARG;
   }
-  if (hprog[H_MAGIC] != kMagic || hprog[H_VER] != kVersion || hprog[H_K] != K || hprog[H_NREG] != K - 8) {
+  if (hprog[H_MAGIC] != kMagic || hprog[H_VER] != kVersion || hprog[H_K] != K || hprog[H_NREG] != K - kThrBits) {
     set_error("qsb_run_pass: program header mismatch (magic/version/K)");
     return QSB_ERR_ARG;
   }
@@ -595,19 +791,10 @@ static int launch(const void* src, void* dst, const int64_t* hprog, int64_t n_wo
     set_error("qsb_run_pass: too many pivot ops");
     return QSB_ERR_ARG;
   }
-  // program words are staged in a small device buffer owned by the library (ring of slots so
-  // consecutive async passes never overwrite a program still in use)
-  static int64_t* d_ring = nullptr;
-  static int slot = 0;
-  constexpr int kSlots = 64;
-  if (!d_ring) {
-    cudaError_t e = cudaMalloc(&d_ring, sizeof(int64_t) * kMaxProgWords * kSlots);
-    if (e != cudaSuccess) return cuda_status(e, "pass program buffer");
-  }
-  int64_t* dprog = d_ring + (size_t)slot * kMaxProgWords;
-  slot = (slot + 1) % kSlots;
-  cudaError_t e = cudaMemcpyAsync(dprog, hprog, sizeof(int64_t) * n_words, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return cuda_status(e, "pass program upload");
+  void* dprog_v = nullptr;
+  if (int rc = stage_words(hprog, sizeof(int64_t) * n_words, &dprog_v, st)) return rc;
+  int64_t* dprog = static_cast<int64_t*>(dprog_v);
+  cudaError_t e;
   const size_t smem = sizeof(Smem<R>);
   static bool attr_set = false;
   if (!attr_set) {
@@ -620,8 +807,18 @@ static int launch(const void* src, void* dst, const int64_t* hprog, int64_t n_wo
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint64_t n_tiles = (uint64_t)hprog[H_NTILES];
   const int grid = (int)(n_tiles < (uint64_t)sms ? n_tiles : (uint64_t)sms);
+  alignas(64) CUtensorMap map;
+  memset(&map, 0, sizeof map);
+  TmaPlan tp;
+  static const bool no_tma = getenv("QSB_NO_TMA_TENSOR") != nullptr;
+  if (no_tma) {
+    memset(&tp, 0, sizeof tp);
+    tp.top_dim = -1;
+  } else {
+    plan_tma(src, (int)hprog[H_N], K, hprog + H_TILEPOS, (int)sizeof(cplx<R>), &map, &tp);
+  }
   k_pass<R><<<grid, kThreads, smem, st>>>(static_cast<const cplx<R>*>(src), static_cast<cplx<R>*>(dst), dprog,
-                                         (int)n_words);
+                                         (int)n_words, map, tp);
   QSB_CHECK_LAUNCH("qsb_run_pass");
   return QSB_OK;
 }

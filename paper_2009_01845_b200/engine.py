@@ -10,10 +10,12 @@ of the same size, after which the buffers trade places.
 from __future__ import annotations
 
 import os
+import warnings
 
 import numpy as np
 
 from . import _native as nat
+from . import jit
 from .fusion import GateStep, PassStep, Plan, plan_circuit
 
 # QSB_FUSION=0 disables pass fusion (every gate becomes its own kernel launch)
@@ -54,6 +56,21 @@ def _apply_gate_step(ptr, n, dtype, g, stream):
     )
 
 
+def _launch_pass(step, words, dtype, src, dst, n, st):
+    """Specialised (NVRTC) kernel when available, else the interpreting pass kernel."""
+    if not step.no_jit and jit.available():
+        try:
+            if step.jit is None:
+                step.jit = jit.compile_words(words, dtype)
+            compiled, coeffs = step.jit
+            jit.run(words, dtype, src, dst, n, st, compiled, coeffs)
+            return
+        except Exception as exc:  # compile / TMA-plan failure: keep going on the interpreter
+            step.no_jit = True
+            warnings.warn(f"pass specialisation unavailable ({exc}); using the interpreted pass kernel")
+    nat.check(nat.lib().qsb_run_pass(src, dst, n, dtype, words.ctypes.data, len(words), st), "run_pass")
+
+
 def run_plan(state, plan: Plan, scratch_holder: dict | None = None, stream=None, events: list | None = None):
     """Execute every step of `plan` on `state` (in place; the tensor object may be swapped).
 
@@ -73,22 +90,20 @@ def run_plan(state, plan: Plan, scratch_holder: dict | None = None, stream=None,
             ev0 = nat.torch_mod().cuda.Event(enable_timing=True)
             ev1 = nat.torch_mod().cuda.Event(enable_timing=True)
             ev0.record(stream)
+        src = state.data_ptr
         if step.ext_perm:
             scratch = holder.get("buf")
             if scratch is None or scratch.numel() != state.n_amps or scratch.dtype != state.tensor.dtype:
                 scratch = nat.torch_mod().empty_like(state.tensor)
-            nat.check(
-                lib.qsb_run_pass(state.data_ptr, scratch.data_ptr(), n, dtype, words.ctypes.data, len(words), st),
-                "run_pass",
-            )
-            old = state._t
-            state._t = scratch
-            holder["buf"] = old
+            dst_t = scratch
         else:
-            nat.check(
-                lib.qsb_run_pass(state.data_ptr, state.data_ptr, n, dtype, words.ctypes.data, len(words), st),
-                "run_pass",
-            )
+            dst_t = None
+        dst = dst_t.data_ptr() if dst_t is not None else src
+        _launch_pass(step, words, dtype, src, dst, n, st)
+        if dst_t is not None:
+            old = state._t
+            state._t = dst_t
+            holder["buf"] = old
         if events is not None:
             ev1.record(stream)
             events.append((ev0, ev1))

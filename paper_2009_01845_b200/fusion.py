@@ -34,6 +34,7 @@ G_COMPLEX, G_REAL, G_SWAPX = 0, 1, 2
 H_TILEPOS = 16
 MAX_PROG_WORDS = 6144
 MAX_PIVOTS = 64
+THREAD_BITS = 9  # 512 consumer threads per CTA: 5 lane bits + 4 warp bits
 
 
 @dataclass(frozen=True)
@@ -44,7 +45,7 @@ class TileGeometry:
 
     @property
     def nreg(self) -> int:
-        return self.K - 8
+        return self.K - THREAD_BITS
 
     @property
     def A(self) -> int:
@@ -152,6 +153,8 @@ class PassStep:
     ext_perm: bool
     n_transposes: int
     n_pivots: int
+    jit: object = None  # (compiled kernel, coefficient array) once specialised
+    no_jit: bool = False
 
     @property
     def n_gates(self) -> int:
@@ -276,14 +279,14 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
 class _Layout:
     def __init__(self, R, Tb):
         self.R = list(R)  # slot bit i <-> tile bit R[i]
-        self.Tb = list(Tb)  # thread bit b <-> tile bit Tb[b] (0..4 lanes, 5..7 warps)
+        self.Tb = list(Tb)  # thread bit b <-> tile bit Tb[b] (0..4 lanes, 5..8 warps)
 
     def slot_of(self, tile_bit):
         return self.R.index(tile_bit)
 
 
 def _order_thread_bits(cands, geo, prefer, natural=False):
-    """Order the 8 thread tile-bits: lanes first.  natural=True keeps tile bits 0..G-1 on
+    """Order the THREAD_BITS thread tile-bits: lanes first.  natural=True keeps tile bits 0..G-1 on
     lanes 0..G-1 (reads of the TMA stage are unswizzled)."""
     cands = sorted(cands)
     if natural:
@@ -575,7 +578,7 @@ def _pivot_op(p, partners, self_w, lay, tile_pos, tidx, A, slot):
         ptype, pval = 1, 1 << p
     ext = []
     ta = np.ones(16, dtype=np.complex128) * self_w
-    tb = np.ones(16, dtype=np.complex128)
+    tb = np.ones(1 << (THREAD_BITS - 4), dtype=np.complex128)
     rt = np.ones(A, dtype=np.complex128)
     for q, w in sorted(partners.items()):
         if q not in tidx:
@@ -594,7 +597,7 @@ def _pivot_op(p, partners, self_w, lay, tile_pos, tidx, A, slot):
                     if (u >> tbit) & 1:
                         ta[u] *= w
             else:
-                for u in range(16):
+                for u in range(len(tb)):
                     if (u >> (tbit - 4)) & 1:
                         tb[u] *= w
     use_rt = int(np.any(rt != 1.0))

@@ -1,0 +1,507 @@
+"""Pass specialisation: generate straight-line CUDA for one fused pass and compile it with NVRTC.
+
+The interpreted pass kernel (csrc/pass.cu) dispatches ops at run time; ptxas then shuffles the
+whole register-resident tile at every op (measured: ~38% of all instructions were register
+moves).  Here the op list of a pass program (the same int64 word stream, fusion.py) becomes
+C++ source: every amplitude is a named register, every gate an unrolled butterfly, every layout
+change a transpose with compile-time slot offsets.  Gate coefficients (matrix entries, phases,
+pivot tables) are NOT baked in: they are read from a per-launch coefficient array, so passes
+with the same structure (e.g. every Trotter step) share one compiled kernel.  Kernels are
+cached in-process by source text.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+import struct
+import threading
+
+import numpy as np
+
+from . import _native as nat
+
+OP_END, OP_LAYOUT, OP_G1, OP_G2, OP_PIVOT, OP_PARITY, OP_TERM, OP_SCALE = range(8)
+H_TILEPOS = 16
+CONSUMERS = 512
+THREADS = CONSUMERS + 32
+STAGES = 2
+MAX_PIV = 64
+
+
+def _w2d(w):
+    return struct.unpack("<d", struct.pack("<q", int(w)))[0]
+
+
+_PRELUDE = r"""
+typedef unsigned long long u64;
+typedef unsigned int u32;
+typedef long long i64;
+struct __align__(64) TMap { u64 w[16]; };
+struct TmaPlan { int mode; int n_gap; int gap_dim[5]; int gap_lo[5]; int gap_nb[5]; int top_dim; int top_lo;
+                 int n_calls; u32 call_bytes; u32 call_coord[32]; };
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* b, u32 c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(c)); }
+__device__ __forceinline__ void mbar_expect_tx(u64* b, u32 n) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(b)), "r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(u64* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(b)) : "memory"); }
+__device__ __forceinline__ void mbar_wait(u64* b, u32 par) {
+  asm volatile("{\n\t.reg .pred P;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t@!P bra W_%=;\n}"
+               :: "r"(smem_u32(b)), "r"(par) : "memory"); }
+__device__ __forceinline__ void tma5(void* d, const TMap* m, const int* c, u64* b) {
+  asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+               :: "r"(smem_u32(d)), "l"((u64)m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(b)) : "memory"); }
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" :: "n"(CONSUMERS) : "memory"); }
+__device__ __forceinline__ void fence_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ C cm(C a, C b) { C r; r.x = a.x * b.x - a.y * b.y; r.y = a.x * b.y + a.y * b.x; return r; }
+__device__ __forceinline__ double2 dm(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ double2 cfz(const double* __restrict__ cf, int k) { return make_double2(cf[k], cf[k + 1]); }
+__device__ __forceinline__ C toC(double2 z) { C r; r.x = (R)z.x; r.y = (R)z.y; return r; }
+__device__ __forceinline__ u32 swz(u32 j) {
+  u32 f = 0;
+#pragma unroll
+  for (int s = GB; s < KB; s += GB) f ^= (j >> s);
+  return j ^ (f & ((1u << GB) - 1u));
+}
+struct Smem { C stage[STAGES][1 << KB]; double2 ep[2][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 base[STAGES][2]; };
+"""
+
+
+class _Gen:
+    def __init__(self, words, dtype):
+        self.w = [int(x) for x in words]
+        self.dtype = dtype
+        w = self.w
+        self.K, self.NREG, self.n = w[2], w[3], w[4]
+        self.TB = self.K - self.NREG
+        self.A = 1 << self.NREG
+        self.G = 3 if dtype == nat.QSB_C128 else 4
+        n, K = self.n, self.K
+        self.tile_pos = w[H_TILEPOS:H_TILEPOS + K]
+        self.ext_pos = w[H_TILEPOS + K:H_TILEPOS + n]
+        self.ext_out = w[H_TILEPOS + n:H_TILEPOS + 2 * n - K]
+        self.ext_perm = bool(w[7] & 1)
+        self.ops0 = H_TILEPOS + 2 * n - K
+        self.coeffs: list = []
+        self.lines: list = []
+
+    # coefficient array (doubles); returns the index of the first entry
+    def cf(self, values):
+        k = len(self.coeffs)
+        self.coeffs.extend(float(v) for v in values)
+        return k
+
+    def emit(self, s):
+        self.lines.append(s)
+
+    # ---- layouts ------------------------------------------------------------------------
+    def parse_layout(self, a):
+        w, NREG, TB, A = self.w, self.NREG, self.TB, self.A
+        R = w[a:a + NREG]
+        Tb = w[a + NREG:a + NREG + TB]
+        goff = w[a + NREG + TB:a + NREG + TB + A]
+        gpos = w[a + NREG + TB + A:a + NREG + 2 * TB + A]
+        ooff = w[a + NREG + 2 * TB + A:a + NREG + 2 * TB + 2 * A]
+        opos = w[a + NREG + 2 * TB + 2 * A:a + NREG + 3 * TB + 2 * A]
+        jt = w[a + NREG + 3 * TB + 2 * A:a + NREG + 3 * TB + 3 * A]
+        return dict(R=R, Tb=Tb, goff=goff, gpos=gpos, ooff=ooff, opos=opos, jt=jt)
+
+    def swz_const(self, j):
+        f = 0
+        s = self.G
+        while s < self.K:
+            f ^= j >> s
+            s += self.G
+        return j ^ (f & ((1 << self.G) - 1))
+
+    def thread_expr(self, positions, width):
+        """OR of ((tid >> i) & 1) << positions[i]  as a C expression of `width` bits."""
+        parts = []
+        for i, p in enumerate(positions):
+            if width == 64:
+                parts.append(f"((u64)((tid >> {i}) & 1) << {p})")
+            else:
+                parts.append(f"(((u32)tid >> {i} & 1u) << {p})")
+        return " | ".join(parts) if parts else "0"
+
+    def set_layout(self, lay, idx):
+        self.emit(f"    const u32 jt{idx} = {self.thread_expr(lay['Tb'], 32)};")
+        self.emit(f"    const u64 gt{idx} = {self.thread_expr(lay['gpos'], 64)};")
+        self.lay = lay
+        self.li = idx
+
+    # ---- generation ---------------------------------------------------------------------
+    def generate(self, name):
+        w = self.w
+        A = self.A
+        p = self.ops0
+        assert w[p] == OP_LAYOUT
+        first = self.parse_layout(p + 2)
+        # pivots (per-tile external factors)
+        piv_ops = []
+        q = p
+        while w[q] != OP_END:
+            if w[q] == OP_PIVOT:
+                piv_ops.append(q)
+            q += w[q + 1]
+        self.npiv = len(piv_ops)
+        body_start = len(self.lines)
+        # external pivot factors: thread t computes pivot t's product over external partners
+        if piv_ops:
+            self.emit("    if (tid < NPIV) {")
+            self.emit("      double2 f = make_double2(1.0, 0.0);")
+            self.emit("      switch (tid) {")
+            for q in piv_ops:
+                a = q + 2
+                slot, ne = w[a], w[a + 4]
+                self.emit(f"        case {slot}: {{")
+                for k in range(ne):
+                    bit = w[a + 5 + 3 * k]
+                    ci = self.cf([_w2d(w[a + 6 + 3 * k]), _w2d(w[a + 7 + 3 * k])])
+                    self.emit(f"          if ((base >> {bit}) & 1ull) f = dm(f, cfz(cf, {ci}));")
+                self.emit("          break; }")
+            self.emit("      }")
+            self.emit("      sm.ep[it & 1][tid] = f;")
+            self.emit("    }")
+        # initial load (natural order stage)
+        self.set_layout(first, 0)
+        for s in range(A):
+            self.emit(f"    C v{s} = buf[jt0 | {first['jt'][s]}u];")
+        self.emit("    csync();")
+        swizzled = False
+        q = p + w[p + 1]
+        li = 0
+        while w[q] != OP_END:
+            op, ln = w[q], w[q + 1]
+            a = q + 2
+            if op == OP_LAYOUT:
+                new = self.parse_layout(a)
+                li += 1
+                if swizzled:
+                    self.emit("    csync();")
+                self.emit("    { const u32 sj = swz(jt%d);" % self.li)
+                for s in range(A):
+                    self.emit(f"      buf[sj ^ {self.swz_const(self.lay['jt'][s])}u] = v{s};")
+                self.emit("    }")
+                self.emit("    csync();")
+                self.set_layout(new, li)
+                self.emit("    { const u32 sj = swz(jt%d);" % li)
+                for s in range(A):
+                    self.emit(f"      v{s} = buf[sj ^ {self.swz_const(new['jt'][s])}u];")
+                self.emit("    }")
+                swizzled = True
+            elif op == OP_G1:
+                self.gen_g1(a)
+            elif op == OP_G2:
+                self.gen_g2(a)
+            elif op == OP_PIVOT:
+                self.gen_pivot(a)
+            elif op == OP_PARITY:
+                self.gen_parity(a)
+            elif op == OP_TERM:
+                self.gen_term(a)
+            elif op == OP_SCALE:
+                ci = self.cf([_w2d(w[a]), _w2d(w[a + 1])])
+                self.emit(f"    {{ const C ph = toC(cfz(cf, {ci}));")
+                for s in range(A):
+                    self.emit(f"      v{s} = cm(v{s}, ph);")
+                self.emit("    }")
+            q += ln
+        body = "\n".join(self.lines[body_start:])
+        # output offsets of the final layout
+        lay = self.lay
+        store = [f"    const u64 ot = obase | {self.thread_expr(lay['opos'], 64)};"]
+        for s in range(A):
+            store.append(f"    dst[ot | {lay['ooff'][s]}ull] = v{s};")
+        return self._kernel(name, body, "\n".join(store))
+
+    def gen_g1(self, a):
+        w, A = self.w, self.A
+        ib, kind, gmask, gval, rmask, rval = w[a:a + 6]
+        m = [_w2d(x) for x in w[a + 6:a + 14]]
+        self.emit(f"    {{ // G1 slot bit {ib} kind {kind}")
+        if gmask:
+            self.emit(f"    if (((base | gt{self.li}) & {gmask}ull) == {gval}ull) {{")
+        if kind == 1:
+            ci = self.cf([m[0], m[2], m[4], m[6]])
+            self.emit(f"      const R a00 = (R)cf[{ci}], a01 = (R)cf[{ci + 1}], a10 = (R)cf[{ci + 2}], a11 = (R)cf[{ci + 3}];")
+        elif kind == 0:
+            ci = self.cf(m)
+            for r, nm in enumerate(("a00", "a01", "a10", "a11")):
+                self.emit(f"      const C {nm} = toC(cfz(cf, {ci + 2 * r}));")
+        for s in range(A):
+            if s & (1 << ib) or (s & rmask) != rval:
+                continue
+            t = s | (1 << ib)
+            if kind == 2:
+                self.emit(f"      {{ const C x = v{s}; v{s} = v{t}; v{t} = x; }}")
+            elif kind == 1:
+                self.emit(f"      {{ const C x0 = v{s}, x1 = v{t};"
+                          f" v{s}.x = fma(a01, x1.x, a00 * x0.x); v{s}.y = fma(a01, x1.y, a00 * x0.y);"
+                          f" v{t}.x = fma(a11, x1.x, a10 * x0.x); v{t}.y = fma(a11, x1.y, a10 * x0.y); }}")
+            else:
+                self.emit(f"      {{ const C x0 = v{s}, x1 = v{t};"
+                          f" C y0 = cm(a00, x0), y1 = cm(a10, x0);"
+                          f" y0.x = fma(a01.x, x1.x, y0.x); y0.x = fma(-a01.y, x1.y, y0.x);"
+                          f" y0.y = fma(a01.x, x1.y, y0.y); y0.y = fma(a01.y, x1.x, y0.y);"
+                          f" y1.x = fma(a11.x, x1.x, y1.x); y1.x = fma(-a11.y, x1.y, y1.x);"
+                          f" y1.y = fma(a11.x, x1.y, y1.y); y1.y = fma(a11.y, x1.x, y1.y);"
+                          f" v{s} = y0; v{t} = y1; }}")
+        if gmask:
+            self.emit("    }")
+        self.emit("    }")
+
+    def gen_g2(self, a):
+        w, A = self.w, self.A
+        ih, il, kind, gmask, gval, rmask, rval = w[a:a + 7]
+        m = [_w2d(x) for x in w[a + 7:a + 39]]
+        self.emit(f"    {{ // G2 slot bits {ih},{il} kind {kind}")
+        if gmask:
+            self.emit(f"    if (((base | gt{self.li}) & {gmask}ull) == {gval}ull) {{")
+        if kind == 1:
+            ci = self.cf([m[2 * k] for k in range(16)])
+            self.emit(f"      R mm[16]; for (int k = 0; k < 16; ++k) mm[k] = (R)cf[{ci} + k];")
+        else:
+            ci = self.cf(m)
+            self.emit(f"      C mm[16]; for (int k = 0; k < 16; ++k) mm[k] = toC(cfz(cf, {ci} + 2 * k));")
+        for s in range(A):
+            if s & ((1 << ih) | (1 << il)) or (s & rmask) != rval:
+                continue
+            idx = [s, s | (1 << il), s | (1 << ih), s | (1 << ih) | (1 << il)]
+            self.emit("      { const C x0 = v%d, x1 = v%d, x2 = v%d, x3 = v%d;" % tuple(idx))
+            for r in range(4):
+                if kind == 1:
+                    self.emit(f"        {{ C y; y.x = mm[{4*r}] * x0.x; y.y = mm[{4*r}] * x0.y;"
+                              f" y.x = fma(mm[{4*r+1}], x1.x, y.x); y.y = fma(mm[{4*r+1}], x1.y, y.y);"
+                              f" y.x = fma(mm[{4*r+2}], x2.x, y.x); y.y = fma(mm[{4*r+2}], x2.y, y.y);"
+                              f" y.x = fma(mm[{4*r+3}], x3.x, y.x); y.y = fma(mm[{4*r+3}], x3.y, y.y); v{idx[r]} = y; }}")
+                else:
+                    terms = []
+                    for c in range(4):
+                        mc = f"mm[{4*r+c}]"
+                        xc = f"x{c}"
+                        if c == 0:
+                            terms.append(f"C y = cm({mc}, {xc});")
+                        else:
+                            terms.append(f"y.x = fma({mc}.x, {xc}.x, y.x); y.x = fma(-{mc}.y, {xc}.y, y.x);"
+                                         f" y.y = fma({mc}.x, {xc}.y, y.y); y.y = fma({mc}.y, {xc}.x, y.y);")
+                    self.emit("        { " + " ".join(terms) + f" v{idx[r]} = y; }}")
+            self.emit("      }")
+        if gmask:
+            self.emit("    }")
+        self.emit("    }")
+
+    def gen_pivot(self, a):
+        w, A, TB = self.w, self.A, self.TB
+        slot, ptype, pval, use_rt, ne = w[a:a + 5]
+        nb = 1 << (TB - 4)
+        ta_w = w[a + 5 + 3 * ne:a + 5 + 3 * ne + 32]
+        tb_w = w[a + 5 + 3 * ne + 32:a + 5 + 3 * ne + 32 + 2 * nb]
+        rt_w = w[a + 5 + 3 * ne + 32 + 2 * nb:a + 5 + 3 * ne + 32 + 2 * nb + 2 * A]
+        ta = [complex(_w2d(ta_w[2 * k]), _w2d(ta_w[2 * k + 1])) for k in range(16)]
+        tb = [complex(_w2d(tb_w[2 * k]), _w2d(tb_w[2 * k + 1])) for k in range(nb)]
+        rt = [complex(_w2d(rt_w[2 * k]), _w2d(rt_w[2 * k + 1])) for k in range(A)]
+        self.emit(f"    {{ // pivot {slot}")
+        if ptype == 1:
+            self.emit(f"    if (((base | gt{self.li}) & {pval}ull) != 0ull) {{")
+        ta_all_one = all(z == 1 for z in ta)
+        tb_all_one = all(z == 1 for z in tb)
+        self.emit(f"      double2 fd = sm.ep[it & 1][{slot}];")
+        if not ta_all_one:
+            ci = self.cf([x for z in ta for x in (z.real, z.imag)])
+            self.emit(f"      fd = dm(fd, cfz(cf, {ci} + 2 * (tid & 15)));")
+        if not tb_all_one:
+            ci = self.cf([x for z in tb for x in (z.real, z.imag)])
+            self.emit(f"      fd = dm(fd, cfz(cf, {ci} + 2 * (tid >> 4)));")
+        self.emit("      const C f = toC(fd);")
+        # which slots carry a register-partner factor (structure: RT entry != 1 from a partner bit)
+        rt_ci = None
+        if use_rt:
+            rt_ci = self.cf([x for z in rt for x in (z.real, z.imag)])
+        for s in range(A):
+            if ptype == 0 and not (s >> pval) & 1:
+                continue
+            if use_rt and rt[s] != 1:
+                self.emit(f"      v{s} = cm(v{s}, cm(f, toC(cfz(cf, {rt_ci + 2 * s}))));")
+            else:
+                self.emit(f"      v{s} = cm(v{s}, f);")
+        if ptype == 1:
+            self.emit("    }")
+        self.emit("    }")
+
+    def gen_parity(self, a):
+        w, A = self.w, self.A
+        s1, nd = w[a], w[a + 1]
+        pairs = [(w[a + 2 + 2 * q], w[a + 3 + 2 * q]) for q in range(nd)]
+        self.emit("    { // parity")
+        for s in range(A):
+            gi = f"(base | gt{self.li} | {self.lay['goff'][s]}ull)"
+            terms = []
+            if s1:
+                terms.append(f"__popcll(gi & {s1}ull)")
+            for d, m in pairs:
+                terms.append(f"__popcll(gi & (gi >> {d}) & {m}ull)")
+            self.emit(f"      {{ const u64 gi = {gi}; if (({' + '.join(terms)}) & 1) {{ v{s}.x = -v{s}.x; v{s}.y = -v{s}.y; }} }}")
+        self.emit("    }")
+
+    def gen_term(self, a):
+        w, A = self.w, self.A
+        mask, val = w[a], w[a + 1]
+        ci = self.cf([_w2d(w[a + 2]), _w2d(w[a + 3])])
+        self.emit(f"    {{ const C ph = toC(cfz(cf, {ci}));")
+        for s in range(A):
+            gi = f"(base | gt{self.li} | {self.lay['goff'][s]}ull)"
+            self.emit(f"      if (({gi} & {mask}ull) == {val}ull) v{s} = cm(v{s}, ph);")
+        self.emit("    }")
+
+    def _kernel(self, name, body, store):
+        K, n = self.K, self.n
+        real = "double" if self.dtype == nat.QSB_C128 else "float"
+        n_ext = n - K
+        base_terms = [f"((c >> {m}) & 1ull) << {self.ext_pos[m]}" for m in range(n_ext)]
+        out_terms = [f"((c >> {m}) & 1ull) << {self.ext_out[m]}" for m in range(n_ext)]
+        base_expr = " | ".join(base_terms) if base_terms else "0ull"
+        out_expr = " | ".join(out_terms) if (out_terms and self.ext_perm) else "base"
+        defs = (f"#define R {real}\n#define C {real}2\n#define KB {K}\n#define GB {self.G}\n#define STAGES {STAGES}\n"
+                f"#define CONSUMERS {CONSUMERS}\n#define MAXPIV {max(1, self.npiv)}\n#define NPIV {self.npiv}\n")
+        return defs + _PRELUDE + f"""
+extern "C" __global__ void __launch_bounds__({THREADS}, 1)
+{name}(const C* __restrict__ src, C* __restrict__ dst, const __grid_constant__ TMap tmap, const TmaPlan tp,
+       const double* __restrict__ cf) {{
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  const int tid = threadIdx.x;
+  if (tid == 0) {{
+    for (int s = 0; s < STAGES; ++s) {{ mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], CONSUMERS); }}
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }}
+  __syncthreads();
+  const u64 n_tiles = {1 << (n - K)}ull;
+  if (tid >= CONSUMERS) {{
+    const int lane = tid - CONSUMERS;
+    int it = 0;
+    for (u64 c = blockIdx.x; c < n_tiles; c += gridDim.x, ++it) {{
+      const int s = it % STAGES;
+      const u32 ph = (it / STAGES) & 1;
+      if (it >= STAGES) mbar_wait(&sm.empty[s], ph ^ 1);
+      if (lane == 0) {{
+        const u64 base = {base_expr};
+        sm.base[s][0] = base;
+        sm.base[s][1] = {out_expr};
+        mbar_expect_tx(&sm.full[s], (u32)((1u << KB) * sizeof(C)));
+        int co[5] = {{0, 0, 0, 0, 0}};
+        for (int g = 0; g < tp.n_gap; ++g) co[tp.gap_dim[g]] = (int)((base >> tp.gap_lo[g]) & ((1ull << tp.gap_nb[g]) - 1ull));
+        const int top0 = tp.top_dim >= 0 ? (int)(base >> tp.top_lo) : 0;
+        char* d = reinterpret_cast<char*>(&sm.stage[s][0]);
+        for (int k = 0; k < tp.n_calls; ++k) {{
+          if (tp.top_dim >= 0) co[tp.top_dim] = top0 + (int)tp.call_coord[k];
+          tma5(d + (u64)k * tp.call_bytes, &tmap, co, &sm.full[s]);
+        }}
+      }}
+      __syncwarp();
+    }}
+    return;
+  }}
+  int it = 0;
+  for (u64 c = blockIdx.x; c < n_tiles; c += gridDim.x, ++it) {{
+    const int s = it % STAGES;
+    const u32 ph = (it / STAGES) & 1;
+    mbar_wait(&sm.full[s], ph);
+    const u64 base = sm.base[s][0];
+    const u64 obase = sm.base[s][1];
+    C* buf = sm.stage[s];
+{body}
+    fence_async();
+    mbar_arrive(&sm.empty[s]);
+{store}
+  }}
+}}
+"""
+
+
+class _Compiled:
+    __slots__ = ("func", "name", "smem")
+
+
+_cache: dict = {}
+_lock = threading.Lock()
+_disabled = os.environ.get("QSB_JIT", "1") == "0"
+_avail = None
+
+
+def _nvrtc_path():
+    for p in ("/usr/local/cuda/lib64/libnvrtc.so.12",):
+        if os.path.exists(p):
+            return p
+    try:
+        import nvidia.cuda_nvrtc as m
+
+        base = list(m.__path__)[0]
+        p = os.path.join(base, "lib", "libnvrtc.so.12")
+        if os.path.exists(p):
+            return p
+    except Exception:
+        pass
+    return ""
+
+
+def available() -> bool:
+    global _avail
+    if _disabled:
+        return False
+    if _avail is None:
+        try:
+            _avail = bool(nat.lib().qsb_jit_available(_nvrtc_path().encode()))
+        except Exception:
+            _avail = False
+    return _avail
+
+
+def generate(words, dtype):
+    """(source, kernel name, coefficients) for a pass program (CPU-only, used by tests)."""
+    g = _Gen(words, dtype)
+    body_probe = g.generate("KNAME")
+    name = "qsb_pass_" + hashlib.sha1(body_probe.encode()).hexdigest()[:16]
+    src = body_probe.replace("KNAME", name)
+    return src, name, np.array(g.coeffs, dtype=np.float64)
+
+
+def smem_bytes(dtype) -> int:
+    K = 12 if dtype == nat.QSB_C128 else 13
+    amp = 16 if dtype == nat.QSB_C128 else 8
+    return STAGES * (1 << K) * amp + 2 * MAX_PIV * 16 + 8 * STAGES * 4 + 256
+
+
+def compile_words(words, dtype):
+    src, name, coeffs = generate(words, dtype)
+    with _lock:
+        hit = _cache.get(src)
+        if hit is None:
+            lib = nat.lib()
+            fn = ctypes.c_void_p()
+            log = ctypes.create_string_buffer(1 << 16)
+            rc = lib.qsb_jit_compile(src.encode(), name.encode(), _nvrtc_path().encode(), ctypes.byref(fn), log,
+                                     len(log))
+            if rc != 0:
+                raise RuntimeError(f"NVRTC failed: {log.value.decode(errors='replace')[:2000]}")
+            hit = _Compiled()
+            hit.func = fn.value
+            hit.name = name
+            hit.smem = smem_bytes(dtype)
+            _cache[src] = hit
+    return hit, coeffs
+
+
+def run(words, dtype, src_ptr, dst_ptr, n_qubits, stream_ptr, compiled=None, coeffs=None):
+    if compiled is None:
+        compiled, coeffs = compile_words(words, dtype)
+    nat.check(
+        nat.lib().qsb_jit_run_pass(compiled.func, src_ptr, dst_ptr, n_qubits, dtype, words.ctypes.data, len(words),
+                                   coeffs.ctypes.data if len(coeffs) else None, len(coeffs), THREADS,
+                                   compiled.smem, stream_ptr),
+        "jit_run_pass",
+    )

@@ -26,6 +26,7 @@ def _cplx(words, i):
 def run_program(psi_in: np.ndarray, words: np.ndarray, dtype=np.complex128) -> np.ndarray:
     w = [int(x) for x in words]
     K, NREG, n = w[2], w[3], w[4]
+    TB = K - NREG  # thread bits
     A = 1 << NREG
     n_tiles = w[6]
     flags = w[7]
@@ -74,7 +75,7 @@ def run_program(psi_in: np.ndarray, words: np.ndarray, dtype=np.complex128) -> n
             a = p + 2
             if op == OP_LAYOUT:
                 R = w[a:a + NREG]
-                Tb = w[a + NREG:a + NREG + 8]
+                Tb = w[a + NREG:a + NREG + TB]
                 slot = np.zeros_like(J)
                 for i, b in enumerate(R):
                     slot |= jbits[b] << i
@@ -83,9 +84,9 @@ def run_program(psi_in: np.ndarray, words: np.ndarray, dtype=np.complex128) -> n
                     tid |= jbits[b] << i
                 gthr = np.zeros_like(J)
                 for i, b in enumerate(Tb):
-                    gthr |= jbits[b] << w[a + NREG + 8 + A + i]
-                reg_ooff = w[a + NREG + 8 + A + 8:a + NREG + 8 + A + 8 + A]
-                thr_opos = w[a + NREG + 8 + 2 * A + 8:a + NREG + 8 + 2 * A + 16]
+                    gthr |= jbits[b] << w[a + NREG + TB + A + i]
+                reg_ooff = w[a + NREG + TB + A + TB:a + NREG + TB + A + TB + A]
+                thr_opos = w[a + NREG + TB + 2 * A + TB:a + NREG + TB + 2 * A + 2 * TB]
                 lay = dict(R=R, Tb=Tb, slot=slot, tid=tid, gthr=gthr, reg_ooff=reg_ooff, thr_opos=thr_opos)
             elif op in (OP_G1, OP_G2):
                 if op == OP_G1:
@@ -119,9 +120,10 @@ def run_program(psi_in: np.ndarray, words: np.ndarray, dtype=np.complex128) -> n
                     v[idx] = mat @ v[idx]
             elif op == OP_PIVOT:
                 slotn, ptype, pval, use_rt, ne = w[a:a + 5]
+                nb = 1 << (TB - 4)
                 ta = w[a + 5 + 3 * ne:a + 5 + 3 * ne + 32]
-                tb = w[a + 5 + 3 * ne + 32:a + 5 + 3 * ne + 64]
-                rt = w[a + 5 + 3 * ne + 64:a + 5 + 3 * ne + 64 + 2 * A]
+                tb = w[a + 5 + 3 * ne + 32:a + 5 + 3 * ne + 32 + 2 * nb]
+                rt = w[a + 5 + 3 * ne + 32 + 2 * nb:a + 5 + 3 * ne + 32 + 2 * nb + 2 * A]
                 if ptype == 0:
                     act = ((lay["slot"] >> pval) & 1) == 1
                 else:
@@ -129,7 +131,7 @@ def run_program(psi_in: np.ndarray, words: np.ndarray, dtype=np.complex128) -> n
                 tid = lay["tid"]
                 e = ep[slotn]
                 taa = np.array([_cplx(ta, 2 * k) for k in range(16)])
-                tba = np.array([_cplx(tb, 2 * k) for k in range(16)])
+                tba = np.array([_cplx(tb, 2 * k) for k in range(nb)])
                 rta = np.array([_cplx(rt, 2 * k) for k in range(A)])
                 f = e * (taa[tid & 15] * tba[tid >> 4])
                 f = f.astype(dtype)
@@ -164,7 +166,7 @@ def run_program(psi_in: np.ndarray, words: np.ndarray, dtype=np.complex128) -> n
         tid = lay["tid"]
         reg_ooff = np.array(lay["reg_ooff"], dtype=np.int64)
         thr_o = np.zeros_like(J)
-        for i in range(8):
+        for i in range(TB):
             thr_o |= ((tid >> i) & 1) << lay["thr_opos"][i]
         oidx = obase | thr_o | reg_ooff[slot]
         out[oidx] = v

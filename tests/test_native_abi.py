@@ -58,3 +58,22 @@ def test_product_never_imports_the_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_pass_programs_pass_the_library_header_check():
+    # without a GPU the call must get past program validation and fail only at the first
+    # CUDA call (status QSB_ERR_CUDA = 4), proving planner and kernel agree on the format
+    import torch
+
+    from paper_2009_01845_b200 import _native, qft_circuit
+    from paper_2009_01845_b200.fusion import PassStep, plan_circuit
+
+    if torch.cuda.is_available():
+        return
+    lib = _native.load_library()
+    for dt in (_native.QSB_C128, _native.QSB_C64):
+        plan = plan_circuit(qft_circuit(16).queue, 16, dt)
+        for s in plan.steps:
+            if isinstance(s, PassStep):
+                rc = lib.qsb_run_pass(None, None, 16, dt, s.words.ctypes.data, len(s.words), None)
+                assert rc == 4, lib.qsb_last_error()
