@@ -33,7 +33,7 @@ OP_END, OP_LAYOUT, OP_G1, OP_G2, OP_PIVOT, OP_PARITY, OP_TERM, OP_SCALE = range(
 G_COMPLEX, G_REAL, G_SWAPX = 0, 1, 2
 H_TILEPOS = 16
 MAX_PROG_WORDS = 6144
-MAX_PIVOTS = 64
+MAX_PIVOTS = 32  # one producer lane per pivot computes its per-tile external factor
 THREAD_BITS = 9  # 512 consumer threads per CTA: 5 lane bits + 4 warp bits
 
 

@@ -27,7 +27,7 @@ H_TILEPOS = 16
 CONSUMERS = 512
 THREADS = CONSUMERS + 32
 STAGES = 2
-MAX_PIV = 64
+MAX_PIV = 32
 
 
 def _w2d(w):
@@ -59,7 +59,7 @@ __device__ __forceinline__ void fence_async() { asm volatile("fence.proxy.async.
 __device__ __forceinline__ C cm(C a, C b) { C r; r.x = a.x * b.x - a.y * b.y; r.y = a.x * b.y + a.y * b.x; return r; }
 __device__ __forceinline__ double2 dm(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
-__device__ __forceinline__ double2 cfz(const double* __restrict__ cf, int k) { return make_double2(cf[k], cf[k + 1]); }
+__device__ __forceinline__ double2 cfz(const double* cf, int k) { return make_double2(cf[k], cf[k + 1]); }
 __device__ __forceinline__ C toC(double2 z) { C r; r.x = (R)z.x; r.y = (R)z.y; return r; }
 __device__ __forceinline__ u32 swz(u32 j) {
   u32 f = 0;
@@ -67,7 +67,7 @@ __device__ __forceinline__ u32 swz(u32 j) {
   for (int s = GB; s < KB; s += GB) f ^= (j >> s);
   return j ^ (f & ((1u << GB) - 1u));
 }
-struct Smem { C stage[STAGES][1 << KB]; double2 ep[2][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 base[STAGES][2]; };
+struct Smem { C stage[STAGES][1 << KB]; C tbuf[1 << KB]; double2 ep[4][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 base[STAGES][2]; };
 """
 
 
@@ -149,30 +149,34 @@ class _Gen:
                 piv_ops.append(q)
             q += w[q + 1]
         self.npiv = len(piv_ops)
-        body_start = len(self.lines)
-        # external pivot factors: thread t computes pivot t's product over external partners
+        # external pivot factors: producer lane p computes pivot p's product over the partner
+        # bits outside the tile (per tile, one stage ahead of the consumers)
+        ep = []
         if piv_ops:
-            self.emit("    if (tid < NPIV) {")
-            self.emit("      double2 f = make_double2(1.0, 0.0);")
-            self.emit("      switch (tid) {")
+            ep.append("        if (lane < NPIV) {")
+            ep.append("          double2 f = make_double2(1.0, 0.0);")
+            ep.append("          switch (lane) {")
             for q in piv_ops:
                 a = q + 2
                 slot, ne = w[a], w[a + 4]
-                self.emit(f"        case {slot}: {{")
+                ep.append(f"            case {slot}: {{")
                 for k in range(ne):
                     bit = w[a + 5 + 3 * k]
                     ci = self.cf([_w2d(w[a + 6 + 3 * k]), _w2d(w[a + 7 + 3 * k])])
-                    self.emit(f"          if ((base >> {bit}) & 1ull) f = dm(f, cfz(cf, {ci}));")
-                self.emit("          break; }")
-            self.emit("      }")
-            self.emit("      sm.ep[it & 1][tid] = f;")
-            self.emit("    }")
+                    ep.append(f"              if ((base >> {bit}) & 1ull) f = dm(f, cfz(scf, {ci}));")
+                ep.append("              break; }")
+            ep.append("          }")
+            ep.append("          sm.ep[it & 3][lane] = f;")
+            ep.append("        }")
+        self.ep_code = "\n".join(ep)
+        body_start = len(self.lines)
         # initial load (natural order stage)
         self.set_layout(first, 0)
         for s in range(A):
             self.emit(f"    C v{s} = buf[jt0 | {first['jt'][s]}u];")
-        self.emit("    csync();")
-        swizzled = False
+        # the stage is consumed: hand it back to the producer before any compute
+        self.emit("    fence_async();")
+        self.emit("    mbar_arrive(&sm.empty[s]);")
         q = p + w[p + 1]
         li = 0
         while w[q] != OP_END:
@@ -181,19 +185,17 @@ class _Gen:
             if op == OP_LAYOUT:
                 new = self.parse_layout(a)
                 li += 1
-                if swizzled:
-                    self.emit("    csync();")
+                self.emit("    csync();")
                 self.emit("    { const u32 sj = swz(jt%d);" % self.li)
                 for s in range(A):
-                    self.emit(f"      buf[sj ^ {self.swz_const(self.lay['jt'][s])}u] = v{s};")
+                    self.emit(f"      sm.tbuf[sj ^ {self.swz_const(self.lay['jt'][s])}u] = v{s};")
                 self.emit("    }")
                 self.emit("    csync();")
                 self.set_layout(new, li)
                 self.emit("    { const u32 sj = swz(jt%d);" % li)
                 for s in range(A):
-                    self.emit(f"      v{s} = buf[sj ^ {self.swz_const(new['jt'][s])}u];")
+                    self.emit(f"      v{s} = sm.tbuf[sj ^ {self.swz_const(new['jt'][s])}u];")
                 self.emit("    }")
-                swizzled = True
             elif op == OP_G1:
                 self.gen_g1(a)
             elif op == OP_G2:
@@ -206,7 +208,7 @@ class _Gen:
                 self.gen_term(a)
             elif op == OP_SCALE:
                 ci = self.cf([_w2d(w[a]), _w2d(w[a + 1])])
-                self.emit(f"    {{ const C ph = toC(cfz(cf, {ci}));")
+                self.emit(f"    {{ const C ph = toC(cfz(scf, {ci}));")
                 for s in range(A):
                     self.emit(f"      v{s} = cm(v{s}, ph);")
                 self.emit("    }")
@@ -228,11 +230,11 @@ class _Gen:
             self.emit(f"    if (((base | gt{self.li}) & {gmask}ull) == {gval}ull) {{")
         if kind == 1:
             ci = self.cf([m[0], m[2], m[4], m[6]])
-            self.emit(f"      const R a00 = (R)cf[{ci}], a01 = (R)cf[{ci + 1}], a10 = (R)cf[{ci + 2}], a11 = (R)cf[{ci + 3}];")
+            self.emit(f"      const R a00 = (R)scf[{ci}], a01 = (R)scf[{ci + 1}], a10 = (R)scf[{ci + 2}], a11 = (R)scf[{ci + 3}];")
         elif kind == 0:
             ci = self.cf(m)
             for r, nm in enumerate(("a00", "a01", "a10", "a11")):
-                self.emit(f"      const C {nm} = toC(cfz(cf, {ci + 2 * r}));")
+                self.emit(f"      const C {nm} = toC(cfz(scf, {ci + 2 * r}));")
         for s in range(A):
             if s & (1 << ib) or (s & rmask) != rval:
                 continue
@@ -264,10 +266,10 @@ class _Gen:
             self.emit(f"    if (((base | gt{self.li}) & {gmask}ull) == {gval}ull) {{")
         if kind == 1:
             ci = self.cf([m[2 * k] for k in range(16)])
-            self.emit(f"      R mm[16]; for (int k = 0; k < 16; ++k) mm[k] = (R)cf[{ci} + k];")
+            self.emit(f"      R mm[16]; for (int k = 0; k < 16; ++k) mm[k] = (R)scf[{ci} + k];")
         else:
             ci = self.cf(m)
-            self.emit(f"      C mm[16]; for (int k = 0; k < 16; ++k) mm[k] = toC(cfz(cf, {ci} + 2 * k));")
+            self.emit(f"      C mm[16]; for (int k = 0; k < 16; ++k) mm[k] = toC(cfz(scf, {ci} + 2 * k));")
         for s in range(A):
             if s & ((1 << ih) | (1 << il)) or (s & rmask) != rval:
                 continue
@@ -310,13 +312,13 @@ class _Gen:
             self.emit(f"    if (((base | gt{self.li}) & {pval}ull) != 0ull) {{")
         ta_all_one = all(z == 1 for z in ta)
         tb_all_one = all(z == 1 for z in tb)
-        self.emit(f"      double2 fd = sm.ep[it & 1][{slot}];")
+        self.emit(f"      double2 fd = sm.ep[it & 3][{slot}];")
         if not ta_all_one:
             ci = self.cf([x for z in ta for x in (z.real, z.imag)])
-            self.emit(f"      fd = dm(fd, cfz(cf, {ci} + 2 * (tid & 15)));")
+            self.emit(f"      fd = dm(fd, cfz(scf, {ci} + 2 * (tid & 15)));")
         if not tb_all_one:
             ci = self.cf([x for z in tb for x in (z.real, z.imag)])
-            self.emit(f"      fd = dm(fd, cfz(cf, {ci} + 2 * (tid >> 4)));")
+            self.emit(f"      fd = dm(fd, cfz(scf, {ci} + 2 * (tid >> 4)));")
         self.emit("      const C f = toC(fd);")
         # which slots carry a register-partner factor (structure: RT entry != 1 from a partner bit)
         rt_ci = None
@@ -326,7 +328,7 @@ class _Gen:
             if ptype == 0 and not (s >> pval) & 1:
                 continue
             if use_rt and rt[s] != 1:
-                self.emit(f"      v{s} = cm(v{s}, cm(f, toC(cfz(cf, {rt_ci + 2 * s}))));")
+                self.emit(f"      v{s} = cm(v{s}, cm(f, toC(cfz(scf, {rt_ci + 2 * s}))));")
             else:
                 self.emit(f"      v{s} = cm(v{s}, f);")
         if ptype == 1:
@@ -352,7 +354,7 @@ class _Gen:
         w, A = self.w, self.A
         mask, val = w[a], w[a + 1]
         ci = self.cf([_w2d(w[a + 2]), _w2d(w[a + 3])])
-        self.emit(f"    {{ const C ph = toC(cfz(cf, {ci}));")
+        self.emit(f"    {{ const C ph = toC(cfz(scf, {ci}));")
         for s in range(A):
             gi = f"(base | gt{self.li} | {self.lay['goff'][s]}ull)"
             self.emit(f"      if (({gi} & {mask}ull) == {val}ull) v{s} = cm(v{s}, ph);")
@@ -367,14 +369,17 @@ class _Gen:
         base_expr = " | ".join(base_terms) if base_terms else "0ull"
         out_expr = " | ".join(out_terms) if (out_terms and self.ext_perm) else "base"
         defs = (f"#define R {real}\n#define C {real}2\n#define KB {K}\n#define GB {self.G}\n#define STAGES {STAGES}\n"
-                f"#define CONSUMERS {CONSUMERS}\n#define MAXPIV {max(1, self.npiv)}\n#define NPIV {self.npiv}\n")
+                f"#define CONSUMERS {CONSUMERS}\n#define MAXPIV {MAX_PIV}\n#define NPIV {self.npiv}\n"
+                f"#define NCOEF {len(self.coeffs)}\n")
         return defs + _PRELUDE + f"""
 extern "C" __global__ void __launch_bounds__({THREADS}, 1)
 {name}(const C* __restrict__ src, C* __restrict__ dst, const __grid_constant__ TMap tmap, const TmaPlan tp,
        const double* __restrict__ cf) {{
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  double* scf = reinterpret_cast<double*>(smem_raw + sizeof(Smem));
   const int tid = threadIdx.x;
+  for (int i = tid; i < NCOEF; i += {THREADS}) scf[i] = cf[i];
   if (tid == 0) {{
     for (int s = 0; s < STAGES; ++s) {{ mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], CONSUMERS); }}
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -388,8 +393,11 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1)
       const int s = it % STAGES;
       const u32 ph = (it / STAGES) & 1;
       if (it >= STAGES) mbar_wait(&sm.empty[s], ph ^ 1);
+      const u64 base = {base_expr};
+{self.ep_code}
+      __threadfence_block();
+      __syncwarp();
       if (lane == 0) {{
-        const u64 base = {base_expr};
         sm.base[s][0] = base;
         sm.base[s][1] = {out_expr};
         mbar_expect_tx(&sm.full[s], (u32)((1u << KB) * sizeof(C)));
@@ -415,8 +423,6 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1)
     const u64 obase = sm.base[s][1];
     C* buf = sm.stage[s];
 {body}
-    fence_async();
-    mbar_arrive(&sm.empty[s]);
 {store}
   }}
 }}
@@ -470,14 +476,20 @@ def generate(words, dtype):
     return src, name, np.array(g.coeffs, dtype=np.float64)
 
 
-def smem_bytes(dtype) -> int:
+MAX_COEFFS = 3072  # 24 KB of coefficients staged in shared memory
+
+
+def smem_bytes(dtype, n_coeffs=MAX_COEFFS) -> int:
     K = 12 if dtype == nat.QSB_C128 else 13
     amp = 16 if dtype == nat.QSB_C128 else 8
-    return STAGES * (1 << K) * amp + 2 * MAX_PIV * 16 + 8 * STAGES * 4 + 256
+    struct_bytes = (STAGES + 1) * (1 << K) * amp + 4 * MAX_PIV * 16 + 8 * STAGES * 4
+    return struct_bytes + 8 * n_coeffs + 128
 
 
 def compile_words(words, dtype):
     src, name, coeffs = generate(words, dtype)
+    if len(coeffs) > MAX_COEFFS:
+        raise RuntimeError(f"{len(coeffs)} coefficients exceed the shared-memory budget")
     with _lock:
         hit = _cache.get(src)
         if hit is None:
@@ -491,7 +503,7 @@ def compile_words(words, dtype):
             hit = _Compiled()
             hit.func = fn.value
             hit.name = name
-            hit.smem = smem_bytes(dtype)
+            hit.smem = smem_bytes(dtype, len(coeffs))
             _cache[src] = hit
     return hit, coeffs
 
