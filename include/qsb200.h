@@ -129,7 +129,14 @@ int qsb_cumsum_serial(const double* probs, uint64_t n, double* cum, void* stream
 int qsb_sample(const double* cum, uint64_t n, uint64_t state_hi, uint64_t state_lo,
                uint64_t inc_hi, uint64_t inc_lo, uint64_t n_shots, int64_t* samples, void* stream);
 
-/* ---- sharded execution helpers (sharding.py:84-111 reshuffle / _exchange_halves) -------- */
+/* ---- sharded execution helpers (sharding.py:53-111 partition / gather / _exchange_halves) - */
+/* dst[i'] = src[i] where bit b of i moves to bit dst_bit[b] of i' (moveaxis of partition /
+ * transpose of gather, sharding.py:65-70, 76-80). */
+int qsb_permute_qubits(const void* src, void* dst, int n_bits, int dtype, const int* dst_bit,
+                       void* stream);
+/* In-process exchange: swap a's half with local `bit` = 1 and b's half with `bit` = 0
+ * (sharding.py:100-111). */
+int qsb_exchange_halves(void* a, void* b, int n_local_bits, int dtype, int bit, void* stream);
 /* Copy the `half` (0 or 1) of a shard selected by local bit `bit` into / out of a contiguous
  * staging buffer, for elements [first, first + count) of that half in index order. */
 int qsb_pack_half(const void* shard, int n_local_bits, int dtype, int bit, int half,

@@ -424,6 +424,41 @@ __global__ void k_unpack_half(cplx<R>* __restrict__ s, int bit, int half, uint64
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// bit-permuting copy (partition / gather) and half exchange between two shards
+// ------------------------------------------------------------------------------------------
+struct BitPerm {
+  int n;
+  uint8_t dst_bit[64];  // destination bit of every source bit
+};
+
+// dst[perm(i)] = src[i]; consecutive threads read consecutive source amplitudes
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_permute(const cplx<R>* __restrict__ src, cplx<R>* __restrict__ dst,
+                                                      uint64_t total, const BitPerm p) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t i = (uint64_t)blockIdx.x * kThreads + threadIdx.x; i < total; i += stride) {
+    uint64_t j = 0;
+    for (int b = 0; b < p.n; ++b) j |= ((i >> b) & 1ull) << p.dst_bit[b];
+    dst[j] = src[i];
+  }
+}
+
+// swap a's half with bit=1 and b's half with bit=0 (sharding.py:100-111 _exchange_halves)
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_exchange_halves(cplx<R>* __restrict__ a, cplx<R>* __restrict__ b,
+                                                              uint64_t half, int bit) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  const uint64_t lowm = (1ull << bit) - 1ull;
+  for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < half; e += stride) {
+    const uint64_t base = ((e & ~lowm) << 1) | (e & lowm);
+    const uint64_t ia = base | (1ull << bit);
+    const cplx<R> t = a[ia];
+    a[ia] = b[base];
+    b[base] = t;
+  }
+}
+
 }  // namespace qsb
 
 using namespace qsb;
@@ -577,6 +612,53 @@ int qsb_vdot(const void* a, const void* b, uint64_t n, int dtype, double* out, v
                                                           static_cast<const float2*>(b), n, part);
   k_fold<double2><<<1, 1024, 0, st>>>(part, kRedBlocks, reinterpret_cast<double2*>(out));
   QSB_CHECK_LAUNCH("qsb_vdot");
+  return QSB_OK;
+}
+
+int qsb_permute_qubits(const void* src, void* dst, int n_bits, int dtype, const int* dst_bit, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  if (n_bits < 1 || n_bits > 40) {
+    set_error("qsb_permute_qubits: bad size");
+    return QSB_ERR_SHAPE;
+  }
+  BitPerm p;
+  p.n = n_bits;
+  uint64_t seen = 0;
+  for (int b = 0; b < n_bits; ++b) {
+    if (dst_bit[b] < 0 || dst_bit[b] >= n_bits || ((seen >> dst_bit[b]) & 1ull)) {
+      set_error("qsb_permute_qubits: not a permutation");
+      return QSB_ERR_SHAPE;
+    }
+    seen |= 1ull << dst_bit[b];
+    p.dst_bit[b] = (uint8_t)dst_bit[b];
+  }
+  const uint64_t total = 1ull << n_bits;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    k_permute<double><<<stream_grid(total), kThreads, 0, st>>>(static_cast<const double2*>(src),
+                                                               static_cast<double2*>(dst), total, p);
+  else
+    k_permute<float><<<stream_grid(total), kThreads, 0, st>>>(static_cast<const float2*>(src),
+                                                              static_cast<float2*>(dst), total, p);
+  QSB_CHECK_LAUNCH("qsb_permute_qubits");
+  return QSB_OK;
+}
+
+int qsb_exchange_halves(void* a, void* b, int n_local_bits, int dtype, int bit, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  if (bit < 0 || bit >= n_local_bits) {
+    set_error("qsb_exchange_halves: bad bit");
+    return QSB_ERR_SHAPE;
+  }
+  const uint64_t half = 1ull << (n_local_bits - 1);
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    k_exchange_halves<double><<<stream_grid(half), kThreads, 0, st>>>(static_cast<double2*>(a),
+                                                                      static_cast<double2*>(b), half, bit);
+  else
+    k_exchange_halves<float><<<stream_grid(half), kThreads, 0, st>>>(static_cast<float2*>(a),
+                                                                     static_cast<float2*>(b), half, bit);
+  QSB_CHECK_LAUNCH("qsb_exchange_halves");
   return QSB_OK;
 }
 

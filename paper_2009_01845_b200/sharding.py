@@ -1,0 +1,627 @@
+"""Sharded execution over global qubits (drop-in for /root/reference/pkg/src/qsim/sharding.py).
+
+A state of n qubits with g global qubits is 2^g shards of 2^(n-g) amplitudes; shard s holds
+the amplitudes whose global-qubit bits spell s (global_qubits[0] = MSB of s), local qubits in
+significance order inside a shard -- sharding.py:30-81.
+
+Two placements share one runner:
+  * in-process (LocalComm): every shard is a separate HBM buffer of this GPU -- the reference's
+    logical devices (SPEC "workers"), used for n_shards > GPUs and for single-GPU parity runs;
+  * distributed (TorchComm): one shard per rank (one process per GPU), global<->local
+    exchanges as NCCL send/recv pairs over NVLink, chunked through bounded staging buffers.
+
+The schedule is the reference's: plan() picks the global qubits and Belady reshuffles with the
+same locality rules (sharding.py:141-216), so reshuffle counts match the reference exactly.
+Inside a LocalSegment every shard runs its own localised gate list through the fused pass
+engine (global controls become shard filters, diagonal gates on global qubits become local
+diagonals or a whole-shard phase, SWAPs with global qubits become half-shard exchanges or shard
+relabels -- sharding.py:219-320).
+"""
+
+from __future__ import annotations
+
+import bisect
+import math
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .circuit import Circuit
+from .errors import CapacityError, ShapeError, SimulationError
+from .fusion import NGate, diag_terms, normalize, plan_circuit
+from .gates import GateKind, gate_matrix
+from .state import Precision, StateVector, _check_cap, zero_state
+
+
+# ------------------------------------------------------------------------------------------
+# plan (reference semantics)
+# ------------------------------------------------------------------------------------------
+@dataclass
+class LocalSegment:
+    """Queue positions executable without moving any qubit."""
+
+    positions: list
+
+
+@dataclass
+class Reshuffle:
+    """Exchange one global qubit with one local qubit."""
+
+    global_qubit: int
+    local_qubit: int
+
+
+@dataclass
+class ExecutionPlan:
+    n_qubits: int
+    n_shards: int
+    global_qubits: tuple
+    steps: list = field(default_factory=list)
+
+    @property
+    def n_reshuffles(self) -> int:
+        return sum(1 for s in self.steps if isinstance(s, Reshuffle))
+
+
+def _kind(spec):
+    k = spec.kind
+    return k if isinstance(k, GateKind) else GateKind(getattr(k, "value", k))
+
+
+def _required_local(spec) -> tuple:
+    """Targets that must be local (sharding.py:141-149)."""
+    kind = _kind(spec)
+    if kind in (GateKind.CZ, GateKind.CZPOW):
+        return ()
+    if kind is GateKind.SWAP and not spec.controls:
+        return ()
+    if kind is GateKind.CNOT:
+        return (spec.targets[1],)
+    return tuple(spec.targets)
+
+
+def plan(circuit: Circuit, n_shards: int, global_qubits=None) -> ExecutionPlan:
+    """Global qubits = the g least-required qubits (ties to the higher index); Belady victims
+    for reshuffles (sharding.py:152-216)."""
+    n = circuit.n_qubits
+    if n_shards < 2 or n_shards & (n_shards - 1):
+        raise ShapeError(f"n_shards must be a power of two >= 2, got {n_shards}")
+    if n_shards > 1 << (n - 1):
+        raise CapacityError(f"{n_shards} shards exceed the cap of {1 << (n - 1)} for {n} qubits")
+    g = n_shards.bit_length() - 1
+    need = [_required_local(s) for s in circuit.queue]
+    if global_qubits is None:
+        count = [0] * n
+        for req in need:
+            for q in req:
+                count[q] += 1
+        order = sorted(range(n), key=lambda q: (count[q], -q))
+        global_qubits = tuple(sorted(order[:g]))
+    else:
+        global_qubits = tuple(global_qubits)
+        if len(global_qubits) != g or len(set(global_qubits)) != g:
+            raise ShapeError(f"{n_shards} shards need {g} distinct global qubits, got {global_qubits}")
+    uses = [[] for _ in range(n)]
+    for pos, req in enumerate(need):
+        for q in req:
+            uses[q].append(pos)
+
+    def next_use(q, pos):
+        i = bisect.bisect_left(uses[q], pos)
+        return uses[q][i] if i < len(uses[q]) else math.inf
+
+    glob = set(global_qubits)
+    steps, seg = [], []
+    for pos, req in enumerate(need):
+        blocked = [q for q in req if q in glob]
+        if blocked:
+            if len(req) > n - g:
+                raise CapacityError(
+                    f"gate at position {pos} needs {len(req)} local qubits but only {n - g} exist with {n_shards} shards"
+                )
+            if seg:
+                steps.append(LocalSegment(seg))
+                seg = []
+            for q in blocked:
+                cands = [c for c in range(n) if c not in glob and c not in req]
+                victim = max(cands, key=lambda c: (next_use(c, pos), c))
+                steps.append(Reshuffle(q, victim))
+                glob.remove(q)
+                glob.add(victim)
+        seg.append(pos)
+    if seg:
+        steps.append(LocalSegment(seg))
+    return ExecutionPlan(n, n_shards, global_qubits, steps)
+
+
+# ------------------------------------------------------------------------------------------
+# device backend (the product path) -- tests inject a CPU stand-in with the same methods
+# ------------------------------------------------------------------------------------------
+class CudaBackend:
+    def __init__(self, precision: Precision):
+        self.precision = precision
+        self.dtype = precision.qsb_dtype
+
+    def empty(self, n_amps):
+        torch = nat.torch_mod()
+        return torch.empty(n_amps, dtype=self.precision.torch_dtype, device=torch.device("cuda", torch.cuda.current_device()))
+
+    def zeros(self, n_amps):
+        t = self.empty(n_amps)
+        t.zero_()
+        return t
+
+    def run_local(self, shard, n_local, ngates, cache):
+        from . import engine
+
+        if not ngates:
+            return shard
+        key = tuple((g.kind, g.targets, g.controls, g.index, None if g.matrix is None else g.matrix.tobytes())
+                    for g in ngates)
+        plan_ = cache.get(key)
+        if plan_ is None:
+            plan_ = plan_circuit(ngates, n_local, self.dtype, allow_ext_perm=False)
+            cache[key] = plan_
+        holder = {}
+        view = _ShardView(shard, n_local, self.precision)
+        engine.run_plan(view, plan_, holder)
+        return view._t
+
+    def scale(self, shard, phase):
+        nat.check(nat.lib().qsb_scale(shard.data_ptr(), shard.numel(), self.dtype, phase.real, phase.imag,
+                                      nat.stream_ptr()), "shard phase")
+
+    def exchange_local(self, a, b, n_local, bit):
+        nat.check(nat.lib().qsb_exchange_halves(a.data_ptr(), b.data_ptr(), n_local, self.dtype, bit,
+                                                nat.stream_ptr()), "exchange_halves")
+
+    def pack(self, shard, n_local, bit, half, first, count, staging):
+        nat.check(nat.lib().qsb_pack_half(shard.data_ptr(), n_local, self.dtype, bit, half, first, count,
+                                          staging.data_ptr(), nat.stream_ptr()), "pack_half")
+
+    def unpack(self, shard, n_local, bit, half, first, count, staging):
+        nat.check(nat.lib().qsb_unpack_half(shard.data_ptr(), n_local, self.dtype, bit, half, first, count,
+                                            staging.data_ptr(), nat.stream_ptr()), "unpack_half")
+
+    def permute(self, src, n_bits, dst_bit):
+        out = self.empty(src.numel())
+        perm = np.ascontiguousarray(dst_bit, dtype=np.int32)
+        nat.check(nat.lib().qsb_permute_qubits(src.data_ptr(), out.data_ptr(), n_bits, self.dtype, perm.ctypes.data,
+                                               nat.stream_ptr()), "permute_qubits")
+        return out
+
+
+class _ShardView:
+    """Minimal StateVector-like wrapper so the fused engine runs on one shard buffer."""
+
+    def __init__(self, t, n, precision):
+        self._t = t
+        self.n_qubits = n
+        self.precision = precision
+
+    @property
+    def tensor(self):
+        return self._t
+
+    @property
+    def data_ptr(self):
+        return int(self._t.data_ptr())
+
+    @property
+    def n_amps(self):
+        return 1 << self.n_qubits
+
+
+# ------------------------------------------------------------------------------------------
+# communicators
+# ------------------------------------------------------------------------------------------
+class LocalComm:
+    """Every shard lives in this process."""
+
+    rank = 0
+    world = 1
+
+    def owns(self, shard_id, owner):
+        return True
+
+
+class TorchComm:
+    """One shard per rank over torch.distributed (NCCL on GPUs; gloo in the CPU tests)."""
+
+    CHUNK_BYTES = int(os.environ.get("QSB_EXCHANGE_CHUNK_BYTES", str(1 << 30)))
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def owns(self, shard_id, owner):
+        return owner[shard_id] == self.rank
+
+    def sendrecv(self, send, recv, peer):
+        dist = self.dist
+        ops = [dist.P2POp(dist.isend, send, peer, self.group), dist.P2POp(dist.irecv, recv, peer, self.group)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+    def all_gather(self, t):
+        out = [t.new_empty(t.shape) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return out
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
+# ------------------------------------------------------------------------------------------
+# sharded state
+# ------------------------------------------------------------------------------------------
+@dataclass
+class ShardedState:
+    """2^g shards addressed by the global-qubit bits (sharding.py:30-50).
+
+    `shards` maps logical shard id -> buffer for the shards this process holds; `owner` maps
+    every logical shard id to the rank holding it (relabels only permute this map)."""
+
+    n_qubits: int
+    global_qubits: tuple
+    shards: dict
+    precision: Precision = Precision.F64
+    local_qubits: tuple = ()
+    owner: list = field(default_factory=list)
+    comm: object = None
+    backend: object = None
+
+    def __post_init__(self):
+        if not self.local_qubits:
+            taken = set(self.global_qubits)
+            self.local_qubits = tuple(q for q in range(self.n_qubits) if q not in taken)
+        if not self.owner:
+            self.owner = [0] * (1 << len(self.global_qubits))
+        if self.comm is None:
+            self.comm = LocalComm()
+        if self.backend is None:
+            self.backend = CudaBackend(self.precision)
+
+    @property
+    def n_global(self):
+        return len(self.global_qubits)
+
+    @property
+    def n_local(self):
+        return self.n_qubits - self.n_global
+
+    def local_bit(self, q):
+        return self.n_local - 1 - self.local_qubits.index(q)
+
+    def shard_bit(self, q):
+        return self.n_global - 1 - self.global_qubits.index(q)
+
+
+def _stacked_to_canonical(n, global_qubits, local_qubits):
+    """dst bit (canonical, qubit q at n-1-q) of every bit of the stacked (shard, local) index."""
+    g = len(global_qubits)
+    nl = n - g
+    dst = [0] * n
+    for j, q in enumerate(global_qubits):
+        dst[n - 1 - j] = n - 1 - q
+    for m, q in enumerate(local_qubits):
+        dst[nl - 1 - m] = n - 1 - q
+    return dst
+
+
+def partition(state: StateVector, global_qubits, comm=None, backend=None) -> ShardedState:
+    """Copy a state into shards addressed by the global-qubit bits (sharding.py:53-71)."""
+    global_qubits = tuple(global_qubits)
+    g = len(global_qubits)
+    n = state.n_qubits
+    if not 1 <= g <= n - 1:
+        raise ShapeError(f"need between 1 and {n - 1} global qubits, got {g}")
+    if len(set(global_qubits)) != g:
+        raise ShapeError(f"duplicate global qubits {global_qubits}")
+    for q in global_qubits:
+        if not 0 <= q < n:
+            raise ShapeError(f"qubit {q} out of range for {n} qubits")
+    backend = backend or CudaBackend(state.precision)
+    comm = comm or LocalComm()
+    sh = ShardedState(n, global_qubits, {}, state.precision, comm=comm, backend=backend)
+    fwd = _stacked_to_canonical(n, global_qubits, sh.local_qubits)
+    inv = [0] * n
+    for b, d in enumerate(fwd):
+        inv[d] = b
+    stacked = backend.permute(state.tensor, n, inv)
+    nl = n - g
+    world = comm.world
+    for s in range(1 << g):
+        sh.owner[s] = (s * world) >> g
+        if comm.owns(s, sh.owner):
+            sh.shards[s] = stacked[s << nl:(s + 1) << nl].clone()
+    return sh
+
+
+def gather(sharded: ShardedState) -> StateVector:
+    """Reassemble the canonical state (sharding.py:74-81); distributed: on every rank."""
+    return StateVector(sharded.n_qubits, gather_tensor(sharded), sharded.precision)
+
+
+def gather_tensor(sharded: ShardedState):
+    """Canonical-order amplitudes of a sharded state as one buffer (on every rank)."""
+    n, g = sharded.n_qubits, sharded.n_global
+    nl = n - g
+    backend = sharded.backend
+    comm = sharded.comm
+    if isinstance(comm, LocalComm):
+        parts = [sharded.shards[s] for s in range(1 << g)]
+    else:
+        mine = [s for s in sharded.shards]
+        if len(mine) != 1:
+            raise SimulationError("distributed gather expects one shard per rank")
+        got = comm.all_gather(sharded.shards[mine[0]])
+        by_rank = {r: t for r, t in enumerate(got)}
+        parts = [by_rank[sharded.owner[s]] for s in range(1 << g)]
+    torch = nat.torch_mod()
+    stacked = torch.cat(parts)
+    _ = nl
+    return backend.permute(stacked, n, _stacked_to_canonical(n, sharded.global_qubits, sharded.local_qubits))
+
+
+def _exchange(sharded: ShardedState, j_bit, p_bit):
+    """Pairwise half exchange (sharding.py:100-111): shard s (jbit clear) trades its p=1 half
+    for shard s|jbit's p=0 half."""
+    g, nl = sharded.n_global, sharded.n_local
+    backend, comm = sharded.backend, sharded.comm
+    jmask = 1 << j_bit
+    if isinstance(comm, LocalComm):
+        for s in range(1 << g):
+            if not s & jmask:
+                backend.exchange_local(sharded.shards[s], sharded.shards[s | jmask], nl, p_bit)
+        return
+    half = 1 << (nl - 1)
+    itemsize = sharded.precision.itemsize
+    chunk = max(1, min(half, comm.CHUNK_BYTES // itemsize))
+    for s, buf in list(sharded.shards.items()):
+        partner_shard = s ^ jmask
+        peer = sharded.owner[partner_shard]
+        my_half = 1 if not s & jmask else 0
+        send = backend.empty(chunk)
+        recv = backend.empty(chunk)
+        for first in range(0, half, chunk):
+            cnt = min(chunk, half - first)
+            backend.pack(buf, nl, p_bit, my_half, first, cnt, send)
+            _sync_stream()
+            comm.sendrecv(send[:cnt], recv[:cnt], peer)
+            backend.unpack(buf, nl, p_bit, my_half, first, cnt, recv)
+
+
+def _sync_stream():
+    torch = nat.torch_mod()
+    if torch.cuda.is_available():
+        torch.cuda.current_stream().synchronize()
+
+
+def reshuffle(sharded: ShardedState, global_qubit: int, local_qubit: int):
+    """Swap the roles of a global and a local qubit in place (sharding.py:84-97)."""
+    gl = list(sharded.global_qubits)
+    lc = list(sharded.local_qubits)
+    j = gl.index(global_qubit)
+    m = lc.index(local_qubit)
+    _exchange(sharded, sharded.n_global - 1 - j, sharded.n_local - 1 - m)
+    gl[j], lc[m] = local_qubit, global_qubit
+    sharded.global_qubits = tuple(gl)
+    sharded.local_qubits = tuple(lc)
+
+
+# ------------------------------------------------------------------------------------------
+# runner
+# ------------------------------------------------------------------------------------------
+class _Runner:
+    def __init__(self, sharded: ShardedState, cache: dict | None = None):
+        self.sh = sharded
+        self.pending = {s: [] for s in sharded.shards}
+        self.cache: dict = {} if cache is None else cache
+
+    def flush(self):
+        sh = self.sh
+        for s, gates in self.pending.items():
+            if gates:
+                sh.shards[s] = sh.backend.run_local(sh.shards[s], sh.n_local, gates, self.cache)
+                gates.clear()
+
+    def _shard_value(self, s, q):
+        return (s >> self.sh.shard_bit(q)) & 1
+
+    def apply(self, spec, index):
+        sh = self.sh
+        kind = _kind(spec)
+        targets, controls = tuple(spec.targets), tuple(spec.controls)
+        glob = set(sh.global_qubits)
+        if kind is GateKind.SWAP and not controls and (set(targets) & glob):
+            self.flush()
+            self._swap(targets)
+            return
+        m = gate_matrix(spec)
+        is_diag = not np.count_nonzero(m - np.diag(np.diagonal(m)))
+        if kind is GateKind.CNOT and targets[0] in glob:
+            # first target acts as a control (sharding.py:253-256)
+            targets, controls = targets[1:], controls + targets[:1]
+            m = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+            is_diag = False
+        for s in self.pending:
+            if any(self._shard_value(s, c) == 0 for c in controls if c in glob):
+                continue
+            lctrl = tuple(c for c in controls if c not in glob)
+            if is_diag:
+                self._diag_on_shard(s, targets, lctrl, np.diagonal(m), index)
+            else:
+                if set(targets) & glob:
+                    raise SimulationError(f"gate at {index} targets a global qubit; the plan should have reshuffled")
+                g = self._local_ngate(targets, lctrl, m, index)
+                if g is not None:
+                    self.pending[s].append(g)
+
+    def _local_ngate(self, targets, controls, m, index):
+        sh = self.sh
+        tb = tuple(sh.local_bit(q) for q in targets)
+        cb = tuple(sh.local_bit(q) for q in controls)
+
+        class _Spec:  # normalize() takes any object with the GateSpec attributes
+            pass
+
+        spec = _Spec()
+        spec.kind = GateKind.UNITARY
+        spec.targets = tuple(sh.n_local - 1 - b for b in tb)
+        spec.controls = tuple(sh.n_local - 1 - b for b in cb)
+        spec.params = ()
+        spec.matrix = m
+        return normalize(spec, sh.n_local, index)
+
+    def _diag_on_shard(self, s, targets, lctrl, d, index):
+        sh = self.sh
+        glob = set(sh.global_qubits)
+        t = len(targets)
+        loc_t = [q for q in targets if q not in glob]
+        # rows of the diagonal consistent with this shard's global target bits
+        sub = []
+        for j in range(1 << t):
+            ok = True
+            for i, q in enumerate(targets):
+                if q in glob and ((j >> (t - 1 - i)) & 1) != self._shard_value(s, q):
+                    ok = False
+                    break
+            if ok:
+                sub.append(d[j])
+        sub = np.array(sub, dtype=np.complex128)
+        if not loc_t:
+            phase = complex(sub[0])
+            if lctrl:
+                dd = np.ones(2, dtype=np.complex128)
+                dd[1] = phase
+                q0, rest = lctrl[0], lctrl[1:]
+                g = self._local_ngate((q0,), rest, np.diag(dd), index)
+                if g is not None:
+                    self.pending[s].append(g)
+            elif phase != 1.0:
+                self.flush_one(s)
+                sh.backend.scale(sh.shards[s], phase)
+            return
+        g = self._local_ngate(tuple(loc_t), lctrl, np.diag(sub), index)
+        if g is not None:
+            self.pending[s].append(g)
+
+    def flush_one(self, s):
+        sh = self.sh
+        if self.pending[s]:
+            sh.shards[s] = sh.backend.run_local(sh.shards[s], sh.n_local, self.pending[s], self.cache)
+            self.pending[s] = []
+
+    def _swap(self, targets):
+        sh = self.sh
+        a, b = targets
+        glob = set(sh.global_qubits)
+        if a in glob and b in glob:
+            # shard relabel, no data movement (sharding.py:315-320)
+            ja, jb = 1 << sh.shard_bit(a), 1 << sh.shard_bit(b)
+            new_shards, new_owner = dict(sh.shards), list(sh.owner)
+            for s in range(1 << sh.n_global):
+                if bool(s & ja) != bool(s & jb):
+                    t = s ^ ja ^ jb
+                    new_owner[s] = sh.owner[t]
+                    if t in sh.shards:
+                        new_shards[s] = sh.shards[t]
+                    elif s in new_shards and s not in sh.shards:
+                        pass
+            # keep only the shards this rank holds under the new labelling
+            held = {s: new_shards[s] for s in range(1 << sh.n_global)
+                    if sh.comm.owns(s, new_owner) and s in new_shards}
+            sh.shards = held
+            sh.owner = new_owner
+            self.pending = {s: [] for s in sh.shards}
+            return
+        g_q, l_q = (a, b) if a in glob else (b, a)
+        # the reshuffle data movement without the label swap is the gate (sharding.py:302-314)
+        _exchange(sh, sh.shard_bit(g_q), sh.local_bit(l_q))
+
+
+def _make_sharded(state, global_qubits, comm, backend, precision, n):
+    if state is not None:
+        return partition(state, global_qubits, comm, backend)
+    # |0..0> built shard by shard (no full state ever materialised)
+    g = len(global_qubits)
+    sh = ShardedState(n, tuple(global_qubits), {}, precision, comm=comm, backend=backend)
+    nl = n - g
+    for s in range(1 << g):
+        sh.owner[s] = (s * comm.world) >> g
+        if comm.owns(s, sh.owner):
+            t = backend.zeros(1 << nl)
+            if s == 0:
+                t[0] = 1.0
+            sh.shards[s] = t
+    return sh
+
+
+def run_sharded(circuit: Circuit, n_shards: int, initial: StateVector | None = None,
+                precision: Precision = Precision.F64, global_qubits=None, comm=None, backend=None,
+                cache: dict | None = None, exec_plan: ExecutionPlan | None = None) -> ShardedState:
+    """Plan + execute; returns the ShardedState (no gather).  `cache` keeps the per-shard fused
+    plans (and their compiled kernels) across calls with the same circuit."""
+    exec_plan = exec_plan or plan(circuit, n_shards, global_qubits)
+    comm = comm or LocalComm()
+    backend = backend or CudaBackend(precision if initial is None else initial.precision)
+    prec = precision if initial is None else initial.precision
+    sh = _make_sharded(initial, exec_plan.global_qubits, comm, backend, prec, circuit.n_qubits)
+    runner = _Runner(sh, cache)
+    for step in exec_plan.steps:
+        if isinstance(step, Reshuffle):
+            runner.flush()
+            reshuffle(sh, step.global_qubit, step.local_qubit)
+        else:
+            for pos in step.positions:
+                runner.apply(circuit.queue[pos], pos)
+    runner.flush()
+    return sh
+
+
+def _dist_comm_for(n_shards):
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() == n_shards:
+            return TorchComm()
+    except Exception:
+        pass
+    return LocalComm()
+
+
+def execute_sharded(circuit: Circuit, n_shards: int, n_workers: int = 1, initial: StateVector | None = None,
+                    precision: Precision = Precision.F64, global_qubits=None) -> StateVector:
+    """Run a circuit over n_shards shards; result equals Circuit.execute (sharding.py:323-364).
+
+    When torch.distributed is initialised with world_size == n_shards, each rank holds one
+    shard and exchanges go over NCCL; otherwise the shards are in-process HBM buffers."""
+    if n_workers < 1:
+        raise ShapeError(f"n_workers must be >= 1, got {n_workers}")
+    if n_shards == 1:
+        return circuit.execute(initial, precision=precision)
+    if initial is not None and initial.n_qubits != circuit.n_qubits:
+        raise ShapeError(f"initial state has {initial.n_qubits} qubits, circuit has {circuit.n_qubits}")
+    comm = _dist_comm_for(n_shards)
+    sh = run_sharded(circuit, n_shards, initial, precision, global_qubits, comm)
+    return gather(sh)
+
+
+def execute_distributed(circuit: Circuit, precision: Precision = Precision.F64, global_qubits=None,
+                        comm=None) -> ShardedState:
+    """One shard per rank of the initialised process group, |0..0> initial state, no gather
+    (states larger than one GPU: up to 36 qubits on 8 B200)."""
+    comm = comm or TorchComm()
+    return run_sharded(circuit, comm.world, None, precision, global_qubits, comm)
+
+
+__all__ = ["ExecutionPlan", "LocalSegment", "Reshuffle", "ShardedState", "execute_distributed", "execute_sharded",
+           "gather", "partition", "plan", "reshuffle"]
+_ = (_check_cap, zero_state, diag_terms, NGate)
