@@ -67,7 +67,7 @@ __device__ __forceinline__ u32 swz(u32 j) {
   for (int s = GB; s < KB; s += GB) f ^= (j >> s);
   return j ^ (f & ((1u << GB) - 1u));
 }
-struct Smem { C stage[STAGES][1 << KB]; C tbuf[1 << KB]; double2 ep[4][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 base[STAGES][2]; };
+struct Smem { C stage[STAGES][1 << KB]; C tbuf[1 << KB]; double2 ep[4][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 epbar[4]; u64 base[STAGES][2]; };
 """
 
 
@@ -88,6 +88,8 @@ class _Gen:
         self.ops0 = H_TILEPOS + 2 * n - K
         self.coeffs: list = []
         self.lines: list = []
+        self.ep_waited = False
+        self.h_scale = 0  # deferred 1/sqrt(2) factors of uncontrolled Hadamard butterflies
 
     # coefficient array (doubles); returns the index of the first entry
     def cf(self, values):
@@ -160,14 +162,33 @@ class _Gen:
                 a = q + 2
                 slot, ne = w[a], w[a + 4]
                 ep.append(f"            case {slot}: {{")
+                terms = []
                 for k in range(ne):
                     bit = w[a + 5 + 3 * k]
                     ci = self.cf([_w2d(w[a + 6 + 3 * k]), _w2d(w[a + 7 + 3 * k])])
-                    ep.append(f"              if ((base >> {bit}) & 1ull) f = dm(f, cfz(scf, {ci}));")
+                    nm = f"t{k}"
+                    ep.append(f"              const double2 {nm} = ((base >> {bit}) & 1ull) ? cfz(scf, {ci}) : make_double2(1.0, 0.0);")
+                    terms.append(nm)
+                # balanced product tree (depth log2) instead of a serial chain
+                lvl = 0
+                while len(terms) > 1:
+                    nxt = []
+                    for i in range(0, len(terms) - 1, 2):
+                        nm = f"u{lvl}_{i}"
+                        ep.append(f"              const double2 {nm} = dm({terms[i]}, {terms[i + 1]});")
+                        nxt.append(nm)
+                    if len(terms) % 2:
+                        nxt.append(terms[-1])
+                    terms = nxt
+                    lvl += 1
+                if terms:
+                    ep.append(f"              f = {terms[0]};")
                 ep.append("              break; }")
             ep.append("          }")
             ep.append("          sm.ep[it & 3][lane] = f;")
             ep.append("        }")
+            ep.append("        __syncwarp();")
+            ep.append("        if (lane == 0) mbar_arrive(&sm.epbar[it & 3]);")
         self.ep_code = "\n".join(ep)
         body_start = len(self.lines)
         # initial load (natural order stage)
@@ -217,6 +238,12 @@ class _Gen:
         # output offsets of the final layout
         lay = self.lay
         store = [f"    const u64 ot = obase | {self.thread_expr(lay['opos'], 64)};"]
+        if self.h_scale:
+            k = self.h_scale
+            scale = 2.0 ** (-(k // 2)) * (0.7071067811865476 if k % 2 else 1.0)
+            store.append(f"    const R hs = (R){scale!r};")
+            for s in range(A):
+                store.append(f"    v{s}.x *= hs; v{s}.y *= hs;")
         for s in range(A):
             store.append(f"    dst[ot | {lay['ooff'][s]}ull] = v{s};")
         return self._kernel(name, body, "\n".join(store))
@@ -225,6 +252,20 @@ class _Gen:
         w, A = self.w, self.A
         ib, kind, gmask, gval, rmask, rval = w[a:a + 6]
         m = [_w2d(x) for x in w[a + 6:a + 14]]
+        hh = 0.7071067811865475
+        if kind == 1 and not gmask and not rmask and m[0] == hh and m[2] == hh and m[4] == hh and m[6] == -hh \
+                and not any(m[1::2]):
+            # uncontrolled Hadamard: sum/difference butterfly, the 1/sqrt(2) is applied once at the store
+            self.h_scale += 1
+            self.emit(f"    {{ // H butterfly slot bit {ib}")
+            for s in range(A):
+                if s & (1 << ib):
+                    continue
+                t = s | (1 << ib)
+                self.emit(f"      {{ const C x0 = v{s}, x1 = v{t}; v{s}.x = x0.x + x1.x; v{s}.y = x0.y + x1.y;"
+                          f" v{t}.x = x0.x - x1.x; v{t}.y = x0.y - x1.y; }}")
+            self.emit("    }")
+            return
         self.emit(f"    {{ // G1 slot bit {ib} kind {kind}")
         if gmask:
             self.emit(f"    if (((base | gt{self.li}) & {gmask}ull) == {gval}ull) {{")
@@ -307,6 +348,9 @@ class _Gen:
         ta = [complex(_w2d(ta_w[2 * k]), _w2d(ta_w[2 * k + 1])) for k in range(16)]
         tb = [complex(_w2d(tb_w[2 * k]), _w2d(tb_w[2 * k + 1])) for k in range(nb)]
         rt = [complex(_w2d(rt_w[2 * k]), _w2d(rt_w[2 * k + 1])) for k in range(A)]
+        if not self.ep_waited:  # unconditional: every consumer thread waits once per tile
+            self.emit("    mbar_wait(&sm.epbar[it & 3], (it >> 2) & 1);")
+            self.ep_waited = True
         self.emit(f"    {{ // pivot {slot}")
         if ptype == 1:
             self.emit(f"    if (((base | gt{self.li}) & {pval}ull) != 0ull) {{")
@@ -382,6 +426,7 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1)
   for (int i = tid; i < NCOEF; i += {THREADS}) scf[i] = cf[i];
   if (tid == 0) {{
     for (int s = 0; s < STAGES; ++s) {{ mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], CONSUMERS); }}
+    for (int s = 0; s < 4; ++s) mbar_init(&sm.epbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }}
   __syncthreads();
@@ -394,9 +439,6 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1)
       const u32 ph = (it / STAGES) & 1;
       if (it >= STAGES) mbar_wait(&sm.empty[s], ph ^ 1);
       const u64 base = {base_expr};
-{self.ep_code}
-      __threadfence_block();
-      __syncwarp();
       if (lane == 0) {{
         sm.base[s][0] = base;
         sm.base[s][1] = {out_expr};
@@ -411,6 +453,7 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1)
         }}
       }}
       __syncwarp();
+{self.ep_code}
     }}
     return;
   }}
