@@ -155,35 +155,29 @@ class _Gen:
         # bits outside the tile (per tile, one stage ahead of the consumers)
         ep = []
         if piv_ops:
-            ep.append("        if (lane < NPIV) {")
-            ep.append("          double2 f = make_double2(1.0, 0.0);")
-            ep.append("          switch (lane) {")
+            # per-pivot partner tables in the coefficient array: [count, bits..., (re, im)...];
+            # lane p walks pivot p's table in a uniform loop (no divergent per-lane code paths)
+            tables = []
+            maxn = 1
             for q in piv_ops:
                 a = q + 2
                 slot, ne = w[a], w[a + 4]
-                ep.append(f"            case {slot}: {{")
-                terms = []
+                maxn = max(maxn, ne)
+                tables.append((slot, ne, a))
+            offs = [0] * len(tables)
+            for slot, ne, a in tables:
+                vals = [float(ne)] + [float(w[a + 5 + 3 * k]) for k in range(ne)]
                 for k in range(ne):
-                    bit = w[a + 5 + 3 * k]
-                    ci = self.cf([_w2d(w[a + 6 + 3 * k]), _w2d(w[a + 7 + 3 * k])])
-                    nm = f"t{k}"
-                    ep.append(f"              const double2 {nm} = ((base >> {bit}) & 1ull) ? cfz(scf, {ci}) : make_double2(1.0, 0.0);")
-                    terms.append(nm)
-                # balanced product tree (depth log2) instead of a serial chain
-                lvl = 0
-                while len(terms) > 1:
-                    nxt = []
-                    for i in range(0, len(terms) - 1, 2):
-                        nm = f"u{lvl}_{i}"
-                        ep.append(f"              const double2 {nm} = dm({terms[i]}, {terms[i + 1]});")
-                        nxt.append(nm)
-                    if len(terms) % 2:
-                        nxt.append(terms[-1])
-                    terms = nxt
-                    lvl += 1
-                if terms:
-                    ep.append(f"              f = {terms[0]};")
-                ep.append("              break; }")
+                    vals += [_w2d(w[a + 6 + 3 * k]), _w2d(w[a + 7 + 3 * k])]
+                offs[slot] = self.cf(vals)
+            offtab = self.cf([float(o) for o in offs])
+            ep.append("        if (lane < NPIV) {")
+            ep.append(f"          const int o = (int)scf[{offtab} + lane];")
+            ep.append("          const int cnt = (int)scf[o];")
+            ep.append("          double2 f = make_double2(1.0, 0.0);")
+            ep.append(f"          for (int k = 0; k < cnt; ++k) {{")
+            ep.append("            const int bit = (int)scf[o + 1 + k];")
+            ep.append("            if ((base >> bit) & 1ull) f = dm(f, cfz(scf, o + 1 + cnt + 2 * k));")
             ep.append("          }")
             ep.append("          sm.ep[it & 3][lane] = f;")
             ep.append("        }")
