@@ -90,11 +90,11 @@ int qsb_jit_available(const char* nvrtc_path);
 /* Compile CUDA C++ `source` for sm_100a and return the CUfunction `name` in *func_out. */
 int qsb_jit_compile(const char* source, const char* name, const char* nvrtc_path, void** func_out,
                     char* log_out, size_t log_cap);
-/* Launch a specialised pass kernel on the tile geometry of `program` (same word stream as
- * qsb_run_pass) with the per-launch gate coefficients `coeffs`. */
-int qsb_jit_run_pass(void* func, const void* src, void* dst, int n_qubits, int dtype,
-                     const int64_t* program, int64_t n_words, const double* coeffs, int64_t n_coeffs,
-                     int threads, int smem_bytes, void* stream);
+/* Launch a specialised pass kernel over `n_tiles` tiles.  `tma_desc` describes the state as the
+ * rank-5 tensor the kernel's tile loads address (15 words: rank, global dims[5], byte strides of
+ * dims 1..4, box dims[5]; jit.py tma_plan); `coeffs` are the per-launch gate coefficients. */
+int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tma_desc, uint64_t n_tiles,
+                     const double* coeffs, int64_t n_coeffs, int threads, int smem_bytes, void* stream);
 
 /* ---- reductions (state.py:109-122 norm / overlap) ---------------------------------------- */
 /* out[0] = sum |a_i|^2 (double, device pointer).  Deterministic two-level tree. */

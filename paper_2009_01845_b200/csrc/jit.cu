@@ -151,36 +151,38 @@ extern "C" int qsb_jit_compile(const char* source, const char* name, const char*
   return QSB_OK;
 }
 
-// Launch a JIT pass kernel: params (src, dst, tmap, tma plan, coefficients).  `program` is the
-// same word stream the interpreter takes (its header gives the tile geometry for the TMA plan).
-extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, int n_qubits, int dtype,
-                                const int64_t* program, int64_t n_words, const double* coeffs, int64_t n_coeffs,
-                                int threads, int smem_bytes, void* stream) {
+// Launch a JIT pass kernel: params (src, dst, tensor map, coefficients).  The tensor map is
+// encoded here from `tdesc` (jit.py tma_plan: rank, dims[5], byte strides[4], box[5]) over the
+// 8-byte elements of the state at `src`.
+extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tdesc, uint64_t n_tiles,
+                                const double* coeffs, int64_t n_coeffs, int threads, int smem_bytes, void* stream) {
   jit::Driver* dr = jit::driver();
   if (!dr || !func) {
     set_error("qsb_jit_run_pass: no driver / function");
     return QSB_ERR_CUDA;
   }
-  if (program[4] != n_qubits || program[5] != dtype) {
-    set_error("qsb_jit_run_pass: program built for another state");
+  if (!tdesc || tdesc[0] != 5 || n_tiles == 0) {
+    set_error("qsb_jit_run_pass: bad tile descriptor");
     return QSB_ERR_ARG;
   }
   cudaStream_t st = as_stream(stream);
-  const int K = (int)program[2];
   void* dcoef = nullptr;
   if (n_coeffs > 0) {
     if (int rc = pass::stage_words(coeffs, sizeof(double) * n_coeffs, &dcoef, st)) return rc;
   }
   alignas(64) CUtensorMap map;
   memset(&map, 0, sizeof map);
-  pass::TmaPlan tp;
-  pass::plan_tma(src, n_qubits, K, program + 16, dtype == QSB_C128 ? 16 : 8, &map, &tp);
-  if (tp.mode != 1) {
-    set_error("qsb_jit_run_pass: tile needs the bulk-copy fallback (use the interpreter)");
-    return QSB_ERR_ARG;
+  cuuint64_t gdim[5], gstride[4];
+  cuuint32_t box[5], estride[5];
+  for (int d = 0; d < 5; ++d) {
+    gdim[d] = (cuuint64_t)tdesc[1 + d];
+    box[d] = (cuuint32_t)tdesc[10 + d];
+    estride[d] = 1;
+    if (d < 4) gstride[d] = (cuuint64_t)tdesc[6 + d];
   }
+  if (int rc = pass::encode_tensor_map(&map, const_cast<void*>(src), gdim, gstride, box, estride)) return rc;
   CUfunction fn = reinterpret_cast<CUfunction>(func);
-  static CUfunction attr_done[64];
+  static CUfunction attr_done[256];
   static int n_attr = 0;
   bool seen = false;
   for (int i = 0; i < n_attr; ++i) seen |= attr_done[i] == fn;
@@ -190,17 +192,16 @@ extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, int n_qu
       set_error("cuFuncSetAttribute failed (%d)", (int)r);
       return QSB_ERR_CUDA;
     }
-    if (n_attr < 64) attr_done[n_attr++] = fn;
+    if (n_attr < 256) attr_done[n_attr++] = fn;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const uint64_t n_tiles = 1ull << (n_qubits - K);
   const unsigned grid = (unsigned)(n_tiles < (uint64_t)sms ? n_tiles : (uint64_t)sms);
   const void* a_src = src;
   void* a_dst = dst;
   const double* a_cf = static_cast<const double*>(dcoef);
-  void* args[] = {(void*)&a_src, (void*)&a_dst, (void*)&map, (void*)&tp, (void*)&a_cf};
+  void* args[] = {(void*)&a_src, (void*)&a_dst, (void*)&map, (void*)&a_cf};
   CUresult r = dr->launch(fn, grid, 1, 1, (unsigned)threads, 1, 1, (unsigned)smem_bytes, (CUstream)st, args, nullptr);
   if (r != CUDA_SUCCESS) {
     set_error("cuLaunchKernel failed (%d)", (int)r);

@@ -647,6 +647,23 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+int encode_tensor_map(CUtensorMap* map, void* base, const cuuint64_t* gdim, const cuuint64_t* gstride,
+                      const cuuint32_t* box, const cuuint32_t* estride) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return QSB_ERR_CUDA;
+  }
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, base, gdim, gstride, box, estride,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return QSB_ERR_ARG;
+  }
+  return QSB_OK;
+}
+
 // Describe the state as a rank-5 tensor of 8-byte elements whose box is one tile.
 void plan_tma(const void* src, int n, int K, const int64_t* tile_pos, int amp_bytes, CUtensorMap* map,
               TmaPlan* tp) {

@@ -30,6 +30,10 @@ struct TmaPlan {
 // tp->mode stays 0 (bulk-copy fallback) when no tensor map fits.
 void plan_tma(const void* src, int n, int K, const int64_t* tile_pos, int amp_bytes, CUtensorMap* map, TmaPlan* tp);
 
+// Encode a rank-5 FLOAT64 tiled tensor map (no swizzle, 256-B L2 promotion) over `base`.
+int encode_tensor_map(CUtensorMap* map, void* base, const cuuint64_t* gdim, const cuuint64_t* gstride,
+                      const cuuint32_t* box, const cuuint32_t* estride);
+
 // Stage `n` int64 words / doubles in a library-owned device ring (stream-ordered copies).
 int stage_words(const void* host, size_t bytes, void** device_out, cudaStream_t st);
 

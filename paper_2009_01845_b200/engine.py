@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _native as nat
 from . import jit
-from .fusion import GateStep, PassStep, Plan, plan_circuit
+from .fusion import GEOMETRY, GEOMETRY_JIT, GateStep, PassStep, Plan, compile_pass, plan_circuit
 
 # QSB_FUSION=0 disables pass fusion (every gate becomes its own kernel launch)
 FUSION_DEFAULT = os.environ.get("QSB_FUSION", "1") != "0"
@@ -28,11 +28,19 @@ def _free_bytes() -> int:
     return int(free)
 
 
+def default_geometry(dtype: int):
+    """Tile geometry of the kernels that will run the plan: the specialised (NVRTC) kernels'
+    when they are available, else the interpreter's."""
+    return GEOMETRY_JIT[dtype] if jit.available() else GEOMETRY[dtype]
+
+
 def plan_for_state(state, specs, fuse: bool | None = None) -> Plan:
     fuse = FUSION_DEFAULT if fuse is None else fuse
     bytes_needed = state.n_amps * state.precision.itemsize
     allow_ext = _free_bytes() > bytes_needed + (512 << 20)
-    return plan_circuit(specs, state.n_qubits, state.precision.qsb_dtype, allow_ext_perm=allow_ext, fuse=fuse)
+    dtype = state.precision.qsb_dtype
+    geo = default_geometry(dtype)
+    return plan_circuit(specs, state.n_qubits, dtype, allow_ext_perm=allow_ext, fuse=fuse, geometry=geo)
 
 
 def _apply_gate_step(ptr, n, dtype, g, stream):
@@ -68,6 +76,11 @@ def _launch_pass(step, words, dtype, src, dst, n, st):
         except Exception as exc:  # compile / TMA-plan failure: keep going on the interpreter
             step.no_jit = True
             warnings.warn(f"pass specialisation unavailable ({exc}); using the interpreted pass kernel")
+    if int(words[3]) != GEOMETRY[dtype].nreg:
+        # planned for the specialised kernel's register geometry: re-encode for the interpreter
+        if getattr(step, "interp_words", None) is None:
+            step.interp_words, _ = compile_pass(step.gates, set(step.tile_pos), n, dtype, GEOMETRY[dtype])
+        words = step.interp_words
     nat.check(nat.lib().qsb_run_pass(src, dst, n, dtype, words.ctypes.data, len(words), st), "run_pass")
 
 

@@ -34,7 +34,7 @@ G_COMPLEX, G_REAL, G_SWAPX = 0, 1, 2
 H_TILEPOS = 16
 MAX_PROG_WORDS = 6144
 MAX_PIVOTS = 32  # one producer lane per pivot computes its per-tile external factor
-THREAD_BITS = 9  # 512 consumer threads per CTA: 5 lane bits + 4 warp bits
+THREAD_BITS = 9  # interpreter: 512 consumer threads per CTA (5 lane bits + 4 warp bits)
 
 
 @dataclass(frozen=True)
@@ -42,17 +42,25 @@ class TileGeometry:
     K: int  # tile bits
     G: int  # swizzle group (bank-conflict) bits
     L: int  # low bits always in the tile (256-byte runs)
+    R: int = 0  # register (slot) bits per thread; 0 = K - THREAD_BITS (the interpreter's)
 
     @property
     def nreg(self) -> int:
-        return self.K - THREAD_BITS
+        return self.R if self.R else self.K - THREAD_BITS
+
+    @property
+    def thread_bits(self) -> int:
+        return self.K - self.nreg
 
     @property
     def A(self) -> int:
         return 1 << self.nreg
 
 
+# interpreter (csrc/pass.cu, fixed 512 consumers) and specialised-kernel (jit.py, 256 consumers
+# holding 16 c128 / 32 c64 amplitudes each: fewer layout changes for 2-qubit-gate-heavy passes)
 GEOMETRY = {nat.QSB_C128: TileGeometry(12, 3, 4), nat.QSB_C64: TileGeometry(13, 4, 5)}
+GEOMETRY_JIT = {nat.QSB_C128: TileGeometry(12, 3, 4, 4), nat.QSB_C64: TileGeometry(13, 4, 5, 5)}
 
 
 def _f2w(x: float) -> int:
@@ -155,6 +163,7 @@ class PassStep:
     n_pivots: int
     jit: object = None  # (compiled kernel, coefficient array) once specialised
     no_jit: bool = False
+    interp_words: object = None  # re-encoding for the interpreter's geometry (fallback only)
 
     @property
     def n_gates(self) -> int:
@@ -241,9 +250,11 @@ def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool):
     return absorbed, deferred, T
 
 
-def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, fuse: bool = True) -> Plan:
-    """Plan a gate list into PassSteps (fused) and GateSteps (stand-alone kernels)."""
-    geo = GEOMETRY[dtype]
+def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, fuse: bool = True,
+                 geometry: TileGeometry | None = None) -> Plan:
+    """Plan a gate list into PassSteps (fused) and GateSteps (stand-alone kernels).  `geometry`
+    defaults to the interpreter's (GEOMETRY); the specialised kernels use GEOMETRY_JIT."""
+    geo = geometry or GEOMETRY[dtype]
     gates = []
     for i, spec in enumerate(specs):
         g = spec if isinstance(spec, NGate) else normalize(spec, n_qubits, i)
@@ -266,7 +277,7 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
             # cheaper as sparse single-gate kernels than as a full sweep
             plan.steps.extend(GateStep(g) for g in absorbed)
         else:
-            words, info = compile_pass(absorbed, T, n_qubits, dtype)
+            words, info = compile_pass(absorbed, T, n_qubits, dtype, geo)
             plan.steps.append(PassStep(words, absorbed, tuple(sorted(T)), info["ext_perm"],
                                        info["transposes"], info["pivots"]))
         remaining = deferred
@@ -313,8 +324,8 @@ def _order_thread_bits(cands, geo, prefer, natural=False):
     return lanes + rest
 
 
-def compile_pass(absorbed, T, n, dtype):
-    geo = GEOMETRY[dtype]
+def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None):
+    geo = geo or GEOMETRY[dtype]
     K, NREG, A = geo.K, geo.nreg, geo.A
     tile_pos = sorted(T)
     tidx = {p: b for b, p in enumerate(tile_pos)}
@@ -556,7 +567,7 @@ def _compile_diag(terms, lay, tile_pos, tidx, geo, slot0):
     npiv = 0
     for p, partners in pivots:
         self_w = singles.pop(p, 1.0 + 0j)
-        ops += _pivot_op(p, partners, self_w, lay, tile_pos, tidx, A, slot0 + npiv)
+        ops += _pivot_op(p, partners, self_w, lay, tile_pos, tidx, A, slot0 + npiv, geo.thread_bits)
         npiv += 1
     for b, w in singles.items():
         generic.append((1 << b, 1 << b, w))
@@ -571,14 +582,14 @@ def _compile_diag(terms, lay, tile_pos, tidx, geo, slot0):
     return ops, npiv
 
 
-def _pivot_op(p, partners, self_w, lay, tile_pos, tidx, A, slot):
+def _pivot_op(p, partners, self_w, lay, tile_pos, tidx, A, slot, thread_bits):
     if p in tidx and tidx[p] in lay.R:
         ptype, pval = 0, lay.slot_of(tidx[p])
     else:
         ptype, pval = 1, 1 << p
     ext = []
     ta = np.ones(16, dtype=np.complex128) * self_w
-    tb = np.ones(1 << (THREAD_BITS - 4), dtype=np.complex128)
+    tb = np.ones(1 << (thread_bits - 4), dtype=np.complex128)
     rt = np.ones(A, dtype=np.complex128)
     for q, w in sorted(partners.items()):
         if q not in tidx:

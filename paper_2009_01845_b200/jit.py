@@ -24,10 +24,13 @@ from . import _native as nat
 
 OP_END, OP_LAYOUT, OP_G1, OP_G2, OP_PIVOT, OP_PARITY, OP_TERM, OP_SCALE = range(8)
 H_TILEPOS = 16
-CONSUMERS = 512
+CONSUMERS = 512  # default (interpreter geometry); a kernel uses 2**(K - NREG) consumer threads
 THREADS = CONSUMERS + 32
 STAGES = 2
 MAX_PIV = 32
+# setmaxnreg split for 256 consumers + a 128-thread producer warpgroup: 256*232 + 128*40 <= 64K
+PRODUCER_REGS = 40
+CONSUMER_REGS = 232
 
 
 def _w2d(w):
@@ -39,8 +42,6 @@ typedef unsigned long long u64;
 typedef unsigned int u32;
 typedef long long i64;
 struct __align__(64) TMap { u64 w[16]; };
-struct TmaPlan { int mode; int n_gap; int gap_dim[5]; int gap_lo[5]; int gap_nb[5]; int top_dim; int top_lo;
-                 int n_calls; u32 call_bytes; u32 call_coord[32]; };
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u64* b, u32 c) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(c)); }
@@ -67,8 +68,87 @@ __device__ __forceinline__ u32 swz(u32 j) {
   for (int s = GB; s < KB; s += GB) f ^= (j >> s);
   return j ^ (f & ((1u << GB) - 1u));
 }
-struct Smem { C stage[STAGES][1 << KB]; C tbuf[1 << KB]; double2 ep[4][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 epbar[4]; u64 base[STAGES][2]; };
+struct Smem { C stage[STAGES][1 << KB]; C tbuf[1 << KB]; double2 ep[4][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 base[STAGES][2]; };
 """
+
+
+MAX_TMA_ITER_BITS = 7  # at most 128 TMA calls per tile
+
+
+def tma_plan(tile_pos, n, amp_bytes, max_iter=MAX_TMA_ITER_BITS):
+    """Cover one tile (amplitudes whose index bits outside `tile_pos` are fixed) with rank-5
+    TMA tensor loads.
+
+    The state is described as a rank-5 tensor whose dims are contiguous ranges of index bits:
+    a *box* dim spans only tile bits (box extent = dim extent), a *coordinate* dim has box
+    extent 1 and its coordinate comes from the tile base.  Tile bits inside coordinate dims are
+    *iterated*: one TMA call per combination.  A DP over the bit ranges picks the <= 5 dims that
+    minimise the iterated bits (= log2 calls).  The stage then holds the tile in order
+    [call index | box index] -- `sigma[b]` is the stage bit of tile bit b.
+
+    Returns dict(dims=[(lo, nb, is_box)], iter_pos=[...], sigma=[...], tdesc=[15 ints]) or None.
+    """
+    tile = set(int(p) for p in tile_pos)
+    epa = amp_bytes // 8  # 8-byte TMA elements per amplitude
+    INF = (1 << 30, 0)
+    # dp[d][p]: ((iterated bits, -innermost box width), back-pointer) covering bits [0, p) with d
+    # dims; among equal call counts the widest innermost box (longest TMA rows) wins
+    dp = [[(INF, None)] * (n + 1) for _ in range(6)]
+    dp[0][0] = ((0, 0), None)
+    tile_prefix = [0] * (n + 1)
+    for p in range(n):
+        tile_prefix[p + 1] = tile_prefix[p] + (1 if p in tile else 0)
+    for d in range(5):
+        for p in range(n):
+            c0 = dp[d][p][0]
+            if c0 >= INF:
+                continue
+            # box range: only tile bits, extent <= 256 elements
+            lim = (8 if epa == 1 else 7) if d == 0 else 8
+            w = 0
+            while w < lim and p + w < n and (p + w) in tile:
+                w += 1
+                cand = ((c0[0], -w) if d == 0 else c0, (p, d, True))
+                if cand[0] < dp[d + 1][p + w][0]:
+                    dp[d + 1][p + w] = cand
+            if d == 0:
+                continue  # the innermost dim must be a (contiguous) box
+            for w in range(1, min(31, n - p) + 1):
+                cost = (c0[0] + tile_prefix[p + w] - tile_prefix[p], c0[1])
+                if cost < dp[d + 1][p + w][0]:
+                    dp[d + 1][p + w] = (cost, (p, d, False))
+    best = min(range(1, 6), key=lambda d: (dp[d][n][0], d))
+    if dp[best][n][0][0] > max_iter:
+        return None
+    dims = []
+    p, d = n, best
+    while d > 0:
+        cost, bp = dp[d][p]
+        lo, dprev, is_box = bp
+        dims.append((lo, p - lo, is_box))
+        p, d = lo, dprev
+    dims.reverse()
+    box_bits = [b for lo, nb, bx in dims if bx for b in range(lo, lo + nb)]
+    iter_pos = [b for lo, nb, bx in dims if not bx for b in range(lo, lo + nb) if b in tile]
+    order = sorted(int(p) for p in tile_pos)
+    stage_of = {p: i for i, p in enumerate(box_bits)}
+    stage_of.update({p: len(box_bits) + i for i, p in enumerate(iter_pos)})
+    sigma = [stage_of[p] for p in order]
+    gdim, gstride, box = [], [], []
+    for i in range(5):
+        if i < len(dims):
+            lo, nb, bx = dims[i]
+            ext = (1 << nb) * (epa if i == 0 else 1)
+            gdim.append(ext)
+            box.append(ext if bx else 1)
+            if i > 0:
+                gstride.append((1 << lo) * amp_bytes)
+        else:
+            gdim.append(1)
+            box.append(1)
+            gstride.append((1 << n) * amp_bytes)
+    return dict(dims=dims, iter_pos=iter_pos, sigma=sigma, tdesc=[5] + gdim + gstride + box,
+                box_amps=1 << len(box_bits))
 
 
 class _Gen:
@@ -79,6 +159,7 @@ class _Gen:
         self.K, self.NREG, self.n = w[2], w[3], w[4]
         self.TB = self.K - self.NREG
         self.A = 1 << self.NREG
+        self.consumers = 1 << self.TB
         self.G = 3 if dtype == nat.QSB_C128 else 4
         n, K = self.n, self.K
         self.tile_pos = w[H_TILEPOS:H_TILEPOS + K]
@@ -179,19 +260,25 @@ class _Gen:
             ep.append("            const int bit = (int)scf[o + 1 + k];")
             ep.append("            if ((base >> bit) & 1ull) f = dm(f, cfz(scf, o + 1 + cnt + 2 * k));")
             ep.append("          }")
-            ep.append("          sm.ep[it & 3][lane] = f;")
+            ep.append("          sm.ep[tno & 3][lane] = f;")
             ep.append("        }")
-            ep.append("        __syncwarp();")
-            ep.append("        if (lane == 0) mbar_arrive(&sm.epbar[it & 3]);")
         self.ep_code = "\n".join(ep)
         body_start = len(self.lines)
-        # initial load (natural order stage)
+        # initial load: the TMA stage holds tile bit b at stage bit sigma[b] (tma_plan)
+        amp_bytes = 16 if self.dtype == nat.QSB_C128 else 8
+        self.tplan = tma_plan(self.tile_pos, self.n, amp_bytes)
+        if self.tplan is None:
+            raise ValueError("tile has too many bit runs for the TMA tile fetch")
+        sig = self.tplan["sigma"]
         self.set_layout(first, 0)
+        self.emit(f"    const u32 sg0 = {self.thread_expr([sig[b] for b in first['Tb']], 32)};")
         for s in range(A):
-            self.emit(f"    C v{s} = buf[jt0 | {first['jt'][s]}u];")
+            off = sum(1 << sig[first['R'][i]] for i in range(self.NREG) if (s >> i) & 1)
+            self.emit(f"    C v{s} = buf[sg0 | {off}u];")
         # the stage is consumed: hand it back to the producer before any compute
         self.emit("    fence_async();")
         self.emit("    mbar_arrive(&sm.empty[s]);")
+        self.emit("@@REFILL@@")
         q = p + w[p + 1]
         li = 0
         while w[q] != OP_END:
@@ -342,9 +429,6 @@ class _Gen:
         ta = [complex(_w2d(ta_w[2 * k]), _w2d(ta_w[2 * k + 1])) for k in range(16)]
         tb = [complex(_w2d(tb_w[2 * k]), _w2d(tb_w[2 * k + 1])) for k in range(nb)]
         rt = [complex(_w2d(rt_w[2 * k]), _w2d(rt_w[2 * k + 1])) for k in range(A)]
-        if not self.ep_waited:  # unconditional: every consumer thread waits once per tile
-            self.emit("    mbar_wait(&sm.epbar[it & 3], (it >> 2) & 1);")
-            self.ep_waited = True
         self.emit(f"    {{ // pivot {slot}")
         if ptype == 1:
             self.emit(f"    if (((base | gt{self.li}) & {pval}ull) != 0ull) {{")
@@ -406,51 +490,69 @@ class _Gen:
         out_terms = [f"((c >> {m}) & 1ull) << {self.ext_out[m]}" for m in range(n_ext)]
         base_expr = " | ".join(base_terms) if base_terms else "0ull"
         out_expr = " | ".join(out_terms) if (out_terms and self.ext_perm) else "base"
+        tp = self.tplan
+        ncalls = 1 << len(tp["iter_pos"])
+        koff = " | ".join(f"((u64)((k >> {j}) & 1) << {b})" for j, b in enumerate(tp["iter_pos"])) or "0ull"
+        coords = []
+        for lo, nb, bx in tp["dims"]:
+            coords.append("0" if bx else f"(int)((b >> {lo}) & {(1 << nb) - 1}ull)")
+        coords += ["0"] * (5 - len(coords))
+        call_bytes = tp["box_amps"] * (16 if self.dtype == nat.QSB_C128 else 8)
+        produce = (f"        for (int k = lane; k < {ncalls}; k += 32) {{\n"
+                   f"          const u64 b = base | {koff};\n"
+                   f"          const int co[5] = {{{', '.join(coords)}}};\n"
+                   f"          tma5(d + (u64)k * {call_bytes}u, &tmap, co, &sm.full[s]);\n"
+                   f"        }}")
         defs = (f"#define R {real}\n#define C {real}2\n#define KB {K}\n#define GB {self.G}\n#define STAGES {STAGES}\n"
-                f"#define CONSUMERS {CONSUMERS}\n#define MAXPIV {MAX_PIV}\n#define NPIV {self.npiv}\n"
+                f"#define CONSUMERS {self.consumers}\n#define MAXPIV {MAX_PIV}\n#define NPIV {self.npiv}\n"
                 f"#define NCOEF {len(self.coeffs)}\n")
+        issue = f"""      {{ // producer warp: fetch tile c into stage s (tile number tno)
+        const u64 base = {base_expr};
+{self.ep_code}
+        __syncwarp();
+        if (lane == 0) {{
+          sm.base[s][0] = base;
+          sm.base[s][1] = {out_expr};
+          mbar_expect_tx(&sm.full[s], (u32)((1u << KB) * sizeof(C)));
+        }}
+        __syncwarp();
+        char* d = reinterpret_cast<char*>(&sm.stage[s][0]);
+{produce}
+      }}"""
+        body = body.replace("@@REFILL@@", "")
         return defs + _PRELUDE + f"""
-extern "C" __global__ void __launch_bounds__({THREADS}, 1)
-{name}(const C* __restrict__ src, C* __restrict__ dst, const __grid_constant__ TMap tmap, const TmaPlan tp,
+// {self.consumers} consumer threads + one producer warpgroup (one active warp: TMA tile fetches and
+// per-tile pivot factors, STAGES tiles ahead); setmaxnreg moves the producers' registers to the
+// consumers, which hold the tile in registers.
+extern "C" __global__ void __launch_bounds__({self.consumers + 128}, 1)
+{name}(const C* __restrict__ src, C* __restrict__ dst, const __grid_constant__ TMap tmap,
        const double* __restrict__ cf) {{
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   double* scf = reinterpret_cast<double*>(smem_raw + sizeof(Smem));
   const int tid = threadIdx.x;
-  for (int i = tid; i < NCOEF; i += {THREADS}) scf[i] = cf[i];
+  for (int i = tid; i < NCOEF; i += {self.consumers + 128}) scf[i] = cf[i];
   if (tid == 0) {{
     for (int s = 0; s < STAGES; ++s) {{ mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], CONSUMERS); }}
-    for (int s = 0; s < 4; ++s) mbar_init(&sm.epbar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }}
   __syncthreads();
   const u64 n_tiles = {1 << (n - K)}ull;
   if (tid >= CONSUMERS) {{
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 {PRODUCER_REGS};" ::: "memory");
+    if (tid >= CONSUMERS + 32) return;
     const int lane = tid - CONSUMERS;
     int it = 0;
     for (u64 c = blockIdx.x; c < n_tiles; c += gridDim.x, ++it) {{
       const int s = it % STAGES;
       const u32 ph = (it / STAGES) & 1;
       if (it >= STAGES) mbar_wait(&sm.empty[s], ph ^ 1);
-      const u64 base = {base_expr};
-      if (lane == 0) {{
-        sm.base[s][0] = base;
-        sm.base[s][1] = {out_expr};
-        mbar_expect_tx(&sm.full[s], (u32)((1u << KB) * sizeof(C)));
-        int co[5] = {{0, 0, 0, 0, 0}};
-        for (int g = 0; g < tp.n_gap; ++g) co[tp.gap_dim[g]] = (int)((base >> tp.gap_lo[g]) & ((1ull << tp.gap_nb[g]) - 1ull));
-        const int top0 = tp.top_dim >= 0 ? (int)(base >> tp.top_lo) : 0;
-        char* d = reinterpret_cast<char*>(&sm.stage[s][0]);
-        for (int k = 0; k < tp.n_calls; ++k) {{
-          if (tp.top_dim >= 0) co[tp.top_dim] = top0 + (int)tp.call_coord[k];
-          tma5(d + (u64)k * tp.call_bytes, &tmap, co, &sm.full[s]);
-        }}
-      }}
-      __syncwarp();
-{self.ep_code}
+      const int tno = it;
+{issue}
     }}
     return;
   }}
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 {CONSUMER_REGS};" ::: "memory");
   int it = 0;
   for (u64 c = blockIdx.x; c < n_tiles; c += gridDim.x, ++it) {{
     const int s = it % STAGES;
@@ -467,7 +569,7 @@ extern "C" __global__ void __launch_bounds__({THREADS}, 1)
 
 
 class _Compiled:
-    __slots__ = ("func", "name", "smem")
+    __slots__ = ("func", "name", "smem", "tdesc", "n_tiles", "threads")
 
 
 _cache: dict = {}
@@ -504,13 +606,18 @@ def available() -> bool:
     return _avail
 
 
-def generate(words, dtype):
-    """(source, kernel name, coefficients) for a pass program (CPU-only, used by tests)."""
+def generate_full(words, dtype):
+    """(source, kernel name, coefficients, TMA plan) for a pass program (CPU-only)."""
     g = _Gen(words, dtype)
     body_probe = g.generate("KNAME")
     name = "qsb_pass_" + hashlib.sha1(body_probe.encode()).hexdigest()[:16]
     src = body_probe.replace("KNAME", name)
-    return src, name, np.array(g.coeffs, dtype=np.float64)
+    return src, name, np.array(g.coeffs, dtype=np.float64), g.tplan
+
+
+def generate(words, dtype):
+    """(source, kernel name, coefficients) for a pass program (CPU-only, used by tests)."""
+    return generate_full(words, dtype)[:3]
 
 
 MAX_COEFFS = 3072  # 24 KB of coefficients staged in shared memory
@@ -524,7 +631,7 @@ def smem_bytes(dtype, n_coeffs=MAX_COEFFS) -> int:
 
 
 def compile_words(words, dtype):
-    src, name, coeffs = generate(words, dtype)
+    src, name, coeffs, tplan = generate_full(words, dtype)
     if len(coeffs) > MAX_COEFFS:
         raise RuntimeError(f"{len(coeffs)} coefficients exceed the shared-memory budget")
     with _lock:
@@ -541,6 +648,9 @@ def compile_words(words, dtype):
             hit.func = fn.value
             hit.name = name
             hit.smem = smem_bytes(dtype, len(coeffs))
+            hit.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
+            hit.n_tiles = 1 << (int(words[4]) - int(words[2]))
+            hit.threads = (1 << (int(words[2]) - int(words[3]))) + 128
             _cache[src] = hit
     return hit, coeffs
 
@@ -549,8 +659,8 @@ def run(words, dtype, src_ptr, dst_ptr, n_qubits, stream_ptr, compiled=None, coe
     if compiled is None:
         compiled, coeffs = compile_words(words, dtype)
     nat.check(
-        nat.lib().qsb_jit_run_pass(compiled.func, src_ptr, dst_ptr, n_qubits, dtype, words.ctypes.data, len(words),
-                                   coeffs.ctypes.data if len(coeffs) else None, len(coeffs), THREADS,
+        nat.lib().qsb_jit_run_pass(compiled.func, src_ptr, dst_ptr, compiled.tdesc.ctypes.data, compiled.n_tiles,
+                                   coeffs.ctypes.data if len(coeffs) else None, len(coeffs), compiled.threads,
                                    compiled.smem, stream_ptr),
         "jit_run_pass",
     )

@@ -162,7 +162,8 @@ class CudaBackend:
                     for g in ngates)
         plan_ = cache.get(key)
         if plan_ is None:
-            plan_ = plan_circuit(ngates, n_local, self.dtype, allow_ext_perm=False)
+            plan_ = plan_circuit(ngates, n_local, self.dtype, allow_ext_perm=False,
+                                 geometry=engine.default_geometry(self.dtype))
             cache[key] = plan_
         holder = {}
         view = _ShardView(shard, n_local, self.precision)

@@ -39,8 +39,15 @@ def run_circuit(name, circ, n, prec):
     holder = {}
     ms = timed(lambda: engine.run_plan(st, plan, holder))
     sweep_bytes = 2 * (1 << n) * prec.itemsize
+    evs = []
+    engine.run_plan(st, plan, holder, events=evs)
+    torch.cuda.synchronize()
+    per = [a.elapsed_time(b) for a, b in evs]
+    ps = [s for s in plan.steps if isinstance(s, PassStep)]
     print(f"{name:28s} n={n} {prec.value} gates={len(circ.queue)} {plan_stats(plan)} plan={tp*1e3:.0f}ms "
           f"run={ms:.2f} ms  eff={plan.state_sweeps() * sweep_bytes / ms / 1e6:.0f} GB/s", flush=True)
+    print("    per pass ms: " + " ".join(f"{x:.2f}{'' if (s.jit is not None and not s.no_jit) else '(I)'}[{s.n_gates}g/{s.n_transposes}t]"
+                                      for x, s in zip(per, ps)), flush=True)
     del st, holder
     torch.cuda.empty_cache()
 
