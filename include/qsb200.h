@@ -92,9 +92,12 @@ int qsb_jit_compile(const char* source, const char* name, const char* nvrtc_path
                     char* log_out, size_t log_cap);
 /* Launch a specialised pass kernel over `n_tiles` tiles.  `tma_desc` describes the state as the
  * rank-5 tensor the kernel's tile loads address (15 words: rank, global dims[5], byte strides of
- * dims 1..4, box dims[5]; jit.py tma_plan); `coeffs` are the per-launch gate coefficients. */
+ * dims 1..4, box dims[5]; jit.py tma_plan).  `tables` (doubles, staged to the device) are the
+ * per-thread pivot tables; `params` (`param_bytes`, passed by value as the kernel's last
+ * parameter) are the uniform gate coefficients. */
 int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tma_desc, uint64_t n_tiles,
-                     const double* coeffs, int64_t n_coeffs, int threads, int smem_bytes, void* stream);
+                     const double* tables, int64_t n_tables, const void* params, int64_t param_bytes,
+                     int threads, int smem_bytes, void* stream);
 
 /* ---- reductions (state.py:109-122 norm / overlap) ---------------------------------------- */
 /* out[0] = sum |a_i|^2 (double, device pointer).  Deterministic two-level tree. */

@@ -57,7 +57,8 @@ SIGNATURES = {
     "qsb_jit_compile": (_c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _c_void_p, _c_void_p, _c_size_t]),
     "qsb_jit_run_pass": (
         _c_int,
-        [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_u64, _c_void_p, _c_i64, _c_int, _c_int, _c_void_p],
+        [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_u64, _c_void_p, _c_i64, _c_void_p, _c_i64, _c_int, _c_int,
+         _c_void_p],
     ),
     "qsb_permute_qubits": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_int, _c_void_p, _c_void_p]),
     "qsb_exchange_halves": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_void_p]),

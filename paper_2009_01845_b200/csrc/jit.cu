@@ -155,13 +155,14 @@ extern "C" int qsb_jit_compile(const char* source, const char* name, const char*
 // encoded here from `tdesc` (jit.py tma_plan: rank, dims[5], byte strides[4], box[5]) over the
 // 8-byte elements of the state at `src`.
 extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tdesc, uint64_t n_tiles,
-                                const double* coeffs, int64_t n_coeffs, int threads, int smem_bytes, void* stream) {
+                                const double* coeffs, int64_t n_coeffs, const void* params, int64_t param_bytes,
+                                int threads, int smem_bytes, void* stream) {
   jit::Driver* dr = jit::driver();
   if (!dr || !func) {
     set_error("qsb_jit_run_pass: no driver / function");
     return QSB_ERR_CUDA;
   }
-  if (!tdesc || tdesc[0] != 5 || n_tiles == 0) {
+  if (!tdesc || tdesc[0] != 5 || n_tiles == 0 || !params || param_bytes <= 0 || param_bytes > 32000) {
     set_error("qsb_jit_run_pass: bad tile descriptor");
     return QSB_ERR_ARG;
   }
@@ -201,7 +202,8 @@ extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, const in
   const void* a_src = src;
   void* a_dst = dst;
   const double* a_cf = static_cast<const double*>(dcoef);
-  void* args[] = {(void*)&a_src, (void*)&a_dst, (void*)&map, (void*)&a_cf};
+  // the last kernel parameter is the coefficient struct, copied by value from `params`
+  void* args[] = {(void*)&a_src, (void*)&a_dst, (void*)&map, (void*)&a_cf, const_cast<void*>(params)};
   CUresult r = dr->launch(fn, grid, 1, 1, (unsigned)threads, 1, 1, (unsigned)smem_bytes, (CUstream)st, args, nullptr);
   if (r != CUDA_SUCCESS) {
     set_error("cuLaunchKernel failed (%d)", (int)r);

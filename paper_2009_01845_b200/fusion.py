@@ -43,6 +43,7 @@ class TileGeometry:
     G: int  # swizzle group (bank-conflict) bits
     L: int  # low bits always in the tile (256-byte runs)
     R: int = 0  # register (slot) bits per thread; 0 = K - THREAD_BITS (the interpreter's)
+    halves: bool = False  # tile staged as two halves split on tile bit K-1 (128 KB tiles)
 
     @property
     def nreg(self) -> int:
@@ -61,6 +62,10 @@ class TileGeometry:
 # holding 16 c128 / 32 c64 amplitudes each: fewer layout changes for 2-qubit-gate-heavy passes)
 GEOMETRY = {nat.QSB_C128: TileGeometry(12, 3, 4), nat.QSB_C64: TileGeometry(13, 4, 5)}
 GEOMETRY_JIT = {nat.QSB_C128: TileGeometry(12, 3, 4, 4), nat.QSB_C64: TileGeometry(13, 4, 5, 5)}
+# 128 KB tiles (two 64 KB halves, 32/64 amplitudes per thread): 3-pass QFT-30 plans, but the
+# straight-line kernels outgrow the instruction cache on 2-qubit-gate-heavy passes (measured
+# round 1: variational c64 55 -> 74 ms, grid 799 -> 1166 ms), so they are opt-in
+GEOMETRY_JIT_WIDE = {nat.QSB_C128: TileGeometry(13, 3, 4, 5, True), nat.QSB_C64: TileGeometry(14, 4, 5, 6, True)}
 
 
 def _f2w(x: float) -> int:
@@ -225,6 +230,13 @@ def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool):
                 if len(T) < K and other not in frozen:
                     T.add(other)
                     take = True
+                elif allow_ext and other not in frozen and min(px, py) >= L:
+                    # tile bit <-> external bit relabel (out of place): the tile bit is stored
+                    # to the external position and vice versa.  Never for the low L bits: the
+                    # output's contiguous runs must come from tile bits (measured: strided
+                    # 16-byte stores made such a QFT-30 pass 2.5x slower)
+                    frozen.add(other)
+                    take = True
             if take:
                 loc[x], loc[y] = loc[y], loc[x]
         else:
@@ -358,28 +370,43 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None):
     for x, p in enumerate(loc):
         inv[p] = x
     out_pos = [inv[p] for p in tile_pos]  # output global bit of each tile bit
+    # tile counter order: external bits that land on the low (contiguous-run) output bits vary
+    # fastest, so the tiles that together fill each output run are processed concurrently
+    ext_pos.sort(key=lambda p: (inv[p] >= geo.L, p))
     ext_out = [inv[p] for p in ext_pos]
     ext_perm = ext_out != ext_pos
     store_bits = {b for b in range(K) if out_pos[b] < geo.L}
 
     needs = [frozenset(tidx[p] for p in ev[2]) for ev in events if ev[0] in ("g1", "g2")]
 
-    def pick_R(i, forbid=frozenset()):
-        R = []
-        j = i
-        while j < len(needs):
-            nd = needs[j]
-            if nd & forbid:
-                break
-            merged = set(R) | nd
-            if len(merged) > NREG:
-                break
-            for b in sorted(nd):
-                if b not in R:
-                    R.append(b)
-            j += 1
+    def pick_R(i, forbid=frozenset(), keep=None, must=()):
+        """Register bits of the next layout: the tile bits of as many upcoming gates as fit.
+        `must` bits are always included; with `keep` (split-tile geometry) the new layout
+        shares at least one register bit with `keep` (transposes run in two halves on it)."""
+
+        def greedy(cap):
+            R = [b for b in must]
+            j = i
+            while j < len(needs):
+                nd = needs[j]
+                if nd & forbid:
+                    break
+                merged = set(R) | nd
+                if len(merged) > cap:
+                    break
+                for b in sorted(nd):
+                    if b not in R:
+                        R.append(b)
+                j += 1
+            return R
+
+        R = greedy(NREG)
+        if keep is not None and not set(R) & set(keep):
+            R = greedy(NREG - 1)
+            if not set(R) & set(keep):
+                R.append(sorted(keep, key=lambda b: (b in store_bits, -b))[0])
         filler = sorted((b for b in range(K) if b not in R and b not in forbid),
-                        key=lambda b: (b in store_bits, -b))
+                        key=lambda b: (keep is not None and b not in keep, b in store_bits, -b))
         for b in filler:
             if len(R) >= NREG:
                 break
@@ -410,7 +437,7 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None):
 
     # initial layout: its lanes 0..G-1 must be tile bits 0..G-1 (natural-order stage read)
     nat_forbid = frozenset(range(geo.G))
-    R0 = pick_R(0, nat_forbid)
+    R0 = pick_R(0, nat_forbid, must=(K - 1,) if geo.halves else ())
     cur = make_layout(R0, natural=True)
     words += layout_words(cur)
 
@@ -435,7 +462,7 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None):
         need = needs[gi]
         if not need <= set(cur.R):
             flush_diag()
-            cur = make_layout(pick_R(gi))
+            cur = make_layout(pick_R(gi, keep=cur.R if geo.halves else None))
             words += layout_words(cur)
             n_trans += 1
         flush_diag()

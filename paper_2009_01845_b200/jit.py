@@ -62,13 +62,22 @@ __device__ __forceinline__ double2 dm(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
 __device__ __forceinline__ double2 cfz(const double* cf, int k) { return make_double2(cf[k], cf[k + 1]); }
 __device__ __forceinline__ C toC(double2 z) { C r; r.x = (R)z.x; r.y = (R)z.y; return r; }
+struct CP { R v[NCOEF]; };
+__device__ __forceinline__ C mkC(R a, R b) { C r; r.x = a; r.y = b; return r; }
+// coefficient reads are indexed by `zo` (always 0, re-read from shared memory before every op):
+// ptxas can neither hoist them out of the tile loop nor bundle them across ops, so each op's
+// coefficients occupy (uniform) registers only while that op runs
+#define PZ(k) mkC(cp.v[(k) + zo], cp.v[(k) + 1 + zo])
+#define PV(k) cp.v[(k) + zo]
+__device__ __forceinline__ int zpin(const u32* z) {
+  u32 v; asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(z))); return (int)(v & 1u); }
 __device__ __forceinline__ u32 swz(u32 j) {
   u32 f = 0;
 #pragma unroll
-  for (int s = GB; s < KB; s += GB) f ^= (j >> s);
+  for (int s = GB; s < HBB; s += GB) f ^= (j >> s);
   return j ^ (f & ((1u << GB) - 1u));
 }
-struct Smem { C stage[STAGES][1 << KB]; C tbuf[1 << KB]; double2 ep[4][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 base[STAGES][2]; };
+struct Smem { C stage[STAGES][1 << HBB]; C tbuf[1 << HBB]; double2 ep[4][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 base[STAGES][2]; u32 zero; };
 """
 
 
@@ -168,14 +177,28 @@ class _Gen:
         self.ext_perm = bool(w[7] & 1)
         self.ops0 = H_TILEPOS + 2 * n - K
         self.coeffs: list = []
+        self.tables: list = []
         self.lines: list = []
         self.ep_waited = False
         self.h_scale = 0  # deferred 1/sqrt(2) factors of uncontrolled Hadamard butterflies
+        self.vm = list(range(self.A))  # slot of the current layout -> register variable v<i>
+        amp_bytes = 16 if dtype == nat.QSB_C128 else 8
+        # 128 KB tiles are staged as two 64 KB halves split on tile bit K-1 (a register bit of
+        # the first layout); layout changes then run in two rounds through a 64 KB buffer
+        self.halves = (1 << K) * amp_bytes > 65536
+        self.HB = K - 1 if self.halves else K  # bits of a stage / transpose-buffer index
 
-    # coefficient array (doubles); returns the index of the first entry
+    # uniform coefficients (gate matrices, phases): a kernel-parameter array of R, read as
+    # constant-bank operands (no registers held across the tile); returns the first index
     def cf(self, values):
         k = len(self.coeffs)
         self.coeffs.extend(float(v) for v in values)
+        return k
+
+    # per-thread-indexed tables (pivot factor tables): doubles staged in shared memory
+    def tf(self, values):
+        k = len(self.tables)
+        self.tables.extend(float(v) for v in values)
         return k
 
     def emit(self, s):
@@ -196,7 +219,7 @@ class _Gen:
     def swz_const(self, j):
         f = 0
         s = self.G
-        while s < self.K:
+        while s < self.HB:
             f ^= j >> s
             s += self.G
         return j ^ (f & ((1 << self.G) - 1))
@@ -250,8 +273,8 @@ class _Gen:
                 vals = [float(ne)] + [float(w[a + 5 + 3 * k]) for k in range(ne)]
                 for k in range(ne):
                     vals += [_w2d(w[a + 6 + 3 * k]), _w2d(w[a + 7 + 3 * k])]
-                offs[slot] = self.cf(vals)
-            offtab = self.cf([float(o) for o in offs])
+                offs[slot] = self.tf(vals)
+            offtab = self.tf([float(o) for o in offs])
             ep.append("        if (lane < NPIV) {")
             ep.append(f"          const int o = (int)scf[{offtab} + lane];")
             ep.append("          const int cnt = (int)scf[o];")
@@ -266,18 +289,33 @@ class _Gen:
         body_start = len(self.lines)
         # initial load: the TMA stage holds tile bit b at stage bit sigma[b] (tma_plan)
         amp_bytes = 16 if self.dtype == nat.QSB_C128 else 8
-        self.tplan = tma_plan(self.tile_pos, self.n, amp_bytes)
+        stage_pos = self.tile_pos[:self.HB]
+        self.tplan = tma_plan(stage_pos, self.n, amp_bytes)
         if self.tplan is None:
             raise ValueError("tile has too many bit runs for the TMA tile fetch")
         sig = self.tplan["sigma"]
         self.set_layout(first, 0)
         self.emit(f"    const u32 sg0 = {self.thread_expr([sig[b] for b in first['Tb']], 32)};")
-        for s in range(A):
-            off = sum(1 << sig[first['R'][i]] for i in range(self.NREG) if (s >> i) & 1)
-            self.emit(f"    C v{s} = buf[sg0 | {off}u];")
-        # the stage is consumed: hand it back to the producer before any compute
-        self.emit("    fence_async();")
-        self.emit("    mbar_arrive(&sm.empty[s]);")
+        if not self.halves:
+            for s in range(A):
+                off = sum(1 << sig[first['R'][i]] for i in range(self.NREG) if (s >> i) & 1)
+                self.emit(f"    C v{s} = buf[sg0 | {off}u];")
+            # the stage is consumed: hand it back to the producer before any compute
+            self.emit("    fence_async();")
+            self.emit("    mbar_arrive(&sm.empty[s]);")
+        else:
+            ih = first['R'].index(self.K - 1)
+            self.emit(f"    C {', '.join(f'v{s}' for s in range(A))};")
+            for half in (0, 1):
+                if half:
+                    self.emit("    mbar_wait(&sm.full[1], it & 1);")
+                for s in range(A):
+                    if ((s >> ih) & 1) != half:
+                        continue
+                    off = sum(1 << sig[first['R'][i]] for i in range(self.NREG) if (s >> i) & 1 and i != ih)
+                    self.emit(f"    v{s} = sm.stage[{half}][sg0 | {off}u];")
+                self.emit("    fence_async();")
+                self.emit(f"    mbar_arrive(&sm.empty[{half}]);")
         self.emit("@@REFILL@@")
         q = p + w[p + 1]
         li = 0
@@ -287,33 +325,27 @@ class _Gen:
             if op == OP_LAYOUT:
                 new = self.parse_layout(a)
                 li += 1
-                self.emit("    csync();")
-                self.emit("    { const u32 sj = swz(jt%d);" % self.li)
-                for s in range(A):
-                    self.emit(f"      sm.tbuf[sj ^ {self.swz_const(self.lay['jt'][s])}u] = v{s};")
-                self.emit("    }")
-                self.emit("    csync();")
-                self.set_layout(new, li)
-                self.emit("    { const u32 sj = swz(jt%d);" % li)
-                for s in range(A):
-                    self.emit(f"      v{s} = sm.tbuf[sj ^ {self.swz_const(new['jt'][s])}u];")
-                self.emit("    }")
-            elif op == OP_G1:
-                self.gen_g1(a)
-            elif op == OP_G2:
-                self.gen_g2(a)
-            elif op == OP_PIVOT:
-                self.gen_pivot(a)
+                if not self.halves:
+                    self.emit("    csync();")
+                    self.emit("    { const u32 sj = swz(jt%d);" % self.li)
+                    for s in range(A):
+                        self.emit(f"      sm.tbuf[sj ^ {self.swz_const(self.lay['jt'][s])}u] = v{self.vm[s]};")
+                    self.emit("    }")
+                    self.emit("    csync();")
+                    self.set_layout(new, li)
+                    self.emit("    { const u32 sj = swz(jt%d);" % li)
+                    for s in range(A):
+                        self.emit(f"      v{self.vm[s]} = sm.tbuf[sj ^ {self.swz_const(new['jt'][s])}u];")
+                    self.emit("    }")
+                else:
+                    self.gen_split_transpose(new, li)
             elif op == OP_PARITY:
                 self.gen_parity(a)
-            elif op == OP_TERM:
-                self.gen_term(a)
-            elif op == OP_SCALE:
-                ci = self.cf([_w2d(w[a]), _w2d(w[a + 1])])
-                self.emit(f"    {{ const C ph = toC(cfz(scf, {ci}));")
-                for s in range(A):
-                    self.emit(f"      v{s} = cm(v{s}, ph);")
-                self.emit("    }")
+            else:
+                gen = {OP_G1: self.gen_g1, OP_G2: self.gen_g2, OP_PIVOT: self.gen_pivot, OP_TERM: self.gen_term,
+                       OP_SCALE: self.gen_scale}[op]
+                self.emit("    zo = zpin(&sm.zero);")  # pin this op's coefficient reads here
+                gen(a)
             q += ln
         body = "\n".join(self.lines[body_start:])
         # output offsets of the final layout
@@ -324,10 +356,66 @@ class _Gen:
             scale = 2.0 ** (-(k // 2)) * (0.7071067811865476 if k % 2 else 1.0)
             store.append(f"    const R hs = (R){scale!r};")
             for s in range(A):
-                store.append(f"    v{s}.x *= hs; v{s}.y *= hs;")
+                store.append(f"    v{self.vm[s]}.x *= hs; v{self.vm[s]}.y *= hs;")
         for s in range(A):
-            store.append(f"    dst[ot | {lay['ooff'][s]}ull] = v{s};")
+            store.append(f"    dst[ot | {lay['ooff'][s]}ull] = v{self.vm[s]};")
         return self._kernel(name, body, "\n".join(store))
+
+    def gen_scale(self, a):
+        w = self.w
+        ci = self.cf([_w2d(w[a]), _w2d(w[a + 1])])
+        self.emit(f"    {{ const C ph = PZ({ci});")
+        for s in range(self.A):
+            self.emit(f"      v{self.vm[s]} = cm(v{self.vm[s]}, ph);")
+        self.emit("    }")
+
+    def gen_split_transpose(self, new, li):
+        """Layout change through the 64 KB buffer in two rounds: round r moves the amplitudes
+        whose tile bit h (a register bit of both layouts) is r.  Buffer index = tile index with
+        bit h removed; the register variables of round r are reused for the same round's
+        reads (slot -> variable map), so no temporaries are needed."""
+        old = self.lay
+        A, G = self.A, self.G
+        common = [b for b in old['R'] if b in new['R']]
+        assert common, "split transposes need a common register bit"
+
+        def squeeze(p, h):
+            return p - 1 if p > h else p
+
+        def ok(h, Tb):
+            res = {squeeze(b, h) % G for b in Tb[:G]}
+            return len(res) == G
+
+        h = sorted(common, key=lambda b: (not (ok(b, old['Tb']) and ok(b, new['Tb'])), b))[0]
+        io, inew = old['R'].index(h), new['R'].index(h)
+
+        def slot_index(R, s):
+            j = 0
+            for i, b in enumerate(R):
+                if (s >> i) & 1 and b != h:
+                    j |= 1 << squeeze(b, h)
+            return j
+
+        jw = self.thread_expr([squeeze(b, h) for b in old['Tb']], 32)
+        jr = self.thread_expr([squeeze(b, h) for b in new['Tb']], 32)
+        nvm = [0] * A
+        for r in (0, 1):
+            olds = [s for s in range(A) if ((s >> io) & 1) == r]
+            news = [s for s in range(A) if ((s >> inew) & 1) == r]
+            for s_new, s_old in zip(news, olds):
+                nvm[s_new] = self.vm[s_old]
+            self.emit("    csync();")
+            self.emit(f"    {{ const u32 sj = swz({jw});")
+            for s in olds:
+                self.emit(f"      sm.tbuf[sj ^ {self.swz_const(slot_index(old['R'], s))}u] = v{self.vm[s]};")
+            self.emit("    }")
+            self.emit("    csync();")
+            self.emit(f"    {{ const u32 sj = swz({jr});")
+            for s in news:
+                self.emit(f"      v{nvm[s]} = sm.tbuf[sj ^ {self.swz_const(slot_index(new['R'], s))}u];")
+            self.emit("    }")
+        self.vm = nvm
+        self.set_layout(new, li)
 
     def gen_g1(self, a):
         w, A = self.w, self.A
@@ -343,8 +431,8 @@ class _Gen:
                 if s & (1 << ib):
                     continue
                 t = s | (1 << ib)
-                self.emit(f"      {{ const C x0 = v{s}, x1 = v{t}; v{s}.x = x0.x + x1.x; v{s}.y = x0.y + x1.y;"
-                          f" v{t}.x = x0.x - x1.x; v{t}.y = x0.y - x1.y; }}")
+                self.emit(f"      {{ const C x0 = v{self.vm[s]}, x1 = v{self.vm[t]}; v{self.vm[s]}.x = x0.x + x1.x; v{self.vm[s]}.y = x0.y + x1.y;"
+                          f" v{self.vm[t]}.x = x0.x - x1.x; v{self.vm[t]}.y = x0.y - x1.y; }}")
             self.emit("    }")
             return
         self.emit(f"    {{ // G1 slot bit {ib} kind {kind}")
@@ -352,29 +440,29 @@ class _Gen:
             self.emit(f"    if (((base | gt{self.li}) & {gmask}ull) == {gval}ull) {{")
         if kind == 1:
             ci = self.cf([m[0], m[2], m[4], m[6]])
-            self.emit(f"      const R a00 = (R)scf[{ci}], a01 = (R)scf[{ci + 1}], a10 = (R)scf[{ci + 2}], a11 = (R)scf[{ci + 3}];")
+            self.emit(f"      const R a00 = PV({ci}), a01 = PV({ci + 1}), a10 = PV({ci + 2}), a11 = PV({ci + 3});")
         elif kind == 0:
             ci = self.cf(m)
             for r, nm in enumerate(("a00", "a01", "a10", "a11")):
-                self.emit(f"      const C {nm} = toC(cfz(scf, {ci + 2 * r}));")
+                self.emit(f"      const C {nm} = PZ({ci + 2 * r});")
         for s in range(A):
             if s & (1 << ib) or (s & rmask) != rval:
                 continue
             t = s | (1 << ib)
             if kind == 2:
-                self.emit(f"      {{ const C x = v{s}; v{s} = v{t}; v{t} = x; }}")
+                self.emit(f"      {{ const C x = v{self.vm[s]}; v{self.vm[s]} = v{self.vm[t]}; v{self.vm[t]} = x; }}")
             elif kind == 1:
-                self.emit(f"      {{ const C x0 = v{s}, x1 = v{t};"
-                          f" v{s}.x = fma(a01, x1.x, a00 * x0.x); v{s}.y = fma(a01, x1.y, a00 * x0.y);"
-                          f" v{t}.x = fma(a11, x1.x, a10 * x0.x); v{t}.y = fma(a11, x1.y, a10 * x0.y); }}")
+                self.emit(f"      {{ const C x0 = v{self.vm[s]}, x1 = v{self.vm[t]};"
+                          f" v{self.vm[s]}.x = fma(a01, x1.x, a00 * x0.x); v{self.vm[s]}.y = fma(a01, x1.y, a00 * x0.y);"
+                          f" v{self.vm[t]}.x = fma(a11, x1.x, a10 * x0.x); v{self.vm[t]}.y = fma(a11, x1.y, a10 * x0.y); }}")
             else:
-                self.emit(f"      {{ const C x0 = v{s}, x1 = v{t};"
+                self.emit(f"      {{ const C x0 = v{self.vm[s]}, x1 = v{self.vm[t]};"
                           f" C y0 = cm(a00, x0), y1 = cm(a10, x0);"
                           f" y0.x = fma(a01.x, x1.x, y0.x); y0.x = fma(-a01.y, x1.y, y0.x);"
                           f" y0.y = fma(a01.x, x1.y, y0.y); y0.y = fma(a01.y, x1.x, y0.y);"
                           f" y1.x = fma(a11.x, x1.x, y1.x); y1.x = fma(-a11.y, x1.y, y1.x);"
                           f" y1.y = fma(a11.x, x1.y, y1.y); y1.y = fma(a11.y, x1.x, y1.y);"
-                          f" v{s} = y0; v{t} = y1; }}")
+                          f" v{self.vm[s]} = y0; v{self.vm[t]} = y1; }}")
         if gmask:
             self.emit("    }")
         self.emit("    }")
@@ -388,32 +476,32 @@ class _Gen:
             self.emit(f"    if (((base | gt{self.li}) & {gmask}ull) == {gval}ull) {{")
         if kind == 1:
             ci = self.cf([m[2 * k] for k in range(16)])
-            self.emit(f"      R mm[16]; for (int k = 0; k < 16; ++k) mm[k] = (R)scf[{ci} + k];")
+            self.emit("      const R " + ", ".join(f"mm{k} = PV({ci + k})" for k in range(16)) + ";")
         else:
             ci = self.cf(m)
-            self.emit(f"      C mm[16]; for (int k = 0; k < 16; ++k) mm[k] = toC(cfz(scf, {ci} + 2 * k));")
+            self.emit("      const C " + ", ".join(f"mm{k} = PZ({ci + 2 * k})" for k in range(16)) + ";")
         for s in range(A):
             if s & ((1 << ih) | (1 << il)) or (s & rmask) != rval:
                 continue
             idx = [s, s | (1 << il), s | (1 << ih), s | (1 << ih) | (1 << il)]
-            self.emit("      { const C x0 = v%d, x1 = v%d, x2 = v%d, x3 = v%d;" % tuple(idx))
+            self.emit("      { const C x0 = v%d, x1 = v%d, x2 = v%d, x3 = v%d;" % tuple(self.vm[i] for i in idx))
             for r in range(4):
                 if kind == 1:
-                    self.emit(f"        {{ C y; y.x = mm[{4*r}] * x0.x; y.y = mm[{4*r}] * x0.y;"
-                              f" y.x = fma(mm[{4*r+1}], x1.x, y.x); y.y = fma(mm[{4*r+1}], x1.y, y.y);"
-                              f" y.x = fma(mm[{4*r+2}], x2.x, y.x); y.y = fma(mm[{4*r+2}], x2.y, y.y);"
-                              f" y.x = fma(mm[{4*r+3}], x3.x, y.x); y.y = fma(mm[{4*r+3}], x3.y, y.y); v{idx[r]} = y; }}")
+                    self.emit(f"        {{ C y; y.x = mm{4*r} * x0.x; y.y = mm{4*r} * x0.y;"
+                              f" y.x = fma(mm{4*r+1}, x1.x, y.x); y.y = fma(mm{4*r+1}, x1.y, y.y);"
+                              f" y.x = fma(mm{4*r+2}, x2.x, y.x); y.y = fma(mm{4*r+2}, x2.y, y.y);"
+                              f" y.x = fma(mm{4*r+3}, x3.x, y.x); y.y = fma(mm{4*r+3}, x3.y, y.y); v{self.vm[idx[r]]} = y; }}")
                 else:
                     terms = []
                     for c in range(4):
-                        mc = f"mm[{4*r+c}]"
+                        mc = f"mm{4*r+c}"
                         xc = f"x{c}"
                         if c == 0:
                             terms.append(f"C y = cm({mc}, {xc});")
                         else:
                             terms.append(f"y.x = fma({mc}.x, {xc}.x, y.x); y.x = fma(-{mc}.y, {xc}.y, y.x);"
                                          f" y.y = fma({mc}.x, {xc}.y, y.y); y.y = fma({mc}.y, {xc}.x, y.y);")
-                    self.emit("        { " + " ".join(terms) + f" v{idx[r]} = y; }}")
+                    self.emit("        { " + " ".join(terms) + f" v{self.vm[idx[r]]} = y; }}")
             self.emit("      }")
         if gmask:
             self.emit("    }")
@@ -436,10 +524,10 @@ class _Gen:
         tb_all_one = all(z == 1 for z in tb)
         self.emit(f"      double2 fd = sm.ep[it & 3][{slot}];")
         if not ta_all_one:
-            ci = self.cf([x for z in ta for x in (z.real, z.imag)])
+            ci = self.tf([x for z in ta for x in (z.real, z.imag)])
             self.emit(f"      fd = dm(fd, cfz(scf, {ci} + 2 * (tid & 15)));")
         if not tb_all_one:
-            ci = self.cf([x for z in tb for x in (z.real, z.imag)])
+            ci = self.tf([x for z in tb for x in (z.real, z.imag)])
             self.emit(f"      fd = dm(fd, cfz(scf, {ci} + 2 * (tid >> 4)));")
         self.emit("      const C f = toC(fd);")
         # which slots carry a register-partner factor (structure: RT entry != 1 from a partner bit)
@@ -450,9 +538,9 @@ class _Gen:
             if ptype == 0 and not (s >> pval) & 1:
                 continue
             if use_rt and rt[s] != 1:
-                self.emit(f"      v{s} = cm(v{s}, cm(f, toC(cfz(scf, {rt_ci + 2 * s}))));")
+                self.emit(f"      v{self.vm[s]} = cm(v{self.vm[s]}, cm(f, PZ({rt_ci + 2 * s})));")
             else:
-                self.emit(f"      v{s} = cm(v{s}, f);")
+                self.emit(f"      v{self.vm[s]} = cm(v{self.vm[s]}, f);")
         if ptype == 1:
             self.emit("    }")
         self.emit("    }")
@@ -469,17 +557,17 @@ class _Gen:
                 terms.append(f"__popcll(gi & {s1}ull)")
             for d, m in pairs:
                 terms.append(f"__popcll(gi & (gi >> {d}) & {m}ull)")
-            self.emit(f"      {{ const u64 gi = {gi}; if (({' + '.join(terms)}) & 1) {{ v{s}.x = -v{s}.x; v{s}.y = -v{s}.y; }} }}")
+            self.emit(f"      {{ const u64 gi = {gi}; if (({' + '.join(terms)}) & 1) {{ v{self.vm[s]}.x = -v{self.vm[s]}.x; v{self.vm[s]}.y = -v{self.vm[s]}.y; }} }}")
         self.emit("    }")
 
     def gen_term(self, a):
         w, A = self.w, self.A
         mask, val = w[a], w[a + 1]
         ci = self.cf([_w2d(w[a + 2]), _w2d(w[a + 3])])
-        self.emit(f"    {{ const C ph = toC(cfz(scf, {ci}));")
+        self.emit(f"    {{ const C ph = PZ({ci});")
         for s in range(A):
             gi = f"(base | gt{self.li} | {self.lay['goff'][s]}ull)"
-            self.emit(f"      if (({gi} & {mask}ull) == {val}ull) v{s} = cm(v{s}, ph);")
+            self.emit(f"      if (({gi} & {mask}ull) == {val}ull) v{self.vm[s]} = cm(v{self.vm[s]}, ph);")
         self.emit("    }")
 
     def _kernel(self, name, body, store):
@@ -498,14 +586,15 @@ class _Gen:
             coords.append("0" if bx else f"(int)((b >> {lo}) & {(1 << nb) - 1}ull)")
         coords += ["0"] * (5 - len(coords))
         call_bytes = tp["box_amps"] * (16 if self.dtype == nat.QSB_C128 else 8)
+        hbit = f" | ((u64)HALF << {self.tile_pos[K - 1]})" if self.halves else ""
         produce = (f"        for (int k = lane; k < {ncalls}; k += 32) {{\n"
-                   f"          const u64 b = base | {koff};\n"
+                   f"          const u64 b = base{hbit} | {koff};\n"
                    f"          const int co[5] = {{{', '.join(coords)}}};\n"
                    f"          tma5(d + (u64)k * {call_bytes}u, &tmap, co, &sm.full[s]);\n"
                    f"        }}")
-        defs = (f"#define R {real}\n#define C {real}2\n#define KB {K}\n#define GB {self.G}\n#define STAGES {STAGES}\n"
+        defs = (f"#define R {real}\n#define C {real}2\n#define KB {K}\n#define HBB {self.HB}\n#define GB {self.G}\n#define STAGES {STAGES}\n"
                 f"#define CONSUMERS {self.consumers}\n#define MAXPIV {MAX_PIV}\n#define NPIV {self.npiv}\n"
-                f"#define NCOEF {len(self.coeffs)}\n")
+                f"#define NCOEF {max(1, len(self.coeffs))}\n#define NTAB {len(self.tables)}\n")
         issue = f"""      {{ // producer warp: fetch tile c into stage s (tile number tno)
         const u64 base = {base_expr};
 {self.ep_code}
@@ -519,21 +608,52 @@ class _Gen:
         char* d = reinterpret_cast<char*>(&sm.stage[s][0]);
 {produce}
       }}"""
+        if self.halves:
+            # both stages hold one tile: half h (tile bit K-1 = h) in stage h
+            halves_code = []
+            for h in (0, 1):
+                halves_code.append(f"""      {{ // producer warp: half {h} of tile c -> stage {h}
+        const int s = {h};
+        if (it >= 1) mbar_wait(&sm.empty[{h}], (it & 1) ^ 1);""")
+                if h == 0:
+                    halves_code.append(f"""        const u64 base = {base_expr};
+{self.ep_code}
+        __syncwarp();
+        if (lane == 0) {{ sm.base[0][0] = base; sm.base[0][1] = {out_expr}; }}""")
+                else:
+                    halves_code.append(f"""        const u64 base = {base_expr};""")
+                halves_code.append(f"""        if (lane == 0) mbar_expect_tx(&sm.full[{h}], (u32)((1u << HBB) * sizeof(C)));
+        __syncwarp();
+        char* d = reinterpret_cast<char*>(&sm.stage[{h}][0]);
+        constexpr u64 HALF = {h};
+{produce}
+      }}""")
+            issue = "\n".join(halves_code)
         body = body.replace("@@REFILL@@", "")
+        if self.halves:
+            head = """    mbar_wait(&sm.full[0], it & 1);
+    const u64 base = sm.base[0][0];
+    const u64 obase = sm.base[0][1];"""
+        else:
+            head = """    mbar_wait(&sm.full[s], ph);
+    const u64 base = sm.base[s][0];
+    const u64 obase = sm.base[s][1];
+    C* buf = sm.stage[s];"""
         return defs + _PRELUDE + f"""
 // {self.consumers} consumer threads + one producer warpgroup (one active warp: TMA tile fetches and
 // per-tile pivot factors, STAGES tiles ahead); setmaxnreg moves the producers' registers to the
 // consumers, which hold the tile in registers.
 extern "C" __global__ void __launch_bounds__({self.consumers + 128}, 1)
 {name}(const C* __restrict__ src, C* __restrict__ dst, const __grid_constant__ TMap tmap,
-       const double* __restrict__ cf) {{
+       const double* __restrict__ cf, const __grid_constant__ CP cp) {{
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-  double* scf = reinterpret_cast<double*>(smem_raw + sizeof(Smem));
+  double* scf = reinterpret_cast<double*>(smem_raw + sizeof(Smem));  // pivot tables
   const int tid = threadIdx.x;
-  for (int i = tid; i < NCOEF; i += {self.consumers + 128}) scf[i] = cf[i];
+  for (int i = tid; i < NTAB; i += {self.consumers + 128}) scf[i] = cf[i];
   if (tid == 0) {{
     for (int s = 0; s < STAGES; ++s) {{ mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], CONSUMERS); }}
+    sm.zero = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }}
   __syncthreads();
@@ -546,7 +666,7 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, 1)
     for (u64 c = blockIdx.x; c < n_tiles; c += gridDim.x, ++it) {{
       const int s = it % STAGES;
       const u32 ph = (it / STAGES) & 1;
-      if (it >= STAGES) mbar_wait(&sm.empty[s], ph ^ 1);
+{"" if self.halves else "      if (it >= STAGES) mbar_wait(&sm.empty[s], ph ^ 1);"}
       const int tno = it;
 {issue}
     }}
@@ -554,13 +674,11 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, 1)
   }}
   asm volatile("setmaxnreg.inc.sync.aligned.u32 {CONSUMER_REGS};" ::: "memory");
   int it = 0;
+  int zo = 0;
   for (u64 c = blockIdx.x; c < n_tiles; c += gridDim.x, ++it) {{
     const int s = it % STAGES;
     const u32 ph = (it / STAGES) & 1;
-    mbar_wait(&sm.full[s], ph);
-    const u64 base = sm.base[s][0];
-    const u64 obase = sm.base[s][1];
-    C* buf = sm.stage[s];
+{head}
 {body}
 {store}
   }}
@@ -607,33 +725,39 @@ def available() -> bool:
 
 
 def generate_full(words, dtype):
-    """(source, kernel name, coefficients, TMA plan) for a pass program (CPU-only)."""
+    """(source, kernel name, parameter coefficients, table coefficients, TMA plan) for a pass
+    program (CPU-only)."""
     g = _Gen(words, dtype)
     body_probe = g.generate("KNAME")
     name = "qsb_pass_" + hashlib.sha1(body_probe.encode()).hexdigest()[:16]
     src = body_probe.replace("KNAME", name)
-    return src, name, np.array(g.coeffs, dtype=np.float64), g.tplan
+    return src, name, np.array(g.coeffs, dtype=np.float64), np.array(g.tables, dtype=np.float64), g.tplan
 
 
 def generate(words, dtype):
-    """(source, kernel name, coefficients) for a pass program (CPU-only, used by tests)."""
+    """(source, kernel name, parameter coefficients) for a pass program (CPU-only, tests)."""
     return generate_full(words, dtype)[:3]
 
 
-MAX_COEFFS = 3072  # 24 KB of coefficients staged in shared memory
+MAX_COEFFS = 3072  # 24 KB of pivot tables staged in shared memory
+MAX_PARAM_BYTES = 31744  # kernel parameter space: 32764 B minus the pointers and the tensor map
 
 
 def smem_bytes(dtype, n_coeffs=MAX_COEFFS) -> int:
-    K = 12 if dtype == nat.QSB_C128 else 13
-    amp = 16 if dtype == nat.QSB_C128 else 8
-    struct_bytes = (STAGES + 1) * (1 << K) * amp + 4 * MAX_PIV * 16 + 8 * STAGES * 4
+    # every geometry stages 64 KB per stage (whole 64 KB tiles or halves of 128 KB tiles)
+    struct_bytes = (STAGES + 1) * 65536 + 4 * MAX_PIV * 16 + 8 * STAGES * 4
     return struct_bytes + 8 * n_coeffs + 128
 
 
 def compile_words(words, dtype):
-    src, name, coeffs, tplan = generate_full(words, dtype)
-    if len(coeffs) > MAX_COEFFS:
-        raise RuntimeError(f"{len(coeffs)} coefficients exceed the shared-memory budget")
+    src, name, params, tables, tplan = generate_full(words, dtype)
+    if len(tables) > MAX_COEFFS:
+        raise RuntimeError(f"{len(tables)} table entries exceed the shared-memory budget")
+    pbytes = params.astype(np.float64 if dtype == nat.QSB_C128 else np.float32)
+    if pbytes.nbytes > MAX_PARAM_BYTES:
+        raise RuntimeError(f"{pbytes.nbytes} bytes of gate coefficients exceed the kernel parameter space")
+    if len(pbytes) == 0:
+        pbytes = np.zeros(1, dtype=pbytes.dtype)
     with _lock:
         hit = _cache.get(src)
         if hit is None:
@@ -647,20 +771,21 @@ def compile_words(words, dtype):
             hit = _Compiled()
             hit.func = fn.value
             hit.name = name
-            hit.smem = smem_bytes(dtype, len(coeffs))
+            hit.smem = smem_bytes(dtype, len(tables))
             hit.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
             hit.n_tiles = 1 << (int(words[4]) - int(words[2]))
             hit.threads = (1 << (int(words[2]) - int(words[3]))) + 128
             _cache[src] = hit
-    return hit, coeffs
+    return hit, (np.ascontiguousarray(pbytes), tables)
 
 
 def run(words, dtype, src_ptr, dst_ptr, n_qubits, stream_ptr, compiled=None, coeffs=None):
     if compiled is None:
         compiled, coeffs = compile_words(words, dtype)
+    params, tables = coeffs
     nat.check(
         nat.lib().qsb_jit_run_pass(compiled.func, src_ptr, dst_ptr, compiled.tdesc.ctypes.data, compiled.n_tiles,
-                                   coeffs.ctypes.data if len(coeffs) else None, len(coeffs), compiled.threads,
-                                   compiled.smem, stream_ptr),
+                                   tables.ctypes.data if len(tables) else None, len(tables),
+                                   params.ctypes.data, params.nbytes, compiled.threads, compiled.smem, stream_ptr),
         "jit_run_pass",
     )
