@@ -64,6 +64,22 @@ __device__ __forceinline__ double2 cfz(const double* cf, int k) { return make_do
 __device__ __forceinline__ C toC(double2 z) { C r; r.x = (R)z.x; r.y = (R)z.y; return r; }
 struct CP { R v[NCOEF]; };
 __device__ __forceinline__ C mkC(R a, R b) { C r; r.x = a; r.y = b; return r; }
+#if QSB_F32X2
+// packed FP32 pairs (sm_100 FFMA2/FADD2): one instruction per complex64 component pair
+__device__ __forceinline__ unsigned long long pk(float2 v) {
+  unsigned long long r; asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y)); return r; }
+__device__ __forceinline__ float2 upk(unsigned long long v) {
+  float2 r; asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v)); return r; }
+__device__ __forceinline__ float2 f2fma(float s, float2 x, float2 y) {  // s*x + y
+  unsigned long long r; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(make_float2(s, s))), "l"(pk(x)), "l"(pk(y)));
+  return upk(r); }
+__device__ __forceinline__ float2 f2mul(float s, float2 x) {
+  unsigned long long r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(make_float2(s, s))), "l"(pk(x))); return upk(r); }
+__device__ __forceinline__ float2 f2add(float2 x, float2 y) {
+  unsigned long long r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(x)), "l"(pk(y))); return upk(r); }
+__device__ __forceinline__ float2 f2sub(float2 x, float2 y) {
+  unsigned long long r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(x)), "l"(pk(y))); return upk(r); }
+#endif
 // coefficient reads are indexed by `zo` (always 0, re-read from shared memory before every op):
 // ptxas can neither hoist them out of the tile loop nor bundle them across ops, so each op's
 // coefficients occupy (uniform) registers only while that op runs
@@ -431,78 +447,143 @@ class _Gen:
                 if s & (1 << ib):
                     continue
                 t = s | (1 << ib)
+                if self.dtype == nat.QSB_C64:
+                    self.emit(f"      {{ const C x0 = v{self.vm[s]}, x1 = v{self.vm[t]}; v{self.vm[s]} = f2add(x0, x1);"
+                              f" v{self.vm[t]} = f2sub(x0, x1); }}")
+                    continue
                 self.emit(f"      {{ const C x0 = v{self.vm[s]}, x1 = v{self.vm[t]}; v{self.vm[s]}.x = x0.x + x1.x; v{self.vm[s]}.y = x0.y + x1.y;"
                           f" v{self.vm[t]}.x = x0.x - x1.x; v{self.vm[t]}.y = x0.y - x1.y; }}")
             self.emit("    }")
             return
-        self.emit(f"    {{ // G1 slot bit {ib} kind {kind}")
+        self.emit(f"    {{ // G1 slot bit {ib}")
         if gmask:
             self.emit(f"    if (((base | gt{self.li}) & {gmask}ull) == {gval}ull) {{")
-        if kind == 1:
-            ci = self.cf([m[0], m[2], m[4], m[6]])
-            self.emit(f"      const R a00 = PV({ci}), a01 = PV({ci + 1}), a10 = PV({ci + 2}), a11 = PV({ci + 3});")
-        elif kind == 0:
-            ci = self.cf(m)
-            for r, nm in enumerate(("a00", "a01", "a10", "a11")):
-                self.emit(f"      const C {nm} = PZ({ci + 2 * r});")
-        for s in range(A):
-            if s & (1 << ib) or (s & rmask) != rval:
-                continue
-            t = s | (1 << ib)
-            if kind == 2:
+        if kind == 2:
+            for s in range(A):
+                if s & (1 << ib) or (s & rmask) != rval:
+                    continue
+                t = s | (1 << ib)
                 self.emit(f"      {{ const C x = v{self.vm[s]}; v{self.vm[s]} = v{self.vm[t]}; v{self.vm[t]} = x; }}")
-            elif kind == 1:
-                self.emit(f"      {{ const C x0 = v{self.vm[s]}, x1 = v{self.vm[t]};"
-                          f" v{self.vm[s]}.x = fma(a01, x1.x, a00 * x0.x); v{self.vm[s]}.y = fma(a01, x1.y, a00 * x0.y);"
-                          f" v{self.vm[t]}.x = fma(a11, x1.x, a10 * x0.x); v{self.vm[t]}.y = fma(a11, x1.y, a10 * x0.y); }}")
-            else:
-                self.emit(f"      {{ const C x0 = v{self.vm[s]}, x1 = v{self.vm[t]};"
-                          f" C y0 = cm(a00, x0), y1 = cm(a10, x0);"
-                          f" y0.x = fma(a01.x, x1.x, y0.x); y0.x = fma(-a01.y, x1.y, y0.x);"
-                          f" y0.y = fma(a01.x, x1.y, y0.y); y0.y = fma(a01.y, x1.x, y0.y);"
-                          f" y1.x = fma(a11.x, x1.x, y1.x); y1.x = fma(-a11.y, x1.y, y1.x);"
-                          f" y1.y = fma(a11.x, x1.y, y1.y); y1.y = fma(a11.y, x1.x, y1.y);"
-                          f" v{self.vm[s]} = y0; v{self.vm[t]} = y1; }}")
+        else:
+            mat = [complex(m[2 * k], m[2 * k + 1]) for k in range(4)]
+            coef = self.matrix_coeffs(mat, 2)
+            for s in range(A):
+                if s & (1 << ib) or (s & rmask) != rval:
+                    continue
+                self.emit_matvec(coef, [s, s | (1 << ib)])
         if gmask:
             self.emit("    }")
         self.emit("    }")
+
+    def matrix_coeffs(self, mat, d):
+        """Per-entry structure of a d x d gate matrix: ('z',) exact zero (skipped), ('1',)/('-1',)
+        exact +-1 (no multiply), ('r', k) real, ('i', k) imaginary, ('c', k) complex -- k indexes
+        the parameter array.  The structure is part of the kernel source (so e.g. every fSim or
+        every Trotter ZZ+X term shares one kernel), the values are runtime coefficients."""
+        out = []
+        for z in mat:
+            if z == 0:
+                out.append(("z",))
+            elif z == 1:
+                out.append(("1",))
+            elif z == -1:
+                out.append(("-1",))
+            elif z.imag == 0:
+                out.append(("r", self.cf([z.real])))
+            elif z.real == 0:
+                out.append(("i", self.cf([z.imag])))
+            else:
+                out.append(("c", self.cf([z.real, z.imag])))
+        return out
+
+    def emit_matvec_f32x2(self, coef, slots):
+        """complex64 y = M x with packed FP32 pairs: a real entry is one FFMA2 on (x.re, x.im),
+        an imaginary one an FFMA2 on i*x = (-x.im, x.re) (formed once per input column)."""
+        d = len(slots)
+        names = [f"v{self.vm[s]}" for s in slots]
+        self.emit("      { const C " + ", ".join(f"x{c} = {names[c]}" for c in range(d)) + ";")
+        for c in range(d):
+            if any(coef[r * d + c][0] in ("i", "c") for r in range(d)):
+                self.emit(f"        const C ix{c} = mkC(-x{c}.y, x{c}.x);")
+        for r in range(d):
+            y = None
+            for c in range(d):
+                e = coef[r * d + c]
+                if e[0] == "z":
+                    continue
+                if e[0] == "1":
+                    y = f"x{c}" if y is None else f"f2add({y}, x{c})"
+                elif e[0] == "-1":
+                    y = f"mkC(-x{c}.x, -x{c}.y)" if y is None else f"f2sub({y}, x{c})"
+                elif e[0] == "r":
+                    y = f"f2mul(PV({e[1]}), x{c})" if y is None else f"f2fma(PV({e[1]}), x{c}, {y})"
+                elif e[0] == "i":
+                    y = f"f2mul(PV({e[1]}), ix{c})" if y is None else f"f2fma(PV({e[1]}), ix{c}, {y})"
+                else:
+                    y = f"f2mul(PV({e[1]}), x{c})" if y is None else f"f2fma(PV({e[1]}), x{c}, {y})"
+                    y = f"f2fma(PV({e[1] + 1}), ix{c}, {y})"
+            self.emit(f"        {names[r]} = {y if y is not None else 'mkC(0.f, 0.f)'};")
+        self.emit("      }")
+
+    def emit_matvec(self, coef, slots):
+        """y = M x over the amplitudes in `slots` (matrix row/col index = position in `slots`),
+        skipping zero entries; one FMA chain per output component."""
+        if self.dtype == nat.QSB_C64:
+            return self.emit_matvec_f32x2(coef, slots)
+        d = len(slots)
+        names = [f"v{self.vm[s]}" for s in slots]
+        self.emit("      { const C " + ", ".join(f"x{c} = {names[c]}" for c in range(d)) + ";")
+        for r in range(d):
+            ex, ey = None, None  # expressions accumulated so far (strings) for .x and .y
+
+            def acc(cur, term_mul, a, b):
+                # cur + a*b (a*b when cur is None); a may be None for +-1 (pure add / copy)
+                if cur is None:
+                    return term_mul
+                return f"fma({a}, {b}, {cur})" if a is not None else f"({cur} + {b})"
+
+            lines = []
+            for c in range(d):
+                e = coef[r * d + c]
+                xc = f"x{c}"
+                if e[0] == "z":
+                    continue
+                if e[0] in ("1", "-1"):
+                    sg = "" if e[0] == "1" else "-"
+                    ex = f"{sg}{xc}.x" if ex is None else (f"({ex} + {xc}.x)" if not sg else f"({ex} - {xc}.x)")
+                    ey = f"{sg}{xc}.y" if ey is None else (f"({ey} + {xc}.y)" if not sg else f"({ey} - {xc}.y)")
+                elif e[0] == "r":
+                    a = f"PV({e[1]})"
+                    ex = f"{a} * {xc}.x" if ex is None else f"fma({a}, {xc}.x, {ex})"
+                    ey = f"{a} * {xc}.y" if ey is None else f"fma({a}, {xc}.y, {ey})"
+                elif e[0] == "i":
+                    b = f"PV({e[1]})"
+                    ex = f"-{b} * {xc}.y" if ex is None else f"fma(-{b}, {xc}.y, {ex})"
+                    ey = f"{b} * {xc}.x" if ey is None else f"fma({b}, {xc}.x, {ey})"
+                else:
+                    a, b = f"PV({e[1]})", f"PV({e[1] + 1})"
+                    ex = f"{a} * {xc}.x" if ex is None else f"fma({a}, {xc}.x, {ex})"
+                    ex = f"fma(-{b}, {xc}.y, {ex})"
+                    ey = f"{a} * {xc}.y" if ey is None else f"fma({a}, {xc}.y, {ey})"
+                    ey = f"fma({b}, {xc}.x, {ey})"
+            if ex is None:
+                ex = ey = "(R)0"
+            self.emit(f"        {names[r]}.x = {ex}; {names[r]}.y = {ey};")
+        self.emit("      }")
 
     def gen_g2(self, a):
         w, A = self.w, self.A
         ih, il, kind, gmask, gval, rmask, rval = w[a:a + 7]
         m = [_w2d(x) for x in w[a + 7:a + 39]]
-        self.emit(f"    {{ // G2 slot bits {ih},{il} kind {kind}")
+        self.emit(f"    {{ // G2 slot bits {ih},{il}")
         if gmask:
             self.emit(f"    if (((base | gt{self.li}) & {gmask}ull) == {gval}ull) {{")
-        if kind == 1:
-            ci = self.cf([m[2 * k] for k in range(16)])
-            self.emit("      const R " + ", ".join(f"mm{k} = PV({ci + k})" for k in range(16)) + ";")
-        else:
-            ci = self.cf(m)
-            self.emit("      const C " + ", ".join(f"mm{k} = PZ({ci + 2 * k})" for k in range(16)) + ";")
+        mat = [complex(m[2 * k], m[2 * k + 1]) for k in range(16)]
+        coef = self.matrix_coeffs(mat, 4)
         for s in range(A):
             if s & ((1 << ih) | (1 << il)) or (s & rmask) != rval:
                 continue
-            idx = [s, s | (1 << il), s | (1 << ih), s | (1 << ih) | (1 << il)]
-            self.emit("      { const C x0 = v%d, x1 = v%d, x2 = v%d, x3 = v%d;" % tuple(self.vm[i] for i in idx))
-            for r in range(4):
-                if kind == 1:
-                    self.emit(f"        {{ C y; y.x = mm{4*r} * x0.x; y.y = mm{4*r} * x0.y;"
-                              f" y.x = fma(mm{4*r+1}, x1.x, y.x); y.y = fma(mm{4*r+1}, x1.y, y.y);"
-                              f" y.x = fma(mm{4*r+2}, x2.x, y.x); y.y = fma(mm{4*r+2}, x2.y, y.y);"
-                              f" y.x = fma(mm{4*r+3}, x3.x, y.x); y.y = fma(mm{4*r+3}, x3.y, y.y); v{self.vm[idx[r]]} = y; }}")
-                else:
-                    terms = []
-                    for c in range(4):
-                        mc = f"mm{4*r+c}"
-                        xc = f"x{c}"
-                        if c == 0:
-                            terms.append(f"C y = cm({mc}, {xc});")
-                        else:
-                            terms.append(f"y.x = fma({mc}.x, {xc}.x, y.x); y.x = fma(-{mc}.y, {xc}.y, y.x);"
-                                         f" y.y = fma({mc}.x, {xc}.y, y.y); y.y = fma({mc}.y, {xc}.x, y.y);")
-                    self.emit("        { " + " ".join(terms) + f" v{self.vm[idx[r]]} = y; }}")
-            self.emit("      }")
+            self.emit_matvec(coef, [s, s | (1 << il), s | (1 << ih), s | (1 << ih) | (1 << il)])
         if gmask:
             self.emit("    }")
         self.emit("    }")
@@ -592,7 +673,7 @@ class _Gen:
                    f"          const int co[5] = {{{', '.join(coords)}}};\n"
                    f"          tma5(d + (u64)k * {call_bytes}u, &tmap, co, &sm.full[s]);\n"
                    f"        }}")
-        defs = (f"#define R {real}\n#define C {real}2\n#define KB {K}\n#define HBB {self.HB}\n#define GB {self.G}\n#define STAGES {STAGES}\n"
+        defs = (f"#define QSB_F32X2 {1 if self.dtype == nat.QSB_C64 else 0}\n#define R {real}\n#define C {real}2\n#define KB {K}\n#define HBB {self.HB}\n#define GB {self.G}\n#define STAGES {STAGES}\n"
                 f"#define CONSUMERS {self.consumers}\n#define MAXPIV {MAX_PIV}\n#define NPIV {self.npiv}\n"
                 f"#define NCOEF {max(1, len(self.coeffs))}\n#define NTAB {len(self.tables)}\n")
         issue = f"""      {{ // producer warp: fetch tile c into stage s (tile number tno)
