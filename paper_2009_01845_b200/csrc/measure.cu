@@ -233,19 +233,32 @@ __global__ void __launch_bounds__(1024) k_scan_top(double* __restrict__ v, uint6
   }
 }
 
-// Binade of an approximate prefix value: -100000 for zero.  "risky" when within 2^-16
-// (relative) of a power of two or in the subnormal-adjacent range.
-__device__ __forceinline__ int approx_binade(double s, bool* risky) {
+// Binade of an approximate prefix value: -100000 for zero.  "risky" when within `margin`
+// (relative) of a power of two or in the subnormal-adjacent range.  The strictly sequential
+// prefix of n nonnegative terms differs from the exact one by at most (n-1)*2^-53 relative, the
+// approximate (blocked) prefix by far less, so margin = 4 * 2^ceil(log2 n) * 2^-53 (at least
+// 2^-40, at most 2^-16) classifies every element whose true prefix could sit on the other side
+// of a power of two as serial.
+__device__ __forceinline__ int approx_binade(double s, double margin, bool* risky) {
   if (s <= 0.0) {
     *risky = false;
     return -100000;
   }
   int e;
   const double m = frexp(s, &e);  // s = m * 2^e, m in [0.5, 1)
-  const double lo = 0.5 * (1.0 + 1.52587890625e-05);   // 2^-16 margins
-  const double hi = 1.0 - 1.52587890625e-05;
+  const double lo = 0.5 * (1.0 + margin);
+  const double hi = 1.0 - margin;
   *risky = (m < lo) || (m > hi) || (e < -1000);
   return e - 1;  // s in [2^(e-1), 2^e)
+}
+
+static double risky_margin(uint64_t n) {
+  int lg = 0;
+  while ((1ull << lg) < n) ++lg;
+  int ex = lg + 2 - 53;
+  if (ex < -40) ex = -40;
+  if (ex > -16) ex = -16;
+  return ldexp(1.0, ex);
 }
 
 // Pass B: classify every element, build per-block head pieces / serial lists.
@@ -287,7 +300,7 @@ __device__ __forceinline__ Piece elem_piece(double p, int e) {
 // then a block-level scan of pieces with "serial" resets.  To keep the block code simple the
 // per-element classification is written to global scratch and the block structure is
 // assembled by a warp-serial walk over thread chunks.
-__global__ void __launch_bounds__(kMT) k_classify(const double* __restrict__ p, uint64_t n,
+__global__ void __launch_bounds__(kMT) k_classify(const double* __restrict__ p, uint64_t n, double margin,
                                                   const double* __restrict__ block_prefix,
                                                   unsigned char* __restrict__ serial,
                                                   int* __restrict__ binade) {
@@ -316,14 +329,14 @@ __global__ void __launch_bounds__(kMT) k_classify(const double* __restrict__ p, 
   double s = sh[threadIdx.x];
   // previous element's class needs the prefix of element t0-1 = s (exclusive prefix)
   bool prev_risky;
-  int prev_e = (t0 == 0) ? -100001 : approx_binade(s, &prev_risky);
+  int prev_e = (t0 == 0) ? -100001 : approx_binade(s, margin, &prev_risky);
   if (t0 == 0) prev_risky = false;
 #pragma unroll
   for (int it = 0; it < kScanItems; ++it) {
     const uint64_t i = t0 + it;
     s += vals[it];
     bool risky;
-    const int e = approx_binade(s, &risky);
+    const int e = approx_binade(s, margin, &risky);
     if (i < n) {
       const bool ser = risky || prev_risky || (e != prev_e && e != -100000) || (e == -100000 && prev_e != -100000 && prev_e != -100001);
       serial[i] = ser ? 1 : 0;
@@ -433,24 +446,157 @@ __global__ void __launch_bounds__(32) k_block_pieces(const double* __restrict__ 
   }
 }
 
-// Pass D: one thread walks blocks and serial points in order.
-__global__ void k_stitch(const double* __restrict__ p, uint64_t n_blocks, const Piece* __restrict__ head,
-                         const unsigned int* __restrict__ serial_count, const Piece* __restrict__ after,
-                         const unsigned long long* __restrict__ serial_idx, double* __restrict__ block_start,
-                         double* __restrict__ serial_val) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double c = 0.0;
-  unsigned int slot = 0;
-  for (uint64_t b = 0; b < n_blocks; ++b) {
-    block_start[b] = c;
-    c = piece_apply(head[b], c);
-    const unsigned int ns = serial_count[b];
-    for (unsigned int k = 0; k < ns; ++k, ++slot) {
-      c = __dadd_rn(c, p[serial_idx[slot]]);
-      serial_val[slot] = c;
-      c = piece_apply(after[slot], c);
+// Pass D (parallel form): the chain visits every block head, but between two serial points
+// every map is a piece of one binade, so the heads of consecutive blocks compose with a
+// segmented scan (segments start after blocks that contain serial points).  A single thread
+// then walks only the serial points: c = fl(c + p_serial), the serial's after-piece, and (for
+// the last serial of a block) the composed heads up to the next serial's block.  Finally
+// every block start is its run's start value mapped through the run prefix.
+struct SegP {
+  Piece p;             // composed heads from the segment start through this block
+  unsigned int start;  // first block of the segment
+  int flag;            // a segment starts inside the combined range
+};
+
+__device__ __forceinline__ SegP seg_then(const SegP& a, const SegP& b) {
+  if (b.flag) return b;
+  SegP r;
+  r.p = piece_then(a.p, b.p);
+  r.start = a.start;
+  r.flag = a.flag;
+  return r;
+}
+
+constexpr int kSegPer = 4;                    // blocks per thread
+constexpr int kSegCta = kMT * kSegPer;        // blocks per CTA
+
+__device__ __forceinline__ SegP seg_leaf(const Piece* head, const unsigned int* cnt, uint64_t b) {
+  SegP v;
+  v.p = head[b];
+  v.start = (unsigned int)b;
+  v.flag = (b == 0 || cnt[b - 1] != 0) ? 1 : 0;
+  return v;
+}
+
+// per-CTA inclusive segmented scan of block heads; CTA aggregate out
+__global__ void __launch_bounds__(kMT) k_seg_local(const Piece* __restrict__ head, const unsigned int* __restrict__ cnt,
+                                                   uint64_t nb, SegP* __restrict__ out, SegP* __restrict__ agg) {
+  __shared__ SegP sh[kMT];
+  const uint64_t b0 = (uint64_t)blockIdx.x * kSegCta + (uint64_t)threadIdx.x * kSegPer;
+  SegP v[kSegPer];
+  SegP acc;
+  bool have = false;
+  for (int k = 0; k < kSegPer; ++k) {
+    const uint64_t b = b0 + k;
+    if (b < nb) {
+      v[k] = seg_leaf(head, cnt, b);
+      acc = have ? seg_then(acc, v[k]) : v[k];
+      have = true;
     }
   }
+  if (!have) {
+    acc.p = piece_id();
+    acc.start = 0;
+    acc.flag = 0;
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 1; o < kMT; o <<= 1) {
+    SegP x = sh[threadIdx.x];
+    if ((int)threadIdx.x >= o) x = seg_then(sh[threadIdx.x - o], x);
+    __syncthreads();
+    sh[threadIdx.x] = x;
+    __syncthreads();
+  }
+  SegP run;
+  bool hrun = threadIdx.x > 0;
+  if (hrun) run = sh[threadIdx.x - 1];
+  for (int k = 0; k < kSegPer; ++k) {
+    const uint64_t b = b0 + k;
+    if (b >= nb) break;
+    run = hrun ? seg_then(run, v[k]) : v[k];
+    hrun = true;
+    out[b] = run;
+  }
+  if (threadIdx.x == kMT - 1) agg[blockIdx.x] = sh[kMT - 1];
+}
+
+// exclusive scan of the CTA aggregates (one CTA; serial chunks per thread)
+__global__ void __launch_bounds__(kMT) k_seg_top(SegP* __restrict__ agg, uint64_t na) {
+  __shared__ SegP sh[kMT];
+  const uint64_t per = (na + kMT - 1) / kMT;
+  const uint64_t lo = threadIdx.x * per;
+  SegP acc;
+  bool have = false;
+  for (uint64_t i = lo; i < lo + per && i < na; ++i) {
+    acc = have ? seg_then(acc, agg[i]) : agg[i];
+    have = true;
+  }
+  if (!have) {
+    acc.p = piece_id();
+    acc.start = 0;
+    acc.flag = 0;
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 1; o < kMT; o <<= 1) {
+    SegP x = sh[threadIdx.x];
+    if ((int)threadIdx.x >= o) x = seg_then(sh[threadIdx.x - o], x);
+    __syncthreads();
+    sh[threadIdx.x] = x;
+    __syncthreads();
+  }
+  // rewrite as exclusive prefixes: agg[i] = combination of agg[0..i-1] (only read for i > 0)
+  SegP run;
+  bool hrun = threadIdx.x > 0;
+  if (hrun) run = sh[threadIdx.x - 1];
+  for (uint64_t i = lo; i < lo + per && i < na; ++i) {
+    const SegP x = agg[i];
+    if (hrun) agg[i] = run;
+    run = hrun ? seg_then(run, x) : x;
+    hrun = true;
+  }
+}
+
+__global__ void __launch_bounds__(kMT) k_seg_fix(SegP* __restrict__ out, uint64_t nb, const SegP* __restrict__ agg) {
+  const uint64_t b = (uint64_t)blockIdx.x * kMT + threadIdx.x;
+  if (b >= nb) return;
+  const uint64_t c = b / kSegCta;
+  if (c == 0) return;
+  SegP v = out[b];
+  if (!v.flag) out[b] = seg_then(agg[c], v);
+}
+
+// the serial walk: only serial points (ns of them, sorted by index)
+__global__ void k_stitch_serial(const double* __restrict__ p, uint64_t ns, const unsigned long long* __restrict__ sidx,
+                                const Piece* __restrict__ after, const SegP* __restrict__ run,
+                                double* __restrict__ serial_val, double* __restrict__ run_start) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  run_start[0] = 0.0;
+  if (ns == 0) return;
+  unsigned long long b = sidx[0] / kScanBlock;
+  double c = piece_apply(run[b].p, 0.0);
+  for (uint64_t k = 0; k < ns; ++k) {
+    c = __dadd_rn(c, p[sidx[k]]);
+    serial_val[k] = c;
+    c = piece_apply(after[k], c);
+    const unsigned long long bn = (k + 1 < ns) ? sidx[k + 1] / kScanBlock : ~0ull;
+    if (bn != b) {  // last serial of block b: the next run starts at block b + 1
+      run_start[b + 1] = c;
+      if (bn != ~0ull) c = piece_apply(run[bn].p, c);
+      b = bn;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kMT) k_block_starts(const SegP* __restrict__ run, uint64_t nb,
+                                                      const double* __restrict__ run_start,
+                                                      double* __restrict__ block_start) {
+  const uint64_t b = (uint64_t)blockIdx.x * kMT + threadIdx.x;
+  if (b >= nb) return;
+  const unsigned int s = run[b].start;
+  const double c0 = run_start[s];
+  block_start[b] = (b == s) ? c0 : piece_apply(run[b - 1].p, c0);
 }
 
 // Pass E: materialize c_i per element (one thread per 16-element chunk after a block-level
@@ -744,6 +890,11 @@ extern "C" size_t qsb_cumsum_scratch_bytes(uint64_t n) {
   b = (b + 255) & ~(size_t)255;
   b += nb * sizeof(Piece);               // heads
   b += nb * sizeof(double);              // block starts
+  b = (b + 255) & ~(size_t)255;
+  b += nb * sizeof(SegP);                // segmented head prefixes
+  b += ((nb + kSegCta - 1) / kSegCta + 1) * sizeof(SegP);  // CTA aggregates
+  b = (b + 255) & ~(size_t)255;
+  b += (nb + 1) * sizeof(double);        // run start values
   b += 256;
   return b;
 }
@@ -777,10 +928,19 @@ extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cu
   Piece* head = reinterpret_cast<Piece*>(w);
   w += nb * sizeof(Piece);
   double* bstart = reinterpret_cast<double*>(w);
+  w += nb * sizeof(double);
+  w = reinterpret_cast<char*>(((uintptr_t)w + 255) & ~(uintptr_t)255);
+  SegP* runp = reinterpret_cast<SegP*>(w);
+  w += nb * sizeof(SegP);
+  const uint64_t na = (nb + kSegCta - 1) / kSegCta;
+  SegP* agg = reinterpret_cast<SegP*>(w);
+  w += (na + 1) * sizeof(SegP);
+  w = reinterpret_cast<char*>(((uintptr_t)w + 255) & ~(uintptr_t)255);
+  double* rstart = reinterpret_cast<double*>(w);
 
   k_scan_block_sums<<<(int)nb, kMT, 0, st>>>(probs, n, bpre);
   k_scan_top<<<1, 1024, 0, st>>>(bpre, nb);
-  k_classify<<<(int)nb, kMT, 0, st>>>(probs, n, bpre, serial, binade);
+  k_classify<<<(int)nb, kMT, 0, st>>>(probs, n, risky_margin(n), bpre, serial, binade);
   k_count_serial<<<(int)nb, kMT, 0, st>>>(serial, n, cnt);
   unsigned int* d_total = nullptr;
   // total count lives right after `base` in pinned host-visible memory would need a sync; we
@@ -821,7 +981,11 @@ extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cu
   double* sval = reinterpret_cast<double*>(sb);
 
   k_block_pieces<<<(int)nb, 32, 0, st>>>(probs, n, serial, binade, base, head, after, sidx);
-  k_stitch<<<1, 1, 0, st>>>(probs, nb, head, cnt, after, sidx, bstart, sval);
+  k_seg_local<<<(int)na, kMT, 0, st>>>(head, cnt, nb, runp, agg);
+  k_seg_top<<<1, kMT, 0, st>>>(agg, na);
+  k_seg_fix<<<(int)((nb + kMT - 1) / kMT), kMT, 0, st>>>(runp, nb, agg);
+  k_stitch_serial<<<1, 1, 0, st>>>(probs, ns, sidx, after, runp, sval, rstart);
+  k_block_starts<<<(int)((nb + kMT - 1) / kMT), kMT, 0, st>>>(runp, nb, rstart, bstart);
   k_materialize<<<(int)nb, 32, 0, st>>>(probs, n, serial, binade, bstart, base, sval, cum);
   k_copy_last<<<1, 1, 0, st>>>(cum, n, reinterpret_cast<double*>(d_tot) + 1);
   k_normalize<<<grid_for(n), kMT, 0, st>>>(cum, n, reinterpret_cast<const double*>(d_tot) + 1);

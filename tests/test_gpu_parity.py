@@ -246,7 +246,8 @@ def test_cli_shots_digest(cuda, nq, shots, seed):
     assert hashlib.sha256(res.samples.tobytes()).hexdigest() == str(g[f"digest_{nq}_{shots}_{seed}"])
 
 
-@pytest.mark.parametrize("n,kind", [(16, "random"), (20, "random"), (20, "qft"), (22, "sparse"), (21, "tiny")])
+@pytest.mark.parametrize("n,kind", [(16, "random"), (20, "random"), (20, "qft"), (22, "sparse"), (21, "tiny"),
+                                    (24, "uniform"), (24, "near_uniform"), (25, "random")])
 def test_exact_parallel_cumsum_equals_sequential(cuda, n, kind):
     import torch
 
@@ -263,6 +264,10 @@ def test_exact_parallel_cumsum_equals_sequential(cuda, n, kind):
     elif kind == "sparse":
         p = rng.random(1 << n) * (rng.random(1 << n) < 0.01)
         p[:1000] = 0.0
+    elif kind == "uniform":  # prefixes hit powers of two exactly
+        p = np.full(1 << n, 2.0 ** -n)
+    elif kind == "near_uniform":  # prefixes graze powers of two
+        p = (1.0 + 1e-13 * rng.standard_normal(1 << n)) * 2.0 ** -n
     else:
         p = rng.random(1 << n) * 10.0 ** rng.integers(-300, 1, 1 << n)
     want = np.cumsum(p)
