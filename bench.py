@@ -250,6 +250,8 @@ def run_gpu_arm(args, rank, world):
             e2e_times.append(dt)
     e2e = statistics.mean(e2e_times)
 
+    others = {} if args.no_extra_workloads else extra_workloads(q, engine, n, peak)
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         threads = cpu_threads()
@@ -277,12 +279,52 @@ def run_gpu_arm(args, rank, world):
                      "bytes_per_launch": pass_bytes, "launches": len(launches)},
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "qft_circuit(n).execute() + state D2H (pinned)"},
+        "workloads": others,
         "gpu_launches": len(plan.steps) * args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def extra_workloads(q, engine, n, peak):
+    """The other BASELINE configs that fit one GPU, timed the same way (device time per circuit,
+    state resident, warm-ups first): variational (RY layers + CZ ladder, L=5, fused) in c128 and
+    c64, and the QFT in c64.  hbm_frac = state sweeps x sweep bytes / time / measured peak."""
+    import numpy as np
+    import torch
+
+    from paper_2009_01845_b200.fusion import PassStep
+
+    out = {}
+    params = np.random.default_rng(42).uniform(0, 2 * math.pi, n * 11)
+    cases = [("variational_L5_fused_c128", q.variational_circuit(n, 5, params, fused=True), q.Precision.F64),
+             ("variational_L5_fused_c64", q.variational_circuit(n, 5, params, fused=True), q.Precision.F32),
+             ("qft_c64", q.qft_circuit(n), q.Precision.F32)]
+    for name, circ, prec in cases:
+        st = q.uniform_state(n, prec)
+        plan = engine.plan_for_state(st, circ.queue)
+        holder: dict = {}
+        for _ in range(3):
+            engine.run_plan(st, plan, holder)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        a.record()
+        for _ in range(reps):
+            engine.run_plan(st, plan, holder)
+        b.record()
+        torch.cuda.synchronize()
+        sec = a.elapsed_time(b) / reps / 1e3
+        sweeps = plan.state_sweeps()
+        gbs = sweeps * 2 * (1 << n) * prec.itemsize / sec / 1e9
+        out[name] = {"seconds": sec, "gates": len(circ.queue),
+                     "passes": sum(1 for s_ in plan.steps if isinstance(s_, PassStep)),
+                     "effective_gbs": gbs, "hbm_frac": gbs / peak}
+        del st, holder
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_distributed_arm(args, rank, world):
@@ -368,6 +410,7 @@ def main():
     ap.add_argument("--precision", choices=["f64", "f32"], default="f64")
     ap.add_argument("--workload", choices=["qft", "variational"], default="qft")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra-workloads", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
