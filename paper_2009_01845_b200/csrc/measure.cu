@@ -167,12 +167,19 @@ __device__ __forceinline__ Piece piece_then(const Piece& a, const Piece& b) {
   return r;
 }
 
+// x * 2^k, exact (power-of-two scaling of a value whose result is normal): one multiply when
+// 2^k is a normal double, else the library ldexp
+__device__ __forceinline__ double pow2_scale(double x, int k) {
+  if (k >= -1022 && k <= 1023) return x * __longlong_as_double((long long)(1023 + k) << 52);
+  return ldexp(x, k);
+}
+
 __device__ __forceinline__ double piece_apply(const Piece& q, double c) {
   if (q.e == -100000 || (q.d0 == 0 && q.d1 == 0)) return c;
   // K = c / 2^(e-52) exactly
-  const long long K = (long long)ldexp(c, 52 - q.e);
+  const long long K = (long long)pow2_scale(c, 52 - q.e);
   const long long K2 = K + ((K & 1) ? q.d1 : q.d0);
-  return ldexp((double)K2, q.e - 52);
+  return pow2_scale((double)K2, q.e - 52);
 }
 
 // Fast single-thread fallback (also the reference semantics): c_i = fl(c_{i-1} + p_i).
@@ -187,25 +194,6 @@ __global__ void k_cumsum_serial(const double* __restrict__ p, uint64_t n, double
 
 constexpr int kScanItems = 16;                 // elements per thread
 constexpr int kScanBlock = kMT * kScanItems;   // 4096 elements per block
-
-// Pass A: per block, an approximate inclusive prefix of p (plain fp64), block totals
-__global__ void __launch_bounds__(kMT) k_scan_block_sums(const double* __restrict__ p, uint64_t n,
-                                                         double* __restrict__ block_sum) {
-  __shared__ double sh[kMT];
-  const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
-  double acc = 0.0;
-  for (int it = 0; it < kScanItems; ++it) {
-    const uint64_t i = b0 + (uint64_t)threadIdx.x * kScanItems + it;
-    if (i < n) acc += p[i];
-  }
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  for (int s = kMT / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) block_sum[blockIdx.x] = sh[0];
-}
 
 // exclusive scan of the block sums (one block, sequential chunks per thread; approximate)
 __global__ void __launch_bounds__(1024) k_scan_top(double* __restrict__ v, uint64_t nb) {
@@ -261,15 +249,7 @@ static double risky_margin(uint64_t n) {
   return ldexp(1.0, ex);
 }
 
-// Pass B: classify every element, build per-block head pieces / serial lists.
-// Outputs per element: flag (serial?) stored in `cls` (1 = serial), piece of safe elements
-// folded per block into head / per-serial "after" pieces.
-struct BlockInfo {
-  Piece head;            // composed map from block start to the first serial element (excl.)
-  unsigned int n_serial; // serial elements in this block
-  unsigned int first_serial_slot;  // filled by the counting prefix
-};
-
+// piece of one safe element p inside binade e: K -> K + round(p / 2^(e-52)) (ties to even K+d)
 __device__ __forceinline__ Piece elem_piece(double p, int e) {
   Piece q;
   q.e = e;
@@ -279,7 +259,7 @@ __device__ __forceinline__ Piece elem_piece(double p, int e) {
     q.d1 = 0;
     return q;
   }
-  const double v = ldexp(p, 52 - e);  // p / u, exact
+  const double v = pow2_scale(p, 52 - e);  // p / u, exact
   const double m = floor(v);
   const double f = v - m;
   const long long mi = (long long)m;
@@ -296,155 +276,6 @@ __device__ __forceinline__ Piece elem_piece(double p, int e) {
   return q;
 }
 
-// Each block: sequentially (per thread chunk) compute approximate prefix, classes and pieces;
-// then a block-level scan of pieces with "serial" resets.  To keep the block code simple the
-// per-element classification is written to global scratch and the block structure is
-// assembled by a warp-serial walk over thread chunks.
-__global__ void __launch_bounds__(kMT) k_classify(const double* __restrict__ p, uint64_t n, double margin,
-                                                  const double* __restrict__ block_prefix,
-                                                  unsigned char* __restrict__ serial,
-                                                  int* __restrict__ binade) {
-  __shared__ double sh[kMT];
-  const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
-  const uint64_t t0 = b0 + (uint64_t)threadIdx.x * kScanItems;
-  double loc = 0.0;
-  double vals[kScanItems];
-#pragma unroll
-  for (int it = 0; it < kScanItems; ++it) {
-    const uint64_t i = t0 + it;
-    vals[it] = (i < n) ? p[i] : 0.0;
-    loc += vals[it];
-  }
-  sh[threadIdx.x] = loc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double run = block_prefix[blockIdx.x];
-    for (int t = 0; t < kMT; ++t) {
-      const double x = sh[t];
-      sh[t] = run;
-      run += x;
-    }
-  }
-  __syncthreads();
-  double s = sh[threadIdx.x];
-  // previous element's class needs the prefix of element t0-1 = s (exclusive prefix)
-  bool prev_risky;
-  int prev_e = (t0 == 0) ? -100001 : approx_binade(s, margin, &prev_risky);
-  if (t0 == 0) prev_risky = false;
-#pragma unroll
-  for (int it = 0; it < kScanItems; ++it) {
-    const uint64_t i = t0 + it;
-    s += vals[it];
-    bool risky;
-    const int e = approx_binade(s, margin, &risky);
-    if (i < n) {
-      const bool ser = risky || prev_risky || (e != prev_e && e != -100000) || (e == -100000 && prev_e != -100000 && prev_e != -100001);
-      serial[i] = ser ? 1 : 0;
-      binade[i] = e;
-    }
-    prev_e = e;
-    prev_risky = risky;
-  }
-}
-
-// Pass C: per block, compose pieces of the safe elements between serial points.
-//   head[b]      : map from block start to first serial (or block end)
-//   after[slot]  : for each serial element (in global order), the map of the safe run after it
-//                  up to the next serial element or block end
-__global__ void __launch_bounds__(32) k_block_pieces(const double* __restrict__ p, uint64_t n,
-                                                     const unsigned char* __restrict__ serial,
-                                                     const int* __restrict__ binade,
-                                                     const unsigned int* __restrict__ serial_base,
-                                                     Piece* __restrict__ head, Piece* __restrict__ after,
-                                                     unsigned long long* __restrict__ serial_idx) {
-  // one warp per block of kScanBlock elements; lane-chunked composition then a serial walk
-  // over the 32 lane chunks by lane 0 (pieces are tiny).
-  const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
-  const int per = kScanBlock / 32;
-  const uint64_t l0 = b0 + (uint64_t)threadIdx.x * per;
-  // lane-local: head piece (before first serial in chunk), count of serials, tail piece
-  Piece lhead = piece_id(), ltail = piece_id();
-  int nser = 0;
-  for (int k = 0; k < per; ++k) {
-    const uint64_t i = l0 + k;
-    if (i >= n) break;
-    if (serial[i]) {
-      ++nser;
-      ltail = piece_id();
-    } else {
-      const Piece q = elem_piece(p[i], binade[i]);
-      if (nser == 0)
-        lhead = piece_then(lhead, q);
-      else
-        ltail = piece_then(ltail, q);
-    }
-  }
-  // exclusive count of serials before this lane within the block
-  int incl = nser;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if ((int)threadIdx.x >= o) incl += v;
-  }
-  const int excl = incl - nser;
-  const unsigned int base = serial_base[blockIdx.x] + excl;
-  // per-lane: fill serial_idx and the "after" pieces of serials inside the chunk except the
-  // last one (whose after-piece continues into later lanes)
-  {
-    int s = 0;
-    Piece run = piece_id();
-    for (int k = 0; k < per; ++k) {
-      const uint64_t i = l0 + k;
-      if (i >= n) break;
-      if (serial[i]) {
-        if (s > 0) after[base + s - 1] = run;
-        serial_idx[base + s] = i;
-        ++s;
-        run = piece_id();
-      } else if (s > 0) {
-        run = piece_then(run, elem_piece(p[i], binade[i]));
-      }
-    }
-  }
-  // stitch lanes: the after-piece of the last serial of lane L continues through lanes L+1..
-  // until a lane that has a serial (absorbing that lane's head).  Block head = lanes' heads
-  // composed until the first lane with a serial.  Done serially by lane 0 via shared memory.
-  __shared__ Piece sh_head[32], sh_tail[32];
-  __shared__ int sh_n[32];
-  sh_head[threadIdx.x] = lhead;
-  sh_tail[threadIdx.x] = ltail;
-  sh_n[threadIdx.x] = nser;
-  __syncwarp();
-  if (threadIdx.x == 0) {
-    Piece bh = piece_id();
-    int L = 0;
-    for (; L < 32; ++L) {
-      bh = piece_then(bh, sh_head[L]);
-      if (sh_n[L]) break;
-    }
-    head[blockIdx.x] = bh;
-    // open "after" runs
-    unsigned int slot = serial_base[blockIdx.x];
-    bool open = false;
-    Piece run = piece_id();
-    unsigned int open_slot = 0;
-    for (int l = 0; l < 32; ++l) {
-      if (open) {
-        run = piece_then(run, sh_head[l]);
-        if (sh_n[l]) {
-          after[open_slot] = run;
-          open = false;
-        }
-      }
-      if (sh_n[l]) {
-        slot += sh_n[l];
-        open = true;
-        open_slot = slot - 1;
-        run = sh_tail[l];
-      }
-    }
-    if (open) after[open_slot] = run;
-  }
-}
 
 // Pass D (parallel form): the chain visits every block head, but between two serial points
 // every map is a piece of one binade, so the heads of consecutive blocks compose with a
@@ -599,95 +430,354 @@ __global__ void __launch_bounds__(kMT) k_block_starts(const SegP* __restrict__ r
   block_start[b] = (b == s) ? c0 : piece_apply(run[b - 1].p, c0);
 }
 
-// Pass E: materialize c_i per element (one thread per 16-element chunk after a block-level
-// walk of chunk starts), then normalise by the total.
-__global__ void __launch_bounds__(32) k_materialize(const double* __restrict__ p, uint64_t n,
-                                                    const unsigned char* __restrict__ serial,
-                                                    const int* __restrict__ binade,
-                                                    const double* __restrict__ block_start,
-                                                    const unsigned int* __restrict__ serial_base,
-                                                    const double* __restrict__ serial_val,
-                                                    double* __restrict__ c_out) {
-  const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
-  const int per = kScanBlock / 32;
-  const uint64_t l0 = b0 + (uint64_t)threadIdx.x * per;
-  // lane pieces: map over the lane chunk ignoring serials -> need value at chunk start.
-  // Compose per lane: if the chunk has a serial, the value at chunk end is "constant" from the
-  // last serial; else a pure piece.
-  Piece pure = piece_id();
-  int nser = 0;
-  Piece tail = piece_id();
-  for (int k = 0; k < per; ++k) {
-    const uint64_t i = l0 + k;
-    if (i >= n) break;
-    if (serial[i]) {
-      ++nser;
-      tail = piece_id();
-    } else {
-      const Piece q = elem_piece(p[i], binade[i]);
-      if (nser == 0)
-        pure = piece_then(pure, q);
-      else
-        tail = piece_then(tail, q);
-    }
+// ---- coalesced block kernels (round 1b) -----------------------------------------------------
+// Each 4096-element block is loaded with coalesced reads into a padded shared array (row of 16
+// elements per thread, stride 17 doubles: at most 2-way bank conflicts), every thread then walks
+// its 16 consecutive elements.  The classification (approximate prefix -> binade / risky) is a
+// shared device function, so the count, pieces and materialize kernels agree bit for bit.
+constexpr int kRow = kScanItems + 1;
+
+__device__ __forceinline__ void load_block(const double* __restrict__ p, uint64_t n, uint64_t b0, double* sh) {
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int j = threadIdx.x + k * kMT;
+    const uint64_t i = b0 + j;
+    sh[(j / kScanItems) * kRow + (j % kScanItems)] = (i < n) ? p[i] : 0.0;
   }
-  int incl = nser;
+  __syncthreads();
+}
+
+// exclusive block scan of one double per thread (warp shuffles + one warp over warp totals)
+__device__ __forceinline__ double block_excl_scan(double v, double* wsum) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double x = v;
+#pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if ((int)threadIdx.x >= o) incl += v;
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
-  const int excl = incl - nser;
-  __shared__ Piece sh_pure[32], sh_tail[32];
-  __shared__ int sh_n[32], sh_excl[32];
-  sh_pure[threadIdx.x] = pure;
-  sh_tail[threadIdx.x] = tail;
-  sh_n[threadIdx.x] = nser;
-  sh_excl[threadIdx.x] = excl;
-  __syncwarp();
-  __shared__ double sh_start[32];
-  if (threadIdx.x == 0) {
-    double c = block_start[blockIdx.x];
-    for (int l = 0; l < 32; ++l) {
-      sh_start[l] = c;
-      if (sh_n[l]) {
-        const unsigned int last = serial_base[blockIdx.x] + sh_excl[l] + sh_n[l] - 1;
-        c = piece_apply(sh_tail[l], serial_val[last]);
-      } else {
-        c = piece_apply(sh_pure[l], c);
-      }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    double t = (lane < kMT / 32) ? wsum[lane] : 0.0;
+    double u = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, u, o);
+      if (lane >= o) u += y;
     }
+    if (lane < kMT / 32) wsum[lane] = u - t;  // exclusive over warps
   }
-  __syncwarp();
-  double c = sh_start[threadIdx.x];
-  unsigned int slot = serial_base[blockIdx.x] + excl;
-  for (int k = 0; k < per; ++k) {
-    const uint64_t i = l0 + k;
-    if (i >= n) break;
-    if (serial[i]) {
-      c = serial_val[slot++];
-    } else {
-      Piece q = elem_piece(p[i], binade[i]);
-      c = piece_apply(q, c);
-    }
-    c_out[i] = c;
+  __syncthreads();
+  return wsum[w] + (x - v);
+}
+
+// per-thread classification of its 16 elements: serial bits and binades
+struct RowClass {
+  unsigned int serial;  // bit k: element k is serial
+  int e[kScanItems];
+};
+
+__device__ __forceinline__ void classify_row(const double* row, double s, bool first_elem_of_all, double margin,
+                                             uint64_t i0, uint64_t n, RowClass& rc) {
+  bool prev_risky = false;
+  int prev_e = first_elem_of_all ? -100001 : approx_binade(s, margin, &prev_risky);
+  rc.serial = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    s += row[k];
+    bool risky;
+    const int e = approx_binade(s, margin, &risky);
+    const bool ser = risky || prev_risky || (e != prev_e && e != -100000) ||
+                     (e == -100000 && prev_e != -100000 && prev_e != -100001);
+    if (i0 + k < n && ser) rc.serial |= 1u << k;
+    rc.e[k] = e;
+    prev_e = e;
+    prev_risky = risky;
   }
 }
 
-__global__ void k_count_serial(const unsigned char* __restrict__ serial, uint64_t n, unsigned int* __restrict__ cnt) {
-  __shared__ unsigned int sh[kMT];
+// common prologue: block load + approximate thread prefix + classification
+__device__ __forceinline__ void block_classify(const double* __restrict__ p, uint64_t n, double margin,
+                                               const double* __restrict__ block_prefix, double* sh, double* wsum,
+                                               RowClass& rc, uint64_t& i0) {
   const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
-  unsigned int c = 0;
-  for (int it = 0; it < kScanItems; ++it) {
-    const uint64_t i = b0 + (uint64_t)threadIdx.x * kScanItems + it;
-    if (i < n) c += serial[i];
+  load_block(p, n, b0, sh);
+  const double* row = sh + threadIdx.x * kRow;
+  double loc = 0.0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) loc += row[k];
+  const double s = block_prefix[blockIdx.x] + block_excl_scan(loc, wsum);
+  i0 = b0 + (uint64_t)threadIdx.x * kScanItems;
+  classify_row(row, s, i0 == 0, margin, i0, n, rc);
+}
+
+__global__ void __launch_bounds__(kMT) k_block_sums2(const double* __restrict__ p, uint64_t n,
+                                                     double* __restrict__ block_sum) {
+  __shared__ double wsum[kMT / 32];
+  const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const uint64_t i = b0 + threadIdx.x + (uint64_t)k * kMT;
+    if (i < n) acc += p[i];
   }
-  sh[threadIdx.x] = c;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
   __syncthreads();
-  for (int s = kMT / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-    __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kMT / 32; ++w) t += wsum[w];
+    block_sum[blockIdx.x] = t;
   }
-  if (threadIdx.x == 0) cnt[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(kMT) k_count2(const double* __restrict__ p, uint64_t n, double margin,
+                                                const double* __restrict__ block_prefix,
+                                                unsigned int* __restrict__ cnt) {
+  __shared__ double sh[kMT * kRow];
+  __shared__ double wsum[kMT / 32];
+  __shared__ unsigned int csum[kMT / 32];
+  RowClass rc;
+  uint64_t i0;
+  block_classify(p, n, margin, block_prefix, sh, wsum, rc, i0);
+  unsigned int c = __popc(rc.serial);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) csum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int t = 0;
+    for (int w = 0; w < kMT / 32; ++w) t += csum[w];
+    cnt[blockIdx.x] = t;
+  }
+}
+
+// element segments: a serial element starts a new (empty) segment; V_i = composition of the
+// safe elements' pieces since the last serial (or the block start).  Thread rows are combined
+// with a segmented scan over (has-serial, tail piece) pairs.
+struct RowSeg {
+  Piece v;   // composition over the combined range since its last serial (or its start)
+  int ser;   // the combined range contains a serial element
+};
+
+__device__ __forceinline__ RowSeg rowseg_then(const RowSeg& a, const RowSeg& b) {
+  if (b.ser) return b;
+  RowSeg r;
+  r.v = piece_then(a.v, b.v);
+  r.ser = a.ser;
+  return r;
+}
+
+__device__ __forceinline__ RowSeg rowseg_shfl_up(const RowSeg& x, int o) {
+  RowSeg r;
+  r.v.d0 = __shfl_up_sync(0xffffffffu, x.v.d0, o);
+  r.v.d1 = __shfl_up_sync(0xffffffffu, x.v.d1, o);
+  r.v.e = __shfl_up_sync(0xffffffffu, x.v.e, o);
+  r.v.pad = 0;
+  r.ser = __shfl_up_sync(0xffffffffu, x.ser, o);
+  return r;
+}
+
+// exclusive segmented scan of one RowSeg per thread: warp shuffles, then one warp over the
+// warp aggregates (combination order is the serial order, so results equal a serial walk)
+__device__ RowSeg block_excl_rowseg(RowSeg mine, RowSeg* sh) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  RowSeg x = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const RowSeg y = rowseg_shfl_up(x, o);
+    if (lane >= o) x = rowseg_then(y, x);
+  }
+  if (lane == 31) sh[w] = x;  // warp aggregate
+  __syncthreads();
+  if (w == 0) {
+    RowSeg t;
+    if (lane < kMT / 32) {
+      t = sh[lane];
+    } else {
+      t.v = piece_id();
+      t.ser = 0;
+    }
+    RowSeg u = t;
+#pragma unroll
+    for (int o = 1; o < kMT / 32; o <<= 1) {
+      const RowSeg y = rowseg_shfl_up(u, o);
+      if (lane >= o) u = rowseg_then(y, u);
+    }
+    if (lane < kMT / 32) sh[kMT / 32 + lane] = u;  // inclusive over warps
+  }
+  __syncthreads();
+  // exclusive value for this thread: (warps before) then (lanes before in this warp)
+  RowSeg in_warp = rowseg_shfl_up(x, 1);
+  RowSeg ex;
+  const bool have_w = w > 0;
+  const bool have_l = lane > 0;
+  if (have_w && have_l) ex = rowseg_then(sh[kMT / 32 + w - 1], in_warp);
+  else if (have_w) ex = sh[kMT / 32 + w - 1];
+  else if (have_l) ex = in_warp;
+  else {
+    ex.v = piece_id();
+    ex.ser = 0;
+  }
+  __syncthreads();
+  return ex;
+}
+
+__device__ __forceinline__ unsigned int block_excl_count(unsigned int c, unsigned int* wsum) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned int x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int run = 0;
+    for (int k = 0; k < kMT / 32; ++k) {
+      const unsigned int t = wsum[k];
+      wsum[k] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+  const unsigned int r = wsum[w] + (x - c);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kMT) k_pieces2(const double* __restrict__ p, uint64_t n, double margin,
+                                                 const double* __restrict__ block_prefix,
+                                                 const unsigned int* __restrict__ serial_base,
+                                                 Piece* __restrict__ head, Piece* __restrict__ after,
+                                                 unsigned long long* __restrict__ serial_idx) {
+  __shared__ double sh[kMT * kRow];
+  __shared__ double wsum[kMT / 32];
+  __shared__ unsigned int usum[kMT / 32];
+  __shared__ RowSeg ssh[kMT];
+  RowClass rc;
+  uint64_t i0;
+  block_classify(p, n, margin, block_prefix, sh, wsum, rc, i0);
+  const double* row = sh + threadIdx.x * kRow;
+  // thread-local segment of the row (pieces after the last serial in the row)
+  RowSeg mine;
+  mine.v = piece_id();
+  mine.ser = rc.serial ? 1 : 0;
+  const int last_ser = rc.serial ? 31 - __clz(rc.serial) : -1;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (k > last_ser && i0 + k < n) mine.v = piece_then(mine.v, elem_piece(row[k], rc.e[k]));
+  const RowSeg in = block_excl_rowseg(mine, ssh);
+  const unsigned int slot0 = serial_base[blockIdx.x] + block_excl_count(__popc(rc.serial), usum);
+  // walk the row: V = running segment value; at segment ends write head / after
+  if (threadIdx.x == 0 && (rc.serial & 1u)) head[blockIdx.x] = piece_id();  // empty head segment
+  Piece V = in.v;
+  bool seen = in.ser;              // a serial precedes the current element inside the block
+  unsigned int slot = slot0;       // slot of the next serial; the current segment's is slot - 1
+  const uint64_t bend = min((uint64_t)(blockIdx.x + 1) * kScanBlock, n);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const uint64_t i = i0 + k;
+    if (i >= n) break;
+    if ((rc.serial >> k) & 1u) {
+      serial_idx[slot] = i;
+      ++slot;
+      seen = true;
+      V = piece_id();
+    } else {
+      V = piece_then(V, elem_piece(row[k], rc.e[k]));
+    }
+    bool end = (i + 1 == bend);
+    if (!end) {
+      // next element serial?  within the row use the bits, else the next thread's first bit
+      end = (k + 1 < kScanItems) ? ((rc.serial >> (k + 1)) & 1u) != 0 : false;
+    }
+    if (end) {
+      if (seen) after[slot - 1] = V;
+      else head[blockIdx.x] = V;
+    }
+  }
+  // the row's last element ends a segment when the next row starts with a serial
+  __shared__ unsigned int first_bits[kMT];
+  first_bits[threadIdx.x] = rc.serial & 1u;
+  __syncthreads();
+  const bool next_ser = (threadIdx.x + 1 < kMT) ? first_bits[threadIdx.x + 1] != 0 : false;
+  const uint64_t ilast = i0 + kScanItems - 1;
+  if (next_ser && ilast < n && ilast + 1 != bend) {
+    if (seen) after[slot - 1] = V;
+    else head[blockIdx.x] = V;
+  }
+}
+
+// total = c[n-1]: the final segment's value (the last block's head, or the last serial's)
+__global__ void k_total2(const Piece* __restrict__ head, const unsigned int* __restrict__ cnt, uint64_t nb,
+                         const double* __restrict__ block_start, const Piece* __restrict__ after,
+                         const double* __restrict__ serial_val, uint64_t ns, double* __restrict__ total) {
+  if (threadIdx.x || blockIdx.x) return;
+  if (cnt[nb - 1] == 0)
+    *total = piece_apply(head[nb - 1], block_start[nb - 1]);
+  else
+    *total = piece_apply(after[ns - 1], serial_val[ns - 1]);
+}
+
+// materialize + normalise: c_i / c_{n-1}, written coalesced through the padded shared row
+__global__ void __launch_bounds__(kMT) k_materialize2(const double* __restrict__ p, uint64_t n, double margin,
+                                                      const double* __restrict__ block_prefix,
+                                                      const unsigned int* __restrict__ serial_base,
+                                                      const double* __restrict__ block_start,
+                                                      const double* __restrict__ serial_val,
+                                                      const double* __restrict__ total,
+                                                      double* __restrict__ c_out) {
+  __shared__ double sh[kMT * kRow];
+  __shared__ double wsum[kMT / 32];
+  __shared__ unsigned int usum[kMT / 32];
+  __shared__ RowSeg ssh[kMT];
+  RowClass rc;
+  uint64_t i0;
+  block_classify(p, n, margin, block_prefix, sh, wsum, rc, i0);
+  double* row = sh + threadIdx.x * kRow;
+  RowSeg mine;
+  mine.v = piece_id();
+  mine.ser = rc.serial ? 1 : 0;
+  const int last_ser = rc.serial ? 31 - __clz(rc.serial) : -1;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (k > last_ser && i0 + k < n) mine.v = piece_then(mine.v, elem_piece(row[k], rc.e[k]));
+  const RowSeg in = block_excl_rowseg(mine, ssh);
+  const unsigned int slot0 = serial_base[blockIdx.x] + block_excl_count(__popc(rc.serial), usum);
+  const double tot = *total;
+  // start value of the current segment
+  double c0 = in.ser ? serial_val[slot0 - 1] : block_start[blockIdx.x];
+  Piece V = in.v;
+  unsigned int slot = slot0;
+  double outv[kScanItems];
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    double c;
+    if ((rc.serial >> k) & 1u) {
+      c = serial_val[slot++];
+      c0 = c;
+      V = piece_id();
+    } else {
+      V = piece_then(V, elem_piece(row[k], rc.e[k]));
+      c = piece_apply(V, c0);
+    }
+    outv[k] = __ddiv_rn(c, tot);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) row[k] = outv[k];
+  __syncthreads();
+  const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const int j = threadIdx.x + k * kMT;
+    const uint64_t i = b0 + j;
+    if (i < n) c_out[i] = sh[(j / kScanItems) * kRow + (j % kScanItems)];
+  }
 }
 
 // exclusive scan of counts (single block), writes total to cnt_total
@@ -718,14 +808,6 @@ __global__ void __launch_bounds__(1024) k_scan_counts(const unsigned int* __rest
 }
 
 // total is read from a separate copy: c[n-1] itself is overwritten by the normalisation
-__global__ void k_copy_last(const double* __restrict__ c, uint64_t n, double* __restrict__ total) { *total = c[n - 1]; }
-
-__global__ void __launch_bounds__(kMT) k_normalize(double* __restrict__ c, uint64_t n, const double* __restrict__ tot) {
-  const double total = *tot;
-  const uint64_t stride = (uint64_t)gridDim.x * kMT;
-  for (uint64_t i = (uint64_t)blockIdx.x * kMT + threadIdx.x; i < n; i += stride) c[i] = c[i] / total;
-}
-
 // ---- PCG64 ---------------------------------------------------------------------------------
 typedef unsigned __int128 u128;
 __device__ __forceinline__ u128 pcg_mult() {
@@ -881,10 +963,6 @@ extern "C" int qsb_marginal(const double* probs, int n_bits, int k, const int* k
 extern "C" size_t qsb_cumsum_scratch_bytes(uint64_t n) {
   const uint64_t nb = (n + kScanBlock - 1) / kScanBlock;
   size_t b = 0;
-  b += n * sizeof(unsigned char);        // serial flags
-  b = (b + 255) & ~(size_t)255;
-  b += n * sizeof(int);                  // binade
-  b = (b + 255) & ~(size_t)255;
   b += nb * sizeof(double);              // block prefix
   b += nb * sizeof(unsigned int) * 2;    // counts, bases
   b = (b + 255) & ~(size_t)255;
@@ -913,11 +991,8 @@ extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cu
     return QSB_ERR_ARG;
   }
   const uint64_t nb = (n + kScanBlock - 1) / kScanBlock;
+  const double margin = risky_margin(n);
   char* w = static_cast<char*>(scratch);
-  unsigned char* serial = reinterpret_cast<unsigned char*>(w);
-  w += (n + 255) & ~(uint64_t)255;
-  int* binade = reinterpret_cast<int*>(w);
-  w += ((n * sizeof(int)) + 255) & ~(uint64_t)255;
   double* bpre = reinterpret_cast<double*>(w);
   w += nb * sizeof(double);
   unsigned int* cnt = reinterpret_cast<unsigned int*>(w);
@@ -938,13 +1013,11 @@ extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cu
   w = reinterpret_cast<char*>(((uintptr_t)w + 255) & ~(uintptr_t)255);
   double* rstart = reinterpret_cast<double*>(w);
 
-  k_scan_block_sums<<<(int)nb, kMT, 0, st>>>(probs, n, bpre);
+  // A: approximate block sums and their exclusive scan (only used to classify)
+  k_block_sums2<<<(int)nb, kMT, 0, st>>>(probs, n, bpre);
   k_scan_top<<<1, 1024, 0, st>>>(bpre, nb);
-  k_classify<<<(int)nb, kMT, 0, st>>>(probs, n, risky_margin(n), bpre, serial, binade);
-  k_count_serial<<<(int)nb, kMT, 0, st>>>(serial, n, cnt);
-  unsigned int* d_total = nullptr;
-  // total count lives right after `base` in pinned host-visible memory would need a sync; we
-  // size the serial arrays conservatively instead: read the total back synchronously.
+  // B: serial points per block, their exclusive scan and total (read back to size the lists)
+  k_count2<<<(int)nb, kMT, 0, st>>>(probs, n, margin, bpre, cnt);
   static unsigned int* h_total = nullptr;
   if (!h_total) {
     cudaError_t e = cudaMallocHost(&h_total, sizeof(unsigned int) * 2);
@@ -955,9 +1028,8 @@ extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cu
     cudaError_t e = cudaMalloc(&d_tot, sizeof(double) * 2);
     if (e != cudaSuccess) return cuda_status(e, "device total");
   }
-  d_total = d_tot;
-  k_scan_counts<<<1, 1024, 0, st>>>(cnt, nb, base, d_total);
-  cudaError_t e = cudaMemcpyAsync(h_total, d_total, sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
+  k_scan_counts<<<1, 1024, 0, st>>>(cnt, nb, base, d_tot);
+  cudaError_t e = cudaMemcpyAsync(h_total, d_tot, sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return cuda_status(e, "serial count copy");
   e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_status(e, "serial count sync");
@@ -979,16 +1051,19 @@ extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cu
   unsigned long long* sidx = reinterpret_cast<unsigned long long*>(sb);
   sb += (ns + 1) * sizeof(unsigned long long);
   double* sval = reinterpret_cast<double*>(sb);
+  double* d_total = reinterpret_cast<double*>(d_tot) + 1;
 
-  k_block_pieces<<<(int)nb, 32, 0, st>>>(probs, n, serial, binade, base, head, after, sidx);
+  // C: block head pieces, serial indices and their after-pieces
+  k_pieces2<<<(int)nb, kMT, 0, st>>>(probs, n, margin, bpre, base, head, after, sidx);
+  // D: stitch (segmented scan of heads, serial walk, block starts, total)
   k_seg_local<<<(int)na, kMT, 0, st>>>(head, cnt, nb, runp, agg);
   k_seg_top<<<1, kMT, 0, st>>>(agg, na);
   k_seg_fix<<<(int)((nb + kMT - 1) / kMT), kMT, 0, st>>>(runp, nb, agg);
   k_stitch_serial<<<1, 1, 0, st>>>(probs, ns, sidx, after, runp, sval, rstart);
   k_block_starts<<<(int)((nb + kMT - 1) / kMT), kMT, 0, st>>>(runp, nb, rstart, bstart);
-  k_materialize<<<(int)nb, 32, 0, st>>>(probs, n, serial, binade, bstart, base, sval, cum);
-  k_copy_last<<<1, 1, 0, st>>>(cum, n, reinterpret_cast<double*>(d_tot) + 1);
-  k_normalize<<<grid_for(n), kMT, 0, st>>>(cum, n, reinterpret_cast<const double*>(d_tot) + 1);
+  k_total2<<<1, 1, 0, st>>>(head, cnt, nb, bstart, after, sval, ns, d_total);
+  // E: every c_i, divided by c_{n-1}
+  k_materialize2<<<(int)nb, kMT, 0, st>>>(probs, n, margin, bpre, base, bstart, sval, d_total, cum);
   QSB_CHECK_LAUNCH("qsb_cumsum_normalized");
   return QSB_OK;
 }
