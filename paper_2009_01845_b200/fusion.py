@@ -19,6 +19,7 @@ The program word format is documented in paper_2009_01845_b200/csrc/pass.cu.
 
 from __future__ import annotations
 
+import os
 import struct
 from dataclasses import dataclass, field
 
@@ -66,6 +67,13 @@ GEOMETRY_JIT = {nat.QSB_C128: TileGeometry(12, 3, 4, 4), nat.QSB_C64: TileGeomet
 # straight-line kernels outgrow the instruction cache on 2-qubit-gate-heavy passes (measured
 # round 1: variational c64 55 -> 74 ms, grid 799 -> 1166 ms), so they are opt-in
 GEOMETRY_JIT_WIDE = {nat.QSB_C128: TileGeometry(13, 3, 4, 5, True), nat.QSB_C64: TileGeometry(14, 4, 5, 6, True)}
+# 128 KB tiles held by 512 consumers (16 / 32 amplitudes each: 4 warps per scheduler)
+GEOMETRY_JIT_WIDE512 = {nat.QSB_C128: TileGeometry(13, 3, 4, 4, True), nat.QSB_C64: TileGeometry(14, 4, 5, 5, True)}
+_GEO_ENV = os.environ.get("QSB_JIT_GEOMETRY", "")
+if _GEO_ENV == "wide":
+    GEOMETRY_JIT = GEOMETRY_JIT_WIDE
+elif _GEO_ENV == "wide512":
+    GEOMETRY_JIT = GEOMETRY_JIT_WIDE512
 
 
 def _f2w(x: float) -> int:
@@ -477,6 +485,12 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None):
                 break
             if b not in Rs and b not in store_bits:
                 Rs.append(b)
+        if geo.halves and not set(Rs) & set(cur.R):
+            # split-tile transposes need a common register bit: go through an intermediate layout
+            Rm = list(cur.R[:NREG // 2]) + [b for b in Rs if b not in cur.R][:NREG - NREG // 2]
+            cur = make_layout(Rm)
+            words += layout_words(cur)
+            n_trans += 1
         cur = make_layout(Rs)
         words += layout_words(cur)
         n_trans += 1

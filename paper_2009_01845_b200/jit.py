@@ -28,9 +28,20 @@ CONSUMERS = 512  # default (interpreter geometry); a kernel uses 2**(K - NREG) c
 THREADS = CONSUMERS + 32
 STAGES = 2
 MAX_PIV = 32
-# setmaxnreg split for 256 consumers + a 128-thread producer warpgroup: 256*232 + 128*40 <= 64K
-PRODUCER_REGS = 40
-CONSUMER_REGS = 232
+# setmaxnreg split between the consumers and the 128-thread producer warpgroup.  setmaxnreg.inc
+# can only take registers the CTA was launched with (threads x the launch-bound register count,
+# a multiple of 8), or it waits forever: 384 threads launch with 168 each = 64,512 -> 256 x 232 +
+# 128 x 40; 640 threads launch with 96 each = 61,440 -> 512 x 112 + 128 x 24.
+def _reg_split(consumers: int):
+    threads = consumers + 128
+    per = min(255, 65536 // threads) // 8 * 8
+    pool = per * threads
+    prod = 40 if consumers <= 256 else 24
+    cons = min(248, (pool - 128 * prod) // consumers // 8 * 8)
+    return cons, prod
+
+
+REG_SPLIT = {c: _reg_split(c) for c in (256, 512)}
 
 
 def _w2d(w):
@@ -740,7 +751,7 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, 1)
   __syncthreads();
   const u64 n_tiles = {1 << (n - K)}ull;
   if (tid >= CONSUMERS) {{
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 {PRODUCER_REGS};" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 {REG_SPLIT[self.consumers][1]};" ::: "memory");
     if (tid >= CONSUMERS + 32) return;
     const int lane = tid - CONSUMERS;
     int it = 0;
@@ -753,7 +764,7 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, 1)
     }}
     return;
   }}
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 {CONSUMER_REGS};" ::: "memory");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 {REG_SPLIT[self.consumers][0]};" ::: "memory");
   int it = 0;
   int zo = 0;
   for (u64 c = blockIdx.x; c < n_tiles; c += gridDim.x, ++it) {{
