@@ -94,10 +94,10 @@ int qsb_jit_compile(const char* source, const char* name, const char* nvrtc_path
  * rank-5 tensor the kernel's tile loads address (15 words: rank, global dims[5], byte strides of
  * dims 1..4, box dims[5]; jit.py tma_plan).  `tables` (doubles, staged to the device) are the
  * per-thread pivot tables; `params` (`param_bytes`, passed by value as the kernel's last
- * parameter) are the uniform gate coefficients. */
+ * parameter) are the uniform gate coefficients; the grid is min(n_tiles, SMs * ctas_per_sm). */
 int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tma_desc, uint64_t n_tiles,
                      const double* tables, int64_t n_tables, const void* params, int64_t param_bytes,
-                     int threads, int smem_bytes, void* stream);
+                     int threads, int smem_bytes, int ctas_per_sm, void* stream);
 
 /* ---- reductions (state.py:109-122 norm / overlap) ---------------------------------------- */
 /* out[0] = sum |a_i|^2 (double, device pointer).  Deterministic two-level tree. */

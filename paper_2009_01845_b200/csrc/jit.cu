@@ -156,7 +156,7 @@ extern "C" int qsb_jit_compile(const char* source, const char* name, const char*
 // 8-byte elements of the state at `src`.
 extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tdesc, uint64_t n_tiles,
                                 const double* coeffs, int64_t n_coeffs, const void* params, int64_t param_bytes,
-                                int threads, int smem_bytes, void* stream) {
+                                int threads, int smem_bytes, int ctas_per_sm, void* stream) {
   jit::Driver* dr = jit::driver();
   if (!dr || !func) {
     set_error("qsb_jit_run_pass: no driver / function");
@@ -198,7 +198,8 @@ extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, const in
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned grid = (unsigned)(n_tiles < (uint64_t)sms ? n_tiles : (uint64_t)sms);
+  const uint64_t slots = (uint64_t)sms * (uint64_t)(ctas_per_sm > 0 ? ctas_per_sm : 1);
+  const unsigned grid = (unsigned)(n_tiles < slots ? n_tiles : slots);
   const void* a_src = src;
   void* a_dst = dst;
   const double* a_cf = static_cast<const double*>(dcoef);

@@ -69,11 +69,15 @@ GEOMETRY_JIT = {nat.QSB_C128: TileGeometry(12, 3, 4, 4), nat.QSB_C64: TileGeomet
 GEOMETRY_JIT_WIDE = {nat.QSB_C128: TileGeometry(13, 3, 4, 5, True), nat.QSB_C64: TileGeometry(14, 4, 5, 6, True)}
 # 128 KB tiles held by 512 consumers (16 / 32 amplitudes each: 4 warps per scheduler)
 GEOMETRY_JIT_WIDE512 = {nat.QSB_C128: TileGeometry(13, 3, 4, 4, True), nat.QSB_C64: TileGeometry(14, 4, 5, 5, True)}
+# 32 KB tiles, 128 consumers, two CTAs per SM
+GEOMETRY_JIT_K11 = {nat.QSB_C128: TileGeometry(11, 3, 4, 4), nat.QSB_C64: TileGeometry(12, 4, 5, 5)}
 _GEO_ENV = os.environ.get("QSB_JIT_GEOMETRY", "")
 if _GEO_ENV == "wide":
     GEOMETRY_JIT = GEOMETRY_JIT_WIDE
 elif _GEO_ENV == "wide512":
     GEOMETRY_JIT = GEOMETRY_JIT_WIDE512
+elif _GEO_ENV == "k11":
+    GEOMETRY_JIT = GEOMETRY_JIT_K11
 
 
 def _f2w(x: float) -> int:

@@ -32,16 +32,22 @@ MAX_PIV = 32
 # can only take registers the CTA was launched with (threads x the launch-bound register count,
 # a multiple of 8), or it waits forever: 384 threads launch with 168 each = 64,512 -> 256 x 232 +
 # 128 x 40; 640 threads launch with 96 each = 61,440 -> 512 x 112 + 128 x 24.
-def _reg_split(consumers: int):
+def _reg_split(consumers: int, ctas: int = 1):
     threads = consumers + 128
-    per = min(255, 65536 // threads) // 8 * 8
+    per = min(255, 65536 // (threads * ctas)) // 8 * 8
     pool = per * threads
     prod = 40 if consumers <= 256 else 24
     cons = min(248, (pool - 128 * prod) // consumers // 8 * 8)
     return cons, prod
 
 
-REG_SPLIT = {c: _reg_split(c) for c in (256, 512)}
+def ctas_per_sm(consumers: int) -> int:
+    """Resident CTAs per SM: 128-consumer kernels (32 KB tiles) run two per SM so one CTA's
+    transposes / stores overlap the other's FP64 work."""
+    return 2 if consumers <= 128 else 1
+
+
+REG_SPLIT = {c: _reg_split(c, ctas_per_sm(c)) for c in (128, 256, 512)}
 
 
 def _w2d(w):
@@ -735,7 +741,7 @@ class _Gen:
 // {self.consumers} consumer threads + one producer warpgroup (one active warp: TMA tile fetches and
 // per-tile pivot factors, STAGES tiles ahead); setmaxnreg moves the producers' registers to the
 // consumers, which hold the tile in registers.
-extern "C" __global__ void __launch_bounds__({self.consumers + 128}, 1)
+extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_sm(self.consumers)})
 {name}(const C* __restrict__ src, C* __restrict__ dst, const __grid_constant__ TMap tmap,
        const double* __restrict__ cf, const __grid_constant__ CP cp) {{
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -779,7 +785,7 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, 1)
 
 
 class _Compiled:
-    __slots__ = ("func", "name", "smem", "tdesc", "n_tiles", "threads")
+    __slots__ = ("func", "name", "smem", "tdesc", "n_tiles", "threads", "ctas")
 
 
 _cache: dict = {}
@@ -835,9 +841,9 @@ MAX_COEFFS = 3072  # 24 KB of pivot tables staged in shared memory
 MAX_PARAM_BYTES = 31744  # kernel parameter space: 32764 B minus the pointers and the tensor map
 
 
-def smem_bytes(dtype, n_coeffs=MAX_COEFFS) -> int:
-    # every geometry stages 64 KB per stage (whole 64 KB tiles or halves of 128 KB tiles)
-    struct_bytes = (STAGES + 1) * 65536 + 4 * MAX_PIV * 16 + 8 * STAGES * 4
+def smem_bytes(stage_bytes: int, n_coeffs=MAX_COEFFS) -> int:
+    # STAGES stages + one transpose buffer of stage_bytes (a whole tile, or half of a 128 KB tile)
+    struct_bytes = (STAGES + 1) * stage_bytes + 4 * MAX_PIV * 16 + 8 * STAGES * 4 + 16
     return struct_bytes + 8 * n_coeffs + 128
 
 
@@ -863,7 +869,11 @@ def compile_words(words, dtype):
             hit = _Compiled()
             hit.func = fn.value
             hit.name = name
-            hit.smem = smem_bytes(dtype, len(tables))
+            K, nreg = int(words[2]), int(words[3])
+            amp = 16 if dtype == nat.QSB_C128 else 8
+            stage_amps = 1 << (K - 1 if (1 << K) * amp > 65536 else K)
+            hit.smem = smem_bytes(stage_amps * amp, len(tables))
+            hit.ctas = ctas_per_sm(1 << (K - nreg))
             hit.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
             hit.n_tiles = 1 << (int(words[4]) - int(words[2]))
             hit.threads = (1 << (int(words[2]) - int(words[3]))) + 128
@@ -878,6 +888,7 @@ def run(words, dtype, src_ptr, dst_ptr, n_qubits, stream_ptr, compiled=None, coe
     nat.check(
         nat.lib().qsb_jit_run_pass(compiled.func, src_ptr, dst_ptr, compiled.tdesc.ctypes.data, compiled.n_tiles,
                                    tables.ctypes.data if len(tables) else None, len(tables),
-                                   params.ctypes.data, params.nbytes, compiled.threads, compiled.smem, stream_ptr),
+                                   params.ctypes.data, params.nbytes, compiled.threads, compiled.smem, compiled.ctas,
+                                   stream_ptr),
         "jit_run_pass",
     )

@@ -158,11 +158,13 @@ class CudaBackend:
 
         if not ngates:
             return shard
-        key = tuple((g.kind, g.targets, g.controls, g.index, None if g.matrix is None else g.matrix.tobytes())
-                    for g in ngates)
+        # out-of-place passes (folded SWAPs) need one more shard-sized buffer
+        allow_ext = engine._free_bytes() > shard.numel() * shard.element_size() + (512 << 20)
+        key = (allow_ext,) + tuple((g.kind, g.targets, g.controls, g.index,
+                                    None if g.matrix is None else g.matrix.tobytes()) for g in ngates)
         plan_ = cache.get(key)
         if plan_ is None:
-            plan_ = plan_circuit(ngates, n_local, self.dtype, allow_ext_perm=False,
+            plan_ = plan_circuit(ngates, n_local, self.dtype, allow_ext_perm=allow_ext,
                                  geometry=engine.default_geometry(self.dtype))
             cache[key] = plan_
         holder = {}
