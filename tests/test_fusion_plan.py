@@ -123,3 +123,23 @@ def test_geometry():
         assert geo.K - geo.nreg == 9 and geo.A == 1 << geo.nreg
         # 2^L amplitudes per contiguous run = 256 bytes
         assert (1 << geo.L) * (16 if dt == C128 else 8) == 256
+
+
+@pytest.mark.parametrize("dtype,tol", [(C128, 1e-12), (C64, 1e-5)])
+def test_single_qubit_folding_trotter_and_grid(dtype, tol):
+    """1-qubit gates folded into neighbouring 2-qubit gates (cost model) keep the state."""
+    from paper_2009_01845_b200.fusion import GEOMETRY_JIT, merge_single_qubit, normalize
+
+    n = 16
+    rng = np.random.default_rng(5)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    npd = np.complex128 if dtype == C128 else np.complex64
+    trot = ov.trotter_step(ov.combine(ov.x_terms(n), 0.3, ov.tfim_terms(n, 1.0), 0.7), 0.1)
+    for gates in (trot, ov.grid_supremacy(4, 4, 8, 42)):
+        specs = spec_tuples_to_specs(gates)
+        plan = plan_circuit(specs, n, dtype, geometry=GEOMETRY_JIT[dtype])
+        assert max_abs(emulate_plan(plan, psi, npd), ov.run(gates, n, psi)) <= tol
+    ng = [g for g in (normalize(s, n, i) for i, s in enumerate(spec_tuples_to_specs(trot))) if g is not None]
+    # the X rotation on each ZZ+hX term's first qubit folds into it: 56 -> 40 gates at n = 16
+    assert len(merge_single_qubit(ng)) < len(ng)
