@@ -299,9 +299,12 @@ def extra_workloads(q, engine, n, peak):
 
     out = {}
     params = np.random.default_rng(42).uniform(0, 2 * math.pi, n * 11)
+    rows = 3 if n % 3 == 0 else 2
+    grid = q.random_grid_circuit(rows, n // rows, 20, 42)
     cases = [("variational_L5_fused_c128", q.variational_circuit(n, 5, params, fused=True), q.Precision.F64),
              ("variational_L5_fused_c64", q.variational_circuit(n, 5, params, fused=True), q.Precision.F32),
-             ("qft_c64", q.qft_circuit(n), q.Precision.F32)]
+             ("qft_c64", q.qft_circuit(n), q.Precision.F32),
+             (f"random_grid_{rows}x{n // rows}_20cycles_c128", grid, q.Precision.F64)]
     for name, circ, prec in cases:
         st = q.uniform_state(n, prec)
         plan = engine.plan_for_state(st, circ.queue)

@@ -73,6 +73,11 @@ int qsb_apply_matrix(void* amps, int n_qubits, int dtype, int n_targets, const i
 /* Multiply every amplitude of [amps, amps + n_amps) by (re, im) -- the all-global phase of the
  * sharded executor (sharding.py:281-283) and from_amplitudes(normalize=True) (state.py:101-105). */
 int qsb_scale(void* amps, uint64_t n_amps, int dtype, double re, double im, void* stream);
+/* Projective collapse (extension: the reference has no mid-circuit measurement):
+ * amplitudes with (index & mask) == value are multiplied by `scale` (1/sqrt(p) of the outcome),
+ * every other amplitude is set to zero. */
+int qsb_collapse(void* amps, uint64_t n_amps, int dtype, uint64_t mask, uint64_t value, double scale,
+                 void* stream);
 
 /* ---- fused multi-gate pass (one HBM sweep for a run of gates) --- */
 /* `program` is a flat little-endian int64 word stream produced by the host planner

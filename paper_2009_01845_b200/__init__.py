@@ -15,6 +15,7 @@ from .circuit import (
     circuit_to_dict,
     fuse,
     qft_circuit,
+    random_grid_circuit,
     variational_circuit,
 )
 from .errors import ArityError, CapacityError, FormError, ParseError, ShapeError, SimulationError
@@ -62,7 +63,7 @@ from .hamiltonians import (
     expectation,
     ground_state_vector,
 )
-from .measurement import MeasurementResult, frequencies, marginal_probabilities, sample
+from .measurement import MeasurementResult, collapse, frequencies, marginal_probabilities, measure, sample
 from .state import (
     MAX_QUBITS,
     Precision,

@@ -64,6 +64,25 @@ __global__ void k_scale(cplx<R>* __restrict__ a, uint64_t n, cplx<R> s) {
     a[i] = cmul(a[i], s);
 }
 
+// projective collapse: amplitudes whose bits under `mask` equal `value` are scaled by `s`, the
+// rest are zeroed without being read (only the kept fraction is loaded)
+template <typename R>
+__global__ void k_collapse(cplx<R>* __restrict__ a, uint64_t n, uint64_t mask, uint64_t value, R s) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    cplx<R> v;
+    if ((i & mask) == value) {
+      v = a[i];
+      v.x *= s;
+      v.y *= s;
+    } else {
+      v.x = (R)0;
+      v.y = (R)0;
+    }
+    a[i] = v;
+  }
+}
+
 static int stream_grid(uint64_t n) {
   // enough CTAs for 8 resident per SM on 148 SMs, capped by the work
   uint64_t want = (n + kThreads - 1) / kThreads;
@@ -582,6 +601,22 @@ int qsb_scale(void* amps, uint64_t n, int dtype, double re, double im, void* str
     k_scale<float><<<stream_grid(n), kThreads, 0, st>>>(static_cast<float2*>(amps), n,
                                                         make_float2((float)re, (float)im));
   QSB_CHECK_LAUNCH("qsb_scale");
+  return QSB_OK;
+}
+
+int qsb_collapse(void* amps, uint64_t n, int dtype, uint64_t mask, uint64_t value, double scale, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  if ((value & ~mask) != 0) {
+    set_error("qsb_collapse: value has bits outside the mask");
+    return QSB_ERR_ARG;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    k_collapse<double><<<stream_grid(n), kThreads, 0, st>>>(static_cast<double2*>(amps), n, mask, value, scale);
+  else
+    k_collapse<float><<<stream_grid(n), kThreads, 0, st>>>(static_cast<float2*>(amps), n, mask, value,
+                                                           (float)scale);
+  QSB_CHECK_LAUNCH("qsb_collapse");
   return QSB_OK;
 }
 

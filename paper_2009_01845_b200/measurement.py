@@ -147,6 +147,41 @@ def sample(state, qubits, n_shots: int, seed: int, registers: dict | None = None
     return MeasurementResult(int(n_shots), qubits, samples, int(seed), regs)
 
 
+def collapse(state, qubits, outcome: int) -> float:
+    """Project `state` in place onto `outcome` of `qubits` (qubits[0] = MSB of the outcome, as
+    in `sample`) and renormalise; returns the outcome's probability.
+
+    Extension beyond the reference (which has no mid-circuit measurement): the
+    probability is the bit-exact marginal of `marginal_probabilities`, the kept amplitudes are
+    scaled by 1/sqrt(p) in the state's precision, all others become exact zeros."""
+    qubits = _validate_qubits(state, qubits)
+    k = len(qubits)
+    outcome = int(outcome)
+    if not 0 <= outcome < (1 << k):
+        raise ShapeError(f"outcome {outcome} out of range for {k} qubits")
+    p = float(device_marginal(state, qubits)[outcome].item())
+    if p <= 0.0:
+        raise ValueError(f"outcome {outcome} has probability 0")
+    n = state.n_qubits
+    mask = value = 0
+    for j, q in enumerate(qubits):
+        bit = 1 << (n - 1 - q)
+        mask |= bit
+        if (outcome >> (k - 1 - j)) & 1:
+            value |= bit
+    nat.check(nat.lib().qsb_collapse(state.data_ptr, state.n_amps, state.precision.qsb_dtype, mask, value,
+                                     1.0 / np.sqrt(p), nat.stream_ptr()), "collapse")
+    return p
+
+
+def measure(state, qubits, seed: int) -> int:
+    """Mid-circuit measurement: draw one outcome exactly as `sample(state, qubits, 1, seed)` and
+    collapse the state onto it (in place).  Returns the outcome."""
+    outcome = int(sample(state, qubits, 1, seed).samples[0])
+    collapse(state, qubits, outcome)
+    return outcome
+
+
 def frequencies(result: MeasurementResult, register: str | None = None) -> dict:
     """Outcome counts, optionally projected onto a named register (measurement.py:90-103)."""
     samples = result.samples

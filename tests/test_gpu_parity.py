@@ -345,3 +345,32 @@ def _random_spec(q, n, rng):
     if k in ("H", "Y"):
         return getattr(q, k)(tg[0], controls=ct)
     return getattr(q, k)(tg[0], tg[1], controls=ct)
+
+
+@pytest.mark.parametrize("n,qubits,prec", [(12, (3,), "f64"), (14, (0, 5, 13), "f64"), (16, (2, 9), "f32")])
+def test_collapse_and_measure(cuda, n, qubits, prec):
+    """Projective collapse against a numpy projection (extension: no reference semantics)."""
+    import paper_2009_01845_b200 as q
+
+    rng = np.random.default_rng(n)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    P = q.Precision.F64 if prec == "f64" else q.Precision.F32
+    tol = 1e-12 if prec == "f64" else 1e-5
+    st = q.from_amplitudes(psi, precision=P)
+    k = len(qubits)
+    outcome = (1 << k) - 2 if k > 1 else 1
+    p = q.collapse(st, qubits, outcome)
+    idx = np.arange(1 << n)
+    keep = np.ones(1 << n, dtype=bool)
+    for j, qb in enumerate(qubits):
+        keep &= ((idx >> (n - 1 - qb)) & 1) == ((outcome >> (k - 1 - j)) & 1)
+    want = np.where(keep, psi, 0) / np.sqrt(np.sum(np.abs(psi[keep]) ** 2))
+    assert abs(p - np.sum(np.abs(psi[keep]) ** 2)) <= 1e-6
+    assert max_abs(st.amplitudes, want) <= tol
+    # measure = one draw of sample() + collapse; a second measurement repeats the outcome
+    st2 = q.from_amplitudes(psi, precision=P)
+    o = q.measure(st2, qubits, seed=3)
+    assert o == int(q.sample(q.from_amplitudes(psi, precision=P), qubits, 1, 3).samples[0])
+    assert q.measure(st2, qubits, seed=11) == o
+    assert abs(q.norm(st2) - 1.0) <= (1e-12 if prec == "f64" else 1e-5)

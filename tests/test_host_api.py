@@ -174,3 +174,17 @@ def test_numpy_abs_formula_on_this_host():
     fma = np.array([float(Fraction(float(x)) ** 2 + 1) if np.isfinite(x) else np.nan for x in r])
     v = np.where(big == 0, 0.0, big * np.sqrt(fma))
     assert np.array_equal(v * v, ref)
+
+
+def test_random_grid_builder_matches_oracle_generator():
+    """The package's supremacy-style builder emits the oracle generator's gates exactly."""
+    import paper_2009_01845_b200 as q
+    from oracle import statevec as ov
+
+    for rows, cols, cyc, seed in ((3, 4, 10, 42), (2, 5, 20, 7)):
+        c = q.random_grid_circuit(rows, cols, cyc, seed)
+        ref = ov.grid_supremacy(rows, cols, cyc, seed)
+        assert len(c.queue) == len(ref)
+        for g, (_k, tg, _ct, _p, m) in zip(c.queue, ref):
+            assert tuple(g.targets) == tuple(tg)
+            assert np.array_equal(q.gate_matrix(g), m)

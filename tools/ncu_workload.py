@@ -25,11 +25,8 @@ def build(workload, n):
         h = q.combine(q.build_x(n), 0.5, q.build_tfim(n, 1.0), 0.5)
         return q.trotter_step_circuit(h, 0.05)
     if workload == "grid":
-        from oracle import statevec as ov
-        from plan_helpers import spec_tuples_to_specs
-
         rows = 3 if n % 3 == 0 else 2
-        return q.Circuit(n).add(spec_tuples_to_specs(ov.grid_supremacy(rows, n // rows, 20, 42)))
+        return q.random_grid_circuit(rows, n // rows, 20, 42)
     raise SystemExit(f"unknown workload {workload}")
 
 

@@ -67,7 +67,7 @@ def main():
 
     rows = 3 if n % 3 == 0 else 2
     cols = n // rows
-    grid = q.Circuit(rows * cols).add(spec_tuples_to_specs(ov.grid_supremacy(rows, cols, 20, 42)))
+    grid = q.random_grid_circuit(rows, cols, 20, 42)
     run_circuit(f"grid {rows}x{cols} 20 cycles", grid, rows * cols, q.Precision.F64)
     # sampling
     st = q.qft_circuit(n).execute(q.basis_state(n, 12345))
