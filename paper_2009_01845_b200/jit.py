@@ -100,8 +100,8 @@ __device__ __forceinline__ float2 f2sub(float2 x, float2 y) {
 // coefficient reads are indexed by `zo` (always 0, re-read from shared memory before every op):
 // ptxas can neither hoist them out of the tile loop nor bundle them across ops, so each op's
 // coefficients occupy (uniform) registers only while that op runs
-#define PZ(k) mkC(cp.v[(k) + zo], cp.v[(k) + 1 + zo])
-#define PV(k) cp.v[(k) + zo]
+#define PZ(k) mkC(cp.v[(k) + ZO], cp.v[(k) + 1 + ZO])
+#define PV(k) cp.v[(k) + ZO]
 __device__ __forceinline__ int zpin(const u32* z) {
   u32 v; asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(z))); return (int)(v & 1u); }
 __device__ __forceinline__ u32 swz(u32 j) {
@@ -215,6 +215,7 @@ class _Gen:
         self.ep_waited = False
         self.h_scale = 0  # deferred 1/sqrt(2) factors of uncontrolled Hadamard butterflies
         self.vm = list(range(self.A))  # slot of the current layout -> register variable v<i>
+        self.n_cops = 0  # ops with coefficient reads emitted so far
         amp_bytes = 16 if dtype == nat.QSB_C128 else 8
         # 128 KB tiles are staged as two 64 KB halves split on tile bit K-1 (a register bit of
         # the first layout); layout changes then run in two rounds through a 64 KB buffer
@@ -355,7 +356,12 @@ class _Gen:
         while w[q] != OP_END:
             op, ln = w[q], w[q + 1]
             a = q + 2
-            if op == OP_LAYOUT:
+            if op == OP_LAYOUT and _PROBE == "notransposes":
+                # timing probe only: relabel without moving data (results are wrong)
+                new = self.parse_layout(a)
+                li += 1
+                self.set_layout(new, li)
+            elif op == OP_LAYOUT:
                 new = self.parse_layout(a)
                 li += 1
                 if not self.halves:
@@ -374,11 +380,21 @@ class _Gen:
                     self.gen_split_transpose(new, li)
             elif op == OP_PARITY:
                 self.gen_parity(a)
+            elif _PROBE == "nogates":
+                pass  # timing probe only: gate bodies omitted (results are wrong)
             else:
                 gen = {OP_G1: self.gen_g1, OP_G2: self.gen_g2, OP_PIVOT: self.gen_pivot, OP_TERM: self.gen_term,
                        OP_SCALE: self.gen_scale}[op]
-                self.emit("    zo = zpin(&sm.zero);")  # pin this op's coefficient reads here
+                # this op's coefficient reads are indexed by zo<k>; zo<k+1> is loaded now so the
+                # next op's coefficients can be fetched while this op computes
+                k = self.n_cops
+                if k == 0:
+                    self.emit("    const int zo0 = zpin(&sm.zero);")
+                self.emit(f"    const int zo{k + 1} = zpin(&sm.zero);")
+                self.emit(f"#define ZO zo{k}")
                 gen(a)
+                self.emit("#undef ZO")
+                self.n_cops += 1
             q += ln
         body = "\n".join(self.lines[body_start:])
         # output offsets of the final layout
@@ -772,7 +788,6 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
   }}
   asm volatile("setmaxnreg.inc.sync.aligned.u32 {REG_SPLIT[self.consumers][0]};" ::: "memory");
   int it = 0;
-  int zo = 0;
   for (u64 c = blockIdx.x; c < n_tiles; c += gridDim.x, ++it) {{
     const int s = it % STAGES;
     const u32 ph = (it / STAGES) & 1;
@@ -791,6 +806,8 @@ class _Compiled:
 _cache: dict = {}
 _lock = threading.Lock()
 _disabled = os.environ.get("QSB_JIT", "1") == "0"
+# QSB_JIT_PROBE=nogates|notransposes: timing experiments only (kernels compute wrong results)
+_PROBE = os.environ.get("QSB_JIT_PROBE", "")
 _avail = None
 
 
