@@ -374,3 +374,25 @@ def test_collapse_and_measure(cuda, n, qubits, prec):
     assert o == int(q.sample(q.from_amplitudes(psi, precision=P), qubits, 1, 3).samples[0])
     assert q.measure(st2, qubits, seed=11) == o
     assert abs(q.norm(st2) - 1.0) <= (1e-12 if prec == "f64" else 1e-5)
+
+
+def test_interpreted_pass_kernel_without_nvrtc(cuda, monkeypatch):
+    """With NVRTC unavailable the same plans run on the interpreted pass kernel (csrc/pass.cu,
+    its own 512-thread geometry) -- still the CUDA path, still parity-exact."""
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200 import jit
+
+    monkeypatch.setattr(jit, "_disabled", True)
+    monkeypatch.setattr(jit, "_avail", None)
+    assert not jit.available()
+    g = golden("qft")
+    n = 14
+    c = q.qft_circuit(n)
+    assert c.plan().n_passes >= 1
+    assert max_abs(c.execute(_sv(g[f"rin{n}"])).amplitudes, g[f"rout{n}"]) <= TOL64
+    gv = golden("variational")
+    vc = q.variational_circuit(14, 3, gv["params14"], fused=True)
+    assert max_abs(vc.execute().amplitudes, gv["f64_14_1"]) <= TOL64
+    assert max_abs(vc.execute(precision=q.Precision.F32).amplitudes, gv["f32_14_1"]) <= TOL32
+    g15 = golden("grid15")
+    assert max_abs(circuit_from_json(g15["circuit"]).execute().amplitudes, g15["out"]) <= TOL64
