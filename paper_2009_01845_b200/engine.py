@@ -122,7 +122,26 @@ def run_plan(state, plan: Plan, scratch_holder: dict | None = None, stream=None,
             events.append((ev0, ev1))
 
 
-def run_gates(state, specs, fuse: bool | None = None, scratch_holder: dict | None = None):
-    plan = plan_for_state(state, specs, fuse)
+def run_gates(state, specs, fuse: bool | None = None, scratch_holder: dict | None = None,
+              plan_cache: dict | None = None):
+    """Plan and run `specs` on `state`.  With `plan_cache` (a Circuit's), the plan -- and the
+    specialised kernels and coefficients attached to its passes -- is reused while the gate
+    objects, precision, fusion switch and scratch availability are unchanged."""
+    if plan_cache is None:
+        plan = plan_for_state(state, specs, fuse)
+    else:
+        fuse_ = FUSION_DEFAULT if fuse is None else fuse
+        allow_ext = _free_bytes() > state.n_amps * state.precision.itemsize + (512 << 20)
+        key = (state.n_qubits, state.precision.qsb_dtype, fuse_, allow_ext, jit.available(),
+               tuple(id(s) for s in specs))
+        hit = plan_cache.get(key)
+        if hit is None:
+            if len(plan_cache) >= 8:
+                plan_cache.clear()
+            plan = plan_circuit(list(specs), state.n_qubits, state.precision.qsb_dtype, allow_ext_perm=allow_ext,
+                                fuse=fuse_, geometry=default_geometry(state.precision.qsb_dtype))
+            plan_cache[key] = (plan, list(specs))  # the specs are kept alive so their ids stay unique
+        else:
+            plan = hit[0]
     run_plan(state, plan, scratch_holder)
     return plan
