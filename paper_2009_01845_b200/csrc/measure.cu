@@ -232,12 +232,19 @@ __device__ __forceinline__ int approx_binade(double s, double margin, bool* risk
     *risky = false;
     return -100000;
   }
-  int e;
-  const double m = frexp(s, &e);  // s = m * 2^e, m in [0.5, 1)
-  const double lo = 0.5 * (1.0 + margin);
-  const double hi = 1.0 - margin;
-  *risky = (m < lo) || (m > hi) || (e < -1000);
-  return e - 1;  // s in [2^(e-1), 2^e)
+  const unsigned long long b = (unsigned long long)__double_as_longlong(s);
+  const int ef = (int)(b >> 52) & 0x7ff;
+  if (ef == 0) {  // subnormal (always risky): exponent from frexp
+    int e;
+    frexp(s, &e);
+    *risky = true;
+    return e - 1;
+  }
+  // s = m2 * 2^e with m2 in [1, 2) taken from the bits (exactly frexp's 2m, e = frexp's e - 1)
+  const double m2 = __longlong_as_double((long long)((b & 0x000fffffffffffffull) | 0x3ff0000000000000ull));
+  const int e = ef - 1023;
+  *risky = (m2 < 1.0 + margin) || (m2 > 2.0 - 2.0 * margin) || (e < -1001);
+  return e;  // s in [2^e, 2^(e+1))
 }
 
 static double risky_margin(uint64_t n) {
@@ -259,10 +266,9 @@ __device__ __forceinline__ Piece elem_piece(double p, int e) {
     q.d1 = 0;
     return q;
   }
-  const double v = pow2_scale(p, 52 - e);  // p / u, exact
-  const double m = floor(v);
-  const double f = v - m;
-  const long long mi = (long long)m;
+  const double v = pow2_scale(p, 52 - e);  // p / u, exact (< 2^53)
+  const long long mi = __double2ll_rd(v);   // floor
+  const double f = v - (double)mi;          // exact
   if (f < 0.5) {
     q.d0 = mi;
     q.d1 = mi;
@@ -533,7 +539,7 @@ __global__ void __launch_bounds__(kMT) k_block_sums2(const double* __restrict__ 
   }
 }
 
-__global__ void __launch_bounds__(kMT) k_count2(const double* __restrict__ p, uint64_t n, double margin,
+__global__ void __launch_bounds__(kMT, 3) k_count2(const double* __restrict__ p, uint64_t n, double margin,
                                                 const double* __restrict__ block_prefix,
                                                 unsigned int* __restrict__ cnt) {
   __shared__ double sh[kMT * kRow];
@@ -649,7 +655,7 @@ __device__ __forceinline__ unsigned int block_excl_count(unsigned int c, unsigne
   return r;
 }
 
-__global__ void __launch_bounds__(kMT) k_pieces2(const double* __restrict__ p, uint64_t n, double margin,
+__global__ void __launch_bounds__(kMT, 3) k_pieces2(const double* __restrict__ p, uint64_t n, double margin,
                                                  const double* __restrict__ block_prefix,
                                                  const unsigned int* __restrict__ serial_base,
                                                  Piece* __restrict__ head, Piece* __restrict__ after,
@@ -724,7 +730,7 @@ __global__ void k_total2(const Piece* __restrict__ head, const unsigned int* __r
 }
 
 // materialize + normalise: c_i / c_{n-1}, written coalesced through the padded shared row
-__global__ void __launch_bounds__(kMT) k_materialize2(const double* __restrict__ p, uint64_t n, double margin,
+__global__ void __launch_bounds__(kMT, 3) k_materialize2(const double* __restrict__ p, uint64_t n, double margin,
                                                       const double* __restrict__ block_prefix,
                                                       const unsigned int* __restrict__ serial_base,
                                                       const double* __restrict__ block_start,
@@ -753,7 +759,7 @@ __global__ void __launch_bounds__(kMT) k_materialize2(const double* __restrict__
   double c0 = in.ser ? serial_val[slot0 - 1] : block_start[blockIdx.x];
   Piece V = in.v;
   unsigned int slot = slot0;
-  double outv[kScanItems];
+  // the row is private to this thread: each element's result replaces its probability in place
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     double c;
@@ -765,11 +771,8 @@ __global__ void __launch_bounds__(kMT) k_materialize2(const double* __restrict__
       V = piece_then(V, elem_piece(row[k], rc.e[k]));
       c = piece_apply(V, c0);
     }
-    outv[k] = __ddiv_rn(c, tot);
+    row[k] = __ddiv_rn(c, tot);
   }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) row[k] = outv[k];
   __syncthreads();
   const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
 #pragma unroll
