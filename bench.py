@@ -295,9 +295,14 @@ def extra_workloads(q, engine, n, peak):
     import numpy as np
     import torch
 
-    from paper_2009_01845_b200.fusion import PassStep
+    from paper_2009_01845_b200.fusion import PassStep, matrix_cost
 
     out = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            sm_mhz = float(json.load(f).get("sm_max_mhz", 1965.0))
+    except Exception:
+        sm_mhz = 1965.0
     params = np.random.default_rng(42).uniform(0, 2 * math.pi, n * 11)
     rows = 3 if n % 3 == 0 else 2
     grid = q.random_grid_circuit(rows, n // rows, 20, 42)
@@ -322,9 +327,21 @@ def extra_workloads(q, engine, n, peak):
         sec = a.elapsed_time(b) / reps / 1e3
         sweeps = plan.state_sweeps()
         gbs = sweeps * 2 * (1 << n) * prec.itemsize / sec / 1e9
+        # FP roofline of the gate arithmetic: FMAs per amplitude of the (structure-specialised)
+        # gate bodies the plan applies, at the B200 FMA rate of that precision (FP64: 64 / clk /
+        # SM, FP32: 128 / clk / SM) and the max SM clock
+        fmas = sum(matrix_cost(g.matrix) for s_ in plan.steps if isinstance(s_, PassStep)
+                   for g in s_.gates if g.kind in ("g1", "g2")) * (1 << n)
+        rate = (64 if prec is q.Precision.F64 else 128) * 148 * sm_mhz * 1e6
+        fp_s = fmas / rate
+        hbm_s = sweeps * 2 * (1 << n) * prec.itemsize / (peak * 1e9)
         out[name] = {"seconds": sec, "gates": len(circ.queue),
                      "passes": sum(1 for s_ in plan.steps if isinstance(s_, PassStep)),
-                     "effective_gbs": gbs, "hbm_frac": gbs / peak}
+                     "effective_gbs": gbs, "hbm_frac": gbs / peak,
+                     "hbm_floor_s": hbm_s, "fp_floor_s": fp_s,
+                     "bound": "fp64" if (fp_s > hbm_s and prec is q.Precision.F64) else
+                              ("fp32" if fp_s > hbm_s else "hbm"),
+                     "roofline_frac": max(hbm_s, fp_s) / sec}
         del st, holder
         torch.cuda.empty_cache()
     return out

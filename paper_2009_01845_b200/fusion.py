@@ -378,7 +378,7 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
             # cheaper as sparse single-gate kernels than as a full sweep
             plan.steps.extend(GateStep(g) for g in absorbed)
         else:
-            words, info = compile_pass(absorbed, T, n_qubits, dtype, geo)
+            words, info = compile_pass(absorbed, T, n_qubits, dtype, geo, minimal=MINIMAL_LAYOUT_CHANGES)
             plan.steps.append(PassStep(words, absorbed, tuple(sorted(T)), info["ext_perm"],
                                        info["transposes"], info["pivots"]))
         remaining = deferred
@@ -425,7 +425,17 @@ def _order_thread_bits(cands, geo, prefer, natural=False):
     return lanes + rest
 
 
-def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None):
+# Minimal layout changes (swap only the needed bits; jit emits predicated transposes that move
+# only the amplitudes whose swapped bits differ).  Measured round 1: slower on every workload
+# (variational-30 c128 100 -> 146 ms, QFT-30 22.6 -> 23.6 ms) -- the kept lane assignment loses
+# the conflict-free swizzle and predicated half-warp accesses save no wavefronts -- so off.
+MINIMAL_LAYOUT_CHANGES = os.environ.get("QSB_MINIMAL_LAYOUT", "0") == "1"
+
+
+def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal: bool = False):
+    """Encode one pass.  `minimal`: layout changes swap only the needed bits (see
+    MINIMAL_LAYOUT_CHANGES); otherwise every change re-lays the thread bits for a conflict-free
+    swizzle and the coalesced store."""
     geo = geo or GEOMETRY[dtype]
     K, NREG, A = geo.K, geo.nreg, geo.A
     tile_pos = sorted(T)
@@ -468,7 +478,7 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None):
 
     needs = [frozenset(tidx[p] for p in ev[2]) for ev in events if ev[0] in ("g1", "g2")]
 
-    def pick_R(i, forbid=frozenset(), keep=None, must=()):
+    def pick_R(i, forbid=frozenset(), keep=None, must=(), sticky=()):
         """Register bits of the next layout: the tile bits of as many upcoming gates as fit.
         `must` bits are always included; with `keep` (split-tile geometry) the new layout
         shares at least one register bit with `keep` (transposes run in two halves on it)."""
@@ -495,7 +505,7 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None):
             if not set(R) & set(keep):
                 R.append(sorted(keep, key=lambda b: (b in store_bits, -b))[0])
         filler = sorted((b for b in range(K) if b not in R and b not in forbid),
-                        key=lambda b: (keep is not None and b not in keep, b in store_bits, -b))
+                        key=lambda b: (keep is not None and b not in keep, b not in sticky, b in store_bits, -b))
         for b in filler:
             if len(R) >= NREG:
                 break
@@ -524,6 +534,28 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None):
         cands = [b for b in range(K) if b not in R]
         return _Layout(R, _order_thread_bits(cands, geo, store_bits, natural))
 
+    def change_layout(cur, R):
+        """Minimal change from `cur` to register set R: every incoming tile bit takes the slot of
+        an outgoing one and vice versa (other slots and thread positions unchanged), so the
+        transpose only moves the amplitudes whose swapped bits differ (jit: predicated
+        transposes).  Lane positions < G keep distinct residues mod G where possible."""
+        incoming = [b for b in R if b not in cur.R]
+        outgoing = [b for b in cur.R if b not in R]
+        newR, newTb = list(cur.R), list(cur.Tb)
+        # incoming bits in lane positions first, so outgoing store bits (which must end on lanes
+        # for the coalesced store) can take lane positions
+        incoming.sort(key=lambda x: cur.Tb.index(x))
+        left = sorted(outgoing, key=lambda y: y not in store_bits)
+        for x in incoming:
+            j = cur.Tb.index(x)
+            y = left[0]
+            if j < geo.G and y not in store_bits:
+                y = next((c for c in left if c % geo.G == x % geo.G), left[0])
+            left.remove(y)
+            newR[newR.index(y)] = x
+            newTb[j] = y
+        return _Layout(newR, newTb)
+
     # initial layout: its lanes 0..G-1 must be tile bits 0..G-1 (natural-order stage read)
     nat_forbid = frozenset(range(geo.G))
     R0 = pick_R(0, nat_forbid, must=(K - 1,) if geo.halves else ())
@@ -551,7 +583,12 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None):
         need = needs[gi]
         if not need <= set(cur.R):
             flush_diag()
-            cur = make_layout(pick_R(gi, keep=cur.R if geo.halves else None))
+            if geo.halves:
+                cur = make_layout(pick_R(gi, keep=cur.R))
+            elif not minimal:
+                cur = make_layout(pick_R(gi))
+            else:
+                cur = change_layout(cur, pick_R(gi, sticky=tuple(cur.R)))
             words += layout_words(cur)
             n_trans += 1
         flush_diag()

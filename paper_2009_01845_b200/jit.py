@@ -364,7 +364,10 @@ class _Gen:
             elif op == OP_LAYOUT:
                 new = self.parse_layout(a)
                 li += 1
-                if not self.halves:
+                pairs = None if self.halves else self.swap_pairs(self.lay, new)
+                if pairs:
+                    self.gen_predicated_transpose(new, li, pairs)
+                elif not self.halves:
                     self.emit("    csync();")
                     self.emit("    { const u32 sj = swz(jt%d);" % self.li)
                     for s in range(A):
@@ -416,6 +419,48 @@ class _Gen:
         self.emit(f"    {{ const C ph = PZ({ci});")
         for s in range(self.A):
             self.emit(f"      v{self.vm[s]} = cm(v{self.vm[s]}, ph);")
+        self.emit("    }")
+
+    def swap_pairs(self, old, new):
+        """[(slot i, thread position j)] when `new` differs from `old` only by exchanging register
+        slot i's tile bit with thread position j's (fusion.compile_pass change_layout), else None."""
+        pairs = []
+        for i in range(self.NREG):
+            if new['R'][i] == old['R'][i]:
+                continue
+            if new['R'][i] not in old['Tb']:
+                return None
+            j = old['Tb'].index(new['R'][i])
+            if new['Tb'][j] != old['R'][i]:
+                return None
+            pairs.append((i, j))
+        for j in range(self.TB):
+            if new['Tb'][j] != old['Tb'][j] and not any(j == jj for _, jj in pairs):
+                return None
+        return pairs or None
+
+    def gen_predicated_transpose(self, new, li, pairs):
+        """Layout change that exchanges register slots with thread positions: an amplitude whose
+        swapped slot bits equal the thread's swapped thread bits stays in its register, so only
+        the others go through shared memory (1 pair: half, 2 pairs: 3/4 of the tile)."""
+        A = self.A
+        old = self.lay
+        tp = " | ".join(f"((((u32)tid >> {j}) & 1u) << {p})" for p, (_, j) in enumerate(pairs))
+
+        def pat(s):
+            return sum(((s >> i) & 1) << p for p, (i, _) in enumerate(pairs))
+
+        self.emit("    csync();")
+        self.emit(f"    const u32 tp{li} = {tp};")
+        self.emit("    { const u32 sj = swz(jt%d);" % self.li)
+        for s in range(A):
+            self.emit(f"      if (tp{li} != {pat(s)}u) sm.tbuf[sj ^ {self.swz_const(old['jt'][s])}u] = v{self.vm[s]};")
+        self.emit("    }")
+        self.emit("    csync();")
+        self.set_layout(new, li)
+        self.emit("    { const u32 sj = swz(jt%d);" % li)
+        for s in range(A):
+            self.emit(f"      if (tp{li} != {pat(s)}u) v{self.vm[s]} = sm.tbuf[sj ^ {self.swz_const(new['jt'][s])}u];")
         self.emit("    }")
 
     def gen_split_transpose(self, new, li):
