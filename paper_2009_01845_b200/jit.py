@@ -364,7 +364,7 @@ class _Gen:
             elif op == OP_LAYOUT:
                 new = self.parse_layout(a)
                 li += 1
-                pairs = None if self.halves else self.swap_pairs(self.lay, new)
+                pairs = None if (self.halves or not _MINIMAL) else self.swap_pairs(self.lay, new)
                 if pairs:
                     self.gen_predicated_transpose(new, li, pairs)
                 elif not self.halves:
@@ -853,6 +853,7 @@ _lock = threading.Lock()
 _disabled = os.environ.get("QSB_JIT", "1") == "0"
 # QSB_JIT_PROBE=nogates|notransposes: timing experiments only (kernels compute wrong results)
 _PROBE = os.environ.get("QSB_JIT_PROBE", "")
+_MINIMAL = os.environ.get("QSB_MINIMAL_LAYOUT", "0") == "1"  # predicated transposes (fusion.MINIMAL_LAYOUT_CHANGES)
 _avail = None
 
 
