@@ -110,6 +110,13 @@ int qsb_norm2(const void* amps, uint64_t n_amps, int dtype, double* out, void* s
 /* out[0..1] = <a|b> (conjugate-linear in a), complex128 on device.  Deterministic. */
 int qsb_vdot(const void* a, const void* b, uint64_t n_amps, int dtype, double* out, void* stream);
 
+/* out[0..1] = sum_t <psi| M_t |psi> over n_terms 1- or 2-qubit terms (hamiltonians.py:192-207
+ * `expectation`): ks[t] in {1, 2}, bits[2t] = bit of targets[0] (matrix MSB), bits[2t+1] = bit of
+ * targets[1]; mats = 32 doubles per term (row-major complex 2^k x 2^k).  One read-only sweep per
+ * term, no state copy; deterministic. */
+int qsb_expect_terms(const void* amps, int n_qubits, int dtype, int n_terms, const int* ks, const int* bits,
+                     const double* mats, double* out, void* stream);
+
 /* ---- measurement (measurement.py:36-87) -------------------------------------------------- */
 /* probs[i] = |a_i|^2 computed exactly as numpy's np.abs(a.astype(complex128))**2
  * (SURVEY.md Appendix B.1), float64 on device. */

@@ -43,6 +43,8 @@ SIGNATURES = {
     ),
     "qsb_scale": (_c_int, [_c_void_p, _c_u64, _c_int, _c_double, _c_double, _c_void_p]),
     "qsb_collapse": (_c_int, [_c_void_p, _c_u64, _c_int, _c_u64, _c_u64, _c_double, _c_void_p]),
+    "qsb_expect_terms": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+                                  _c_void_p]),
     "qsb_run_pass": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_int, _c_void_p, _c_i64, _c_void_p]),
     "qsb_pass_max_tile_bits": (_c_int, [_c_int]),
     "qsb_norm2": (_c_int, [_c_void_p, _c_u64, _c_int, _c_void_p, _c_void_p]),

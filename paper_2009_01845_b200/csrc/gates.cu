@@ -407,6 +407,94 @@ __global__ void __launch_bounds__(1024) k_fold<double2>(const double2* __restric
   if (threadIdx.x == 0) out[0] = sh[0];
 }
 
+// <psi| M_t |psi> summed over up to kExpMax 1- or 2-qubit terms in one launch: per term one
+// read-only sweep of the state (no copy, no scratch state), the term matrices are kernel
+// parameters (constant-bank operands), accumulation in double, fixed grid => deterministic.
+constexpr int kExpMax = 64;
+struct ExpTerm {
+  int k;       // 1 or 2 target bits
+  int hi, lo;  // bit positions: hi = matrix MSB (targets[0]); lo = targets[1] (k = 2)
+  int pad;
+  double m[32];  // row-major complex (re, im) of the 2^k x 2^k matrix
+};
+struct ExpTerms {
+  int count;
+  int pad;
+  ExpTerm t[kExpMax];
+};
+
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_expect_partial(const cplx<R>* __restrict__ a, int n,
+                                                             const __grid_constant__ ExpTerms T,
+                                                             double2* __restrict__ part) {
+  __shared__ double2 sh[kThreads];
+  double2 acc = make_double2(0.0, 0.0);
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (int t = 0; t < T.count; ++t) {
+    const ExpTerm& e = T.t[t];
+    const int k = e.k;
+    const uint64_t groups = 1ull << (n - k);
+    const int b1 = e.hi, b0 = (k == 2) ? e.lo : e.hi;
+    const int lo = b1 < b0 ? b1 : b0, hi = b1 < b0 ? b0 : b1;
+    for (uint64_t g = (uint64_t)blockIdx.x * kThreads + threadIdx.x; g < groups; g += stride) {
+      uint64_t i = g;
+      {
+        const uint64_t l = i & ((1ull << lo) - 1ull);
+        i = ((i ^ l) << 1) | l;
+      }
+      if (k == 2) {
+        const uint64_t l = i & ((1ull << hi) - 1ull);
+        i = ((i ^ l) << 1) | l;
+      }
+      double xr[4], xi[4];
+      const int d = 1 << k;
+      for (int r = 0; r < d; ++r) {
+        // matrix row r: bit (k-1) <-> targets[0] (hi), bit 0 <-> targets[1]
+        uint64_t idx = i;
+        if (k == 1) {
+          if (r & 1) idx |= 1ull << e.hi;
+        } else {
+          if (r & 2) idx |= 1ull << e.hi;
+          if (r & 1) idx |= 1ull << e.lo;
+        }
+        const cplx<R> v = a[idx];
+        xr[r] = (double)v.x;
+        xi[r] = (double)v.y;
+      }
+      for (int r = 0; r < d; ++r) {
+        double yr = 0.0, yi = 0.0;
+        for (int c = 0; c < d; ++c) {
+          const double mr = e.m[2 * (r * d + c)], mi = e.m[2 * (r * d + c) + 1];
+          yr = fma(mr, xr[c], yr);
+          yr = fma(-mi, xi[c], yr);
+          yi = fma(mr, xi[c], yi);
+          yi = fma(mi, xr[c], yi);
+        }
+        // conj(x_r) * y_r
+        acc.x = fma(xr[r], yr, acc.x);
+        acc.x = fma(xi[r], yi, acc.x);
+        acc.y = fma(xr[r], yi, acc.y);
+        acc.y = fma(-xi[r], yr, acc.y);
+      }
+    }
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      sh[threadIdx.x].x += sh[threadIdx.x + s].x;
+      sh[threadIdx.x].y += sh[threadIdx.x + s].y;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void k_add2(double2* out, const double2* v) {
+  out->x += v->x;
+  out->y += v->y;
+}
+
 // scratch for the partials: one lazily grown device buffer per process (tiny)
 static void* g_red_scratch = nullptr;
 static int ensure_red_scratch() {
@@ -601,6 +689,57 @@ int qsb_scale(void* amps, uint64_t n, int dtype, double re, double im, void* str
     k_scale<float><<<stream_grid(n), kThreads, 0, st>>>(static_cast<float2*>(amps), n,
                                                         make_float2((float)re, (float)im));
   QSB_CHECK_LAUNCH("qsb_scale");
+  return QSB_OK;
+}
+
+int qsb_expect_terms(const void* amps, int n_qubits, int dtype, int n_terms, const int* ks, const int* bits,
+                     const double* mats, double* out, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  if (n_terms < 0 || (n_terms > 0 && (!ks || !bits || !mats))) {
+    set_error("qsb_expect_terms: bad term arrays");
+    return QSB_ERR_ARG;
+  }
+  if (int s = ensure_red_scratch()) return s;
+  cudaStream_t st = as_stream(stream);
+  double2* part = static_cast<double2*>(g_red_scratch);
+  static double2* acc = nullptr;  // running (re, im) over term chunks
+  if (!acc) {
+    cudaError_t e = cudaMalloc(&acc, 2 * sizeof(double2));
+    if (e != cudaSuccess) return cuda_status(e, "expectation accumulator");
+  }
+  const uint64_t n = 1ull << n_qubits;
+  cudaMemsetAsync(out, 0, 2 * sizeof(double), st);
+  for (int t0 = 0; t0 < n_terms || (t0 == 0 && n_terms == 0); t0 += kExpMax) {
+    ExpTerms T;
+    memset(&T, 0, sizeof T);
+    T.count = n_terms - t0 < kExpMax ? n_terms - t0 : kExpMax;
+    for (int j = 0; j < T.count; ++j) {
+      const int t = t0 + j;
+      const int k = ks[t];
+      if (k != 1 && k != 2) {
+        set_error("qsb_expect_terms: terms act on 1 or 2 qubits, got %d", k);
+        return QSB_ERR_SHAPE;
+      }
+      const int hi = bits[2 * t], lo = bits[2 * t + 1];
+      if (hi < 0 || hi >= n_qubits || (k == 2 && (lo < 0 || lo >= n_qubits || lo == hi))) {
+        set_error("qsb_expect_terms: bad bit positions");
+        return QSB_ERR_SHAPE;
+      }
+      T.t[j].k = k;
+      T.t[j].hi = hi;
+      T.t[j].lo = k == 2 ? lo : hi;
+      memcpy(T.t[j].m, mats + 32 * (size_t)t, sizeof(double) * 2 * (1 << k) * (1 << k));
+    }
+    if (T.count == 0) break;
+    if (dtype == QSB_C128)
+      k_expect_partial<double><<<kRedBlocks, kThreads, 0, st>>>(static_cast<const double2*>(amps), n_qubits, T, part);
+    else
+      k_expect_partial<float><<<kRedBlocks, kThreads, 0, st>>>(static_cast<const float2*>(amps), n_qubits, T, part);
+    k_fold<double2><<<1, 1024, 0, st>>>(part, kRedBlocks, acc);
+    k_add2<<<1, 1, 0, st>>>(reinterpret_cast<double2*>(out), acc);
+  }
+  (void)n;
+  QSB_CHECK_LAUNCH("qsb_expect_terms");
   return QSB_OK;
 }
 

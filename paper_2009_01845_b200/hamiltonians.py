@@ -123,29 +123,31 @@ def combine(a, coeff_a: float, b, coeff_b: float):
 
 
 def expectation(h, state: StateVector) -> float:
-    """<psi|H|psi> (real part) term by term on the device (hamiltonians.py:192-207): per term
-    one D2D copy, one term kernel, one deterministic <psi|H_t psi> reduction."""
+    """<psi|H|psi> (real part) on the device (hamiltonians.py:192-207): every term's
+    <psi|H_t|psi> is accumulated by `qsb_expect_terms` -- one read-only sweep of the state per
+    term, no state copy (the reference copies the state and applies each term to the copy)."""
     if h.n_qubits != state.n_qubits:
         raise ShapeError(f"Hamiltonian has {h.n_qubits} qubits, state has {state.n_qubits}")
     if not isinstance(h, TrotterHamiltonian):
         _dense_unsupported()
-    from .gates import apply_matrix_device
-
     torch = nat.torch_mod()
-    psi = state.tensor
-    if psi.dtype != torch.complex128:
-        psi = psi.to(torch.complex128)
-    scratch = torch.empty_like(psi)
-    out = torch.empty(2, dtype=torch.float64, device=psi.device)
-    lib = nat.lib()
-    total = 0.0
-    for qubits, m in h.terms:
-        scratch.copy_(psi)
-        apply_matrix_device(scratch.data_ptr(), h.n_qubits, nat.QSB_C128, qubits, m, (), kernel=None)
-        nat.check(lib.qsb_vdot(psi.data_ptr(), scratch.data_ptr(), psi.numel(), nat.QSB_C128, out.data_ptr(),
-                               nat.stream_ptr()), "expectation")
-        total += float(out[0].item())
-    return float(total)
+    n = h.n_qubits
+    terms = list(h.terms)
+    ks = np.array([len(q) for q, _ in terms], dtype=np.int32)
+    bits = np.zeros(2 * max(1, len(terms)), dtype=np.int32)
+    mats = np.zeros(32 * max(1, len(terms)), dtype=np.float64)
+    for t, (qubits, m) in enumerate(terms):
+        if len(qubits) not in (1, 2):
+            raise ShapeError(f"expectation supports 1- and 2-qubit terms, got {len(qubits)}")
+        bits[2 * t] = n - 1 - qubits[0]
+        bits[2 * t + 1] = n - 1 - qubits[-1]
+        mm = np.ascontiguousarray(np.asarray(m, dtype=np.complex128))
+        mats[32 * t:32 * t + 2 * mm.size] = mm.view(np.float64).reshape(-1)
+    out = torch.empty(2, dtype=torch.float64, device=state.tensor.device)
+    nat.check(nat.lib().qsb_expect_terms(state.data_ptr, n, state.precision.qsb_dtype, len(terms), ks.ctypes.data,
+                                         bits.ctypes.data, mats.ctypes.data, out.data_ptr(), nat.stream_ptr()),
+              "expectation")
+    return float(out[0].item())
 
 
 def ground_state_vector(h, precision: Precision = Precision.F64) -> StateVector:

@@ -396,3 +396,34 @@ def test_interpreted_pass_kernel_without_nvrtc(cuda, monkeypatch):
     assert max_abs(vc.execute(precision=q.Precision.F32).amplitudes, gv["f32_14_1"]) <= TOL32
     g15 = golden("grid15")
     assert max_abs(circuit_from_json(g15["circuit"]).execute().amplitudes, g15["out"]) <= TOL64
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_expectation_fused_terms(cuda, prec):
+    """qsb_expect_terms: mixed 1-/2-qubit terms, reversed target order, > 64 terms (chunked),
+    complex64 states read in float64 exactly as the reference's astype(complex128)."""
+    import paper_2009_01845_b200 as q
+
+    n = 14
+    rng = np.random.default_rng(11)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    P = q.Precision.F64 if prec == "f64" else q.Precision.F32
+    st = q.from_amplitudes(psi, precision=P)
+    base = st.amplitudes.astype(np.complex128)
+    terms = []
+    for i in range(n):
+        a = rng.standard_normal((2, 2)) + 1j * rng.standard_normal((2, 2))
+        terms.append(((i,), a + a.conj().T))
+    for i in range(n):
+        for j in ((i + 3) % n, (i + 5) % n, (i + 1) % n, (i + 7) % n):
+            b = rng.standard_normal((4, 4)) + 1j * rng.standard_normal((4, 4))
+            terms.append(((j, i), b + b.conj().T))
+    h = q.TrotterHamiltonian(n, terms)
+    want = 0.0
+    for qs, m in h.terms:
+        t = base.copy()
+        ov.apply_matrix(t, n, qs, m)
+        want += np.vdot(base, t).real
+    assert len(h.terms) > 64
+    assert abs(q.expectation(h, st) - want) <= 1e-10 * max(1.0, abs(want))

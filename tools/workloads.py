@@ -69,6 +69,12 @@ def main():
     cols = n // rows
     grid = q.random_grid_circuit(rows, cols, 20, 42)
     run_circuit(f"grid {rows}x{cols} 20 cycles", grid, rows * cols, q.Precision.F64)
+    # Trotter-form energy (EnergyCallback / CLI final_energy): 2n terms
+    st = q.uniform_state(n)
+    ms = timed(lambda: q.expectation(h, st), reps=2)
+    print(f"expectation <H> ({len(h.terms)} terms) n={n}: {ms:.1f} ms "
+          f"({len(h.terms)} read sweeps at {len(h.terms) * (1 << n) * 16 / ms / 1e6:.0f} GB/s)", flush=True)
+    del st
     # sampling
     st = q.qft_circuit(n).execute(q.basis_state(n, 12345))
     for shots in (100000, 1000000):
