@@ -423,6 +423,68 @@ struct ExpTerms {
   ExpTerm t[kExpMax];
 };
 
+// one term, K target bits: kItems groups per thread per round with all loads issued before any
+// math; fully unrolled so the amplitudes stay in registers
+template <typename R, int K>
+__device__ __forceinline__ void expect_term(const cplx<R>* __restrict__ a, int n, const ExpTerm& e, uint64_t stride,
+                                            double2& acc) {
+  constexpr int kItems = 4;
+  constexpr int D = 1 << K;
+  const uint64_t groups = 1ull << (n - K);
+  const int b1 = e.hi, b0 = (K == 2) ? e.lo : e.hi;
+  const int lo = b1 < b0 ? b1 : b0, hi = b1 < b0 ? b0 : b1;
+  const uint64_t off1 = 1ull << e.hi;
+  const uint64_t off0 = (K == 2) ? (1ull << e.lo) : 0ull;
+  for (uint64_t g0 = (uint64_t)blockIdx.x * kThreads * kItems + threadIdx.x; g0 < groups; g0 += stride * kItems) {
+    double xr[kItems][D], xi[kItems][D];
+    bool ok[kItems];
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const uint64_t g = g0 + (uint64_t)it * kThreads;
+      ok[it] = g < groups;
+      uint64_t i = ok[it] ? g : 0;
+      {
+        const uint64_t l = i & ((1ull << lo) - 1ull);
+        i = ((i ^ l) << 1) | l;
+      }
+      if (K == 2) {
+        const uint64_t l = i & ((1ull << hi) - 1ull);
+        i = ((i ^ l) << 1) | l;
+      }
+      // matrix row r: bit (K-1) <-> targets[0] (hi), bit 0 <-> targets[1]
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        const uint64_t idx = i | ((K == 1) ? ((r & 1) ? off1 : 0ull)
+                                           : (((r & 2) ? off1 : 0ull) | ((r & 1) ? off0 : 0ull)));
+        const cplx<R> v = a[idx];
+        xr[it][r] = (double)v.x;
+        xi[it][r] = (double)v.y;
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      if (!ok[it]) continue;
+#pragma unroll
+      for (int r = 0; r < D; ++r) {
+        double yr = 0.0, yi = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const double mr = e.m[2 * (r * D + c)], mi = e.m[2 * (r * D + c) + 1];
+          yr = fma(mr, xr[it][c], yr);
+          yr = fma(-mi, xi[it][c], yr);
+          yi = fma(mr, xi[it][c], yi);
+          yi = fma(mi, xr[it][c], yi);
+        }
+        // conj(x_r) * y_r
+        acc.x = fma(xr[it][r], yr, acc.x);
+        acc.x = fma(xi[it][r], yi, acc.x);
+        acc.y = fma(xr[it][r], yi, acc.y);
+        acc.y = fma(-xi[it][r], yr, acc.y);
+      }
+    }
+  }
+}
+
 template <typename R>
 __global__ void __launch_bounds__(kThreads) k_expect_partial(const cplx<R>* __restrict__ a, int n,
                                                              const __grid_constant__ ExpTerms T,
@@ -431,52 +493,10 @@ __global__ void __launch_bounds__(kThreads) k_expect_partial(const cplx<R>* __re
   double2 acc = make_double2(0.0, 0.0);
   const uint64_t stride = (uint64_t)gridDim.x * kThreads;
   for (int t = 0; t < T.count; ++t) {
-    const ExpTerm& e = T.t[t];
-    const int k = e.k;
-    const uint64_t groups = 1ull << (n - k);
-    const int b1 = e.hi, b0 = (k == 2) ? e.lo : e.hi;
-    const int lo = b1 < b0 ? b1 : b0, hi = b1 < b0 ? b0 : b1;
-    for (uint64_t g = (uint64_t)blockIdx.x * kThreads + threadIdx.x; g < groups; g += stride) {
-      uint64_t i = g;
-      {
-        const uint64_t l = i & ((1ull << lo) - 1ull);
-        i = ((i ^ l) << 1) | l;
-      }
-      if (k == 2) {
-        const uint64_t l = i & ((1ull << hi) - 1ull);
-        i = ((i ^ l) << 1) | l;
-      }
-      double xr[4], xi[4];
-      const int d = 1 << k;
-      for (int r = 0; r < d; ++r) {
-        // matrix row r: bit (k-1) <-> targets[0] (hi), bit 0 <-> targets[1]
-        uint64_t idx = i;
-        if (k == 1) {
-          if (r & 1) idx |= 1ull << e.hi;
-        } else {
-          if (r & 2) idx |= 1ull << e.hi;
-          if (r & 1) idx |= 1ull << e.lo;
-        }
-        const cplx<R> v = a[idx];
-        xr[r] = (double)v.x;
-        xi[r] = (double)v.y;
-      }
-      for (int r = 0; r < d; ++r) {
-        double yr = 0.0, yi = 0.0;
-        for (int c = 0; c < d; ++c) {
-          const double mr = e.m[2 * (r * d + c)], mi = e.m[2 * (r * d + c) + 1];
-          yr = fma(mr, xr[c], yr);
-          yr = fma(-mi, xi[c], yr);
-          yi = fma(mr, xi[c], yi);
-          yi = fma(mi, xr[c], yi);
-        }
-        // conj(x_r) * y_r
-        acc.x = fma(xr[r], yr, acc.x);
-        acc.x = fma(xi[r], yi, acc.x);
-        acc.y = fma(xr[r], yi, acc.y);
-        acc.y = fma(-xi[r], yr, acc.y);
-      }
-    }
+    if (T.t[t].k == 1)
+      expect_term<R, 1>(a, n, T.t[t], stride, acc);
+    else
+      expect_term<R, 2>(a, n, T.t[t], stride, acc);
   }
   sh[threadIdx.x] = acc;
   __syncthreads();

@@ -94,6 +94,7 @@ def run_plan(state, plan: Plan, scratch_holder: dict | None = None, stream=None,
     n = state.n_qubits
     dtype = state.precision.qsb_dtype
     holder = scratch_holder if scratch_holder is not None else {}
+    jit.precompile([s for s in plan.steps if isinstance(s, PassStep)], dtype)
     for step in plan.steps:
         if isinstance(step, GateStep):
             _apply_gate_step(state.data_ptr, n, dtype, step.gate, st)

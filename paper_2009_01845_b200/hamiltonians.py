@@ -122,6 +122,26 @@ def combine(a, coeff_a: float, b, coeff_b: float):
     return TrotterHamiltonian(a.n_qubits, [(q, acc[q]) for q in order])
 
 
+def _fold_single_terms(terms):
+    """Sum each 1-qubit term into a 2-qubit term on the same qubit (M2 + M1 (x) I, exact
+    algebra): one read sweep per remaining term instead of one per term (TFIM + X: 2N -> N)."""
+    terms = [(tuple(q), np.asarray(m, dtype=np.complex128)) for q, m in terms]
+    pairs = [i for i, (q, _) in enumerate(terms) if len(q) == 2]
+    out = {i: terms[i][1].copy() for i in pairs}
+    keep = []
+    eye = np.eye(2, dtype=np.complex128)
+    for i, (q, m) in enumerate(terms):
+        if len(q) == 2:
+            continue
+        host = next((j for j in pairs if q[0] in terms[j][0]), None)
+        if host is None:
+            keep.append((q, m))
+            continue
+        pos = terms[host][0].index(q[0])
+        out[host] += np.kron(m, eye) if pos == 0 else np.kron(eye, m)
+    return [(terms[i][0], out[i]) for i in pairs] + keep
+
+
 def expectation(h, state: StateVector) -> float:
     """<psi|H|psi> (real part) on the device (hamiltonians.py:192-207): every term's
     <psi|H_t|psi> is accumulated by `qsb_expect_terms` -- one read-only sweep of the state per
@@ -132,7 +152,7 @@ def expectation(h, state: StateVector) -> float:
         _dense_unsupported()
     torch = nat.torch_mod()
     n = h.n_qubits
-    terms = list(h.terms)
+    terms = _fold_single_terms(h.terms)
     ks = np.array([len(q) for q, _ in terms], dtype=np.int32)
     bits = np.zeros(2 * max(1, len(terms)), dtype=np.int32)
     mats = np.zeros(32 * max(1, len(terms)), dtype=np.float64)

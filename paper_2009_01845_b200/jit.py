@@ -921,27 +921,52 @@ def compile_words(words, dtype):
         pbytes = np.zeros(1, dtype=pbytes.dtype)
     with _lock:
         hit = _cache.get(src)
-        if hit is None:
-            lib = nat.lib()
-            fn = ctypes.c_void_p()
-            log = ctypes.create_string_buffer(1 << 16)
-            rc = lib.qsb_jit_compile(src.encode(), name.encode(), _nvrtc_path().encode(), ctypes.byref(fn), log,
-                                     len(log))
-            if rc != 0:
-                raise RuntimeError(f"NVRTC failed: {log.value.decode(errors='replace')[:2000]}")
-            hit = _Compiled()
-            hit.func = fn.value
-            hit.name = name
-            K, nreg = int(words[2]), int(words[3])
-            amp = 16 if dtype == nat.QSB_C128 else 8
-            stage_amps = 1 << (K - 1 if (1 << K) * amp > 65536 else K)
-            hit.smem = smem_bytes(stage_amps * amp, len(tables))
-            hit.ctas = ctas_per_sm(1 << (K - nreg))
-            hit.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
-            hit.n_tiles = 1 << (int(words[4]) - int(words[2]))
-            hit.threads = (1 << (int(words[2]) - int(words[3]))) + 128
-            _cache[src] = hit
+    if hit is None:
+        # NVRTC + module load outside the lock: passes of one plan compile concurrently
+        lib = nat.lib()
+        fn = ctypes.c_void_p()
+        log = ctypes.create_string_buffer(1 << 16)
+        rc = lib.qsb_jit_compile(src.encode(), name.encode(), _nvrtc_path().encode(), ctypes.byref(fn), log,
+                                 len(log))
+        if rc != 0:
+            raise RuntimeError(f"NVRTC failed: {log.value.decode(errors='replace')[:2000]}")
+        K, nreg = int(words[2]), int(words[3])
+        amp = 16 if dtype == nat.QSB_C128 else 8
+        stage_amps = 1 << (K - 1 if (1 << K) * amp > 65536 else K)
+        fresh = _Compiled()
+        fresh.func = fn.value
+        fresh.name = name
+        fresh.smem = smem_bytes(stage_amps * amp, len(tables))
+        fresh.ctas = ctas_per_sm(1 << (K - nreg))
+        fresh.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
+        fresh.n_tiles = 1 << (int(words[4]) - K)
+        fresh.threads = (1 << (K - nreg)) + 128
+        with _lock:
+            hit = _cache.setdefault(src, fresh)
     return hit, (np.ascontiguousarray(pbytes), tables)
+
+
+def precompile(steps, dtype, device: int | None = None) -> None:
+    """Specialise the passes of a plan concurrently (NVRTC runs outside the GIL and the cache
+    lock); each worker binds the caller's CUDA device before loading its module.  Steps that
+    fail keep `jit = None` and are retried (then fall back) when they run."""
+    todo = [s for s in steps if getattr(s, "jit", None) is None and not getattr(s, "no_jit", False)]
+    if len(todo) < 2 or not available():
+        return
+    torch = nat.torch_mod()
+    dev = torch.cuda.current_device() if device is None else device
+
+    def work(step):
+        try:
+            torch.cuda.set_device(dev)
+            step.jit = compile_words(step.words, dtype)
+        except Exception:
+            pass
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(todo), max(1, min(16, os.cpu_count() or 1)))) as ex:
+        list(ex.map(work, todo))
 
 
 def run(words, dtype, src_ptr, dst_ptr, n_qubits, stream_ptr, compiled=None, coeffs=None):
