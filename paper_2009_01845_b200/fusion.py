@@ -78,6 +78,10 @@ elif _GEO_ENV == "wide512":
     GEOMETRY_JIT = GEOMETRY_JIT_WIDE512
 elif _GEO_ENV == "k11":
     GEOMETRY_JIT = GEOMETRY_JIT_K11
+elif _GEO_ENV == "k12x2":
+    # c128: 64 KB tiles, 128 consumers x 32 amplitudes, two CTAs per SM (one stage each, reused
+    # as the transpose buffer) so one CTA's FP64 work overlaps the other's loads / transposes
+    GEOMETRY_JIT = {nat.QSB_C128: TileGeometry(12, 3, 4, 5), nat.QSB_C64: GEOMETRY_JIT[nat.QSB_C64]}
 
 
 def _f2w(x: float) -> int:

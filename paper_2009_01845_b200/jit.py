@@ -110,7 +110,7 @@ __device__ __forceinline__ u32 swz(u32 j) {
   for (int s = GB; s < HBB; s += GB) f ^= (j >> s);
   return j ^ (f & ((1u << GB) - 1u));
 }
-struct Smem { C stage[STAGES][1 << HBB]; C tbuf[1 << HBB]; double2 ep[4][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 base[STAGES][2]; u32 zero; };
+struct Smem { C stage[STAGES][1 << HBB]; C tbuf[ALIAS ? 1 : (1 << HBB)]; double2 ep[4][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 base[STAGES][2]; u32 zero; };
 """
 
 
@@ -220,6 +220,9 @@ class _Gen:
         # 128 KB tiles are staged as two 64 KB halves split on tile bit K-1 (a register bit of
         # the first layout); layout changes then run in two rounds through a 64 KB buffer
         self.halves = (1 << K) * amp_bytes > 65536
+        # two CTAs per SM with 64 KB tiles: one stage per CTA, reused as the transpose buffer
+        self.alias = (not self.halves) and ctas_per_sm(self.consumers) == 2 and (1 << K) * amp_bytes == 65536
+        self.stages = 1 if self.alias else STAGES
         self.HB = K - 1 if self.halves else K  # bits of a stage / transpose-buffer index
 
     # uniform coefficients (gate matrices, phases): a kernel-parameter array of R, read as
@@ -335,8 +338,11 @@ class _Gen:
                 off = sum(1 << sig[first['R'][i]] for i in range(self.NREG) if (s >> i) & 1)
                 self.emit(f"    C v{s} = buf[sg0 | {off}u];")
             # the stage is consumed: hand it back to the producer before any compute
-            self.emit("    fence_async();")
-            self.emit("    mbar_arrive(&sm.empty[s]);")
+            if self.alias:
+                self.emit("@@RELEASE@@")  # the stage doubles as the transpose buffer: release at tile end
+            else:
+                self.emit("    fence_async();")
+                self.emit("    mbar_arrive(&sm.empty[s]);")
         else:
             ih = first['R'].index(self.K - 1)
             self.emit(f"    C {', '.join(f'v{s}' for s in range(A))};")
@@ -371,13 +377,13 @@ class _Gen:
                     self.emit("    csync();")
                     self.emit("    { const u32 sj = swz(jt%d);" % self.li)
                     for s in range(A):
-                        self.emit(f"      sm.tbuf[sj ^ {self.swz_const(self.lay['jt'][s])}u] = v{self.vm[s]};")
+                        self.emit(f"      TBUF[sj ^ {self.swz_const(self.lay['jt'][s])}u] = v{self.vm[s]};")
                     self.emit("    }")
                     self.emit("    csync();")
                     self.set_layout(new, li)
                     self.emit("    { const u32 sj = swz(jt%d);" % li)
                     for s in range(A):
-                        self.emit(f"      v{self.vm[s]} = sm.tbuf[sj ^ {self.swz_const(new['jt'][s])}u];")
+                        self.emit(f"      v{self.vm[s]} = TBUF[sj ^ {self.swz_const(new['jt'][s])}u];")
                     self.emit("    }")
                 else:
                     self.gen_split_transpose(new, li)
@@ -454,13 +460,13 @@ class _Gen:
         self.emit(f"    const u32 tp{li} = {tp};")
         self.emit("    { const u32 sj = swz(jt%d);" % self.li)
         for s in range(A):
-            self.emit(f"      if (tp{li} != {pat(s)}u) sm.tbuf[sj ^ {self.swz_const(old['jt'][s])}u] = v{self.vm[s]};")
+            self.emit(f"      if (tp{li} != {pat(s)}u) TBUF[sj ^ {self.swz_const(old['jt'][s])}u] = v{self.vm[s]};")
         self.emit("    }")
         self.emit("    csync();")
         self.set_layout(new, li)
         self.emit("    { const u32 sj = swz(jt%d);" % li)
         for s in range(A):
-            self.emit(f"      if (tp{li} != {pat(s)}u) v{self.vm[s]} = sm.tbuf[sj ^ {self.swz_const(new['jt'][s])}u];")
+            self.emit(f"      if (tp{li} != {pat(s)}u) v{self.vm[s]} = TBUF[sj ^ {self.swz_const(new['jt'][s])}u];")
         self.emit("    }")
 
     def gen_split_transpose(self, new, li):
@@ -501,12 +507,12 @@ class _Gen:
             self.emit("    csync();")
             self.emit(f"    {{ const u32 sj = swz({jw});")
             for s in olds:
-                self.emit(f"      sm.tbuf[sj ^ {self.swz_const(slot_index(old['R'], s))}u] = v{self.vm[s]};")
+                self.emit(f"      TBUF[sj ^ {self.swz_const(slot_index(old['R'], s))}u] = v{self.vm[s]};")
             self.emit("    }")
             self.emit("    csync();")
             self.emit(f"    {{ const u32 sj = swz({jr});")
             for s in news:
-                self.emit(f"      v{nvm[s]} = sm.tbuf[sj ^ {self.swz_const(slot_index(new['R'], s))}u];")
+                self.emit(f"      v{nvm[s]} = TBUF[sj ^ {self.swz_const(slot_index(new['R'], s))}u];")
             self.emit("    }")
         self.vm = nvm
         self.set_layout(new, li)
@@ -751,7 +757,7 @@ class _Gen:
                    f"          const int co[5] = {{{', '.join(coords)}}};\n"
                    f"          tma5(d + (u64)k * {call_bytes}u, &tmap, co, &sm.full[s]);\n"
                    f"        }}")
-        defs = (f"#define QSB_F32X2 {1 if self.dtype == nat.QSB_C64 else 0}\n#define R {real}\n#define C {real}2\n#define KB {K}\n#define HBB {self.HB}\n#define GB {self.G}\n#define STAGES {STAGES}\n"
+        defs = (f"#define QSB_F32X2 {1 if self.dtype == nat.QSB_C64 else 0}\n#define R {real}\n#define C {real}2\n#define KB {K}\n#define HBB {self.HB}\n#define GB {self.G}\n#define STAGES {self.stages}\n#define ALIAS {1 if self.alias else 0}\n#define TBUF {"sm.stage[s]" if self.alias else "sm.tbuf"}\n"
                 f"#define CONSUMERS {self.consumers}\n#define MAXPIV {MAX_PIV}\n#define NPIV {self.npiv}\n"
                 f"#define NCOEF {max(1, len(self.coeffs))}\n#define NTAB {len(self.tables)}\n")
         issue = f"""      {{ // producer warp: fetch tile c into stage s (tile number tno)
@@ -789,6 +795,10 @@ class _Gen:
       }}""")
             issue = "\n".join(halves_code)
         body = body.replace("@@REFILL@@", "")
+        if self.alias:
+            body = body.replace("@@RELEASE@@", "")
+            body += "\n    csync();  // every thread is done with the stage (loads and transposes)\n" \
+                    "    fence_async();\n    mbar_arrive(&sm.empty[s]);"
         if self.halves:
             head = """    mbar_wait(&sm.full[0], it & 1);
     const u64 base = sm.base[0][0];
@@ -904,9 +914,11 @@ MAX_COEFFS = 3072  # 24 KB of pivot tables staged in shared memory
 MAX_PARAM_BYTES = 31744  # kernel parameter space: 32764 B minus the pointers and the tensor map
 
 
-def smem_bytes(stage_bytes: int, n_coeffs=MAX_COEFFS) -> int:
-    # STAGES stages + one transpose buffer of stage_bytes (a whole tile, or half of a 128 KB tile)
-    struct_bytes = (STAGES + 1) * stage_bytes + 4 * MAX_PIV * 16 + 8 * STAGES * 4 + 16
+def smem_bytes(stage_bytes: int, n_coeffs=MAX_COEFFS, alias: bool = False) -> int:
+    # STAGES stages + one transpose buffer of stage_bytes (a whole tile, or half of a 128 KB
+    # tile); `alias`: a single stage that doubles as the transpose buffer (two CTAs per SM)
+    n_buf = 1 if alias else STAGES + 1
+    struct_bytes = n_buf * stage_bytes + 4 * MAX_PIV * 16 + 8 * STAGES * 4 + 16 + 16
     return struct_bytes + 8 * n_coeffs + 128
 
 
@@ -936,7 +948,8 @@ def compile_words(words, dtype):
         fresh = _Compiled()
         fresh.func = fn.value
         fresh.name = name
-        fresh.smem = smem_bytes(stage_amps * amp, len(tables))
+        alias = (1 << K) * amp == 65536 and ctas_per_sm(1 << (K - nreg)) == 2
+        fresh.smem = smem_bytes(stage_amps * amp, len(tables), alias)
         fresh.ctas = ctas_per_sm(1 << (K - nreg))
         fresh.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
         fresh.n_tiles = 1 << (int(words[4]) - K)
