@@ -427,3 +427,27 @@ def test_expectation_fused_terms(cuda, prec):
         want += np.vdot(base, t).real
     assert len(h.terms) > 64
     assert abs(q.expectation(h, st) - want) <= 1e-10 * max(1.0, abs(want))
+
+
+@pytest.mark.parametrize("nq,shots,seed", [(3, 500, 7), (20, 100000, 42)])
+def test_cli_shots_record_digest(cuda, capsys, nq, shots, seed):
+    """`python -m paper_2009_01845_b200.cli shots` prints the reference's record with the
+    reference CLI's sample digest (SURVEY.md 8(c) golden values)."""
+    from paper_2009_01845_b200 import cli
+
+    g = golden("sampling")
+    assert cli.main(["shots", "--nqubits", str(nq), "--nshots", str(shots), "--seed", str(seed)]) == 0
+    rec = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert rec["benchmark"] == "shots" and rec["n_shots"] == shots
+    assert rec["sample_digest"] == str(g[f"digest_{nq}_{shots}_{seed}"])
+
+
+def test_cli_qft_verify_and_evolve(cuda, capsys):
+    from paper_2009_01845_b200 import cli
+
+    assert cli.main(["qft", "--nqubits", "16", "--verify"]) == 0
+    rec = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert rec["verify_max_abs_diff"] <= 1e-12 and rec["passes"] >= 1
+    assert cli.main(["evolve", "--nqubits", "8", "--dt", "0.1", "--T", "0.5"]) == 0
+    rec = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert rec["solver"] == "trotter" and np.isfinite(rec["final_energy"])

@@ -188,3 +188,15 @@ def test_random_grid_builder_matches_oracle_generator():
         for g, (_k, tg, _ct, _p, m) in zip(c.queue, ref):
             assert tuple(g.targets) == tuple(tg)
             assert np.array_equal(q.gate_matrix(g), m)
+
+
+def test_cli_errors_without_gpu(tmp_path, capsys):
+    """Parse / form errors exit like the reference CLI (2) before any device work."""
+    from paper_2009_01845_b200 import cli
+
+    bad = tmp_path / "bad.json"
+    bad.write_text("{not json")
+    assert cli.main(["run", "--circuit", str(bad)]) == 2
+    assert cli.main(["run", "--circuit", str(tmp_path / "missing.json")]) == 2
+    assert cli.main(["evolve", "--nqubits", "4", "--solver", "exp"]) == 2
+    assert cli.main(["nosuch"]) == 2
