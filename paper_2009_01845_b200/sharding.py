@@ -242,15 +242,26 @@ class TorchComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # NCCL orders its transfers after the current stream's pending kernels (and wait() orders
+        # the stream after the transfer); other backends need a host sync after packing
+        try:
+            self.stream_ordered = dist.get_backend(group) == "nccl"
+        except Exception:
+            self.stream_ordered = False
 
     def owns(self, shard_id, owner):
         return owner[shard_id] == self.rank
 
     def sendrecv(self, send, recv, peer):
+        for req in self.isendrecv(send, recv, peer):
+            req.wait()
+
+    def isendrecv(self, send, recv, peer):
+        """Start a paired send/recv; returns the works (NCCL: wait() orders the current CUDA stream
+        after the transfer without blocking the host; gloo: wait() blocks)."""
         dist = self.dist
         ops = [dist.P2POp(dist.isend, send, peer, self.group), dist.P2POp(dist.irecv, recv, peer, self.group)]
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        return dist.batch_isend_irecv(ops)
 
     def all_gather(self, t):
         out = [t.new_empty(t.shape) for _ in range(self.world)]
@@ -391,14 +402,31 @@ def _exchange(sharded: ShardedState, j_bit, p_bit):
         partner_shard = s ^ jmask
         peer = sharded.owner[partner_shard]
         my_half = 1 if not s & jmask else 0
-        send = backend.empty(chunk)
-        recv = backend.empty(chunk)
-        for first in range(0, half, chunk):
+        # double-buffered pipeline: pack chunk k+1 and unpack chunk k-1 while chunk k is on the
+        # wire; every wait() orders the stream (NCCL) before a staging buffer is reused
+        send = [backend.empty(chunk), backend.empty(chunk)]
+        recv = [backend.empty(chunk), backend.empty(chunk)]
+        inflight = [None, None]
+
+        def drain(b):
+            works, first, cnt = inflight[b]
+            for w in works:
+                w.wait()
+            backend.unpack(buf, nl, p_bit, my_half, first, cnt, recv[b])
+            inflight[b] = None
+
+        for k, first in enumerate(range(0, half, chunk)):
+            b = k & 1
+            if inflight[b] is not None:
+                drain(b)
             cnt = min(chunk, half - first)
-            backend.pack(buf, nl, p_bit, my_half, first, cnt, send)
-            _sync_stream()
-            comm.sendrecv(send[:cnt], recv[:cnt], peer)
-            backend.unpack(buf, nl, p_bit, my_half, first, cnt, recv)
+            backend.pack(buf, nl, p_bit, my_half, first, cnt, send[b])
+            if not comm.stream_ordered:
+                _sync_stream()
+            inflight[b] = (comm.isendrecv(send[b][:cnt], recv[b][:cnt], peer), first, cnt)
+        for b in (0, 1):
+            if inflight[b] is not None:
+                drain(b)
 
 
 def _sync_stream():
