@@ -766,7 +766,11 @@ void plan_tma(const void* src, int n, int K, const int64_t* tile_pos, int amp_by
 // Device ring for per-launch program / coefficient words.  Copies are stream-ordered; when the
 // ring wraps, the stream is synchronised once so no in-flight launch can see overwritten words.
 int stage_words(const void* host, size_t bytes, void** device_out, cudaStream_t st) {
+  // The words go through a pinned host mirror of the device ring, so the upload is a real
+  // asynchronous DMA (a pageable source would make the driver synchronise with the stream,
+  // stalling the host behind the GPU at every pass).
   static char* ring = nullptr;
+  static char* hring = nullptr;
   static size_t cursor = 0;
   constexpr size_t kRing = 16u << 20;
   if (bytes > kRing / 4) {
@@ -779,15 +783,23 @@ int stage_words(const void* host, size_t bytes, void** device_out, cudaStream_t 
       ring = nullptr;
       return cuda_status(e, "program ring");
     }
+    e = cudaMallocHost(&hring, kRing);
+    if (e != cudaSuccess) {
+      hring = nullptr;
+      return cuda_status(e, "pinned program ring");
+    }
   }
   size_t off = (cursor + 255) & ~(size_t)255;
   if (off + bytes > kRing) {
+    // every earlier copy out of the pinned mirror (and every launch reading the device ring)
+    // is on this stream: after this sync both rings can be reused from the start
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_status(e, "program ring wrap");
     off = 0;
   }
   cursor = off + bytes;
-  cudaError_t e = cudaMemcpyAsync(ring + off, host, bytes, cudaMemcpyHostToDevice, st);
+  memcpy(hring + off, host, bytes);
+  cudaError_t e = cudaMemcpyAsync(ring + off, hring + off, bytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_status(e, "program upload");
   *device_out = ring + off;
   return QSB_OK;

@@ -1,0 +1,24 @@
+"""Wall time of adiabatic_evolve (Trotter, TFIM, dt 0.05, T 1 -> 20 steps) at several n, with the
+host-side share (plan + circuit build) estimated from a CPU-only planning loop."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2009_01845_b200 as q
+
+for n in [int(a) for a in sys.argv[1:]] or [20, 26, 30]:
+    cfg = q.EvolutionConfig(q.Solver.TROTTER, 0.05, 1.0)
+    q.adiabatic_evolve(q.build_x(n), q.build_tfim(n, 1.0), q.Schedule.linear(), cfg)  # compile
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    st = q.adiabatic_evolve(q.build_x(n), q.build_tfim(n, 1.0), q.Schedule.linear(), cfg)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    e = q.expectation(q.build_tfim(n, 1.0), st)
+    print(f"adiabatic TFIM n={n}: 20 Trotter steps {1e3 * (t1 - t0):.1f} ms ({50 * (t1 - t0):.2f} ms/step), "
+          f"final energy {e:.6f}", flush=True)
+    del st
+    torch.cuda.empty_cache()
