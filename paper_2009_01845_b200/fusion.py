@@ -165,8 +165,15 @@ def _entry_cost(z) -> float:
 
 
 def matrix_cost(m: np.ndarray) -> float:
-    """FP ops per amplitude of applying `m` (sum of entry costs / dimension)."""
-    return sum(_entry_cost(complex(z)) for z in np.asarray(m).reshape(-1)) / m.shape[0]
+    """FP ops per amplitude of applying `m` (sum of entry costs / dimension; vectorised form of
+    _entry_cost)."""
+    z = np.asarray(m, dtype=np.complex128).reshape(-1)
+    re, im = z.real, z.imag
+    nz = z != 0
+    unit = (im == 0) & (np.abs(re) == 1)
+    half = (re == 0) | (im == 0)
+    cost = np.where(~nz, 0.0, np.where(unit, 1.0, np.where(half, 2.0, 4.0)))
+    return float(cost.sum()) / m.shape[0]
 
 
 def _embed_1q(u: np.ndarray, pos: int) -> np.ndarray:
