@@ -181,6 +181,44 @@ def _embed_1q(u: np.ndarray, pos: int) -> np.ndarray:
     return np.kron(u, np.eye(2)) if pos == 0 else np.kron(np.eye(2), u)
 
 
+def sandwich_diagonals(gates: list) -> list:
+    """Fold the single-qubit gates adjacent to an uncontrolled two-qubit diagonal gate (before
+    and after it, on both of its bits) into one dense 4x4 when that is cheaper: the unfused
+    variational layer RY RY . CZ . RY RY (4 x 4 FMAs per amplitude) becomes the fused
+    VariationalLayer form (8).  Diagonals with a cheaper sandwich stay diagonal (the QFT's
+    CZPow after an H: pivots make the diagonal nearly free)."""
+    out = list(gates)
+    alive = [True] * len(out)
+
+    def neighbour(i, bit, step):
+        k = i + step
+        while 0 <= k < len(out):
+            if alive[k] and out[k].smask & bit:
+                return k
+            k += step
+        return None
+
+    for i, d in enumerate(out):
+        if not alive[i] or d.kind != "diag" or d.controls or len(d.targets) != 2:
+            continue
+        parts, pre, post = [], [np.eye(2), np.eye(2)], [np.eye(2), np.eye(2)]
+        for pos, t in enumerate(d.targets):
+            bit = 1 << t
+            for step, slot in ((-1, pre), (1, post)):
+                k = neighbour(i, bit, step)
+                if k is not None and out[k].kind == "g1" and not out[k].controls and out[k].targets == (t,):
+                    parts.append(k)
+                    slot[pos] = out[k].matrix
+        if not parts:
+            continue
+        merged = np.kron(post[0], post[1]) @ np.diag(d.matrix) @ np.kron(pre[0], pre[1])
+        if matrix_cost(merged) < sum(matrix_cost(out[k].matrix) for k in parts) - 1e-9:
+            out[i] = NGate("g2", d.targets, (), merged, _bits(d.targets), d.smask, d.index)
+            for k in parts:
+                alive[k] = False
+    return [g for g, a in zip(out, alive) if a]
+
+
 def merge_single_qubit(gates: list) -> list:
     """Fold uncontrolled single-qubit gates into the neighbouring two-qubit gate on the same bit
     when the product is cheaper to apply than the two separately (entry-structure cost model:
@@ -375,7 +413,7 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
     if not fuse or n_qubits < geo.K + 1:
         plan.steps = [GateStep(g) for g in gates]
         return plan
-    gates = merge_single_qubit(gates)
+    gates = merge_single_qubit(sandwich_diagonals(gates))
     remaining = gates
     while remaining:
         absorbed, deferred, T = _select_pass_best(remaining, n_qubits, geo, allow_ext_perm)

@@ -25,7 +25,9 @@ def check(gates, n, psi=None, dtype=C128, tol=1e-12, allow_ext=True, min_fused=0
     got = emulate_plan(plan, psi, npd)
     want = ov.run(gates, n, psi)
     assert max_abs(got, want) <= tol, (plan.n_passes, len(plan.steps))
-    assert sum(s.n_gates for s in plan.steps if isinstance(s, PassStep)) >= min_fused
+    # gates not left to stand-alone kernels (folded single-qubit gates count as fused)
+    stand_alone = sum(1 for s in plan.steps if not isinstance(s, PassStep))
+    assert len(gates) - stand_alone >= min_fused
     return plan
 
 
@@ -143,3 +145,30 @@ def test_single_qubit_folding_trotter_and_grid(dtype, tol):
     ng = [g for g in (normalize(s, n, i) for i, s in enumerate(spec_tuples_to_specs(trot))) if g is not None]
     # the X rotation on each ZZ+hX term's first qubit folds into it: 56 -> 40 gates at n = 16
     assert len(merge_single_qubit(ng)) < len(ng)
+
+
+@pytest.mark.parametrize("dtype,tol", [(C128, 1e-12), (C64, 1e-5)])
+def test_unfused_variational_sandwiches_become_dense(dtype, tol):
+    """RY RY . CZ . RY RY around each even CZ folds into one dense 4x4 (the VariationalLayer
+    form); the QFT's diagonals stay diagonal."""
+    from paper_2009_01845_b200 import gate_matrix, qft_circuit, variational_circuit
+    from paper_2009_01845_b200.fusion import GEOMETRY_JIT, normalize, sandwich_diagonals
+
+    n = 14
+    rng = np.random.default_rng(4)
+    params = rng.uniform(0, 6, n * 7)
+    c = variational_circuit(n, 3, params, fused=False)
+    ng = [g for g in (normalize(s, n, i) for i, s in enumerate(c.queue)) if g is not None]
+    folded = sandwich_diagonals(ng)
+    assert sum(g.kind == "g2" for g in folded) == 3 * n // 2
+    q = qft_circuit(n)
+    nq = [g for g in (normalize(s, n, i) for i, s in enumerate(q.queue)) if g is not None]
+    assert sum(g.kind == "g2" for g in sandwich_diagonals(nq)) == 0
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    ref = psi.copy()
+    for g in c.queue:
+        ov.apply_matrix(ref, n, tuple(g.targets), gate_matrix(g), tuple(g.controls))
+    plan = plan_circuit(c.queue, n, dtype, geometry=GEOMETRY_JIT[dtype])
+    npd = np.complex128 if dtype == C128 else np.complex64
+    assert max_abs(emulate_plan(plan, psi, npd), ref) <= tol
