@@ -181,6 +181,27 @@ def _embed_1q(u: np.ndarray, pos: int) -> np.ndarray:
     return np.kron(u, np.eye(2)) if pos == 0 else np.kron(np.eye(2), u)
 
 
+def merge_1q_runs(gates: list) -> list:
+    """Consecutive uncontrolled single-qubit gates on the same qubit (no other gate on it in
+    between) become their product when that is cheaper (two dense 2x2 -> one)."""
+    out = list(gates)
+    alive = [True] * len(out)
+    for i, g in enumerate(out):
+        if not alive[i] or g.kind != "g1" or g.controls:
+            continue
+        bit = 1 << g.targets[0]
+        j = next((k for k in range(i + 1, len(out)) if alive[k] and out[k].smask & bit), None)
+        if j is None:
+            continue
+        h = out[j]
+        if h.kind == "g1" and not h.controls and h.targets == g.targets:
+            m = h.matrix @ g.matrix
+            if matrix_cost(m) < matrix_cost(h.matrix) + matrix_cost(g.matrix) - 1e-9:
+                out[j] = NGate("g1", h.targets, (), m, h.tmask, h.smask, h.index)
+                alive[i] = False
+    return [g for g, a in zip(out, alive) if a]
+
+
 def sandwich_diagonals(gates: list) -> list:
     """Fold the single-qubit gates adjacent to an uncontrolled two-qubit diagonal gate (before
     and after it, on both of its bits) into one dense 4x4 when that is cheaper: the unfused
@@ -199,7 +220,7 @@ def sandwich_diagonals(gates: list) -> list:
         return None
 
     for i, d in enumerate(out):
-        if not alive[i] or d.kind != "diag" or d.controls or len(d.targets) != 2:
+        if not alive[i] or d.kind not in ("diag", "g2") or d.controls or len(d.targets) != 2:
             continue
         parts, pre, post = [], [np.eye(2), np.eye(2)], [np.eye(2), np.eye(2)]
         for pos, t in enumerate(d.targets):
@@ -211,8 +232,10 @@ def sandwich_diagonals(gates: list) -> list:
                     slot[pos] = out[k].matrix
         if not parts:
             continue
-        merged = np.kron(post[0], post[1]) @ np.diag(d.matrix) @ np.kron(pre[0], pre[1])
-        if matrix_cost(merged) < sum(matrix_cost(out[k].matrix) for k in parts) - 1e-9:
+        core = np.diag(d.matrix) if d.kind == "diag" else d.matrix
+        core_cost = 0.0 if d.kind == "diag" else matrix_cost(d.matrix)
+        merged = np.kron(post[0], post[1]) @ core @ np.kron(pre[0], pre[1])
+        if matrix_cost(merged) < core_cost + sum(matrix_cost(out[k].matrix) for k in parts) - 1e-9:
             out[i] = NGate("g2", d.targets, (), merged, _bits(d.targets), d.smask, d.index)
             for k in parts:
                 alive[k] = False
@@ -413,7 +436,7 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
     if not fuse or n_qubits < geo.K + 1:
         plan.steps = [GateStep(g) for g in gates]
         return plan
-    gates = merge_single_qubit(sandwich_diagonals(gates))
+    gates = merge_single_qubit(sandwich_diagonals(merge_1q_runs(gates)))
     remaining = gates
     while remaining:
         absorbed, deferred, T = _select_pass_best(remaining, n_qubits, geo, allow_ext_perm)
