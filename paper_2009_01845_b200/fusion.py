@@ -71,6 +71,12 @@ GEOMETRY_JIT_WIDE = {nat.QSB_C128: TileGeometry(13, 3, 4, 5, True), nat.QSB_C64:
 GEOMETRY_JIT_WIDE512 = {nat.QSB_C128: TileGeometry(13, 3, 4, 4, True), nat.QSB_C64: TileGeometry(14, 4, 5, 5, True)}
 # 32 KB tiles, 128 consumers, two CTAs per SM
 GEOMETRY_JIT_K11 = {nat.QSB_C128: TileGeometry(11, 3, 4, 4), nat.QSB_C64: TileGeometry(12, 4, 5, 5)}
+# c128 passes with dense two-qubit gates: same 64 KB tile, 128 consumers x 32 amplitudes and two
+# CTAs per SM (one stage each, reused as the transpose buffer), so one CTA's FP64 work overlaps
+# the other's loads and layout changes.  Measured (n = 30): variational 101 -> 94 ms, Trotter
+# step 62 -> 58 ms, grid 366 -> 355 ms; QFT passes (no dense 2-qubit gates) keep the default,
+# where this geometry was slower (22.6 -> 25.1 ms).
+GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 5)}
 _GEO_ENV = os.environ.get("QSB_JIT_GEOMETRY", "")
 if _GEO_ENV == "wide":
     GEOMETRY_JIT = GEOMETRY_JIT_WIDE
@@ -450,7 +456,10 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
             # cheaper as sparse single-gate kernels than as a full sweep
             plan.steps.extend(GateStep(g) for g in absorbed)
         else:
-            words, info = compile_pass(absorbed, T, n_qubits, dtype, geo, minimal=MINIMAL_LAYOUT_CHANGES)
+            pgeo = geo
+            if geo == GEOMETRY_JIT[dtype] and dtype in GEOMETRY_JIT_2Q and any(g.kind == "g2" for g in absorbed):
+                pgeo = GEOMETRY_JIT_2Q[dtype]
+            words, info = compile_pass(absorbed, T, n_qubits, dtype, pgeo, minimal=MINIMAL_LAYOUT_CHANGES)
             plan.steps.append(PassStep(words, absorbed, tuple(sorted(T)), info["ext_perm"],
                                        info["transposes"], info["pivots"]))
         remaining = deferred
