@@ -84,6 +84,10 @@ elif _GEO_ENV == "wide512":
     GEOMETRY_JIT = GEOMETRY_JIT_WIDE512
 elif _GEO_ENV == "k11":
     GEOMETRY_JIT = GEOMETRY_JIT_K11
+elif _GEO_ENV == "q512":
+    # 512 consumers x 8 (c128) / 16 (c64) amplitudes: more warps per scheduler, but twice the
+    # layout changes -- measured QFT-30 c128 22.7 -> 28.1 ms, so not the default
+    GEOMETRY_JIT = {nat.QSB_C128: TileGeometry(12, 3, 4, 3), nat.QSB_C64: TileGeometry(13, 4, 5, 4)}
 elif _GEO_ENV == "k12x2":
     # c128: 64 KB tiles, 128 consumers x 32 amplitudes, two CTAs per SM (one stage each, reused
     # as the transpose buffer) so one CTA's FP64 work overlaps the other's loads / transposes
