@@ -22,12 +22,14 @@ from .errors import ArityError, CapacityError, FormError, ParseError, ShapeError
 from .evolution import (
     Callback,
     EnergyCallback,
+    EntanglementEntropyCallback,
     EvolutionConfig,
     OverlapCallback,
     Schedule,
     ScheduleForm,
     Solver,
     adiabatic_evolve,
+    entanglement_entropy,
     evolve,
     trotter_step_circuit,
 )

@@ -451,3 +451,24 @@ def test_cli_qft_verify_and_evolve(cuda, capsys):
     assert cli.main(["evolve", "--nqubits", "8", "--dt", "0.1", "--T", "0.5"]) == 0
     rec = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
     assert rec["solver"] == "trotter" and np.isfinite(rec["final_energy"])
+
+
+@pytest.mark.parametrize("partition", [(0,), (3, 1), (0, 2, 4, 6), (1, 2, 3, 5, 7, 8, 9)])
+def test_entanglement_entropy_matches_svd(cuda, partition):
+    """Device entropy (GEMM + eigvalsh on the smaller side) against the reference's numpy SVD."""
+    import paper_2009_01845_b200 as q
+
+    n = 10
+    rng = np.random.default_rng(len(partition))
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    t = np.moveaxis(psi.reshape([2] * n), partition, range(len(partition)))
+    sv = np.linalg.svd(t.reshape(1 << len(partition), -1), compute_uv=False)
+    p = sv ** 2
+    p = p[p > 1e-15]
+    want = float(-(p * np.log2(p)).sum())
+    assert abs(q.entanglement_entropy(_sv(psi), partition) - want) <= 1e-10
+    # a product state has zero entropy; a Bell pair across the cut has one bit
+    bell = q.Circuit(n).add([q.H(0), q.CNOT(0, 5)]).execute()
+    assert abs(q.entanglement_entropy(bell, (0,)) - 1.0) <= 1e-12
+    assert abs(q.entanglement_entropy(q.zero_state(n), (0, 1))) <= 1e-12
