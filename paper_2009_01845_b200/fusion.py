@@ -473,6 +473,39 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
 # ------------------------------------------------------------------------------------------
 # compile one pass
 # ------------------------------------------------------------------------------------------
+def plan_expectation(terms, n_qubits: int, dtype: int, geometry: TileGeometry):
+    """Read-only passes evaluating sum_t <psi|M_t|psi> for 1-/2-qubit terms [(bits, matrix)]
+    (bits[0] = matrix MSB): terms are independent (nothing is written), so each pass takes every
+    remaining term whose bits fit its tile; programs are flagged as expectation passes (the JIT
+    kernel accumulates instead of storing).  Returns a list of program word arrays."""
+    geo = geometry
+    gates = []
+    for i, (bits, m) in enumerate(terms):
+        bits = tuple(int(b) for b in bits)
+        kind = "g1" if len(bits) == 1 else "g2"
+        gates.append(NGate(kind, bits, (), np.asarray(m, dtype=np.complex128), _bits(bits), _bits(bits), i))
+    out = []
+    remaining = gates
+    while remaining:
+        T = set(range(geo.L))
+        absorbed, deferred = [], []
+        for g in remaining:
+            new = set(g.targets) - T
+            if len(T) + len(new) <= geo.K:
+                T |= new
+                absorbed.append(g)
+            else:
+                deferred.append(g)
+        for p in range(n_qubits):
+            if len(T) >= geo.K:
+                break
+            T.add(p)
+        words, _ = compile_pass(absorbed, T, n_qubits, dtype, geo, expect=True)
+        out.append(words)
+        remaining = deferred
+    return out
+
+
 class _Layout:
     def __init__(self, R, Tb):
         self.R = list(R)  # slot bit i <-> tile bit R[i]
@@ -517,7 +550,8 @@ def _order_thread_bits(cands, geo, prefer, natural=False):
 MINIMAL_LAYOUT_CHANGES = os.environ.get("QSB_MINIMAL_LAYOUT", "0") == "1"
 
 
-def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal: bool = False):
+def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal: bool = False,
+                 expect: bool = False):
     """Encode one pass.  `minimal`: layout changes swap only the needed bits (see
     MINIMAL_LAYOUT_CHANGES); otherwise every change re-lays the thread bits for a conflict-free
     swizzle and the coalesced store."""
@@ -681,7 +715,7 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
         gi += 1
     flush_diag()
     # store layout: lanes must cover the tile bits that land on the low output bits
-    if not store_bits <= set(cur.Tb[:5]):
+    if not expect and not store_bits <= set(cur.Tb[:5]):
         Rs = [b for b in cur.R if b not in store_bits]
         for b in sorted(range(K), key=lambda b: -b):
             if len(Rs) >= NREG:
@@ -708,7 +742,7 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
     header[4] = n
     header[5] = dtype
     header[6] = 1 << (n - K)
-    header[7] = 1 if ext_perm else 0
+    header[7] = (1 if ext_perm else 0) | (2 if expect else 0)
     contig = 0
     while contig < K and tile_pos[contig] == contig:
         contig += 1

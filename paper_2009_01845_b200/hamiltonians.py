@@ -122,6 +122,42 @@ def combine(a, coeff_a: float, b, coeff_b: float):
     return TrotterHamiltonian(a.n_qubits, [(q, acc[q]) for q in order])
 
 
+_EXPECT_CACHE: dict = {}
+
+
+def _expectation_passes(terms, state):
+    """The terms as read-only fused passes (jit expectation kernels: every term whose bits fit a
+    tile is evaluated from the registers of that tile, one HBM read per pass instead of one per
+    term).  None when the specialised kernels are unavailable or the state is too small."""
+    from . import engine, jit
+    from .fusion import plan_expectation
+
+    n = state.n_qubits
+    dtype = state.precision.qsb_dtype
+    geo = engine.default_geometry(dtype)
+    if not jit.available() or n < geo.K + 1 or geo.halves or dtype != nat.QSB_C128:
+        return None  # complex64 states keep the per-term kernel (double math on 32 amplitudes spills)
+    key = (n, dtype, geo, tuple((tuple(q), np.asarray(m).tobytes()) for q, m in terms))
+    progs = _EXPECT_CACHE.get(key)
+    if progs is None:
+        bits = [(tuple(n - 1 - q for q in qs), m) for qs, m in terms]
+        progs = []
+        for words in plan_expectation(bits, n, dtype, geo):
+            progs.append((words, jit.compile_words(words, dtype)))
+        if len(_EXPECT_CACHE) > 16:
+            _EXPECT_CACHE.clear()
+        _EXPECT_CACHE[key] = progs
+    torch = nat.torch_mod()
+    total = None
+    for words, (compiled, coeffs) in progs:
+        part = torch.zeros(compiled.n_tiles if compiled.n_tiles < 4096 else 4096, dtype=torch.float64,
+                           device=state.tensor.device)
+        jit.run(words, dtype, state.data_ptr, part.data_ptr(), n, nat.stream_ptr(), compiled, coeffs)
+        ssum = part.sum()
+        total = ssum if total is None else total + ssum
+    return float(total.item()) if total is not None else 0.0
+
+
 def _fold_single_terms(terms):
     """Sum each 1-qubit term into a 2-qubit term on the same qubit (M2 + M1 (x) I, exact
     algebra): one read sweep per remaining term instead of one per term (TFIM + X: 2N -> N)."""
@@ -153,6 +189,9 @@ def expectation(h, state: StateVector) -> float:
     torch = nat.torch_mod()
     n = h.n_qubits
     terms = _fold_single_terms(h.terms)
+    fused = _expectation_passes(terms, state)
+    if fused is not None:
+        return fused
     ks = np.array([len(q) for q, _ in terms], dtype=np.int32)
     bits = np.zeros(2 * max(1, len(terms)), dtype=np.int32)
     mats = np.zeros(32 * max(1, len(terms)), dtype=np.float64)

@@ -79,7 +79,7 @@ __device__ __forceinline__ double2 dm(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
 __device__ __forceinline__ double2 cfz(const double* cf, int k) { return make_double2(cf[k], cf[k + 1]); }
 __device__ __forceinline__ C toC(double2 z) { C r; r.x = (R)z.x; r.y = (R)z.y; return r; }
-struct CP { R v[NCOEF]; };
+struct CP { PR v[NCOEF]; };
 __device__ __forceinline__ C mkC(R a, R b) { C r; r.x = a; r.y = b; return r; }
 #if QSB_F32X2
 // packed FP32 pairs (sm_100 FFMA2/FADD2): one instruction per complex64 component pair
@@ -208,6 +208,7 @@ class _Gen:
         self.ext_pos = w[H_TILEPOS + K:H_TILEPOS + n]
         self.ext_out = w[H_TILEPOS + n:H_TILEPOS + 2 * n - K]
         self.ext_perm = bool(w[7] & 1)
+        self.expect = bool(w[7] & 2)  # read-only expectation pass: accumulate, never store
         self.ops0 = H_TILEPOS + 2 * n - K
         self.coeffs: list = []
         self.tables: list = []
@@ -394,6 +395,8 @@ class _Gen:
             else:
                 gen = {OP_G1: self.gen_g1, OP_G2: self.gen_g2, OP_PIVOT: self.gen_pivot, OP_TERM: self.gen_term,
                        OP_SCALE: self.gen_scale}[op]
+                if self.expect and op in (OP_G1, OP_G2):
+                    gen = lambda a_, op_=op: self.gen_expect(a_, op_)  # noqa: E731
                 # this op's coefficient reads are indexed by zo<k>; zo<k+1> is loaded now so the
                 # next op's coefficients can be fetched while this op computes
                 k = self.n_cops
@@ -406,6 +409,8 @@ class _Gen:
                 self.n_cops += 1
             q += ln
         body = "\n".join(self.lines[body_start:])
+        if self.expect:
+            return self._kernel(name, body, "")
         # output offsets of the final layout
         lay = self.lay
         store = [f"    const u64 ot = obase | {self.thread_expr(lay['opos'], 64)};"]
@@ -418,6 +423,51 @@ class _Gen:
         for s in range(A):
             store.append(f"    dst[ot | {lay['ooff'][s]}ull] = v{self.vm[s]};")
         return self._kernel(name, body, "\n".join(store))
+
+    def gen_expect(self, a, op):
+        """Accumulate Re <x| M |x> over this op's pairs / quads (expectation pass).  Per group:
+        sum_r Re(M_rr) |x_r|^2 + sum_{r<c} (Re M_rc + Re M_cr) Re z + (Im M_cr - Im M_rc) Im z
+        with z = conj(x_r) x_c -- exact for any M, zero pairs skipped, in double precision."""
+        w, A = self.w, self.A
+        if op == OP_G1:
+            slots_bits = [w[a]]
+            m = [_w2d(x) for x in w[a + 6:a + 14]]
+            d = 2
+        else:
+            slots_bits = [w[a], w[a + 1]]  # ih, il
+            m = [_w2d(x) for x in w[a + 7:a + 39]]
+            d = 4
+        M = [[complex(m[2 * (r * d + c)], m[2 * (r * d + c) + 1]) for c in range(d)] for r in range(d)]
+        diag = [(r, M[r][r].real) for r in range(d) if M[r][r].real != 0.0]
+        offs = []
+        for r in range(d):
+            for c in range(r + 1, d):
+                ar = M[r][c].real + M[c][r].real
+                bi = M[c][r].imag - M[r][c].imag
+                if ar != 0.0 or bi != 0.0:
+                    offs.append((r, c, ar, bi))
+        dci = self.cf([v for _, v in diag]) if diag else 0
+        oci = self.cf([x for _, _, ar, bi in offs for x in (ar, bi)]) if offs else 0
+        mask = sum(1 << b for b in slots_bits)
+        self.emit(f"    {{ // expectation term on slot bits {slots_bits}")
+        for s in range(A):
+            if s & mask:
+                continue
+            if d == 2:
+                idx = [s, s | (1 << slots_bits[0])]
+            else:
+                ih, il = slots_bits
+                idx = [s, s | (1 << il), s | (1 << ih), s | (1 << ih) | (1 << il)]
+            xs = [f"v{self.vm[i]}" for i in idx]
+            self.emit("      { " + " ".join(f"const double r{c} = (double){xs[c]}.x, i{c} = (double){xs[c]}.y;"
+                                          for c in range(d)))
+            for k, (r, _) in enumerate(diag):
+                self.emit(f"        ea = fma(PV({dci + k}), fma(r{r}, r{r}, i{r} * i{r}), ea);")
+            for k, (r, c, _, _) in enumerate(offs):
+                self.emit(f"        {{ const double zr = fma(r{r}, r{c}, i{r} * i{c}), zi = fma(r{r}, i{c}, -(i{r} * r{c}));"
+                          f" ea = fma(PV({oci + 2 * k}), zr, ea); ea = fma(PV({oci + 2 * k + 1}), zi, ea); }}")
+            self.emit("      }")
+        self.emit("    }")
 
     def gen_scale(self, a):
         w = self.w
@@ -757,7 +807,8 @@ class _Gen:
                    f"          const int co[5] = {{{', '.join(coords)}}};\n"
                    f"          tma5(d + (u64)k * {call_bytes}u, &tmap, co, &sm.full[s]);\n"
                    f"        }}")
-        defs = (f"#define QSB_F32X2 {1 if self.dtype == nat.QSB_C64 else 0}\n#define R {real}\n#define C {real}2\n#define KB {K}\n#define HBB {self.HB}\n#define GB {self.G}\n#define STAGES {self.stages}\n#define ALIAS {1 if self.alias else 0}\n#define TBUF {"sm.stage[s]" if self.alias else "sm.tbuf"}\n"
+        pr = "double" if (self.dtype == nat.QSB_C128 or self.expect) else "float"
+        defs = (f"#define QSB_F32X2 {1 if self.dtype == nat.QSB_C64 else 0}\n#define R {real}\n#define PR {pr}\n#define C {real}2\n#define KB {K}\n#define HBB {self.HB}\n#define GB {self.G}\n#define STAGES {self.stages}\n#define ALIAS {1 if self.alias else 0}\n#define TBUF {"sm.stage[s]" if self.alias else "sm.tbuf"}\n"
                 f"#define CONSUMERS {self.consumers}\n#define MAXPIV {MAX_PIV}\n#define NPIV {self.npiv}\n"
                 f"#define NCOEF {max(1, len(self.coeffs))}\n#define NTAB {len(self.tables)}\n")
         issue = f"""      {{ // producer warp: fetch tile c into stage s (tile number tno)
@@ -843,6 +894,7 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
   }}
   asm volatile("setmaxnreg.inc.sync.aligned.u32 {REG_SPLIT[self.consumers][0]};" ::: "memory");
   int it = 0;
+  double ea = 0.0;  // expectation passes: this thread's sum of Re <x|M|x>
   for (u64 c = blockIdx.x; c < n_tiles; c += gridDim.x, ++it) {{
     const int s = it % STAGES;
     const u32 ph = (it / STAGES) & 1;
@@ -850,8 +902,22 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
 {body}
 {store}
   }}
+{self._expect_epilogue() if self.expect else "  (void)ea;"}
 }}
 """
+
+    def _expect_epilogue(self):
+        """Deterministic CTA reduction of the per-thread sums -> dst[blockIdx.x] (double)."""
+        return f"""  for (int o = 16; o > 0; o >>= 1) ea += __shfl_xor_sync(0xffffffffu, ea, o);
+  csync();
+  double* red = reinterpret_cast<double*>(&sm.ep[0][0]);
+  if ((tid & 31) == 0) red[tid >> 5] = ea;
+  csync();
+  if (tid == 0) {{
+    double t = 0.0;
+    for (int w = 0; w < CONSUMERS / 32; ++w) t += red[w];
+    reinterpret_cast<double*>(dst)[blockIdx.x] = t;
+  }}"""
 
 
 class _Compiled:
@@ -926,7 +992,8 @@ def compile_words(words, dtype):
     src, name, params, tables, tplan = generate_full(words, dtype)
     if len(tables) > MAX_COEFFS:
         raise RuntimeError(f"{len(tables)} table entries exceed the shared-memory budget")
-    pbytes = params.astype(np.float64 if dtype == nat.QSB_C128 else np.float32)
+    expect = bool(int(words[7]) & 2)
+    pbytes = params.astype(np.float64 if (dtype == nat.QSB_C128 or expect) else np.float32)
     if pbytes.nbytes > MAX_PARAM_BYTES:
         raise RuntimeError(f"{pbytes.nbytes} bytes of gate coefficients exceed the kernel parameter space")
     if len(pbytes) == 0:

@@ -472,3 +472,30 @@ def test_entanglement_entropy_matches_svd(cuda, partition):
     bell = q.Circuit(n).add([q.H(0), q.CNOT(0, 5)]).execute()
     assert abs(q.entanglement_entropy(bell, (0,)) - 1.0) <= 1e-12
     assert abs(q.entanglement_entropy(q.zero_state(n), (0, 1))) <= 1e-12
+
+
+@pytest.mark.parametrize("n", [14, 20])
+def test_expectation_fused_passes_match_per_term(cuda, n):
+    """Fused read-only expectation passes (JIT) = the per-term kernel = numpy, for TFIM + X and
+    random dense terms on far-apart qubits."""
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200 import hamiltonians as hm
+
+    rng = np.random.default_rng(n)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    st = _sv(psi)
+    terms = list(q.combine(q.build_x(n), 0.4, q.build_tfim(n, 1.0), 0.6).terms)
+    for i in range(6):
+        a = rng.standard_normal((4, 4)) + 1j * rng.standard_normal((4, 4))
+        terms.append(((i, n - 1 - i), a + a.conj().T))
+    h = q.TrotterHamiltonian(n, terms)
+    want = 0.0
+    for qs, m in h.terms:
+        t = psi.copy()
+        ov.apply_matrix(t, n, qs, m)
+        want += np.vdot(psi, t).real
+    fused = hm._expectation_passes(hm._fold_single_terms(h.terms), st)
+    assert fused is not None
+    assert abs(fused - want) <= 1e-10 * max(1.0, abs(want))
+    assert abs(q.expectation(h, st) - want) <= 1e-10 * max(1.0, abs(want))
