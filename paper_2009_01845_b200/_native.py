@@ -41,6 +41,11 @@ SIGNATURES = {
         _c_int,
         [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_int, _c_void_p, _c_void_p, _c_int, _c_void_p],
     ),
+    "qsb_apply_batch": (
+        _c_int,
+        [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+         _c_void_p],
+    ),
     "qsb_scale": (_c_int, [_c_void_p, _c_u64, _c_int, _c_double, _c_double, _c_void_p]),
     "qsb_collapse": (_c_int, [_c_void_p, _c_u64, _c_int, _c_u64, _c_u64, _c_double, _c_void_p]),
     "qsb_expect_terms": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_void_p, _c_void_p, _c_void_p,

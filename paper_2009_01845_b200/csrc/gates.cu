@@ -232,10 +232,15 @@ static void to_dtype(const double* re_im, cplx<R>* out) {
 static bool is_one(const double* z) { return z[0] == 1.0 && z[1] == 0.0; }
 static bool is_nonzero(const double* z) { return z[0] != 0.0 || z[1] != 0.0; }
 
+// Which body a prepared gate runs (0: nothing to do).
+enum GateBody { kBodyNone = 0, kBodyDiag = 1, kBodyPerm = 2, kBodyGeneral1 = 3, kBodyGeneral2 = 4 };
+
+// Host side of one apply_matrix call: group geometry + the body's rows/coefficients, the
+// classification of gates.py:431-467 (diagonal rows != 1.0, permutation argmax sources,
+// general matrix cast to the state dtype).
 template <typename R>
-static int launch_gate(void* amps, int n_qubits, int t, const int* tbits, int nc, const int* cbits,
-                       const double* mat, int kclass, cudaStream_t st) {
-  GateArgs<R> p;
+static int prepare_gate(int n_qubits, int t, const int* tbits, int nc, const int* cbits, const double* mat,
+                        int kclass, GateArgs<R>& p) {
   memset(&p, 0, sizeof p);
   const int dim = 1 << t;
   // occupied bits, ascending
@@ -260,7 +265,6 @@ static int launch_gate(void* amps, int n_qubits, int t, const int* tbits, int nc
     p.off[j] = off;
   }
   p.n_groups = 1ull << (n_qubits - nocc);
-  cplx<R>* a = static_cast<cplx<R>*>(amps);
 
   if (kclass == QSB_KERNEL_DIAGONAL) {
     int nr = 0;
@@ -272,12 +276,8 @@ static int launch_gate(void* amps, int n_qubits, int t, const int* tbits, int nc
         ++nr;
       }
     }
-    if (nr == 0) return QSB_OK;
     p.nrows = nr;
-    constexpr int IT = 4;
-    k_diag<R, IT><<<blocks_for(p.n_groups, kThreads * IT), kThreads, 0, st>>>(a, p);
-    QSB_CHECK_LAUNCH("qsb_apply_matrix(diagonal)");
-    return QSB_OK;
+    return nr == 0 ? kBodyNone : kBodyDiag;
   }
   if (kclass == QSB_KERNEL_PERMUTATION) {
     int nr = 0;
@@ -298,22 +298,39 @@ static int launch_gate(void* amps, int n_qubits, int t, const int* tbits, int nc
         ++nr;
       }
     }
-    if (nr == 0) return QSB_OK;
     p.nrows = nr;
-    constexpr int IT = 4;
-    k_perm<R, IT><<<blocks_for(p.n_groups, kThreads * IT), kThreads, 0, st>>>(a, p);
-    QSB_CHECK_LAUNCH("qsb_apply_matrix(permutation)");
-    return QSB_OK;
+    return nr == 0 ? kBodyNone : kBodyPerm;
   }
   for (int k = 0; k < dim * dim; ++k) to_dtype<R>(mat + 2 * k, &p.m[k]);
-  if (t == 1) {
-    constexpr int IT = 4;
-    k_general1<R, IT><<<blocks_for(p.n_groups, kThreads * IT), kThreads, 0, st>>>(a, p);
-  } else {
-    constexpr int IT = 2;
-    k_general2<R, IT><<<blocks_for(p.n_groups, kThreads * IT), kThreads, 0, st>>>(a, p);
+  return t == 1 ? kBodyGeneral1 : kBodyGeneral2;
+}
+
+template <typename R>
+static int launch_gate(void* amps, int n_qubits, int t, const int* tbits, int nc, const int* cbits,
+                       const double* mat, int kclass, cudaStream_t st) {
+  GateArgs<R> p;
+  const int body = prepare_gate<R>(n_qubits, t, tbits, nc, cbits, mat, kclass, p);
+  cplx<R>* a = static_cast<cplx<R>*>(amps);
+  switch (body) {
+    case kBodyDiag:
+      k_diag<R, 4><<<blocks_for(p.n_groups, kThreads * 4), kThreads, 0, st>>>(a, p);
+      QSB_CHECK_LAUNCH("qsb_apply_matrix(diagonal)");
+      break;
+    case kBodyPerm:
+      k_perm<R, 4><<<blocks_for(p.n_groups, kThreads * 4), kThreads, 0, st>>>(a, p);
+      QSB_CHECK_LAUNCH("qsb_apply_matrix(permutation)");
+      break;
+    case kBodyGeneral1:
+      k_general1<R, 4><<<blocks_for(p.n_groups, kThreads * 4), kThreads, 0, st>>>(a, p);
+      QSB_CHECK_LAUNCH("qsb_apply_matrix(general)");
+      break;
+    case kBodyGeneral2:
+      k_general2<R, 2><<<blocks_for(p.n_groups, kThreads * 2), kThreads, 0, st>>>(a, p);
+      QSB_CHECK_LAUNCH("qsb_apply_matrix(general)");
+      break;
+    default:
+      break;
   }
-  QSB_CHECK_LAUNCH("qsb_apply_matrix(general)");
   return QSB_OK;
 }
 
@@ -598,6 +615,149 @@ static int check_dtype(int dtype) {
   return QSB_OK;
 }
 
+// ------------------------------------------------------------------------------------------
+// small states: a whole gate list in one launch, state resident in shared memory
+// ------------------------------------------------------------------------------------------
+// Below the fused-pass threshold (n < K + 1) every gate would otherwise be its own launch of a
+// few microseconds on a 64 KB state; here one 512-thread CTA loads the state into shared memory
+// once, runs up to kSmallMaxGates gates back to back (the same bodies and the same operand
+// order as k_general1/k_general2/k_diag/k_perm, so results equal the per-gate kernels') and
+// writes it back.  The gate table travels as a __grid_constant__ kernel parameter: no staging
+// copy, and the launch is capturable in a CUDA graph.
+constexpr int kSmallThreads = 512;
+constexpr int kSmallMaxGates = 64;
+
+template <typename R>
+struct SmallBatch {
+  int n_amps;
+  int n_gates;
+  uint8_t body[kSmallMaxGates];
+  GateArgs<R> g[kSmallMaxGates];
+};
+
+template <typename R>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    k_small_batch(cplx<R>* __restrict__ a, const __grid_constant__ SmallBatch<R> b) {
+  using C = cplx<R>;
+  extern __shared__ __align__(16) unsigned char small_smem[];
+  C* s = reinterpret_cast<C*>(small_smem);
+  for (int i = threadIdx.x; i < b.n_amps; i += kSmallThreads) s[i] = a[i];
+  __syncthreads();
+  for (int k = 0; k < b.n_gates; ++k) {
+    const GateArgs<R>& p = b.g[k];
+    const int body = b.body[k];
+    const uint32_t ng = (uint32_t)p.n_groups;
+    for (uint32_t g = threadIdx.x; g < ng; g += kSmallThreads) {
+      const uint32_t base = (uint32_t)(insert_zero_bits(g, p.occ) | p.cmask);
+      if (body == kBodyGeneral1) {
+        const uint32_t o1 = base | (uint32_t)p.off[1];
+        const C x0 = s[base], x1 = s[o1];
+        s[base] = cmad(p.m[1], x1, cmul(p.m[0], x0));
+        s[o1] = cmad(p.m[3], x1, cmul(p.m[2], x0));
+      } else if (body == kBodyGeneral2) {
+        C x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) x[j] = s[base | (uint32_t)p.off[j]];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          C y = cmul(p.m[4 * r], x[0]);
+          y = cmad(p.m[4 * r + 1], x[1], y);
+          y = cmad(p.m[4 * r + 2], x[2], y);
+          y = cmad(p.m[4 * r + 3], x[3], y);
+          s[base | (uint32_t)p.off[r]] = y;
+        }
+      } else if (body == kBodyDiag) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r < p.nrows) {
+            const uint32_t i = base | (uint32_t)p.off[p.rows[r]];
+            s[i] = cmul(s[i], p.m[r]);
+          }
+        }
+      } else {  // permutation: gather every moved row, then scatter
+        C x[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          if (r < p.nrows) x[r] = s[base | (uint32_t)p.off[p.src[r]]];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r < p.nrows) {
+            C v = x[r];
+            if (p.use_phase & (1u << r)) v = cmul(v, p.m[r]);
+            s[base | (uint32_t)p.off[p.rows[r]]] = v;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < b.n_amps; i += kSmallThreads) a[i] = s[i];
+}
+
+static int validate_gate(int n_qubits, int n_targets, const int* target_bits, int n_controls,
+                         const int* control_bits) {
+  if (n_targets < 1 || n_targets > 2) {
+    set_error("apply_matrix supports 1 or 2 targets, got %d", n_targets);
+    return QSB_ERR_SHAPE;
+  }
+  if (n_qubits < 1 || n_qubits > 40 || n_controls < 0 || n_targets + n_controls > n_qubits) {
+    set_error("bad qubit counts (n=%d, targets=%d, controls=%d)", n_qubits, n_targets, n_controls);
+    return QSB_ERR_SHAPE;
+  }
+  uint64_t seen = 0;
+  for (int i = 0; i < n_targets + n_controls; ++i) {
+    const int b = i < n_targets ? target_bits[i] : control_bits[i - n_targets];
+    if (b < 0 || b >= n_qubits) {
+      set_error("bit %d out of range for %d qubits", b, n_qubits);
+      return QSB_ERR_SHAPE;
+    }
+    if (seen & (1ull << b)) {
+      set_error("targets and controls must be distinct");
+      return QSB_ERR_SHAPE;
+    }
+    seen |= 1ull << b;
+  }
+  return QSB_OK;
+}
+
+template <typename R>
+static int launch_batch(void* amps, int n_qubits, int n_gates, const int* n_targets, const int* target_bits,
+                        const int* n_controls, const int* control_bits, const double* matrices,
+                        const int* kernels, cudaStream_t st) {
+  static bool smem_set = false;
+  const int bytes = (int)(sizeof(cplx<R>) << n_qubits);
+  if (!smem_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_small_batch<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         QSB_BATCH_MAX_STATE_BYTES);
+    if (e != cudaSuccess) return cuda_status(e, "qsb_apply_batch(smem attribute)");
+    smem_set = true;
+  }
+  static SmallBatch<R> b;  // ~27 KB: kept off the host stack; calls are serialised by the GIL
+  b.n_amps = 1 << n_qubits;
+  b.n_gates = 0;
+  cplx<R>* a = static_cast<cplx<R>*>(amps);
+  int coff = 0;
+  for (int i = 0; i < n_gates; ++i) {
+    int kc = kernels[i];
+    if (kc == QSB_KERNEL_AUTO) kc = qsb_classify(matrices + 32 * i, n_targets[i]);
+    const int body = prepare_gate<R>(n_qubits, n_targets[i], target_bits + 2 * i, n_controls[i], control_bits + coff,
+                                     matrices + 32 * i, kc, b.g[b.n_gates]);
+    coff += n_controls[i];
+    if (body == kBodyNone) continue;
+    b.body[b.n_gates++] = (uint8_t)body;
+    if (b.n_gates == kSmallMaxGates) {
+      k_small_batch<R><<<1, kSmallThreads, bytes, st>>>(a, b);
+      QSB_CHECK_LAUNCH("qsb_apply_batch");
+      b.n_gates = 0;
+    }
+  }
+  if (b.n_gates) {
+    k_small_batch<R><<<1, kSmallThreads, bytes, st>>>(a, b);
+    QSB_CHECK_LAUNCH("qsb_apply_batch");
+  }
+  return QSB_OK;
+}
+
 extern "C" {
 
 int qsb_abi_version(void) { return QSB_ABI_VERSION; }
@@ -698,6 +858,39 @@ int qsb_apply_matrix(void* amps, int n_qubits, int dtype, int n_targets, const i
   if (dtype == QSB_C128)
     return launch_gate<double>(amps, n_qubits, n_targets, target_bits, n_controls, control_bits, matrix, kernel, st);
   return launch_gate<float>(amps, n_qubits, n_targets, target_bits, n_controls, control_bits, matrix, kernel, st);
+}
+
+int qsb_apply_batch(void* amps, int n_qubits, int dtype, int n_gates, const int* n_targets, const int* target_bits,
+                    const int* n_controls, const int* control_bits, const double* matrices, const int* kernels,
+                    void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  const size_t isz = dtype == QSB_C128 ? 16 : 8;
+  if (n_qubits < 1 || n_qubits > 20 || (isz << n_qubits) > QSB_BATCH_MAX_STATE_BYTES) {
+    set_error("apply_batch holds the state in shared memory: %d qubits exceed %d bytes", n_qubits,
+              QSB_BATCH_MAX_STATE_BYTES);
+    return QSB_ERR_CAPACITY;
+  }
+  if (n_gates < 0) {
+    set_error("negative gate count");
+    return QSB_ERR_ARG;
+  }
+  int coff = 0;
+  for (int i = 0; i < n_gates; ++i) {  // validate the whole list before any work is enqueued
+    if (int s = validate_gate(n_qubits, n_targets[i], target_bits + 2 * i, n_controls[i], control_bits + coff))
+      return s;
+    coff += n_controls[i];
+    if (kernels[i] < QSB_KERNEL_AUTO || kernels[i] > QSB_KERNEL_PERMUTATION) {
+      set_error("unknown kernel class %d", kernels[i]);
+      return QSB_ERR_ARG;
+    }
+  }
+  if (n_gates == 0) return QSB_OK;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    return launch_batch<double>(amps, n_qubits, n_gates, n_targets, target_bits, n_controls, control_bits, matrices,
+                                kernels, st);
+  return launch_batch<float>(amps, n_qubits, n_gates, n_targets, target_bits, n_controls, control_bits, matrices,
+                             kernels, st);
 }
 
 int qsb_scale(void* amps, uint64_t n, int dtype, double re, double im, void* stream) {

@@ -18,10 +18,14 @@ template <> struct CplxOf<double> { using T = double2; };
 template <> struct CplxOf<float> { using T = float2; };
 template <typename R> using cplx = typename CplxOf<R>::T;
 
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+// a * b with the FMA pattern spelled out (no contraction left to the compiler), so every
+// kernel that applies the same gate -- per-gate, batched or sharded -- rounds identically
 template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
   C r;
-  r.x = a.x * b.x - a.y * b.y;
-  r.y = a.x * b.y + a.y * b.x;
+  r.x = fma(a.x, b.x, -mul_rn(a.y, b.y));
+  r.y = fma(a.x, b.y, mul_rn(a.y, b.x));
   return r;
 }
 // acc + a * b

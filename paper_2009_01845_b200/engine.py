@@ -28,6 +28,15 @@ def _free_bytes() -> int:
     return int(free)
 
 
+# cudaMemGetInfo costs ~2 ms; scratch buffers up to this size are assumed to fit without asking
+_SCRATCH_ASSUMED = 256 << 20
+
+
+def scratch_fits(nbytes: int) -> bool:
+    """Whether an out-of-place pass may allocate a scratch state of `nbytes` (plus headroom)."""
+    return nbytes <= _SCRATCH_ASSUMED or _free_bytes() > nbytes + (512 << 20)
+
+
 def default_geometry(dtype: int):
     """Tile geometry of the kernels that will run the plan: the specialised (NVRTC) kernels'
     when they are available, else the interpreter's."""
@@ -37,7 +46,7 @@ def default_geometry(dtype: int):
 def plan_for_state(state, specs, fuse: bool | None = None) -> Plan:
     fuse = FUSION_DEFAULT if fuse is None else fuse
     bytes_needed = state.n_amps * state.precision.itemsize
-    allow_ext = _free_bytes() > bytes_needed + (512 << 20)
+    allow_ext = scratch_fits(bytes_needed)
     dtype = state.precision.qsb_dtype
     geo = default_geometry(dtype)
     return plan_circuit(specs, state.n_qubits, dtype, allow_ext_perm=allow_ext, fuse=fuse, geometry=geo)
@@ -62,6 +71,56 @@ def _apply_gate_step(ptr, n, dtype, g, stream):
                              mat.ctypes.data, kernel, stream),
         "apply_matrix",
     )
+
+
+# qsb_apply_batch keeps states up to this size in shared memory (include/qsb200.h)
+BATCH_MAX_STATE_BYTES = 131072
+
+
+def _gate_matrix_and_class(g):
+    """The (matrix, kernel class) one stand-alone NGate is launched with (_apply_gate_step)."""
+    if g.kind == "diag":
+        return np.diag(g.matrix), nat.KERNEL_DIAGONAL
+    if g.kind == "swap":
+        return _SWAP4, nat.KERNEL_PERMUTATION
+    return np.asarray(g.matrix, dtype=np.complex128), nat.KERNEL_AUTO
+
+
+_SWAP4 = np.array([[1, 0, 0, 0], [0, 0, 1, 0], [0, 1, 0, 0], [0, 0, 0, 1]], dtype=np.complex128)
+
+
+def pack_gate_batch(gates):
+    """Host arrays of one qsb_apply_batch call: target counts, 2 target bits per gate, control
+    counts, the control bits back to back, 32 doubles of matrix per gate, kernel classes."""
+    k = len(gates)
+    nt = np.zeros(k, dtype=np.int32)
+    tb = np.zeros(2 * k, dtype=np.int32)
+    nc = np.zeros(k, dtype=np.int32)
+    cb = np.zeros(max(1, sum(len(g.controls) for g in gates)), dtype=np.int32)
+    mats = np.zeros((k, 16), dtype=np.complex128)
+    kc = np.zeros(k, dtype=np.int32)
+    c = 0
+    for i, g in enumerate(gates):
+        m, kc[i] = _gate_matrix_and_class(g)
+        t = len(g.targets)
+        nt[i] = t
+        tb[2 * i:2 * i + t] = g.targets
+        nc[i] = len(g.controls)
+        cb[c:c + nc[i]] = g.controls
+        c += nc[i]
+        mats[i, :m.size] = m.reshape(-1)
+    return nt, tb, nc, cb, mats.view(np.float64).reshape(-1), kc
+
+
+def _apply_gate_batch(ptr, n, dtype, packed, stream):
+    nt, tb, nc, cb, mats, kc = packed
+    nat.check(nat.lib().qsb_apply_batch(ptr, n, dtype, len(nt), nt.ctypes.data, tb.ctypes.data, nc.ctypes.data,
+                                        cb.ctypes.data, mats.ctypes.data, kc.ctypes.data, stream),
+              "apply_batch")
+
+
+def _batchable(state) -> bool:
+    return state.n_amps * state.precision.itemsize <= BATCH_MAX_STATE_BYTES
 
 
 def _launch_pass(step, words, dtype, src, dst, n, st):
@@ -95,10 +154,26 @@ def run_plan(state, plan: Plan, scratch_holder: dict | None = None, stream=None,
     dtype = state.precision.qsb_dtype
     holder = scratch_holder if scratch_holder is not None else {}
     jit.precompile([s for s in plan.steps if isinstance(s, PassStep)], dtype)
-    for step in plan.steps:
+    batch = _batchable(state) and events is None
+    packed = plan.__dict__.setdefault("_packed_runs", {}) if batch else None
+    i = 0
+    while i < len(plan.steps):
+        step = plan.steps[i]
         if isinstance(step, GateStep):
-            _apply_gate_step(state.data_ptr, n, dtype, step.gate, st)
+            j = i + 1
+            while batch and j < len(plan.steps) and isinstance(plan.steps[j], GateStep):
+                j += 1
+            if j - i > 1:
+                # a small state: the whole run of stand-alone gates is one shared-memory launch
+                run = packed.get(i)
+                if run is None:
+                    run = packed[i] = pack_gate_batch([s.gate for s in plan.steps[i:j]])
+                _apply_gate_batch(state.data_ptr, n, dtype, run, st)
+            else:
+                _apply_gate_step(state.data_ptr, n, dtype, step.gate, st)
+            i = j
             continue
+        i += 1
         words = step.words
         if events is not None:
             ev0 = nat.torch_mod().cuda.Event(enable_timing=True)
@@ -132,7 +207,7 @@ def run_gates(state, specs, fuse: bool | None = None, scratch_holder: dict | Non
         plan = plan_for_state(state, specs, fuse)
     else:
         fuse_ = FUSION_DEFAULT if fuse is None else fuse
-        allow_ext = _free_bytes() > state.n_amps * state.precision.itemsize + (512 << 20)
+        allow_ext = scratch_fits(state.n_amps * state.precision.itemsize)
         key = (state.n_qubits, state.precision.qsb_dtype, fuse_, allow_ext, jit.available(),
                tuple(id(s) for s in specs))
         hit = plan_cache.get(key)

@@ -159,7 +159,7 @@ class CudaBackend:
         if not ngates:
             return shard
         # out-of-place passes (folded SWAPs) need one more shard-sized buffer
-        allow_ext = engine._free_bytes() > shard.numel() * shard.element_size() + (512 << 20)
+        allow_ext = engine.scratch_fits(shard.numel() * shard.element_size())
         key = (allow_ext,) + tuple((g.kind, g.targets, g.controls, g.index,
                                     None if g.matrix is None else g.matrix.tobytes()) for g in ngates)
         plan_ = cache.get(key)

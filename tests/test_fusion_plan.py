@@ -172,3 +172,24 @@ def test_unfused_variational_sandwiches_become_dense(dtype, tol):
     plan = plan_circuit(c.queue, n, dtype, geometry=GEOMETRY_JIT[dtype])
     npd = np.complex128 if dtype == C128 else np.complex64
     assert max_abs(emulate_plan(plan, psi, npd), ref) <= tol
+
+
+def test_pack_gate_batch_layout():
+    """qsb_apply_batch host arrays (include/qsb200.h): 2 target bits and 32 doubles per gate,
+    control bits back to back, the stand-alone kernel class of each gate kind."""
+    from paper_2009_01845_b200 import CNOT, CZ, RX, SWAP, gate_matrix
+    from paper_2009_01845_b200.engine import pack_gate_batch
+    from paper_2009_01845_b200.fusion import normalize
+
+    n = 6
+    specs = [RX(1, 0.3, controls=(4, 2)), CZ(0, 5), SWAP(2, 3), CNOT(0, 1)]
+    gates = [normalize(s, n, i) for i, s in enumerate(specs)]
+    nt, tb, nc, cb, mats, kc = pack_gate_batch(gates)
+    assert list(nt) == [1, 2, 2, 1]  # CNOT is a controlled X on bit 4
+    assert list(tb) == [4, 0, 5, 0, 3, 2, 4, 0]
+    assert list(nc) == [2, 0, 0, 1] and list(cb) == [1, 3, 5]
+    assert list(kc) == [nat.KERNEL_AUTO, nat.KERNEL_DIAGONAL, nat.KERNEL_PERMUTATION, nat.KERNEL_AUTO]
+    m = mats.view(np.complex128).reshape(4, 16)
+    assert np.array_equal(m[0, :4], gate_matrix(specs[0]).reshape(-1))
+    assert np.array_equal(m[1], np.diag([1, 1, 1, -1]).astype(np.complex128).reshape(-1))
+    assert mats.dtype == np.float64 and mats.size == 32 * 4
