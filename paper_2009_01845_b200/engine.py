@@ -16,7 +16,9 @@ import numpy as np
 
 from . import _native as nat
 from . import jit
+from .errors import ShapeError
 from .fusion import GEOMETRY, GEOMETRY_JIT, GateStep, PassStep, Plan, compile_pass, plan_circuit
+from .gates import gate_matrix
 
 # QSB_FUSION=0 disables pass fusion (every gate becomes its own kernel launch)
 FUSION_DEFAULT = os.environ.get("QSB_FUSION", "1") != "0"
@@ -112,6 +114,29 @@ def pack_gate_batch(gates):
     return nt, tb, nc, cb, mats.view(np.float64).reshape(-1), kc
 
 
+def pack_specs(specs, n):
+    """pack_gate_batch straight from GateSpecs (qubit q -> bit n-1-q, kernel class AUTO)."""
+    k = len(specs)
+    nt = np.zeros(k, dtype=np.int32)
+    tb = np.zeros(2 * k, dtype=np.int32)
+    nc = np.zeros(k, dtype=np.int32)
+    cbits = []
+    mats = np.zeros((k, 16), dtype=np.complex128)
+    for i, spec in enumerate(specs):
+        m = gate_matrix(spec)
+        t = len(spec.targets)
+        if t > 2 or m.shape != (1 << t, 1 << t):
+            raise ShapeError(f"gate {i} ({spec.targets}) is not a 1- or 2-target gate")
+        nt[i] = t
+        tb[2 * i:2 * i + t] = [n - 1 - int(x) for x in spec.targets]
+        nc[i] = len(spec.controls)
+        cbits.extend(n - 1 - int(x) for x in spec.controls)
+        mats[i, :m.size] = m.reshape(-1)
+    cb = np.array(cbits or [0], dtype=np.int32)
+    kc = np.full(k, nat.KERNEL_AUTO, dtype=np.int32)
+    return nt, tb, nc, cb, mats.view(np.float64).reshape(-1), kc
+
+
 def _apply_gate_batch(ptr, n, dtype, packed, stream):
     nt, tb, nc, cb, mats, kc = packed
     nat.check(nat.lib().qsb_apply_batch(ptr, n, dtype, len(nt), nt.ctypes.data, tb.ctypes.data, nc.ctypes.data,
@@ -203,6 +228,20 @@ def run_gates(state, specs, fuse: bool | None = None, scratch_holder: dict | Non
     """Plan and run `specs` on `state`.  With `plan_cache` (a Circuit's), the plan -- and the
     specialised kernels and coefficients attached to its passes -- is reused while the gate
     objects, precision, fusion switch and scratch availability are unchanged."""
+    if _batchable(state):
+        # small state: no planning -- the specs go straight to one shared-memory launch per 64
+        # gates, classified on the device side exactly like apply_matrix's AUTO path
+        key = ("batch", state.n_qubits, state.precision.qsb_dtype, tuple(id(s) for s in specs))
+        hit = plan_cache.get(key) if plan_cache is not None else None
+        if hit is None:
+            hit = (pack_specs(specs, state.n_qubits), list(specs))
+            if plan_cache is not None:
+                if len(plan_cache) >= 8:
+                    plan_cache.clear()
+                plan_cache[key] = hit
+        if len(hit[0][0]):
+            _apply_gate_batch(state.data_ptr, state.n_qubits, state.precision.qsb_dtype, hit[0], nat.stream_ptr())
+        return None
     if plan_cache is None:
         plan = plan_for_state(state, specs, fuse)
     else:
