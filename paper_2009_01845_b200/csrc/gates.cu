@@ -616,24 +616,86 @@ static int check_dtype(int dtype) {
 }
 
 // ------------------------------------------------------------------------------------------
-// small states: a whole gate list in one launch, state resident in shared memory
+// gate lists in one launch: small states in shared memory, mid-size states grid-synchronised
 // ------------------------------------------------------------------------------------------
-// Below the fused-pass threshold (n < K + 1) every gate would otherwise be its own launch of a
-// few microseconds on a 64 KB state; here one 512-thread CTA loads the state into shared memory
-// once, runs up to kSmallMaxGates gates back to back (the same bodies and the same operand
-// order as k_general1/k_general2/k_diag/k_perm, so results equal the per-gate kernels') and
-// writes it back.  The gate table travels as a __grid_constant__ kernel parameter: no staging
-// copy, and the launch is capturable in a CUDA graph.
+// Below the fused-pass threshold every gate would otherwise be its own launch of a few
+// microseconds.  Up to kBatchMaxGates gates travel as one __grid_constant__ kernel parameter
+// (no staging copy; the launch is capturable in a CUDA graph) and run back to back with the
+// bodies and operand order of k_general1/k_general2/k_diag/k_perm, so the result has the
+// per-gate kernels' bits:
+//   * k_small_batch: states <= QSB_BATCH_MAX_STATE_BYTES; one CTA holds the state in shared
+//     memory, __syncthreads between gates.
+//   * k_grid_batch: states <= QSB_GRID_BATCH_MAX_STATE_BYTES (L2-resident); a co-resident
+//     (cooperative) grid walks each gate over global memory with L2-only loads/stores (L1 is not
+//     coherent across SMs) and a grid barrier between gates.
 constexpr int kSmallThreads = 512;
-constexpr int kSmallMaxGates = 64;
+constexpr int kGridThreads = 256;
+constexpr int kBatchMaxGates = 64;
 
 template <typename R>
 struct SmallBatch {
   int n_amps;
   int n_gates;
-  uint8_t body[kSmallMaxGates];
-  GateArgs<R> g[kSmallMaxGates];
+  uint8_t body[kBatchMaxGates];
+  GateArgs<R> g[kBatchMaxGates];
 };
+
+// shared memory: plain accesses; global memory: cache-global (L2) accesses
+template <bool kGlobal, typename C>
+__device__ __forceinline__ C bload(const C* p) {
+  if constexpr (kGlobal) return __ldcg(p);
+  else return *p;
+}
+template <bool kGlobal, typename C>
+__device__ __forceinline__ void bstore(C* p, C v) {
+  if constexpr (kGlobal) __stcg(p, v);
+  else *p = v;
+}
+
+// one group of one gate (the bodies of k_general1 / k_general2 / k_diag / k_perm)
+template <bool kGlobal, typename R, typename I>
+__device__ __forceinline__ void gate_group(cplx<R>* s, const GateArgs<R>& p, int body, I base) {
+  using C = cplx<R>;
+  if (body == kBodyGeneral1) {
+    const I o1 = base | (I)p.off[1];
+    const C x0 = bload<kGlobal>(s + base), x1 = bload<kGlobal>(s + o1);
+    bstore<kGlobal>(s + base, cmad(p.m[1], x1, cmul(p.m[0], x0)));
+    bstore<kGlobal>(s + o1, cmad(p.m[3], x1, cmul(p.m[2], x0)));
+  } else if (body == kBodyGeneral2) {
+    C x[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) x[j] = bload<kGlobal>(s + (base | (I)p.off[j]));
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      C y = cmul(p.m[4 * r], x[0]);
+      y = cmad(p.m[4 * r + 1], x[1], y);
+      y = cmad(p.m[4 * r + 2], x[2], y);
+      y = cmad(p.m[4 * r + 3], x[3], y);
+      bstore<kGlobal>(s + (base | (I)p.off[r]), y);
+    }
+  } else if (body == kBodyDiag) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (r < p.nrows) {
+        C* q = s + (base | (I)p.off[p.rows[r]]);
+        bstore<kGlobal>(q, cmul(bload<kGlobal>(q), p.m[r]));
+      }
+    }
+  } else {  // permutation: gather every moved row, then scatter
+    C x[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      if (r < p.nrows) x[r] = bload<kGlobal>(s + (base | (I)p.off[p.src[r]]));
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (r < p.nrows) {
+        C v = x[r];
+        if (p.use_phase & (1u << r)) v = cmul(v, p.m[r]);
+        bstore<kGlobal>(s + (base | (I)p.off[p.rows[r]]), v);
+      }
+    }
+  }
+}
 
 template <typename R>
 __global__ void __launch_bounds__(kSmallThreads, 1)
@@ -647,51 +709,47 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     const GateArgs<R>& p = b.g[k];
     const int body = b.body[k];
     const uint32_t ng = (uint32_t)p.n_groups;
-    for (uint32_t g = threadIdx.x; g < ng; g += kSmallThreads) {
-      const uint32_t base = (uint32_t)(insert_zero_bits(g, p.occ) | p.cmask);
-      if (body == kBodyGeneral1) {
-        const uint32_t o1 = base | (uint32_t)p.off[1];
-        const C x0 = s[base], x1 = s[o1];
-        s[base] = cmad(p.m[1], x1, cmul(p.m[0], x0));
-        s[o1] = cmad(p.m[3], x1, cmul(p.m[2], x0));
-      } else if (body == kBodyGeneral2) {
-        C x[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) x[j] = s[base | (uint32_t)p.off[j]];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          C y = cmul(p.m[4 * r], x[0]);
-          y = cmad(p.m[4 * r + 1], x[1], y);
-          y = cmad(p.m[4 * r + 2], x[2], y);
-          y = cmad(p.m[4 * r + 3], x[3], y);
-          s[base | (uint32_t)p.off[r]] = y;
-        }
-      } else if (body == kBodyDiag) {
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          if (r < p.nrows) {
-            const uint32_t i = base | (uint32_t)p.off[p.rows[r]];
-            s[i] = cmul(s[i], p.m[r]);
-          }
-        }
-      } else {  // permutation: gather every moved row, then scatter
-        C x[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-          if (r < p.nrows) x[r] = s[base | (uint32_t)p.off[p.src[r]]];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          if (r < p.nrows) {
-            C v = x[r];
-            if (p.use_phase & (1u << r)) v = cmul(v, p.m[r]);
-            s[base | (uint32_t)p.off[p.rows[r]]] = v;
-          }
-        }
-      }
-    }
+    for (uint32_t g = threadIdx.x; g < ng; g += kSmallThreads)
+      gate_group<false, R, uint32_t>(s, p, body, (uint32_t)(insert_zero_bits(g, p.occ) | p.cmask));
     __syncthreads();
   }
   for (int i = threadIdx.x; i < b.n_amps; i += kSmallThreads) a[i] = s[i];
+}
+
+// Sense-by-generation grid barrier on two words {arrived, generation}; the grid is co-resident
+// (cooperative launch).  Each launch gets its own slot, so launches on different streams never
+// share one.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned n_blocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == n_blocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kGridThreads)
+    k_grid_batch(cplx<R>* a, const __grid_constant__ SmallBatch<R> b, unsigned* bar) {
+  const uint32_t tid = blockIdx.x * kGridThreads + threadIdx.x;
+  const uint32_t nth = gridDim.x * kGridThreads;
+  for (int k = 0; k < b.n_gates; ++k) {
+    const GateArgs<R>& p = b.g[k];
+    const int body = b.body[k];
+    const uint32_t ng = (uint32_t)p.n_groups;
+    for (uint32_t g = tid; g < ng; g += nth)
+      gate_group<true, R, uint64_t>(a, p, body, insert_zero_bits(g, p.occ) | p.cmask);
+    if (k + 1 < b.n_gates) grid_barrier(bar, gridDim.x);
+  }
 }
 
 static int validate_gate(int n_qubits, int n_targets, const int* target_bits, int n_controls,
@@ -720,22 +778,56 @@ static int validate_gate(int n_qubits, int n_targets, const int* target_bits, in
   return QSB_OK;
 }
 
+constexpr int kBarrierSlots = 256;
+
 template <typename R>
 static int launch_batch(void* amps, int n_qubits, int n_gates, const int* n_targets, const int* target_bits,
                         const int* n_controls, const int* control_bits, const double* matrices,
                         const int* kernels, cudaStream_t st) {
   static bool smem_set = false;
-  const int bytes = (int)(sizeof(cplx<R>) << n_qubits);
-  if (!smem_set) {
+  static int grid_blocks = 0;
+  static unsigned* barriers = nullptr;  // kBarrierSlots x {arrived, generation}
+  static unsigned next_slot = 0;
+  const size_t bytes = sizeof(cplx<R>) << n_qubits;
+  const bool in_smem = bytes <= QSB_BATCH_MAX_STATE_BYTES;
+  if (in_smem && !smem_set) {
     cudaError_t e = cudaFuncSetAttribute(k_small_batch<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          QSB_BATCH_MAX_STATE_BYTES);
     if (e != cudaSuccess) return cuda_status(e, "qsb_apply_batch(smem attribute)");
     smem_set = true;
   }
+  if (!in_smem && grid_blocks == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_batch<R>, kGridThreads, 0);
+    if (e == cudaSuccess) e = cudaMalloc(&barriers, sizeof(unsigned) * 2 * kBarrierSlots);
+    if (e == cudaSuccess) e = cudaMemset(barriers, 0, sizeof(unsigned) * 2 * kBarrierSlots);
+    if (e != cudaSuccess) return cuda_status(e, "qsb_apply_batch(grid setup)");
+    grid_blocks = sms * (per_sm < 1 ? 1 : per_sm);
+  }
   static SmallBatch<R> b;  // ~27 KB: kept off the host stack; calls are serialised by the GIL
   b.n_amps = 1 << n_qubits;
   b.n_gates = 0;
   cplx<R>* a = static_cast<cplx<R>*>(amps);
+  auto flush = [&]() -> int {
+    if (in_smem) {
+      k_small_batch<R><<<1, kSmallThreads, bytes, st>>>(a, b);
+    } else {
+      unsigned* bar = barriers + 2 * (next_slot++ % kBarrierSlots);
+      uint64_t widest = b.g[0].n_groups;  // the widest gate bounds the useful grid
+      for (int k = 1; k < b.n_gates; ++k) widest = b.g[k].n_groups > widest ? b.g[k].n_groups : widest;
+      uint64_t want = (widest + kGridThreads - 1) / kGridThreads;
+      const int blocks = (int)(want < (uint64_t)grid_blocks ? (want < 1 ? 1 : want) : grid_blocks);
+      void* args[] = {(void*)&a, (void*)&b, (void*)&bar};
+      cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_grid_batch<R>, dim3(blocks), dim3(kGridThreads),
+                                                  args, 0, st);
+      if (e != cudaSuccess) return cuda_status(e, "qsb_apply_batch(cooperative launch)");
+    }
+    QSB_CHECK_LAUNCH("qsb_apply_batch");
+    b.n_gates = 0;
+    return QSB_OK;
+  };
   int coff = 0;
   for (int i = 0; i < n_gates; ++i) {
     int kc = kernels[i];
@@ -745,16 +837,11 @@ static int launch_batch(void* amps, int n_qubits, int n_gates, const int* n_targ
     coff += n_controls[i];
     if (body == kBodyNone) continue;
     b.body[b.n_gates++] = (uint8_t)body;
-    if (b.n_gates == kSmallMaxGates) {
-      k_small_batch<R><<<1, kSmallThreads, bytes, st>>>(a, b);
-      QSB_CHECK_LAUNCH("qsb_apply_batch");
-      b.n_gates = 0;
-    }
+    if (b.n_gates == kBatchMaxGates)
+      if (int s = flush()) return s;
   }
-  if (b.n_gates) {
-    k_small_batch<R><<<1, kSmallThreads, bytes, st>>>(a, b);
-    QSB_CHECK_LAUNCH("qsb_apply_batch");
-  }
+  if (b.n_gates)
+    if (int s = flush()) return s;
   return QSB_OK;
 }
 
@@ -865,9 +952,9 @@ int qsb_apply_batch(void* amps, int n_qubits, int dtype, int n_gates, const int*
                     void* stream) {
   if (int s = check_dtype(dtype)) return s;
   const size_t isz = dtype == QSB_C128 ? 16 : 8;
-  if (n_qubits < 1 || n_qubits > 20 || (isz << n_qubits) > QSB_BATCH_MAX_STATE_BYTES) {
-    set_error("apply_batch holds the state in shared memory: %d qubits exceed %d bytes", n_qubits,
-              QSB_BATCH_MAX_STATE_BYTES);
+  if (n_qubits < 1 || n_qubits > 32 || (isz << n_qubits) > QSB_GRID_BATCH_MAX_STATE_BYTES) {
+    set_error("apply_batch keeps the state on chip: %d qubits exceed %d bytes", n_qubits,
+              QSB_GRID_BATCH_MAX_STATE_BYTES);
     return QSB_ERR_CAPACITY;
   }
   if (n_gates < 0) {

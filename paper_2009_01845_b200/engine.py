@@ -75,8 +75,10 @@ def _apply_gate_step(ptr, n, dtype, g, stream):
     )
 
 
-# qsb_apply_batch keeps states up to this size in shared memory (include/qsb200.h)
+# qsb_apply_batch keeps states up to this size in shared memory, and walks states up to the
+# second size with a grid-synchronised launch (include/qsb200.h)
 BATCH_MAX_STATE_BYTES = 131072
+GRID_BATCH_MAX_STATE_BYTES = 32 << 20
 
 
 def _gate_matrix_and_class(g):
@@ -223,40 +225,75 @@ def run_plan(state, plan: Plan, scratch_holder: dict | None = None, stream=None,
             events.append((ev0, ev1))
 
 
+def _plan_key(n_qubits, dtype, fuse_, allow_ext, specs):
+    return (n_qubits, dtype, fuse_, allow_ext, jit.available(), tuple(id(s) for s in specs))
+
+
+def prepare_plan(n_qubits, precision, specs, fuse: bool | None = None, plan_cache: dict | None = None,
+                 allow_ext: bool | None = None) -> Plan:
+    """The plan run_gates will use for `specs` (from `plan_cache` when present), with its passes'
+    specialised kernels compiled.  `allow_ext=None`: decided from the free device memory, as
+    for an already allocated state of this size."""
+    fuse_ = FUSION_DEFAULT if fuse is None else fuse
+    dtype = precision.qsb_dtype
+    if allow_ext is None:
+        allow_ext = scratch_fits((1 << n_qubits) * precision.itemsize)
+    key = _plan_key(n_qubits, dtype, fuse_, allow_ext, specs)
+    hit = plan_cache.get(key) if plan_cache is not None else None
+    if hit is not None:
+        return hit[0]
+    plan = plan_circuit(list(specs), n_qubits, dtype, allow_ext_perm=allow_ext, fuse=fuse_,
+                        geometry=default_geometry(dtype))
+    steps = [s for s in plan.steps if isinstance(s, PassStep)]
+    jit.precompile(steps, dtype)
+    for s in steps:  # precompile leaves single passes to the caller
+        if s.jit is None and not s.no_jit and jit.available():
+            try:
+                s.jit = jit.compile_words(s.words, dtype)
+            except Exception:  # run_plan retries and falls back to the interpreter with a warning
+                pass
+    if plan_cache is not None:
+        if len(plan_cache) >= 8:
+            plan_cache.clear()
+        plan_cache[key] = (plan, list(specs))  # the specs are kept alive so their ids stay unique
+    return plan
+
+
 def run_gates(state, specs, fuse: bool | None = None, scratch_holder: dict | None = None,
               plan_cache: dict | None = None):
-    """Plan and run `specs` on `state`.  With `plan_cache` (a Circuit's), the plan -- and the
-    specialised kernels and coefficients attached to its passes -- is reused while the gate
-    objects, precision, fusion switch and scratch availability are unchanged."""
-    if _batchable(state):
-        # small state: no planning -- the specs go straight to one shared-memory launch per 64
-        # gates, classified on the device side exactly like apply_matrix's AUTO path
-        key = ("batch", state.n_qubits, state.precision.qsb_dtype, tuple(id(s) for s in specs))
-        hit = plan_cache.get(key) if plan_cache is not None else None
-        if hit is None:
-            hit = (pack_specs(specs, state.n_qubits), list(specs))
-            if plan_cache is not None:
-                if len(plan_cache) >= 8:
-                    plan_cache.clear()
-                plan_cache[key] = hit
-        if len(hit[0][0]):
-            _apply_gate_batch(state.data_ptr, state.n_qubits, state.precision.qsb_dtype, hit[0], nat.stream_ptr())
-        return None
-    if plan_cache is None:
-        plan = plan_for_state(state, specs, fuse)
-    else:
-        fuse_ = FUSION_DEFAULT if fuse is None else fuse
-        allow_ext = scratch_fits(state.n_amps * state.precision.itemsize)
-        key = (state.n_qubits, state.precision.qsb_dtype, fuse_, allow_ext, jit.available(),
-               tuple(id(s) for s in specs))
-        hit = plan_cache.get(key)
-        if hit is None:
-            if len(plan_cache) >= 8:
-                plan_cache.clear()
-            plan = plan_circuit(list(specs), state.n_qubits, state.precision.qsb_dtype, allow_ext_perm=allow_ext,
-                                fuse=fuse_, geometry=default_geometry(state.precision.qsb_dtype))
-            plan_cache[key] = (plan, list(specs))  # the specs are kept alive so their ids stay unique
-        else:
-            plan = hit[0]
+    """Run `specs` on `state`.
+
+    * Small states (<= BATCH_MAX_STATE_BYTES): no planning; the specs go straight to one
+      shared-memory launch per 64 gates.
+    * Mid-size, L2-resident states (<= GRID_BATCH_MAX_STATE_BYTES, fusion on): the first run of a
+      gate list goes through the grid-synchronised batch launch (no host planning, which costs
+      more than the whole circuit at this size); when the same list comes back -- or was
+      prepared with prepare_plan -- it runs as planned fused passes.
+    * Larger states: planned fused passes.
+    With `plan_cache` (a Circuit's), packed lists and plans -- with the specialised kernels and
+    coefficients attached to their passes -- are reused while the gate objects, precision,
+    fusion switch and scratch availability are unchanged."""
+    fuse_ = FUSION_DEFAULT if fuse is None else fuse
+    n, precision = state.n_qubits, state.precision
+    nbytes = state.n_amps * precision.itemsize
+    small = nbytes <= BATCH_MAX_STATE_BYTES
+    if small or (fuse_ and nbytes <= GRID_BATCH_MAX_STATE_BYTES):
+        planned = (not small and plan_cache is not None
+                   and _plan_key(n, precision.qsb_dtype, fuse_, scratch_fits(nbytes), specs) in plan_cache)
+        if not planned:
+            bkey = ("batch", n, precision.qsb_dtype, tuple(id(s) for s in specs))
+            entry = plan_cache.get(bkey) if plan_cache is not None else None
+            if entry is None:
+                entry = [pack_specs(specs, n), list(specs), 0]
+                if plan_cache is not None:
+                    if len(plan_cache) >= 8:
+                        plan_cache.clear()
+                    plan_cache[bkey] = entry
+            if small or entry[2] == 0:
+                entry[2] += 1
+                if len(entry[0][0]):
+                    _apply_gate_batch(state.data_ptr, n, precision.qsb_dtype, entry[0], nat.stream_ptr())
+                return None
+    plan = prepare_plan(n, precision, specs, fuse_, plan_cache)
     run_plan(state, plan, scratch_holder)
     return plan

@@ -53,9 +53,14 @@ def mid_sizes():
     for n in (14, 16, 20):
         rng = np.random.default_rng(7)
         c = q.variational_circuit(n, 5, rng.uniform(0, 2 * np.pi, n * 11), fused=True)
+        t = time.perf_counter()
+        c.execute()
+        torch.cuda.synchronize()
+        first = (time.perf_counter() - t) * 1e3
         cached = wall(lambda: c.execute(), 20)
         fresh = wall(lambda: q.variational_circuit(n, 5, rng.uniform(0, 2 * np.pi, n * 11), fused=True).execute(), 5)
-        print(f"variational n={n} L=5 fused: passes {c.plan().n_passes}; execute (plan cached) {cached:.3f} ms, "
+        print(f"variational n={n} L=5 fused: passes {c.plan().n_passes}; first execute (grid batch) {first:.3f} ms, "
+              f"execute (plan cached) {cached:.3f} ms, "
               f"new parameters each call {fresh:.3f} ms")
 
 
