@@ -169,3 +169,23 @@ def test_distributed_gloo(world, tmp_path):
         res = json.load(open(tmp_path / f"r{r}.json"))
         for name, err in res.items():
             assert err <= 1e-12, (world, r, name, err)
+
+
+def test_bench_distributed_summary():
+    """bench.py's sharded-step roofline/launch accounting: sweeps from the runner's plan cache,
+    exchange time subtracted, pack+unpack per chunk per reshuffle."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_2009_01845_b200 import _native as nat
+    from paper_2009_01845_b200 import qft_circuit
+    from paper_2009_01845_b200.fusion import plan_circuit
+
+    p = plan_circuit(qft_circuit(14).queue, 14, nat.QSB_C128)
+    shard = (1 << 14) * 16
+    roof, launches = bench._dist_summary({"k": p, "other": object()}, 2, 1e-3, 1e-4, shard, 16, 1 << 16)
+    assert roof["sweeps_per_step"] == p.state_sweeps()
+    assert abs(roof["achieved"] - p.state_sweeps() * 2 * shard / 8e-4 / 1e9) < 1e-9
+    assert launches == len(p.steps) + 2 * 2 * ((shard // 32) // 4096) + 1
