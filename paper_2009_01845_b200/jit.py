@@ -421,7 +421,10 @@ class _Gen:
             for s in range(A):
                 store.append(f"    v{self.vm[s]}.x *= hs; v{self.vm[s]}.y *= hs;")
         for s in range(A):
-            store.append(f"    dst[ot | {lay['ooff'][s]}ull] = v{self.vm[s]};")
+            if _PROBE == "nostores":  # timing probe: keep the values live, store (almost) nothing
+                store.append(f"    if (v{self.vm[s]}.x == (R)1234.5) dst[ot | {lay['ooff'][s]}ull] = v{self.vm[s]};")
+            else:
+                store.append(f"    dst[ot | {lay['ooff'][s]}ull] = v{self.vm[s]};")
         return self._kernel(name, body, "\n".join(store))
 
     def gen_expect(self, a, op):
@@ -927,7 +930,7 @@ class _Compiled:
 _cache: dict = {}
 _lock = threading.Lock()
 _disabled = os.environ.get("QSB_JIT", "1") == "0"
-# QSB_JIT_PROBE=nogates|notransposes: timing experiments only (kernels compute wrong results)
+# QSB_JIT_PROBE=nogates|notransposes|nostores: timing experiments only (kernels compute wrong results)
 _PROBE = os.environ.get("QSB_JIT_PROBE", "")
 _MINIMAL = os.environ.get("QSB_MINIMAL_LAYOUT", "0") == "1"  # predicated transposes (fusion.MINIMAL_LAYOUT_CHANGES)
 _avail = None
