@@ -9,6 +9,7 @@ mirror the reference names and error behaviour.
 """
 
 from .circuit import (
+    CircuitGraph,
     Circuit,
     FusedGate,
     circuit_from_dict,

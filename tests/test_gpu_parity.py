@@ -583,3 +583,62 @@ def test_mid_size_first_run_batched_then_planned(cuda, n):
     cache2 = {}
     engine.prepare_plan(n, q.Precision.F64, c2.queue, None, cache2)
     assert engine.run_gates(q.basis_state(n, k), c2.queue, None, {}, cache2) is not None
+
+
+@pytest.mark.parametrize("n", [10, 16])
+def test_execution_is_cuda_graph_capturable(cuda, n):
+    """Gate tables and pass coefficients travel as kernel parameters (no host staging in the
+    launch path), so a planned circuit -- shared-memory batch (n = 10) or fused specialised
+    passes (n = 16) -- can be captured once in a CUDA graph and replayed on new inputs."""
+    import torch
+
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200 import engine
+
+    c = q.variational_circuit(n, 3, np.random.default_rng(n).uniform(0, 6, n * 7), fused=True)
+    cache = {}
+    if n > 13:
+        engine.prepare_plan(n, q.Precision.F64, c.queue, None, cache)
+    st = q.zero_state(n)
+    engine.run_gates(st, c.queue, None, {}, cache)  # warm: packing / module loads outside capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    stream = torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())
+    src = st.tensor  # out-of-place passes may leave the result in the captured scratch buffer
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(graph, stream=stream):
+            engine.run_gates(st, c.queue, None, {}, cache)
+    dst = st.tensor
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(3)
+    for _ in range(2):
+        psi = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)) / math.sqrt(2 << n)
+        src.copy_(torch.from_numpy(psi).to(src.device))
+        graph.replay()
+        torch.cuda.synchronize()
+        want = c.execute(_sv(psi)).amplitudes
+        assert max_abs(dst.cpu().numpy(), want) <= TOL64
+
+
+@pytest.mark.parametrize("n,prec", [(8, "f64"), (16, "f32"), (20, "f64")])
+def test_circuit_graph_replay(cuda, n, prec):
+    """Circuit.capture: execute() contract (default |0..0>, initial copied) from a graph replay."""
+    import paper_2009_01845_b200 as q
+
+    precision = q.Precision(prec)
+    c = q.variational_circuit(n, 2, np.random.default_rng(n).uniform(0, 6, n * 5), fused=False)
+    g = c.capture(precision)
+    tol = TOL64 if prec == "f64" else TOL32
+    assert max_abs(g.execute().amplitudes, c.execute(precision=precision).amplitudes) <= tol
+    rng = np.random.default_rng(5)
+    for _ in range(2):
+        psi = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)) / math.sqrt(2 << n)
+        init = q.from_amplitudes(psi, precision=precision)
+        keep = init.amplitudes
+        a = g.execute(init)
+        b = c.execute(init, precision=precision)
+        assert max_abs(a.amplitudes, b.amplitudes) <= tol
+        assert np.array_equal(init.amplitudes, keep)
+    with pytest.raises(q.ShapeError):
+        g.execute(q.zero_state(n + 1, precision))

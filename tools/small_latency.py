@@ -59,7 +59,10 @@ def mid_sizes():
         first = (time.perf_counter() - t) * 1e3
         cached = wall(lambda: c.execute(), 20)
         fresh = wall(lambda: q.variational_circuit(n, 5, rng.uniform(0, 2 * np.pi, n * 11), fused=True).execute(), 5)
-        print(f"variational n={n} L=5 fused: passes {c.plan().n_passes}; first execute (grid batch) {first:.3f} ms, "
+        g = c.capture()
+        replay = wall(lambda: g.execute(), 20)
+        print(f"variational n={n} L=5 fused: passes {c.plan().n_passes}; graph replay execute {replay:.3f} ms, "
+              f"first execute (grid batch) {first:.3f} ms, "
               f"execute (plan cached) {cached:.3f} ms, "
               f"new parameters each call {fresh:.3f} ms")
 
