@@ -550,6 +550,72 @@ def _order_thread_bits(cands, geo, prefer, natural=False):
 MINIMAL_LAYOUT_CHANGES = os.environ.get("QSB_MINIMAL_LAYOUT", "0") == "1"
 
 
+# Gates of a pass are re-ordered within their dependencies so that each register layout serves as
+# many gates as fit (QSB_REORDER=0: queue order).
+REORDER_GATES = os.environ.get("QSB_REORDER", "1") != "0"
+
+
+def _event_bits(ev) -> int:
+    m = 0
+    if ev[0] == "diag":
+        for pm, _pv, _w in ev[1]:
+            m |= pm
+        return m
+    for p in tuple(ev[2]) + tuple(ev[3]):
+        m |= 1 << p
+    return m
+
+
+def _reorder_events(events, tidx, nreg, first_forbid=frozenset()):
+    """Dependency-respecting order of a pass's events that groups the gates sharing one register
+    layout.  Two events depend on each other when their bit supports (targets, controls, diagonal
+    masks) intersect, except two diagonal events, which commute.  Each round walks the remaining
+    events in queue order: a gate joins the round when its target bits fit the round's register
+    set (at most `nreg` tile bits; the first round may not use `first_forbid`) and nothing it
+    depends on is left behind; skipped events hold back every later event on their bits
+    (skipped diagonals hold back only gates)."""
+    n_ev = len(events)
+    bits = [_event_bits(ev) for ev in events]
+    diag = [ev[0] == "diag" for ev in events]
+    need = [None if diag[i] else frozenset(tidx[p] for p in events[i][2]) for i in range(n_ev)]
+    remaining = list(range(n_ev))
+    order = []
+    first = True
+    while remaining:
+        R = set()
+        blocked_all = 0  # bits of skipped gates: later events on them wait
+        blocked_gates = 0  # bits of skipped diagonals: later gates on them wait
+        taken, left = [], []
+        for i in remaining:
+            if diag[i]:
+                if bits[i] & blocked_all:
+                    blocked_gates |= bits[i]
+                    left.append(i)
+                else:
+                    taken.append(i)
+                continue
+            ok = not (bits[i] & (blocked_all | blocked_gates))
+            if ok and first and need[i] & first_forbid:
+                ok = False
+            if ok and len(R | need[i]) > nreg:
+                ok = False
+            if ok:
+                R |= need[i]
+                taken.append(i)
+            else:
+                blocked_all |= bits[i]
+                left.append(i)
+        if not any(not diag[i] for i in taken) and first and left:
+            first = False  # nothing fits the forbidden-free first layout: drop the restriction
+            order.extend(taken)
+            remaining = left
+            continue
+        order.extend(taken)
+        remaining = left
+        first = False
+    return [events[i] for i in order]
+
+
 def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal: bool = False,
                  expect: bool = False):
     """Encode one pass.  `minimal`: layout changes swap only the needed bits (see
@@ -595,6 +661,8 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
     ext_perm = ext_out != ext_pos
     store_bits = {b for b in range(K) if out_pos[b] < geo.L}
 
+    if REORDER_GATES:
+        events = _reorder_events(events, tidx, NREG, frozenset(range(geo.G)) if not geo.halves else frozenset())
     needs = [frozenset(tidx[p] for p in ev[2]) for ev in events if ev[0] in ("g1", "g2")]
 
     def pick_R(i, forbid=frozenset(), keep=None, must=(), sticky=()):
