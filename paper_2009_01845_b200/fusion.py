@@ -553,6 +553,7 @@ MINIMAL_LAYOUT_CHANGES = os.environ.get("QSB_MINIMAL_LAYOUT", "0") == "1"
 # Gates of a pass are re-ordered within their dependencies so that each register layout serves as
 # many gates as fit (QSB_REORDER=0: queue order).
 REORDER_GATES = os.environ.get("QSB_REORDER", "1") != "0"
+SEED_GATES = int(os.environ.get("QSB_REORDER_SEEDS", "6"))
 
 
 def _event_bits(ev) -> int:
@@ -581,8 +582,9 @@ def _reorder_events(events, tidx, nreg, first_forbid=frozenset()):
     remaining = list(range(n_ev))
     order = []
     first = True
-    while remaining:
-        R = set()
+
+    def walk(seed):
+        R = set(seed)
         blocked_all = 0  # bits of skipped gates: later events on them wait
         blocked_gates = 0  # bits of skipped diagonals: later gates on them wait
         taken, left = [], []
@@ -605,14 +607,35 @@ def _reorder_events(events, tidx, nreg, first_forbid=frozenset()):
             else:
                 blocked_all |= bits[i]
                 left.append(i)
-        if not any(not diag[i] for i in taken) and first and left:
+        return taken, left
+
+    while remaining:
+        # seeds: the register bits of each of the first few gates that could run now; keep the
+        # round that runs the most gates (ties: the earlier seed)
+        best = walk(())
+        seeds, seen, blk, blk_g = [], set(), 0, 0
+        for i in remaining:
+            if len(seeds) >= SEED_GATES:
+                break
+            if diag[i]:
+                if bits[i] & blk:
+                    blk_g |= bits[i]
+                continue
+            if not bits[i] & (blk | blk_g) and need[i] not in seen and not (first and need[i] & first_forbid):
+                seeds.append(need[i])
+                seen.add(need[i])
+            blk |= bits[i]
+        for seed in seeds:
+            cand = walk(seed)
+            if sum(not diag[i] for i in cand[0]) > sum(not diag[i] for i in best[0]):
+                best = cand
+        taken, left = best
+        if first and not any(not diag[i] for i in taken) and left:
             first = False  # nothing fits the forbidden-free first layout: drop the restriction
-            order.extend(taken)
-            remaining = left
-            continue
+        else:
+            first = False
         order.extend(taken)
         remaining = left
-        first = False
     return [events[i] for i in order]
 
 
