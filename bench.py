@@ -7,7 +7,7 @@ qft_circuit(30) (480 gates) applied to a state resident in HBM.  One "step" = on
   e2e        the same through the public API: Circuit.execute() (|0..0> allocation + plan +
              program upload + passes) and a device->host read of the full result state into
              pinned memory, per step;
-  roofline   the dominant kernel (k_pass, the fused pass): algorithmic bytes per launch
+  roofline   the dominant kernel (the specialised fused pass): algorithmic bytes per launch
              (one read + one write of the 2^n-amplitude state) / its mean CUDA-event duration,
              against the measured HBM copy peak (MEASURED_PEAKS.json);
   cpu_baseline  the reference algorithm (oracle/ numpy port, all host threads) on a bounded
@@ -275,7 +275,7 @@ def run_gpu_arm(args, rank, world):
                    "l2": "inputs (state) far larger than the 126 MB L2; no flush needed"},
         "hbm": {"circuit_effective_gbs": circuit_gbs, "per_pass_ms": mean_pass_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "peak_kind": peak_kind, "kernel": "qsb::pass::k_pass",
+                     "traffic": traffic, "peak_kind": peak_kind, "kernel": "qsb_pass_<hash> (NVRTC-specialised fused pass)",
                      "bytes_per_launch": pass_bytes, "launches": len(launches)},
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "qft_circuit(n).execute() + state D2H (pinned)"},
