@@ -7,6 +7,12 @@
  * returns a qsb_status.  No torch / numpy types cross this boundary.  On a non-zero status,
  * qsb_last_error() returns a human-readable message (thread-local).
  *
+ * Concurrency: entry points may be called from several host threads (host-side caches are
+ * locked or thread-local).  The small device scratch buffers of the reductions and the pass
+ * program ring are per device and per process, so work that uses them (norm / vdot / expect /
+ * sampling / interpreted passes) must not run concurrently on two streams of one device --
+ * the reference's contract of one stream per state, serialised calls (gates.py:389-394).
+ *
  * Conventions (identical to the reference):
  *   - the state is 2**n complex numbers, interleaved (re, im), complex64 (dtype QSB_C64) or
  *     complex128 (QSB_C128);

@@ -17,6 +17,9 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
+#include <mutex>
+
 #include "qsb_common.cuh"
 
 namespace qsb {
@@ -784,29 +787,42 @@ template <typename R>
 static int launch_batch(void* amps, int n_qubits, int n_gates, const int* n_targets, const int* target_bits,
                         const int* n_controls, const int* control_bits, const double* matrices,
                         const int* kernels, cudaStream_t st) {
-  static bool smem_set = false;
-  static int grid_blocks = 0;
-  static unsigned* barriers = nullptr;  // kBarrierSlots x {arrived, generation}
-  static unsigned next_slot = 0;
+  // per-device, per-precision setup (function attribute, grid size, barrier slots), once
+  constexpr int kMaxDevices = 64;
+  static std::mutex mu;
+  static bool smem_set[kMaxDevices] = {};
+  static int grid_blocks[kMaxDevices] = {};
+  static unsigned* barriers[kMaxDevices] = {};  // kBarrierSlots x {arrived, generation}
+  static std::atomic<unsigned> next_slot{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "qsb_apply_batch(device)");
+  if (dev < 0 || dev >= kMaxDevices) {
+    set_error("apply_batch: device %d out of range", dev);
+    return QSB_ERR_ARG;
+  }
   const size_t bytes = sizeof(cplx<R>) << n_qubits;
   const bool in_smem = bytes <= QSB_BATCH_MAX_STATE_BYTES;
-  if (in_smem && !smem_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_small_batch<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         QSB_BATCH_MAX_STATE_BYTES);
-    if (e != cudaSuccess) return cuda_status(e, "qsb_apply_batch(smem attribute)");
-    smem_set = true;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (in_smem && !smem_set[dev]) {
+      e = cudaFuncSetAttribute(k_small_batch<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               QSB_BATCH_MAX_STATE_BYTES);
+      if (e != cudaSuccess) return cuda_status(e, "qsb_apply_batch(smem attribute)");
+      smem_set[dev] = true;
+    }
+    if (!in_smem && grid_blocks[dev] == 0) {
+      int sms = 0, per_sm = 0;
+      e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_batch<R>, kGridThreads, 0);
+      if (e == cudaSuccess) e = cudaMalloc(&barriers[dev], sizeof(unsigned) * 2 * kBarrierSlots);
+      if (e == cudaSuccess) e = cudaMemset(barriers[dev], 0, sizeof(unsigned) * 2 * kBarrierSlots);
+      if (e != cudaSuccess) return cuda_status(e, "qsb_apply_batch(grid setup)");
+      grid_blocks[dev] = sms * (per_sm < 1 ? 1 : per_sm);
+    }
   }
-  if (!in_smem && grid_blocks == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_batch<R>, kGridThreads, 0);
-    if (e == cudaSuccess) e = cudaMalloc(&barriers, sizeof(unsigned) * 2 * kBarrierSlots);
-    if (e == cudaSuccess) e = cudaMemset(barriers, 0, sizeof(unsigned) * 2 * kBarrierSlots);
-    if (e != cudaSuccess) return cuda_status(e, "qsb_apply_batch(grid setup)");
-    grid_blocks = sms * (per_sm < 1 ? 1 : per_sm);
-  }
-  static SmallBatch<R> b;  // ~27 KB: kept off the host stack; calls are serialised by the GIL
+  // ~27 KB gate table: off the host stack, one per calling thread (ctypes drops the GIL)
+  static thread_local SmallBatch<R> b;
   b.n_amps = 1 << n_qubits;
   b.n_gates = 0;
   cplx<R>* a = static_cast<cplx<R>*>(amps);
@@ -814,11 +830,11 @@ static int launch_batch(void* amps, int n_qubits, int n_gates, const int* n_targ
     if (in_smem) {
       k_small_batch<R><<<1, kSmallThreads, bytes, st>>>(a, b);
     } else {
-      unsigned* bar = barriers + 2 * (next_slot++ % kBarrierSlots);
+      unsigned* bar = barriers[dev] + 2 * (next_slot.fetch_add(1) % kBarrierSlots);
       uint64_t widest = b.g[0].n_groups;  // the widest gate bounds the useful grid
       for (int k = 1; k < b.n_gates; ++k) widest = b.g[k].n_groups > widest ? b.g[k].n_groups : widest;
       uint64_t want = (widest + kGridThreads - 1) / kGridThreads;
-      const int blocks = (int)(want < (uint64_t)grid_blocks ? (want < 1 ? 1 : want) : grid_blocks);
+      const int blocks = (int)(want < (uint64_t)grid_blocks[dev] ? (want < 1 ? 1 : want) : grid_blocks[dev]);
       void* args[] = {(void*)&a, (void*)&b, (void*)&bar};
       cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_grid_batch<R>, dim3(blocks), dim3(kGridThreads),
                                                   args, 0, st);

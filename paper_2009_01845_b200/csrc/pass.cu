@@ -21,6 +21,7 @@
 //   * the result is written straight from registers to HBM (coalesced: the store layout puts
 //     lane bits on the low output bits), optionally to permuted positions (SWAP gates folded
 //     into the pass as relabels, tile-external swaps as an output tile permutation).
+#include <mutex>
 #include <cuda.h>
 #include <math.h>
 #include <stdlib.h>
@@ -772,6 +773,8 @@ int stage_words(const void* host, size_t bytes, void** device_out, cudaStream_t 
   static char* ring = nullptr;
   static char* hring = nullptr;
   static size_t cursor = 0;
+  static std::mutex mu;  // ctypes drops the GIL: host threads may stage concurrently
+  std::lock_guard<std::mutex> lock(mu);
   constexpr size_t kRing = 16u << 20;
   if (bytes > kRing / 4) {
     set_error("stage_words: %zu bytes too large", bytes);

@@ -642,3 +642,34 @@ def test_circuit_graph_replay(cuda, n, prec):
         assert np.array_equal(init.amplitudes, keep)
     with pytest.raises(q.ShapeError):
         g.execute(q.zero_state(n + 1, precision))
+
+
+def test_concurrent_small_executes_from_threads(cuda):
+    """ctypes drops the GIL around library calls: batched small-state executes from several host
+    threads (thread-local gate tables, locked setup) give the single-threaded results."""
+    import threading
+
+    import paper_2009_01845_b200 as q
+
+    circuits = [q.variational_circuit(n, 3, np.random.default_rng(n + 7 * k).uniform(0, 6, n * 7), fused=k % 2 == 0)
+                for k in range(4) for n in (6, 12, 16)]
+    want = [c.execute().amplitudes for c in circuits]
+    got = [None] * len(circuits)
+    errors = []
+
+    def work(idx):
+        try:
+            for _ in range(5):
+                for i in idx:
+                    got[i] = q.Circuit(circuits[i].n_qubits).add(list(circuits[i].queue)).execute().amplitudes
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    threads = [threading.Thread(target=work, args=(list(range(t, len(circuits), 3)),)) for t in range(3)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
