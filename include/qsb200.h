@@ -79,15 +79,15 @@ int qsb_apply_matrix(void* amps, int n_qubits, int dtype, int n_targets, const i
 /* A gate list on a small or mid-size state in one launch per 64 gates (Circuit.execute without
  * pass planning, circuit.py:96-125 -> gates.py:472-487 per gate).  States up to
  * QSB_BATCH_MAX_STATE_BYTES (13 qubits complex128, 14 complex64) are held in one CTA's shared
- * memory; states up to QSB_GRID_BATCH_MAX_STATE_BYTES (21 / 22 qubits, L2-resident) are walked
- * by a cooperative grid with a grid barrier between gates.  The gates run in queue order with
+ * memory; states up to QSB_GRID_BATCH_MAX_STATE_BYTES (26 / 27 qubits) are walked by a
+ * cooperative grid with a grid barrier between gates (L2-resident up to ~64 MB).  The gates run in queue order with
  * the bodies and semantics of qsb_apply_matrix, so the result equals n_gates qsb_apply_matrix
  * calls bit for bit.  Gate i: n_targets[i] target bits at target_bits[2i..], n_controls[i]
  * control bits taken consecutively from control_bits, its 2**t x 2**t complex128 matrix
  * row-major at matrices[32i..] (interleaved re, im) and its kernel class in kernels[i].  The
  * whole list is validated before any work is enqueued. */
 #define QSB_BATCH_MAX_STATE_BYTES 131072
-#define QSB_GRID_BATCH_MAX_STATE_BYTES 33554432
+#define QSB_GRID_BATCH_MAX_STATE_BYTES 1073741824
 int qsb_apply_batch(void* amps, int n_qubits, int dtype, int n_gates, const int* n_targets,
                     const int* target_bits, const int* n_controls, const int* control_bits,
                     const double* matrices, const int* kernels, void* stream);

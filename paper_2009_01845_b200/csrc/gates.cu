@@ -628,7 +628,7 @@ static int check_dtype(int dtype) {
 // per-gate kernels' bits:
 //   * k_small_batch: states <= QSB_BATCH_MAX_STATE_BYTES; one CTA holds the state in shared
 //     memory, __syncthreads between gates.
-//   * k_grid_batch: states <= QSB_GRID_BATCH_MAX_STATE_BYTES (L2-resident); a co-resident
+//   * k_grid_batch: states <= QSB_GRID_BATCH_MAX_STATE_BYTES; a co-resident
 //     (cooperative) grid walks each gate over global memory with L2-only loads/stores (L1 is not
 //     coherent across SMs) and a grid barrier between gates.
 constexpr int kSmallThreads = 512;

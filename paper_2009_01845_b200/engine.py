@@ -75,10 +75,12 @@ def _apply_gate_step(ptr, n, dtype, g, stream):
     )
 
 
-# qsb_apply_batch keeps states up to this size in shared memory, and walks states up to the
-# second size with a grid-synchronised launch (include/qsb200.h)
+# qsb_apply_batch keeps states up to this size in shared memory, and walks larger ones with a
+# grid-synchronised launch (include/qsb200.h).  A gate list seen for the first time goes through
+# the grid walk up to GRID_BATCH_MAX_STATE_BYTES: below it the per-gate sweeps (L2-resident up to
+# ~64 MB) cost less than planning the list into fused passes on the host (10-50 ms).
 BATCH_MAX_STATE_BYTES = 131072
-GRID_BATCH_MAX_STATE_BYTES = 32 << 20
+GRID_BATCH_MAX_STATE_BYTES = 256 << 20
 
 
 def _gate_matrix_and_class(g):
@@ -265,7 +267,7 @@ def run_gates(state, specs, fuse: bool | None = None, scratch_holder: dict | Non
 
     * Small states (<= BATCH_MAX_STATE_BYTES): no planning; the specs go straight to one
       shared-memory launch per 64 gates.
-    * Mid-size, L2-resident states (<= GRID_BATCH_MAX_STATE_BYTES, fusion on): the first run of a
+    * Mid-size states (<= GRID_BATCH_MAX_STATE_BYTES, fusion on): the first run of a
       gate list goes through the grid-synchronised batch launch (no host planning, which costs
       more than the whole circuit at this size); when the same list comes back -- or was
       prepared with prepare_plan -- it runs as planned fused passes.

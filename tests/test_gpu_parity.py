@@ -502,10 +502,10 @@ def test_expectation_fused_passes_match_per_term(cuda, n):
 
 
 @pytest.mark.parametrize("n,prec", [(4, "f64"), (9, "f32"), (12, "f64"), (13, "f64"), (14, "f32"), (14, "f64"),
-                                    (17, "f32"), (18, "f64"), (21, "f64"), (22, "f32")])
+                                    (17, "f32"), (18, "f64"), (21, "f64"), (22, "f32"), (24, "f64")])
 def test_gate_batch_equals_per_gate_kernels(cuda, n, prec):
     """qsb_apply_batch -- state in one CTA's shared memory up to 128 KB, a grid-synchronised
-    walk of the L2-resident state up to 32 MB -- against the per-gate kernels (same bits) and
+    walk of the state beyond that -- against the per-gate kernels (same bits) and
     the oracle; 150 gates cross the 64-gate launch boundary."""
     import paper_2009_01845_b200 as q
     from paper_2009_01845_b200 import _native as nat
@@ -546,10 +546,11 @@ def test_gate_batch_small_states_and_limits(cuda):
         psi[0] = 1
         want = ov.run([ov.gate("Unitary", s.targets, s.controls, (), q.gate_matrix(s)) for s in specs], n, psi)
         assert max_abs(got, want) <= TOL64
-    big = q.zero_state(22)  # 64 MB complex128: beyond the L2-resident grid walk
-    g = [normalize(q.H(0), 22)]
+    big = q.zero_state(27)  # 2 GB complex128: beyond the grid walk's limit
+    g = [normalize(q.H(0), 27)]
     with pytest.raises(CapacityError):
-        engine._apply_gate_batch(big.data_ptr, 22, nat.QSB_C128, engine.pack_gate_batch(g), nat.stream_ptr())
+        engine._apply_gate_batch(big.data_ptr, 27, nat.QSB_C128, engine.pack_gate_batch(g), nat.stream_ptr())
+    del big
     small = q.zero_state(5)
     bad = engine.pack_gate_batch([normalize(q.SWAP(0, 1), 5)])
     bad[1][1] = bad[1][0]  # duplicate target bit: rejected before any launch
@@ -558,7 +559,7 @@ def test_gate_batch_small_states_and_limits(cuda):
     assert np.array_equal(small.amplitudes, np.eye(1, 32, dtype=np.complex128)[0])
 
 
-@pytest.mark.parametrize("n", [16, 20])
+@pytest.mark.parametrize("n", [16, 20, 24])
 def test_mid_size_first_run_batched_then_planned(cuda, n):
     """A mid-size circuit runs through the grid-synchronised batch first (run_gates returns no
     plan), then as planned fused passes; both match the analytic DFT column."""
