@@ -991,7 +991,25 @@ def smem_bytes(stage_bytes: int, n_coeffs=MAX_COEFFS, alias: bool = False) -> in
     return struct_bytes + 8 * n_coeffs + 128
 
 
+_WORDS_CACHE: dict = {}  # (dtype, program bytes) -> compile_words result: rebuilt identical circuits skip codegen
+_WORDS_CACHE_MAX = 256
+
+
 def compile_words(words, dtype):
+    wkey = (int(dtype), np.asarray(words, dtype=np.int64).tobytes())
+    with _lock:
+        done = _WORDS_CACHE.get(wkey)
+    if done is not None:
+        return done
+    out = _compile_words(words, dtype)
+    with _lock:
+        if len(_WORDS_CACHE) >= _WORDS_CACHE_MAX:
+            _WORDS_CACHE.pop(next(iter(_WORDS_CACHE)))
+        _WORDS_CACHE[wkey] = out
+    return out
+
+
+def _compile_words(words, dtype):
     src, name, params, tables, tplan = generate_full(words, dtype)
     if len(tables) > MAX_COEFFS:
         raise RuntimeError(f"{len(tables)} table entries exceed the shared-memory budget")
