@@ -156,6 +156,10 @@ uint64_t qsb_marginal_scratch_doubles(int n_bits, int k);
 int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cum, void* scratch,
                           size_t scratch_bytes, void* stream);
 size_t qsb_cumsum_scratch_bytes(uint64_t n);
+/* The same exact sequential cumsum; normalize = 0 leaves cum[i] = fl(cum[i-1] + p[i]) undivided
+ * (the sharded sampler chains shards by prepending the previous shard's last value). */
+int qsb_cumsum(const double* probs, uint64_t n, double* cum, void* scratch, size_t scratch_bytes, int normalize,
+               void* stream);
 /* The strictly sequential fl(c + p) chain on one device thread (no normalisation): the
  * cross-check for qsb_cumsum_normalized in the GPU tests. */
 int qsb_cumsum_serial(const double* probs, uint64_t n, double* cum, void* stream);
@@ -164,6 +168,11 @@ int qsb_cumsum_serial(const double* probs, uint64_t n, double* cum, void* stream
  * 0, n-1) -- np.searchsorted(cum, u, side="right") (measurement.py:83-86). */
 int qsb_sample(const double* cum, uint64_t n, uint64_t state_hi, uint64_t state_lo,
                uint64_t inc_hi, uint64_t inc_lo, uint64_t n_shots, int64_t* samples, void* stream);
+/* The same draws; counts[k] = #{i : cum[i] <= u_k} without the clip, so that the counts of the
+ * pieces of a distribution split across shards (in index order) add up to the global
+ * searchsorted index (sharded sampling). */
+int qsb_sample_counts(const double* cum, uint64_t n, uint64_t state_hi, uint64_t state_lo,
+                      uint64_t inc_hi, uint64_t inc_lo, uint64_t n_shots, int64_t* counts, void* stream);
 
 /* ---- sharded execution helpers (sharding.py:53-111 partition / gather / _exchange_halves) - */
 /* dst[i'] = src[i] where bit b of i moves to bit dst_bit[b] of i' (moveaxis of partition /

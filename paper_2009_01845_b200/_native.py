@@ -59,6 +59,8 @@ SIGNATURES = {
     "qsb_marginal_scratch_doubles": (_c_u64, [_c_int, _c_int]),
     "qsb_cumsum_normalized": (_c_int, [_c_void_p, _c_u64, _c_void_p, _c_void_p, _c_size_t, _c_void_p]),
     "qsb_cumsum_scratch_bytes": (_c_size_t, [_c_u64]),
+    "qsb_cumsum": (_c_int, [_c_void_p, _c_u64, _c_void_p, _c_void_p, _c_size_t, _c_int, _c_void_p]),
+    "qsb_sample_counts": (_c_int, [_c_void_p, _c_u64, _c_u64, _c_u64, _c_u64, _c_u64, _c_u64, _c_void_p, _c_void_p]),
     "qsb_cumsum_serial": (_c_int, [_c_void_p, _c_u64, _c_void_p, _c_void_p]),
     "qsb_sample": (_c_int, [_c_void_p, _c_u64, _c_u64, _c_u64, _c_u64, _c_u64, _c_u64, _c_void_p, _c_void_p]),
     "qsb_jit_available": (_c_int, [ctypes.c_char_p]),

@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(kMT, 3) k_materialize2(const double* __restric
                                                       const double* __restrict__ block_start,
                                                       const double* __restrict__ serial_val,
                                                       const double* __restrict__ total,
-                                                      double* __restrict__ c_out) {
+                                                      double* __restrict__ c_out, int normalize) {
   __shared__ double sh[kMT * kRow];
   __shared__ double wsum[kMT / 32];
   __shared__ unsigned int usum[kMT / 32];
@@ -771,7 +771,7 @@ __global__ void __launch_bounds__(kMT, 3) k_materialize2(const double* __restric
       V = piece_then(V, elem_piece(row[k], rc.e[k]));
       c = piece_apply(V, c0);
     }
-    row[k] = __ddiv_rn(c, tot);
+    row[k] = normalize ? __ddiv_rn(c, tot) : c;
   }
   __syncthreads();
   const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
@@ -841,7 +841,7 @@ constexpr int kShotsPerThread = 32;
 
 __global__ void __launch_bounds__(kMT) k_sample(const double* __restrict__ cum, uint64_t n, uint64_t s_hi,
                                                 uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, uint64_t n_shots,
-                                                long long* __restrict__ out) {
+                                                long long* __restrict__ out, uint64_t clip_max) {
   const uint64_t t = (uint64_t)blockIdx.x * kMT + threadIdx.x;
   const uint64_t first = t * kShotsPerThread;
   if (first >= n_shots) return;
@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(kMT) k_sample(const double* __restrict__ cum, 
         hi = mid;
     }
     uint64_t idx = lo;
-    if (idx > n - 1) idx = n - 1;
+    if (idx > clip_max) idx = clip_max;
     out[shot] = (long long)idx;
   }
 }
@@ -987,10 +987,15 @@ static size_t g_ser_cap = 0;
 
 extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cum, void* scratch,
                                      size_t scratch_bytes, void* stream) {
+  return qsb_cumsum(probs, n, cum, scratch, scratch_bytes, 1, stream);
+}
+
+extern "C" int qsb_cumsum(const double* probs, uint64_t n, double* cum, void* scratch, size_t scratch_bytes,
+                          int normalize, void* stream) {
   cudaStream_t st = as_stream(stream);
   if (n == 0) return QSB_OK;
   if (scratch_bytes < qsb_cumsum_scratch_bytes(n)) {
-    set_error("qsb_cumsum_normalized: scratch too small");
+    set_error("qsb_cumsum: scratch too small");
     return QSB_ERR_ARG;
   }
   const uint64_t nb = (n + kScanBlock - 1) / kScanBlock;
@@ -1066,8 +1071,8 @@ extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cu
   k_block_starts<<<(int)((nb + kMT - 1) / kMT), kMT, 0, st>>>(runp, nb, rstart, bstart);
   k_total2<<<1, 1, 0, st>>>(head, cnt, nb, bstart, after, sval, ns, d_total);
   // E: every c_i, divided by c_{n-1}
-  k_materialize2<<<(int)nb, kMT, 0, st>>>(probs, n, margin, bpre, base, bstart, sval, d_total, cum);
-  QSB_CHECK_LAUNCH("qsb_cumsum_normalized");
+  k_materialize2<<<(int)nb, kMT, 0, st>>>(probs, n, margin, bpre, base, bstart, sval, d_total, cum, normalize);
+  QSB_CHECK_LAUNCH("qsb_cumsum");
   return QSB_OK;
 }
 
@@ -1089,7 +1094,21 @@ extern "C" int qsb_sample(const double* cum, uint64_t n, uint64_t s_hi, uint64_t
   }
   const uint64_t threads = (n_shots + kShotsPerThread - 1) / kShotsPerThread;
   k_sample<<<(int)((threads + kMT - 1) / kMT), kMT, 0, st>>>(cum, n, s_hi, s_lo, i_hi, i_lo, n_shots,
-                                                            reinterpret_cast<long long*>(samples));
+                                                            reinterpret_cast<long long*>(samples), n - 1);
   QSB_CHECK_LAUNCH("qsb_sample");
+  return QSB_OK;
+}
+
+extern "C" int qsb_sample_counts(const double* cum, uint64_t n, uint64_t s_hi, uint64_t s_lo, uint64_t i_hi,
+                                 uint64_t i_lo, uint64_t n_shots, int64_t* counts, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (n == 0 || n_shots == 0) {
+    set_error("qsb_sample_counts: empty distribution or no shots");
+    return QSB_ERR_ARG;
+  }
+  const uint64_t threads = (n_shots + kShotsPerThread - 1) / kShotsPerThread;
+  k_sample<<<(int)((threads + kMT - 1) / kMT), kMT, 0, st>>>(cum, n, s_hi, s_lo, i_hi, i_lo, n_shots,
+                                                            reinterpret_cast<long long*>(counts), ~0ull);
+  QSB_CHECK_LAUNCH("qsb_sample_counts");
   return QSB_OK;
 }

@@ -102,8 +102,9 @@ def pcg64_seed_state(seed: int):
     return (s >> 64) & m, s & m, (inc >> 64) & m, inc & m
 
 
-def device_cdf(probs):
-    """Normalised cumulative distribution, bit-identical to numpy's cumsum(p) / cumsum(p)[-1]."""
+def device_cdf(probs, normalize: bool = True):
+    """Normalised cumulative distribution, bit-identical to numpy's cumsum(p) / cumsum(p)[-1];
+    normalize=False: the exact sequential cumsum itself."""
     torch = nat.torch_mod()
     lib = nat.lib()
     n = probs.numel()
@@ -111,10 +112,24 @@ def device_cdf(probs):
     nbytes = int(lib.qsb_cumsum_scratch_bytes(n))
     scratch = torch.empty(nbytes, dtype=torch.uint8, device=probs.device)
     nat.check(
-        lib.qsb_cumsum_normalized(probs.data_ptr(), n, cum.data_ptr(), scratch.data_ptr(), nbytes, nat.stream_ptr()),
+        lib.qsb_cumsum(probs.data_ptr(), n, cum.data_ptr(), scratch.data_ptr(), nbytes, 1 if normalize else 0,
+                       nat.stream_ptr()),
         "cumsum",
     )
     return cum
+
+
+def device_sample_counts(cum, n_shots: int, seed: int):
+    """#{i : cum[i] <= u_k} for the n_shots draws u_k of default_rng(seed), unclipped."""
+    torch = nat.torch_mod()
+    out = torch.empty(int(n_shots), dtype=torch.int64, device=cum.device)
+    sh, sl, ih, il = pcg64_seed_state(seed)
+    nat.check(
+        nat.lib().qsb_sample_counts(cum.data_ptr(), cum.numel(), sh, sl, ih, il, int(n_shots), out.data_ptr(),
+                                    nat.stream_ptr()),
+        "sample_counts",
+    )
+    return out
 
 
 def device_sample(cum, n_shots: int, seed: int):

@@ -617,6 +617,93 @@ def run_sharded(circuit: Circuit, n_shards: int, initial: StateVector | None = N
     return sh
 
 
+def canonicalize(sharded: ShardedState) -> None:
+    """Bring a sharded state to the canonical layout in place: global qubits {0..g-1} (reshuffles
+    with local qubits) and local qubits in significance order (a per-shard bit permutation), so
+    that the shards, taken in index order, are the slices of the 1-GPU state vector."""
+    g = sharded.n_global
+    want = set(range(g))
+    for q in list(sharded.global_qubits):
+        if q not in want:
+            lq = next(x for x in sharded.local_qubits if x in want and x not in sharded.global_qubits)
+            reshuffle(sharded, q, lq)
+    local = list(sharded.local_qubits)
+    if local != sorted(local):
+        nl = sharded.n_local
+        order = sorted(local)
+        dst = [0] * nl
+        for m, q in enumerate(local):  # local slot m holds bit nl-1-m
+            dst[nl - 1 - m] = nl - 1 - order.index(q)
+        for s_id, t in list(sharded.shards.items()):
+            sharded.shards[s_id] = sharded.backend.permute(t, nl, dst)
+        sharded.local_qubits = tuple(order)
+
+
+def _canonical_shard_ids(sharded: ShardedState):
+    """Shard ids in canonical index order (qubit q < g is bit g-1-q of the canonical index)."""
+    g = sharded.n_global
+    ids = []
+    for c in range(1 << g):
+        s_id = 0
+        for j, q in enumerate(sharded.global_qubits):
+            s_id |= ((c >> (g - 1 - q)) & 1) << (g - 1 - j)
+        ids.append(s_id)
+    return ids
+
+
+def sample_sharded(sharded: ShardedState, n_shots: int, seed: int):
+    """Sample every qubit of a sharded state without gathering it -- bit-identical to
+    measurement.sample(gather(sharded), range(n), n_shots, seed) (SURVEY.md section 8(e),
+    exact mode; measurement.py:61-87).
+
+    The state is first brought to the canonical layout (canonicalize).  The sequential cumsum is
+    chained shard by shard in index order: each shard's exact cumsum starts from the previous
+    shard's last value (prepended as element 0), so every partial sum is rounded exactly as in
+    one np.cumsum over the whole vector; the total is the last shard's last value and every
+    piece is divided by it.  Each shard then counts, per draw, its entries <= u (unclipped); the
+    counts summed over shards (all-reduce across ranks) are np.searchsorted(cum, u, 'right'),
+    clipped to [0, 2^n - 1]."""
+    from .measurement import MeasurementResult, device_cdf, device_probabilities, device_sample_counts
+
+    if n_shots < 1:
+        raise ValueError(f"n_shots must be >= 1, got {n_shots}")
+    torch = nat.torch_mod()
+    canonicalize(sharded)
+    comm = sharded.comm
+    order = _canonical_shard_ids(sharded)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    carry = None
+    cums = {}
+    for s_id in order:
+        owned = s_id in sharded.shards
+        if owned:
+            view = _ShardView(sharded.shards[s_id], sharded.n_local, sharded.precision)
+            p = device_probabilities(view)
+            if carry is None:
+                cum = device_cdf(p, normalize=False)
+            else:
+                cum = device_cdf(torch.cat([carry.reshape(1), p]), normalize=False)[1:]
+            last = cum[-1:].clone()
+            cums[s_id] = cum
+        else:
+            last = torch.zeros(1, dtype=torch.float64, device=dev)
+        if isinstance(comm, LocalComm):
+            carry = last
+        else:  # the owner's last value reaches every rank (one element per shard, in order)
+            parts = comm.all_gather(last)
+            carry = parts[sharded.owner[s_id]].to(dev)
+    total = carry
+    counts = torch.zeros(int(n_shots), dtype=torch.int64, device=dev)
+    for s_id, cum in cums.items():
+        cum /= total  # numpy: cum /= cum[-1], element-wise IEEE division
+        counts += device_sample_counts(cum, n_shots, seed)
+    if not isinstance(comm, LocalComm):
+        parts = comm.all_gather(counts)
+        counts = sum(x.to(dev) for x in parts)
+    samples = counts.clamp_(0, (1 << sharded.n_qubits) - 1).cpu().numpy()
+    return MeasurementResult(int(n_shots), tuple(range(sharded.n_qubits)), samples, int(seed), {})
+
+
 def _dist_comm_for(n_shards):
     try:
         import torch.distributed as dist

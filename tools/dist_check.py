@@ -47,6 +47,16 @@ for name, c in [("qft", q.qft_circuit(n)),
     if rank == 0:
         print(f"world {world} {name}-{n}: reshuffles {sd.plan(c, world).n_reshuffles}, max|diff| {err:.2e}", flush=True)
 dist.barrier()
+# sharded sampling across ranks (chained cumsum over all_gather, counts all-reduced)
+c = q.variational_circuit(n, 2, np.random.default_rng(5).uniform(0, 6, n * 5), fused=True)
+sh = sd.execute_distributed(c, q.Precision.F64, comm=HostStagedComm())
+got = sd.sample_sharded(sh, 4000, 9).samples
+want = q.sample(c.execute(), range(n), 4000, 9).samples
+ok = bool(np.array_equal(got, want))
+if rank == 0:
+    print(f"world {world} sharded sampling bit-exact: {ok}", flush=True)
+worst = worst if ok else 1.0
+dist.barrier()
 # the bench's isolated-exchange timing through the same runner pipeline (numbers meaningless here:
 # every rank shares one GPU and chunks are staged through the host)
 import bench  # noqa: E402
