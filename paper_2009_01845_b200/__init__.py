@@ -21,6 +21,8 @@ from .circuit import (
 )
 from .errors import ArityError, CapacityError, FormError, ParseError, ShapeError, SimulationError
 from .evolution import (
+    adiabatic_evolve_sharded,
+    evolve_sharded,
     Callback,
     EnergyCallback,
     EntanglementEntropyCallback,

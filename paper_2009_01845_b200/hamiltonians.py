@@ -125,10 +125,11 @@ def combine(a, coeff_a: float, b, coeff_b: float):
 _EXPECT_CACHE: dict = {}
 
 
-def _expectation_passes(terms, state):
-    """The terms as read-only fused passes (jit expectation kernels: every term whose bits fit a
-    tile is evaluated from the registers of that tile, one HBM read per pass instead of one per
-    term).  None when the specialised kernels are unavailable or the state is too small."""
+def _expectation_passes(bit_terms, state):
+    """The terms (bit positions, MSB first) as read-only fused passes (jit expectation kernels:
+    every term whose bits fit a tile is evaluated from the registers of that tile, one HBM read
+    per pass instead of one per term).  None when the specialised kernels are unavailable or
+    the state is too small."""
     from . import engine, jit
     from .fusion import plan_expectation
 
@@ -137,12 +138,11 @@ def _expectation_passes(terms, state):
     geo = engine.default_geometry(dtype)
     if not jit.available() or n < geo.K + 1 or geo.halves or dtype != nat.QSB_C128:
         return None  # complex64 states keep the per-term kernel (double math on 32 amplitudes spills)
-    key = (n, dtype, geo, tuple((tuple(q), np.asarray(m).tobytes()) for q, m in terms))
+    key = (n, dtype, geo, tuple((tuple(b), np.asarray(m).tobytes()) for b, m in bit_terms))
     progs = _EXPECT_CACHE.get(key)
     if progs is None:
-        bits = [(tuple(n - 1 - q for q in qs), m) for qs, m in terms]
         progs = []
-        for words in plan_expectation(bits, n, dtype, geo):
+        for words in plan_expectation([(tuple(b), m) for b, m in bit_terms], n, dtype, geo):
             progs.append((words, jit.compile_words(words, dtype)))
         if len(_EXPECT_CACHE) > 16:
             _EXPECT_CACHE.clear()
@@ -156,6 +156,31 @@ def _expectation_passes(terms, state):
         ssum = part.sum()
         total = ssum if total is None else total + ssum
     return float(total.item()) if total is not None else 0.0
+
+
+def _expect_bit_terms(bit_terms, state) -> float:
+    """sum_t <psi|H_t|psi> (real part) for terms given on bit positions (MSB of the matrix first)
+    of a state-like object (StateVector or one shard)."""
+    fused = _expectation_passes(bit_terms, state)
+    if fused is not None:
+        return fused
+    torch = nat.torch_mod()
+    ks = np.array([len(b) for b, _ in bit_terms], dtype=np.int32)
+    bits = np.zeros(2 * max(1, len(bit_terms)), dtype=np.int32)
+    mats = np.zeros(32 * max(1, len(bit_terms)), dtype=np.float64)
+    for t, (b, m) in enumerate(bit_terms):
+        if len(b) not in (1, 2):
+            raise ShapeError(f"expectation supports 1- and 2-qubit terms, got {len(b)}")
+        bits[2 * t] = b[0]
+        bits[2 * t + 1] = b[-1]
+        mm = np.ascontiguousarray(np.asarray(m, dtype=np.complex128))
+        mats[32 * t:32 * t + 2 * mm.size] = mm.view(np.float64).reshape(-1)
+    out = torch.empty(2, dtype=torch.float64, device=state.tensor.device)
+    nat.check(nat.lib().qsb_expect_terms(state.data_ptr, state.n_qubits, state.precision.qsb_dtype, len(bit_terms),
+                                         ks.ctypes.data, bits.ctypes.data, mats.ctypes.data, out.data_ptr(),
+                                         nat.stream_ptr()),
+              "expectation")
+    return float(out[0].item())
 
 
 def _fold_single_terms(terms):
@@ -179,34 +204,16 @@ def _fold_single_terms(terms):
 
 
 def expectation(h, state: StateVector) -> float:
-    """<psi|H|psi> (real part) on the device (hamiltonians.py:192-207): every term's
-    <psi|H_t|psi> is accumulated by `qsb_expect_terms` -- one read-only sweep of the state per
-    term, no state copy (the reference copies the state and applies each term to the copy)."""
+    """<psi|H|psi> (real part) on the device (hamiltonians.py:192-207): the terms are evaluated
+    read-only (fused read passes, else `qsb_expect_terms` one sweep per term), no state copy (the
+    reference copies the state and applies each term to the copy)."""
     if h.n_qubits != state.n_qubits:
         raise ShapeError(f"Hamiltonian has {h.n_qubits} qubits, state has {state.n_qubits}")
     if not isinstance(h, TrotterHamiltonian):
         _dense_unsupported()
-    torch = nat.torch_mod()
     n = h.n_qubits
     terms = _fold_single_terms(h.terms)
-    fused = _expectation_passes(terms, state)
-    if fused is not None:
-        return fused
-    ks = np.array([len(q) for q, _ in terms], dtype=np.int32)
-    bits = np.zeros(2 * max(1, len(terms)), dtype=np.int32)
-    mats = np.zeros(32 * max(1, len(terms)), dtype=np.float64)
-    for t, (qubits, m) in enumerate(terms):
-        if len(qubits) not in (1, 2):
-            raise ShapeError(f"expectation supports 1- and 2-qubit terms, got {len(qubits)}")
-        bits[2 * t] = n - 1 - qubits[0]
-        bits[2 * t + 1] = n - 1 - qubits[-1]
-        mm = np.ascontiguousarray(np.asarray(m, dtype=np.complex128))
-        mats[32 * t:32 * t + 2 * mm.size] = mm.view(np.float64).reshape(-1)
-    out = torch.empty(2, dtype=torch.float64, device=state.tensor.device)
-    nat.check(nat.lib().qsb_expect_terms(state.data_ptr, n, state.precision.qsb_dtype, len(terms), ks.ctypes.data,
-                                         bits.ctypes.data, mats.ctypes.data, out.data_ptr(), nat.stream_ptr()),
-              "expectation")
-    return float(out[0].item())
+    return _expect_bit_terms([(tuple(n - 1 - q for q in qs), m) for qs, m in terms], state)
 
 
 def ground_state_vector(h, precision: Precision = Precision.F64) -> StateVector:

@@ -617,6 +617,90 @@ def run_sharded(circuit: Circuit, n_shards: int, initial: StateVector | None = N
     return sh
 
 
+def apply_sharded(sharded: ShardedState, circuit: Circuit, cache: dict | None = None) -> ShardedState:
+    """Run `circuit` on an existing sharded state in place: planned from its current global
+    qubits, the state stays sharded (no partition / gather around the circuit)."""
+    exec_plan = plan(circuit, 1 << sharded.n_global, sharded.global_qubits)
+    runner = _Runner(sharded, cache)
+    for step in exec_plan.steps:
+        if isinstance(step, Reshuffle):
+            runner.flush()
+            reshuffle(sharded, step.global_qubit, step.local_qubit)
+        else:
+            for pos in step.positions:
+                runner.apply(circuit.queue[pos], pos)
+    runner.flush()
+    return sharded
+
+
+def uniform_sharded(n_qubits: int, n_shards: int, precision: Precision = Precision.F64, comm=None, backend=None,
+                    global_qubits=None) -> ShardedState:
+    """|+>^n built shard by shard (every amplitude 2^(-n/2), as uniform_state / _plus_state,
+    hamiltonians.py:115-117); the full state never exists in one place."""
+    comm = comm or LocalComm()
+    backend = backend or CudaBackend(precision)
+    g = n_shards.bit_length() - 1
+    if n_shards < 2 or n_shards & (n_shards - 1) or g >= n_qubits:
+        raise ShapeError(f"n_shards must be a power of two in [2, 2^(n-1)], got {n_shards}")
+    glob = tuple(global_qubits) if global_qubits is not None else tuple(range(g))
+    sh = ShardedState(n_qubits, glob, {}, precision, comm=comm, backend=backend)
+    nl = n_qubits - g
+    value = float(1.0 / np.sqrt(float(1 << n_qubits)))
+    for s_id in range(1 << g):
+        sh.owner[s_id] = (s_id * comm.world) >> g
+        if comm.owns(s_id, sh.owner):
+            t = backend.empty(1 << nl)
+            nat.check(nat.lib().qsb_init_uniform(t.data_ptr(), nl, precision.qsb_dtype, value, 0.0, nat.stream_ptr()),
+                      "uniform shard")
+            sh.shards[s_id] = t
+    return sh
+
+
+def _allreduce_sum(comm, value: float) -> float:
+    if isinstance(comm, LocalComm):
+        return value
+    torch = nat.torch_mod()
+    t = torch.tensor([value], dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+    return float(sum(float(x.item()) for x in comm.all_gather(t)))
+
+
+def expectation_sharded(h, sharded: ShardedState) -> float:
+    """<psi|H|psi> of a Trotter-form Hamiltonian on a sharded state, without gathering it
+    (hamiltonians.py:192-207).  Terms on local qubits are summed shard by shard; for the terms
+    touching global qubits those globals are first reshuffled with local qubits outside the
+    terms' support (the state is unchanged, only its layout)."""
+    from .hamiltonians import TrotterHamiltonian, _expect_bit_terms, _fold_single_terms
+
+    if h.n_qubits != sharded.n_qubits:
+        raise ShapeError(f"Hamiltonian has {h.n_qubits} qubits, state has {sharded.n_qubits}")
+    if not isinstance(h, TrotterHamiltonian):
+        raise ShapeError("expectation_sharded needs a Trotter-form Hamiltonian")
+    terms = _fold_single_terms(h.terms)
+
+    def local_sum(ts):
+        if not ts:
+            return 0.0
+        acc = 0.0
+        for t in sharded.shards.values():
+            view = _ShardView(t, sharded.n_local, sharded.precision)
+            acc += _expect_bit_terms([(tuple(sharded.local_bit(q) for q in qs), m) for qs, m in ts], view)
+        return _allreduce_sum(sharded.comm, acc)
+
+    glob = set(sharded.global_qubits)
+    here = [t for t in terms if not set(t[0]) & glob]
+    rest = [t for t in terms if set(t[0]) & glob]
+    total = local_sum(here)
+    if rest:
+        support = {q for qs, _ in rest for q in qs}
+        for q in [q for q in sharded.global_qubits if q in support]:
+            cand = next((x for x in sharded.local_qubits if x not in support), None)
+            if cand is None:
+                raise CapacityError("too few local qubits outside the terms' support to localise them")
+            reshuffle(sharded, q, cand)
+        total += local_sum(rest)
+    return total
+
+
 def canonicalize(sharded: ShardedState) -> None:
     """Bring a sharded state to the canonical layout in place: global qubits {0..g-1} (reshuffles
     with local qubits) and local qubits in significance order (a per-shard bit permutation), so
@@ -740,6 +824,7 @@ def execute_distributed(circuit: Circuit, precision: Precision = Precision.F64, 
     return run_sharded(circuit, comm.world, None, precision, global_qubits, comm)
 
 
-__all__ = ["ExecutionPlan", "LocalSegment", "Reshuffle", "ShardedState", "execute_distributed", "execute_sharded",
-           "gather", "partition", "plan", "reshuffle"]
+__all__ = ["ExecutionPlan", "LocalSegment", "Reshuffle", "ShardedState", "apply_sharded", "canonicalize",
+           "execute_distributed", "execute_sharded", "expectation_sharded", "gather", "partition", "plan", "reshuffle",
+           "sample_sharded", "uniform_sharded"]
 _ = (_check_cap, zero_state, diag_terms, NGate)

@@ -495,7 +495,7 @@ def test_expectation_fused_passes_match_per_term(cuda, n):
         t = psi.copy()
         ov.apply_matrix(t, n, qs, m)
         want += np.vdot(psi, t).real
-    fused = hm._expectation_passes(hm._fold_single_terms(h.terms), st)
+    fused = hm._expectation_passes([(tuple(n - 1 - x for x in qs), m) for qs, m in hm._fold_single_terms(h.terms)], st)
     assert fused is not None
     assert abs(fused - want) <= 1e-10 * max(1.0, abs(want))
     assert abs(q.expectation(h, st) - want) <= 1e-10 * max(1.0, abs(want))

@@ -121,3 +121,39 @@ def test_chained_cumsum_equals_serial(cuda):
             pieces.append(cum)
         assert torch.equal(torch.cat(pieces), serial)
         assert np.array_equal(torch.cat(pieces).cpu().numpy(), np.cumsum(p))
+
+
+@pytest.mark.parametrize("n,shards", [(10, 2), (12, 4), (13, 8)])
+def test_resident_sharded_adiabatic_evolution(cuda, n, shards):
+    """adiabatic_evolve_sharded keeps the state in shards for all steps (no gather per step): the
+    gathered result, its energy (expectation_sharded, no gather) and its samples match the
+    1-GPU evolution."""
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200 import sharding as sd
+
+    h0, h1 = q.build_x(n), q.build_tfim(n, 1.0)
+    cfg = q.EvolutionConfig(q.Solver.TROTTER, 0.1, 1.0)
+    want = q.adiabatic_evolve(h0, h1, q.Schedule.linear(), cfg)
+    sh = q.adiabatic_evolve_sharded(h0, h1, q.Schedule.linear(), cfg, n_shards=shards)
+    e = sd.expectation_sharded(h1, sh)
+    assert abs(e - q.expectation(h1, want)) <= 1e-10
+    assert abs(sd.expectation_sharded(h0, sh) - q.expectation(h0, want)) <= 1e-10
+    got = sd.gather(sh)
+    assert max_abs(got.amplitudes, want.amplitudes) <= 1e-12
+    # evolving a given state (partitioned once) and a resident ShardedState in place
+    init = q.from_amplitudes(want.amplitudes)
+    a = sd.gather(q.evolve_sharded(h1, cfg, n_shards=shards, initial=init)).amplitudes
+    b = q.evolve(h1, init, cfg).amplitudes
+    assert max_abs(a, b) <= 1e-12
+
+
+def test_cli_evolve_sharded_energy(cuda, capsys):
+    import json
+
+    from paper_2009_01845_b200 import cli
+
+    assert cli.main(["evolve", "--nqubits", "10", "--dt", "0.1", "--T", "1.0"]) == 0
+    one = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert cli.main(["evolve", "--nqubits", "10", "--dt", "0.1", "--T", "1.0", "--shards", "4"]) == 0
+    four = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert abs(one["final_energy"] - four["final_energy"]) <= 1e-10

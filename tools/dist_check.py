@@ -57,6 +57,18 @@ if rank == 0:
     print(f"world {world} sharded sampling bit-exact: {ok}", flush=True)
 worst = worst if ok else 1.0
 dist.barrier()
+# adiabatic evolution resident in the ranks' shards + sharded energy
+cfg = q.EvolutionConfig(q.Solver.TROTTER, 0.1, 1.0)
+h0, h1 = q.build_x(n), q.build_tfim(n, 1.0)
+sh = q.adiabatic_evolve_sharded(h0, h1, q.Schedule.linear(), cfg, comm=HostStagedComm())
+e = sd.expectation_sharded(h1, sh)
+ref = q.adiabatic_evolve(h0, h1, q.Schedule.linear(), cfg)
+err = float(np.max(np.abs(sd.gather(sh).amplitudes - ref.amplitudes)))
+de = abs(e - q.expectation(h1, ref))
+if rank == 0:
+    print(f"world {world} resident adiabatic evolution: max|diff| {err:.2e}, energy diff {de:.2e}", flush=True)
+worst = max(worst, err, de / 100)
+dist.barrier()
 # the bench's isolated-exchange timing through the same runner pipeline (numbers meaningless here:
 # every rank shares one GPU and chunks are staged through the host)
 import bench  # noqa: E402
