@@ -154,6 +154,19 @@ def _worker(rank, world, port, out_dir):
             sh = sd.run_sharded(c, world, init, Precision.F64, None, comm, CpuBackend(Precision.F64))
             got = sd.gather_tensor(sh).numpy()
             results[name] = float(np.max(np.abs(got - oracle_of(c, psi))))
+        # a state resident in the ranks' shards across several circuits (apply_sharded: each
+        # planned from the current global qubits), then brought to the canonical layout
+        c1, c2, c3 = random_circuit(n, 25, 21), qft_circuit(n), random_circuit(n, 25, 22)
+        psi = rand_state(n, 4)
+        sh = sd.run_sharded(c1, world, FakeState(psi), Precision.F64, None, comm, CpuBackend(Precision.F64))
+        sd.apply_sharded(sh, c2)
+        sd.apply_sharded(sh, c3)
+        want = oracle_of(c3, oracle_of(c2, oracle_of(c1, psi)))
+        results["resident"] = float(np.max(np.abs(sd.gather_tensor(sh).numpy() - want)))
+        sd.canonicalize(sh)
+        assert set(sh.global_qubits) == set(range(world.bit_length() - 1))
+        assert list(sh.local_qubits) == sorted(sh.local_qubits)
+        results["canonical"] = float(np.max(np.abs(sd.gather_tensor(sh).numpy() - want)))
         with open(os.path.join(out_dir, f"r{rank}.json"), "w") as f:
             json.dump(results, f)
     finally:
