@@ -78,6 +78,10 @@ ep = sd.plan(c, world)
 nv, _ = bench._time_exchanges(sd, HostStagedComm(), sd.CudaBackend(q.Precision.F64), q.Precision.F64, n, ep,
                               (1 << (n - (world.bit_length() - 1))) * 16, reps=2)
 wl = bench._dist_adiabatic(q, sd, HostStagedComm(), n, world, steps=2)
+wg = bench._dist_grid(q, sd, HostStagedComm(), n, world, q.Precision.F64, cycles=4)
+if rank == 0:
+    print("grid workload:", wg, flush=True)
+    worst = worst if "value" in wg else 1.0
 if rank == 0:
     print("exchange timing:", nv, flush=True)
     print("adiabatic step workload:", wl, flush=True)
