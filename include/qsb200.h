@@ -116,6 +116,12 @@ int qsb_jit_available(const char* nvrtc_path);
 /* Compile CUDA C++ `source` for sm_100a and return the CUfunction `name` in *func_out. */
 int qsb_jit_compile(const char* source, const char* name, const char* nvrtc_path, void** func_out,
                     char* log_out, size_t log_cap);
+/* qsb_jit_compile that also copies the compiled cubin into cubin_out (when it fits cubin_cap;
+ * *cubin_size gets its size either way), for an on-disk kernel cache. */
+int qsb_jit_compile_cubin(const char* source, const char* name, const char* nvrtc_path, void** func_out,
+                          char* log_out, size_t log_cap, void* cubin_out, size_t cubin_cap, size_t* cubin_size);
+/* Load a cubin produced by qsb_jit_compile_cubin (same library build) and return `name`. */
+int qsb_jit_load(const void* cubin, const char* name, void** func_out);
 /* Launch a specialised pass kernel over `n_tiles` tiles.  `tma_desc` describes the state as the
  * rank-5 tensor the kernel's tile loads address (15 words: rank, global dims[5], byte strides of
  * dims 1..4, box dims[5]; jit.py tma_plan).  `tables` (doubles, staged to the device) are the

@@ -65,6 +65,9 @@ SIGNATURES = {
     "qsb_sample": (_c_int, [_c_void_p, _c_u64, _c_u64, _c_u64, _c_u64, _c_u64, _c_u64, _c_void_p, _c_void_p]),
     "qsb_jit_available": (_c_int, [ctypes.c_char_p]),
     "qsb_jit_compile": (_c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _c_void_p, _c_void_p, _c_size_t]),
+    "qsb_jit_compile_cubin": (_c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _c_void_p, _c_void_p,
+                                       _c_size_t, _c_void_p, _c_size_t, _c_void_p]),
+    "qsb_jit_load": (_c_int, [_c_void_p, ctypes.c_char_p, _c_void_p]),
     "qsb_jit_run_pass": (
         _c_int,
         [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_u64, _c_void_p, _c_i64, _c_void_p, _c_i64, _c_int, _c_int,

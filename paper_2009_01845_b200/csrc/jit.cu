@@ -97,6 +97,12 @@ extern "C" int qsb_jit_available(const char* nvrtc_path) {
 // Compile `source` (CUDA C++) with NVRTC for sm_100a and return the CUfunction `name`.
 extern "C" int qsb_jit_compile(const char* source, const char* name, const char* nvrtc_path, void** func_out,
                                char* log_out, size_t log_cap) {
+  return qsb_jit_compile_cubin(source, name, nvrtc_path, func_out, log_out, log_cap, nullptr, 0, nullptr);
+}
+
+extern "C" int qsb_jit_compile_cubin(const char* source, const char* name, const char* nvrtc_path, void** func_out,
+                                     char* log_out, size_t log_cap, void* cubin_out, size_t cubin_cap,
+                                     size_t* cubin_size) {
   jit::Nvrtc* nv = jit::nvrtc(nvrtc_path);
   jit::Driver* dr = jit::driver();
   if (!nv || !dr) {
@@ -134,9 +140,24 @@ extern "C" int qsb_jit_compile(const char* source, const char* name, const char*
   char* cubin = new char[cs];
   nv->cubin(prog, cubin);
   nv->destroy(&prog);
+  if (cubin_out) {  // hand the image to the caller's on-disk cache
+    if (cubin_size) *cubin_size = cs;
+    if (cs <= cubin_cap) memcpy(cubin_out, cubin, cs);
+  }
+  const int st = qsb_jit_load(cubin, name, func_out);
+  delete[] cubin;
+  return st;
+}
+
+extern "C" int qsb_jit_load(const void* cubin, const char* name, void** func_out) {
+  jit::Driver* dr = jit::driver();
+  if (!dr) {
+    set_error("qsb_jit_load: the CUDA driver API is unavailable");
+    return QSB_ERR_CUDA;
+  }
+  cudaFree(nullptr);  // the runtime's primary context current on this thread
   CUmodule mod = nullptr;
   CUresult r = dr->load(&mod, cubin);
-  delete[] cubin;
   if (r != CUDA_SUCCESS) {
     set_error("cuModuleLoadData failed (%d)", (int)r);
     return QSB_ERR_CUDA;

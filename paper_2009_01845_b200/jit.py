@@ -991,6 +991,54 @@ def smem_bytes(stage_bytes: int, n_coeffs=MAX_COEFFS, alias: bool = False) -> in
     return struct_bytes + 8 * n_coeffs + 128
 
 
+def _disk_cache_dir():
+    """On-disk cubin cache (QSB_JIT_CACHE_DIR; default ~/.cache/qsb200; QSB_JIT_CACHE_DIR= (empty)
+    disables).  Purely an optimisation: every read is checked and a miss recompiles."""
+    d = os.environ.get("QSB_JIT_CACHE_DIR")
+    if d is None:
+        d = os.path.join(os.path.expanduser("~"), ".cache", "qsb200")
+    if not d:
+        return None
+    tag = f"abi{int(nat.lib().qsb_abi_version())}-{os.path.basename(_nvrtc_path())}-sm100a"
+    return os.path.join(d, "jit-" + tag)
+
+
+def _load_or_compile(src: str, name: str) -> int:
+    """CUfunction of `name` from the source: the disk cache when it holds this exact source's
+    cubin, else NVRTC (and the cubin is stored for the next process)."""
+    lib = nat.lib()
+    fn = ctypes.c_void_p()
+    digest = hashlib.sha256(src.encode()).hexdigest()
+    ddir = _disk_cache_dir()
+    path = os.path.join(ddir, f"{name}-{digest[:32]}.cubin") if ddir else None
+    if path and os.path.exists(path):
+        try:
+            with open(path, "rb") as f:
+                blob = f.read()
+            if blob and lib.qsb_jit_load(blob, name.encode(), ctypes.byref(fn)) == 0:
+                return fn.value
+        except OSError:
+            pass
+    log = ctypes.create_string_buffer(1 << 16)
+    cap = 8 << 20
+    cubin = ctypes.create_string_buffer(cap) if path else None
+    size = ctypes.c_size_t(0)
+    rc = lib.qsb_jit_compile_cubin(src.encode(), name.encode(), _nvrtc_path().encode(), ctypes.byref(fn), log,
+                                   len(log), cubin, cap if path else 0, ctypes.byref(size))
+    if rc != 0:
+        raise RuntimeError(f"NVRTC failed: {log.value.decode(errors='replace')[:2000]}")
+    if path and 0 < size.value <= cap:
+        try:
+            os.makedirs(ddir, exist_ok=True)
+            tmp = f"{path}.{os.getpid()}.{threading.get_ident()}.tmp"
+            with open(tmp, "wb") as f:
+                f.write(cubin.raw[:size.value])
+            os.replace(tmp, path)
+        except OSError:
+            pass
+    return fn.value
+
+
 _WORDS_CACHE: dict = {}  # (dtype, program bytes) -> compile_words result: rebuilt identical circuits skip codegen
 _WORDS_CACHE_MAX = 256
 
@@ -1023,18 +1071,12 @@ def _compile_words(words, dtype):
         hit = _cache.get(src)
     if hit is None:
         # NVRTC + module load outside the lock: passes of one plan compile concurrently
-        lib = nat.lib()
-        fn = ctypes.c_void_p()
-        log = ctypes.create_string_buffer(1 << 16)
-        rc = lib.qsb_jit_compile(src.encode(), name.encode(), _nvrtc_path().encode(), ctypes.byref(fn), log,
-                                 len(log))
-        if rc != 0:
-            raise RuntimeError(f"NVRTC failed: {log.value.decode(errors='replace')[:2000]}")
+        fn = _load_or_compile(src, name)
         K, nreg = int(words[2]), int(words[3])
         amp = 16 if dtype == nat.QSB_C128 else 8
         stage_amps = 1 << (K - 1 if (1 << K) * amp > 65536 else K)
         fresh = _Compiled()
-        fresh.func = fn.value
+        fresh.func = fn
         fresh.name = name
         alias = (1 << K) * amp == 65536 and ctas_per_sm(1 << (K - nreg)) == 2
         fresh.smem = smem_bytes(stage_amps * amp, len(tables), alias)

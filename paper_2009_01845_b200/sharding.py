@@ -158,6 +158,12 @@ class CudaBackend:
 
         if not ngates:
             return shard
+        if shard.numel() * shard.element_size() <= engine.GRID_BATCH_MAX_STATE_BYTES:
+            # small shards: one batched launch per 64 gates, no planning or kernel specialisation
+            # (every step of an evolution brings new coefficients and often new layouts)
+            engine._apply_gate_batch(shard.data_ptr(), n_local, self.dtype, engine.pack_gate_batch(ngates),
+                                     nat.stream_ptr())
+            return shard
         # out-of-place passes (folded SWAPs) need one more shard-sized buffer
         allow_ext = engine.scratch_fits(shard.numel() * shard.element_size())
         key = (allow_ext,) + tuple((g.kind, g.targets, g.controls, g.index,
