@@ -81,6 +81,8 @@ def _apply_gate_step(ptr, n, dtype, g, stream):
 # ~64 MB) cost less than planning the list into fused passes on the host (10-50 ms).
 BATCH_MAX_STATE_BYTES = 131072
 GRID_BATCH_MAX_STATE_BYTES = 256 << 20
+# QSB_FIRST_RUN_BATCH=0: plan mid-size gate lists into fused passes from their first run
+FIRST_RUN_BATCH = os.environ.get("QSB_FIRST_RUN_BATCH", "1") != "0"
 
 
 def _gate_matrix_and_class(g):
@@ -279,7 +281,7 @@ def run_gates(state, specs, fuse: bool | None = None, scratch_holder: dict | Non
     n, precision = state.n_qubits, state.precision
     nbytes = state.n_amps * precision.itemsize
     small = nbytes <= BATCH_MAX_STATE_BYTES
-    if small or (fuse_ and nbytes <= GRID_BATCH_MAX_STATE_BYTES):
+    if small or (fuse_ and FIRST_RUN_BATCH and nbytes <= GRID_BATCH_MAX_STATE_BYTES):
         planned = (not small and plan_cache is not None
                    and _plan_key(n, precision.qsb_dtype, fuse_, scratch_fits(nbytes), specs) in plan_cache)
         if not planned:

@@ -158,7 +158,7 @@ class CudaBackend:
 
         if not ngates:
             return shard
-        if shard.numel() * shard.element_size() <= engine.GRID_BATCH_MAX_STATE_BYTES:
+        if engine.FIRST_RUN_BATCH and shard.numel() * shard.element_size() <= engine.GRID_BATCH_MAX_STATE_BYTES:
             # small shards: one batched launch per 64 gates, no planning or kernel specialisation
             # (every step of an evolution brings new coefficients and often new layouts)
             engine._apply_gate_batch(shard.data_ptr(), n_local, self.dtype, engine.pack_gate_batch(ngates),

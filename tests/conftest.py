@@ -44,3 +44,13 @@ def circuit_from_json(text):
     from paper_2009_01845_b200.circuit import circuit_from_dict
 
     return circuit_from_dict(json.loads(str(text)))
+
+
+@pytest.fixture(params=["batched", "planned"])
+def mode(request, monkeypatch):
+    """Run a parity test through both execution paths of a first Circuit.execute on a mid-size
+    state: the grid-synchronised batch (default) and planned fused passes (specialised kernels)."""
+    from paper_2009_01845_b200 import engine
+
+    monkeypatch.setattr(engine, "FIRST_RUN_BATCH", request.param == "batched")
+    return request.param

@@ -115,7 +115,7 @@ def test_states_basics(cuda):
 
 # ---------------------------------------------------------------- circuits
 @pytest.mark.parametrize("fuse", [False, True])
-def test_random_circuits_golden(cuda, fuse):
+def test_random_circuits_golden(cuda, fuse, mode):
     g = golden("random_circuits")
     for i, text in enumerate(g["circuits"]):
         c = circuit_from_json(text)
@@ -125,7 +125,7 @@ def test_random_circuits_golden(cuda, fuse):
 
 @pytest.mark.parametrize("n", [10, 14])
 @pytest.mark.parametrize("fuse", [False, True])
-def test_qft_golden(cuda, n, fuse):
+def test_qft_golden(cuda, n, fuse, mode):
     import paper_2009_01845_b200 as q
 
     g = golden("qft")
@@ -140,7 +140,7 @@ def test_qft_golden(cuda, n, fuse):
 
 
 @pytest.mark.parametrize("n", [18, 22])
-def test_qft_analytic_dft_column(cuda, n):
+def test_qft_analytic_dft_column(cuda, n, mode):
     import paper_2009_01845_b200 as q
 
     k = int(np.random.default_rng(n).integers(1 << n))
@@ -153,7 +153,7 @@ def test_qft_analytic_dft_column(cuda, n):
 @pytest.mark.parametrize("n", [10, 14])
 @pytest.mark.parametrize("fused_layers", [False, True])
 @pytest.mark.parametrize("fuse", [False, True])
-def test_variational_golden(cuda, n, fused_layers, fuse):
+def test_variational_golden(cuda, n, fused_layers, fuse, mode):
     import paper_2009_01845_b200 as q
 
     g = golden("variational")
@@ -163,7 +163,7 @@ def test_variational_golden(cuda, n, fused_layers, fuse):
     assert max_abs(got32, g[f"f32_{n}_{int(fused_layers)}"]) <= TOL32
 
 
-def test_grid_supremacy_golden(cuda):
+def test_grid_supremacy_golden(cuda, mode):
     g = golden("grid15")
     c = circuit_from_json(g["circuit"])
     for fuse in (False, True):
@@ -184,7 +184,7 @@ def test_callbacks_split_execution(cuda):
     assert abs(cb.records[0] - 1 / math.sqrt(2)) < 1e-12 and abs(cb.records[1] - 0.5) < 1e-12
 
 
-def test_execute_copies_initial(cuda):
+def test_execute_copies_initial(cuda, mode):
     import paper_2009_01845_b200 as q
 
     init = _sv(np.random.default_rng(5).standard_normal(1 << 14) + 0j)
@@ -293,7 +293,7 @@ def test_large_sample_converges(cuda):
 
 # ---------------------------------------------------------------- size-independent properties
 @pytest.mark.parametrize("n", [24, 26])
-def test_qft_inverse_round_trip_and_norm(cuda, n):
+def test_qft_inverse_round_trip_and_norm(cuda, n, mode):
     import paper_2009_01845_b200 as q
 
     rng = np.random.default_rng(n)
@@ -307,7 +307,7 @@ def test_qft_inverse_round_trip_and_norm(cuda, n):
     assert max_abs(back.amplitudes, psi) <= 1e-12
 
 
-def test_fused_equals_unfused_random_large(cuda):
+def test_fused_equals_unfused_random_large(cuda, mode):
     import paper_2009_01845_b200 as q
 
     n = 20

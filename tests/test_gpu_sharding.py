@@ -19,7 +19,7 @@ def _sv(a):
 
 
 @pytest.mark.parametrize("shards", [2, 4, 8])
-def test_sharded_random_circuits_golden(cuda, shards):
+def test_sharded_random_circuits_golden(cuda, shards, mode):
     from conftest import circuit_from_json
     import paper_2009_01845_b200 as q
 
@@ -31,7 +31,7 @@ def test_sharded_random_circuits_golden(cuda, shards):
 
 
 @pytest.mark.parametrize("shards", [2, 4, 8])
-def test_sharded_qft_variational(cuda, shards):
+def test_sharded_qft_variational(cuda, shards, mode):
     import paper_2009_01845_b200 as q
 
     gq = golden("qft")
@@ -43,7 +43,7 @@ def test_sharded_qft_variational(cuda, shards):
     assert max_abs(q.execute_sharded(c, shards).amplitudes, gv["f64_14_1"]) <= 1e-12
 
 
-def test_sharded_equals_unsharded_large(cuda):
+def test_sharded_equals_unsharded_large(cuda, mode):
     import paper_2009_01845_b200 as q
 
     n = 22
@@ -56,7 +56,7 @@ def test_sharded_equals_unsharded_large(cuda):
         assert max_abs(a, b) <= 1e-12
 
 
-def test_sharded_trotter_step(cuda):
+def test_sharded_trotter_step(cuda, mode):
     import paper_2009_01845_b200 as q
 
     g = golden("adiabatic")
