@@ -466,9 +466,12 @@ class _Gen:
                                           for c in range(d)))
             for k, (r, _) in enumerate(diag):
                 self.emit(f"        ea = fma(PV({dci + k}), fma(r{r}, r{r}, i{r} * i{r}), ea);")
-            for k, (r, c, _, _) in enumerate(offs):
-                self.emit(f"        {{ const double zr = fma(r{r}, r{c}, i{r} * i{c}), zi = fma(r{r}, i{c}, -(i{r} * r{c}));"
-                          f" ea = fma(PV({oci + 2 * k}), zr, ea); ea = fma(PV({oci + 2 * k + 1}), zi, ea); }}")
+            for k, (r, c, ar, bi) in enumerate(offs):
+                # real (imaginary) coupling only: the other half of z is never formed
+                if ar != 0.0:
+                    self.emit(f"        ea = fma(PV({oci + 2 * k}), fma(r{r}, r{c}, i{r} * i{c}), ea);")
+                if bi != 0.0:
+                    self.emit(f"        ea = fma(PV({oci + 2 * k + 1}), fma(r{r}, i{c}, -(i{r} * r{c})), ea);")
             self.emit("      }")
         self.emit("    }")
 
