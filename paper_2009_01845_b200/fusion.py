@@ -76,6 +76,8 @@ GEOMETRY_JIT_K11 = {nat.QSB_C128: TileGeometry(11, 3, 4, 4), nat.QSB_C64: TileGe
 # the other's loads and layout changes.  Measured (n = 30): variational 101 -> 94 ms, Trotter
 # step 62 -> 58 ms, grid 366 -> 355 ms; QFT passes (no dense 2-qubit gates) keep the default,
 # where this geometry was slower (22.6 -> 25.1 ms).
+# (c64 has no such variant: 128 consumers x 64 amplitudes, two CTAs per SM, measured variational-30
+# 44.7 -> 48.2 ms: fewer layout changes, but twice the straight-line code per thread)
 GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 5)}
 _GEO_ENV = os.environ.get("QSB_JIT_GEOMETRY", "")
 if _GEO_ENV == "wide":
