@@ -133,11 +133,17 @@ def _expectation_passes(bit_terms, state):
     from . import engine, jit
     from .fusion import plan_expectation
 
+    from .fusion import TileGeometry
+
     n = state.n_qubits
     dtype = state.precision.qsb_dtype
     geo = engine.default_geometry(dtype)
-    if not jit.available() or n < geo.K + 1 or geo.halves or dtype != nat.QSB_C128:
-        return None  # complex64 states keep the per-term kernel (double math on 32 amplitudes spills)
+    if dtype == nat.QSB_C64 and not geo.halves:
+        # complex64: 512 consumers x 16 amplitudes (the accumulation is in double; 32 amplitudes
+        # per thread would spill)
+        geo = TileGeometry(geo.K, geo.G, geo.L, geo.nreg - 1)
+    if not jit.available() or n < geo.K + 1 or geo.halves:
+        return None
     key = (n, dtype, geo, tuple((tuple(b), np.asarray(m).tobytes()) for b, m in bit_terms))
     progs = _EXPECT_CACHE.get(key)
     if progs is None:

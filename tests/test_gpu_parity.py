@@ -674,3 +674,27 @@ def test_concurrent_small_executes_from_threads(cuda):
     assert not errors, errors
     for g, w in zip(got, want):
         assert np.array_equal(g, w)
+
+
+def test_expectation_fused_passes_complex64(cuda):
+    """complex64 states: fused read-only expectation passes (double accumulation) = numpy."""
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200 import hamiltonians as hm
+
+    n = 16
+    rng = np.random.default_rng(6)
+    psi = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)).astype(np.complex64)
+    psi /= np.linalg.norm(psi)
+    st = q.from_amplitudes(psi)
+    h = q.combine(q.build_x(n), 0.4, q.build_tfim(n, 1.0), 0.6)
+    p64 = psi.astype(np.complex128)
+    want = 0.0
+    for qs, m in h.terms:
+        t = p64.copy()
+        ov.apply_matrix(t, n, qs, m)
+        want += np.vdot(p64, t).real
+    bits = [(tuple(n - 1 - x for x in qs), m) for qs, m in hm._fold_single_terms(h.terms)]
+    fused = hm._expectation_passes(bits, st)
+    assert fused is not None
+    assert abs(fused - want) <= 1e-9 * max(1.0, abs(want))
+    assert abs(q.expectation(h, st) - want) <= 1e-9 * max(1.0, abs(want))
