@@ -69,11 +69,28 @@ __device__ __forceinline__ double np_pairwise_leaf(const double* a, int L) {
 
 // leaf sums of 128-element blocks (rows longer than 128 are power-of-two long, so numpy's
 // recursion splits them into a perfect binary tree of 128-element leaves)
+// Four leaves per warp: lane 8g + j keeps numpy's accumulator r[j] of leaf g (r[j] = a[j] +
+// a[j+8] + ... in order), so every load instruction reads four 64-byte runs (one thread per
+// leaf strided its loads 1 KB apart and re-read each sector ~3x from DRAM); the eight
+// accumulators then combine as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) through xor shuffles
+// (IEEE addition is commutative, so each pair sums to the same bits on both lanes).
 __global__ void __launch_bounds__(kMT) k_leaf128(const double* __restrict__ p, uint64_t n_leaves,
                                                  double* __restrict__ out) {
-  const uint64_t stride = (uint64_t)gridDim.x * kMT;
-  for (uint64_t l = (uint64_t)blockIdx.x * kMT + threadIdx.x; l < n_leaves; l += stride)
-    out[l] = np_pairwise_leaf(p + l * 128, 128);
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 3, j = lane & 7;
+  const uint64_t warps = (uint64_t)gridDim.x * (kMT / 32);
+  for (uint64_t w = (uint64_t)blockIdx.x * (kMT / 32) + (threadIdx.x >> 5); w * 4 < n_leaves; w += warps) {
+    const uint64_t leaf = w * 4 + g;
+    const bool valid = leaf < n_leaves;
+    const double* a = p + leaf * 128;
+    double r = valid ? a[j] : 0.0;
+#pragma unroll
+    for (int i = 8; i < 128; i += 8) r = __dadd_rn(r, valid ? a[i + j] : 0.0);
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    if (valid && j == 0) out[leaf] = r;
+  }
 }
 
 // one level of the pairwise tree: out[i] = in[2i] + in[2i+1]
