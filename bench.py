@@ -491,14 +491,14 @@ def _dist_adiabatic(q, sd, comm, n, world, steps=4):
 
 
 def _dist_grid(q, sd, comm, n, world, prec, cycles=20):
-    """BASELINE config 4 at this scale: the supremacy-style random circuit on a 3 x n/3 grid (1 x n
-    when 3 does not divide n), sharded with the reference's reshuffle plan; device time of one
+    """BASELINE config 4 at this scale: the supremacy-style random circuit on a 3 x n/3 grid (2 x n/2
+    or 1 x n when 3 does not divide n), sharded with the reference's reshuffle plan; device time of one
     circuit after a warm-up run, max over ranks."""
     import torch
     import torch.distributed as dist
 
     try:
-        rows = 3 if n % 3 == 0 else 1
+        rows = 3 if n % 3 == 0 else (2 if n % 2 == 0 else 1)
         circuit = q.random_grid_circuit(rows, n // rows, cycles, 42)
         exec_plan = sd.plan(circuit, world)
         cache: dict = {}
