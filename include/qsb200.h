@@ -155,6 +155,11 @@ int qsb_probabilities(const void* amps, uint64_t n_amps, int dtype, double* prob
  * `scratch` holds qsb_marginal_scratch_doubles(n_bits, k) doubles. */
 int qsb_marginal(const double* probs, int n_bits, int k, const int* kept, double* out,
                  double* scratch, void* stream);
+/* qsb_marginal computed straight from the amplitudes (no 2^n probability array): available when
+ * the 8 lowest bit positions are all reduced (numpy's 128-element leaves are then whole runs);
+ * otherwise QSB_ERR_ARG.  Same bits as qsb_probabilities + qsb_marginal. */
+int qsb_marginal_amps(const void* amps, int dtype, int n_bits, int k, const int* kept, double* out, double* scratch,
+                      void* stream);
 uint64_t qsb_marginal_scratch_doubles(int n_bits, int k);
 /* cum[i] = fl(cum[i-1] + p[i]) -- the exact result of numpy's strictly sequential np.cumsum,
  * computed in parallel (binade-integer scan), then cum /= cum[n-1]

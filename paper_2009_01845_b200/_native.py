@@ -57,6 +57,7 @@ SIGNATURES = {
     "qsb_probabilities": (_c_int, [_c_void_p, _c_u64, _c_int, _c_void_p, _c_void_p]),
     "qsb_marginal": (_c_int, [_c_void_p, _c_int, _c_int, _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "qsb_marginal_scratch_doubles": (_c_u64, [_c_int, _c_int]),
+    "qsb_marginal_amps": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "qsb_cumsum_normalized": (_c_int, [_c_void_p, _c_u64, _c_void_p, _c_void_p, _c_size_t, _c_void_p]),
     "qsb_cumsum_scratch_bytes": (_c_size_t, [_c_u64]),
     "qsb_cumsum": (_c_int, [_c_void_p, _c_u64, _c_void_p, _c_void_p, _c_size_t, _c_int, _c_void_p]),

@@ -93,6 +93,39 @@ __global__ void __launch_bounds__(kMT) k_leaf128(const double* __restrict__ p, u
   }
 }
 
+// k_leaf128 straight from the amplitudes: p = numpy's |z|^2 formed in registers (no 2^n
+// probability array written and read back), then the same warp-cooperative leaf sums.
+template <typename R>
+__global__ void __launch_bounds__(kMT) k_leaf128_amps(const cplx<R>* __restrict__ amps, uint64_t n_leaves,
+                                                      double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 3, j = lane & 7;
+  const uint64_t warps = (uint64_t)gridDim.x * (kMT / 32);
+  for (uint64_t w = (uint64_t)blockIdx.x * (kMT / 32) + (threadIdx.x >> 5); w * 4 < n_leaves; w += warps) {
+    const uint64_t leaf = w * 4 + g;
+    const bool valid = leaf < n_leaves;
+    const cplx<R>* a = amps + leaf * 128;
+    double r = 0.0;
+    if (valid) {
+      const cplx<R> v = a[j];
+      r = np_abs2((double)v.x, (double)v.y);
+    }
+#pragma unroll
+    for (int i = 8; i < 128; i += 8) {
+      double x = 0.0;
+      if (valid) {
+        const cplx<R> v = a[i + j];
+        x = np_abs2((double)v.x, (double)v.y);
+      }
+      r = __dadd_rn(r, x);
+    }
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+    r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+    if (valid && j == 0) out[leaf] = r;
+  }
+}
+
 // one level of the pairwise tree: out[i] = in[2i] + in[2i+1]
 __global__ void __launch_bounds__(kMT) k_pair_level(const double* __restrict__ in, uint64_t n_out,
                                                     double* __restrict__ out) {
@@ -913,9 +946,25 @@ extern "C" uint64_t qsb_marginal_scratch_doubles(int n_bits, int k) {
   return (1ull << k) + (1ull << (n_bits - 1)) + 256;
 }
 
+static int marginal_impl(const double* probs, const void* amps, int dtype, int n_bits, int k, const int* kept,
+                         double* out, double* scratch, cudaStream_t st);
+
 extern "C" int qsb_marginal(const double* probs, int n_bits, int k, const int* kept, double* out, double* scratch,
                             void* stream) {
-  cudaStream_t st = as_stream(stream);
+  return marginal_impl(probs, nullptr, 0, n_bits, k, kept, out, scratch, as_stream(stream));
+}
+
+extern "C" int qsb_marginal_amps(const void* amps, int dtype, int n_bits, int k, const int* kept, double* out,
+                                 double* scratch, void* stream) {
+  if (dtype != QSB_C128 && dtype != QSB_C64) {
+    set_error("unknown dtype %d", dtype);
+    return QSB_ERR_ARG;
+  }
+  return marginal_impl(nullptr, amps, dtype, n_bits, k, kept, out, scratch, as_stream(stream));
+}
+
+static int marginal_impl(const double* probs, const void* amps, int dtype, int n_bits, int k, const int* kept,
+                         double* out, double* scratch, cudaStream_t st) {
   if (n_bits < 1 || n_bits > 40 || k < 1 || k > n_bits) {
     set_error("qsb_marginal: bad sizes (n=%d, k=%d)", n_bits, k);
     return QSB_ERR_SHAPE;
@@ -933,6 +982,14 @@ extern "C" int qsb_marginal(const double* probs, int n_bits, int k, const int* k
   const uint64_t n_keys = 1ull << k;
   const double* asc = scratch;  // 2^k, ascending kept-bit order
   double* work = scratch + n_keys;
+  if (amps) {  // the fused form exists for the leaf branch only: >= 8 low bits reduced
+    int r = 0;
+    while (r < n_bits && ((red >> r) & 1ull)) ++r;
+    if (r < 8) {
+      set_error("qsb_marginal_amps: needs the 8 lowest bits reduced (use qsb_probabilities + qsb_marginal)");
+      return QSB_ERR_ARG;
+    }
+  }
   if (red == 0) {
     asc = probs;
   } else if (red & 1ull) {
@@ -948,7 +1005,12 @@ extern "C" int qsb_marginal(const double* probs, int n_bits, int k, const int* k
       const uint64_t leaves = N / 128;
       double* a = work;
       double* b = work + leaves;
-      k_leaf128<<<grid_for(leaves), kMT, 0, st>>>(probs, leaves, a);
+      if (!amps)
+        k_leaf128<<<grid_for(leaves), kMT, 0, st>>>(probs, leaves, a);
+      else if (dtype == QSB_C128)
+        k_leaf128_amps<double><<<grid_for(leaves), kMT, 0, st>>>(static_cast<const double2*>(amps), leaves, a);
+      else
+        k_leaf128_amps<float><<<grid_for(leaves), kMT, 0, st>>>(static_cast<const float2*>(amps), leaves, a);
       uint64_t cur = leaves;
       while (cur > rows) {
         k_pair_level<<<grid_for(cur / 2), kMT, 0, st>>>(a, cur / 2, b);

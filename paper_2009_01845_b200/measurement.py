@@ -72,12 +72,19 @@ def device_marginal(state, qubits):
     """Marginal distribution over `qubits` as a float64 CUDA tensor (length 2**len(qubits))."""
     qubits = _validate_qubits(state, qubits)
     n = state.n_qubits
-    probs = device_probabilities(state)
-    if qubits == tuple(range(n)):
-        return probs
     lib = nat.lib()
     k = len(qubits)
     kept = np.array([n - 1 - q for q in qubits], dtype=np.int32)
+    if k < n and int(kept.min()) >= 8:
+        # the 8 lowest bits are summed out: leaf sums straight from the amplitudes
+        out = _f64(1 << k)
+        scratch = _f64(int(lib.qsb_marginal_scratch_doubles(n, k)))
+        nat.check(lib.qsb_marginal_amps(state.data_ptr, state.precision.qsb_dtype, n, k, kept.ctypes.data,
+                                        out.data_ptr(), scratch.data_ptr(), nat.stream_ptr()), "marginal")
+        return out
+    probs = device_probabilities(state)
+    if qubits == tuple(range(n)):
+        return probs
     out = _f64(1 << k)
     scratch = _f64(int(lib.qsb_marginal_scratch_doubles(n, k)))
     nat.check(

@@ -698,3 +698,30 @@ def test_expectation_fused_passes_complex64(cuda):
     assert fused is not None
     assert abs(fused - want) <= 1e-9 * max(1.0, abs(want))
     assert abs(q.expectation(h, st) - want) <= 1e-9 * max(1.0, abs(want))
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_marginal_from_amplitudes_equals_probability_path(cuda, prec):
+    """qsb_marginal_amps (leaf sums formed from the amplitudes) = qsb_probabilities +
+    qsb_marginal, bit for bit, for subsets that leave the 8 lowest bits reduced."""
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200 import _native as nat
+    from paper_2009_01845_b200 import measurement as ms
+
+    n = 20
+    rng = np.random.default_rng(12)
+    psi = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)) / math.sqrt(2 << n)
+    st = q.from_amplitudes(psi, precision=q.Precision(prec))
+    probs = ms.device_probabilities(st)
+    for qubits in ((0,), (3, 1), (11, 0, 5), tuple(range(12)), (7, 2, 9, 4)):
+        fused = ms.device_marginal(st, qubits).cpu().numpy()
+        k = len(qubits)
+        kept = np.array([n - 1 - x for x in qubits], dtype=np.int32)
+        out = ms._f64(1 << k)
+        scratch = ms._f64(int(nat.lib().qsb_marginal_scratch_doubles(n, k)))
+        nat.check(nat.lib().qsb_marginal(probs.data_ptr(), n, k, kept.ctypes.data, out.data_ptr(), scratch.data_ptr(),
+                                         nat.stream_ptr()))
+        assert np.array_equal(fused, out.cpu().numpy()), qubits
+        ref = ov.marginal(st.amplitudes, n, qubits) if hasattr(ov, "marginal") else None
+        if ref is not None:
+            assert np.array_equal(fused, ref), qubits
