@@ -79,6 +79,12 @@ GEOMETRY_JIT_K11 = {nat.QSB_C128: TileGeometry(11, 3, 4, 4), nat.QSB_C64: TileGe
 # (c64 has no such variant: 128 consumers x 64 amplitudes, two CTAs per SM, measured variational-30
 # 44.7 -> 48.2 ms: fewer layout changes, but twice the straight-line code per thread)
 GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 5)}
+# ... unless the pass's straight-line gate code per thread (FP operations per amplitude x 32
+# amplitudes) would outgrow the instruction cache: measured on grid-30, the two passes of 16
+# dense complex 4x4 gates (~8,200 FP instructions per thread) ran 21.5 / 32.0 ms in that geometry
+# and 19.0 / 20.0 ms in the default one, while variational's 16 real 4x4 gates (~4,100) and the
+# grid's 10-gate passes (~5,100) are faster in it
+MAX_2Q_CODE = 6500
 _GEO_ENV = os.environ.get("QSB_JIT_GEOMETRY", "")
 if _GEO_ENV == "wide":
     GEOMETRY_JIT = GEOMETRY_JIT_WIDE
@@ -464,7 +470,9 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
         else:
             pgeo = geo
             if geo == GEOMETRY_JIT[dtype] and dtype in GEOMETRY_JIT_2Q and any(g.kind == "g2" for g in absorbed):
-                pgeo = GEOMETRY_JIT_2Q[dtype]
+                code = sum(matrix_cost(g.matrix) for g in absorbed if g.kind in ("g1", "g2"))
+                if code * GEOMETRY_JIT_2Q[dtype].A <= MAX_2Q_CODE:
+                    pgeo = GEOMETRY_JIT_2Q[dtype]
             words, info = compile_pass(absorbed, T, n_qubits, dtype, pgeo, minimal=MINIMAL_LAYOUT_CHANGES)
             plan.steps.append(PassStep(words, absorbed, tuple(sorted(T)), info["ext_perm"],
                                        info["transposes"], info["pivots"]))
