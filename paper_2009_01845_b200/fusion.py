@@ -84,7 +84,7 @@ GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 5)}
 # dense complex 4x4 gates (~8,200 FP instructions per thread) ran 21.5 / 32.0 ms in that geometry
 # and 19.0 / 20.0 ms in the default one, while variational's 16 real 4x4 gates (~4,100) and the
 # grid's 10-gate passes (~5,100) are faster in it
-MAX_2Q_CODE = 6500
+MAX_2Q_CODE = int(os.environ.get("QSB_MAX_2Q_CODE", "6500"))
 _GEO_ENV = os.environ.get("QSB_JIT_GEOMETRY", "")
 if _GEO_ENV == "wide":
     GEOMETRY_JIT = GEOMETRY_JIT_WIDE
