@@ -20,10 +20,13 @@ plan = engine.plan_for_state(st, build(wl, n).queue)
 holder = {}
 engine.run_plan(st, plan, holder)
 torch.cuda.synchronize()
-evs = []
-engine.run_plan(st, plan, holder, events=evs)
-torch.cuda.synchronize()
-per = [a.elapsed_time(b) for a, b in evs]
+runs = []
+for _ in range(3):
+    evs = []
+    engine.run_plan(st, plan, holder, events=evs)
+    torch.cuda.synchronize()
+    runs.append([a.elapsed_time(b) for a, b in evs])
+per = [sorted(x)[1] for x in zip(*runs)]  # median of three
 ps = [s for s in plan.steps if isinstance(s, PassStep)]
 print(f"{wl}-{n} {prec.value}: {sum(per):.2f} ms in {len(ps)} passes")
 for x, s in zip(per, ps):
