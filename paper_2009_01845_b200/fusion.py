@@ -76,9 +76,10 @@ GEOMETRY_JIT_K11 = {nat.QSB_C128: TileGeometry(11, 3, 4, 4), nat.QSB_C64: TileGe
 # the other's loads and layout changes.  Measured (n = 30): variational 101 -> 94 ms, Trotter
 # step 62 -> 58 ms, grid 366 -> 355 ms; QFT passes (no dense 2-qubit gates) keep the default,
 # where this geometry was slower (22.6 -> 25.1 ms).
-# (c64 has no such variant: 128 consumers x 64 amplitudes, two CTAs per SM, measured variational-30
-# 44.7 -> 48.2 ms: fewer layout changes, but twice the straight-line code per thread)
-GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 5)}
+# c64 goes the other way: 512 consumers x 16 amplitudes (half the straight-line code per thread
+# of the default 256 x 32), measured variational-30 c64 44.7 -> 41.7 ms; 128 x 64 with two CTAs
+# per SM measured 48.2 ms
+GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 5), nat.QSB_C64: TileGeometry(13, 4, 5, 4)}
 # ... unless the pass's straight-line gate code per thread (FP operations per amplitude x 32
 # amplitudes) would outgrow the instruction cache: measured on grid-30, the two passes of 16
 # dense complex 4x4 gates (~8,200 FP instructions per thread) ran 21.5 / 32.0 ms in that geometry
