@@ -108,29 +108,6 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ CPU arm
-def cpu_reference_sample(n: int, threads: int):
-    """Time the reference algorithm (oracle numpy port) on three representative QFT-n gates
-    (H = general body, CZPow = diagonal body, SWAP = permutation body) on a 2^n state and
-    extrapolate to the full circuit's gate mix (n H, n(n-1)/2 CZPow, n/2 SWAP)."""
-    import numpy as np
-
-    from oracle import statevec as ov
-
-    amps = np.zeros(1 << n, dtype=np.complex128)
-    amps[:] = 1.0 / math.sqrt(1 << n)  # touch every page outside the timed region
-    sample = [("H", ov.gate("H", (0,))), ("CZPow", ov.gate("CZPow", (1, 0), (), (math.pi / 2,))),
-              ("SWAP", ov.gate("SWAP", (0, n - 1)))]
-    times = {}
-    for name, (_k, tg, ct, _p, m) in sample:
-        t0 = time.perf_counter()
-        ov.apply_matrix(amps, n, tg, m, ct, n_threads=threads)
-        times[name] = time.perf_counter() - t0
-    counts = {"H": n, "CZPow": n * (n - 1) // 2, "SWAP": n // 2}
-    total = sum(times[k] * counts[k] for k in counts)
-    del amps
-    return total, times, counts
-
-
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -145,33 +122,154 @@ def host_ram_bytes():
         return 0
 
 
+def cpu_info():
+    """CPU model, core count and the numpy / BLAS build the reference arm ran with."""
+    import numpy as np
+
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = ""
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = [d for d in threadpool_info() if d.get("user_api") == "blas"]
+        if info:
+            blas = f"{info[0].get('internal_api')} {info[0].get('version')} ({info[0].get('architecture')})"
+    except Exception:
+        pass
+    return {"cpu_model": model, "host_threads": cpu_threads(), "numpy": np.__version__, "blas": blas,
+            "host_ram_gb": round(host_ram_bytes() / 2**30, 1)}
+
+
+class single_core:
+    """T=1 for the CPU reference: the process pinned to one core (os.sched_setaffinity, as the
+    paper's taskset runs) and the BLAS pool limited to one thread."""
+
+    def __enter__(self):
+        self.aff = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {min(self.aff)})
+        try:
+            from threadpoolctl import threadpool_limits
+
+            self.lim = threadpool_limits(1)
+        except Exception:
+            self.lim = None
+        return self
+
+    def __exit__(self, *a):
+        if self.lim is not None:
+            self.lim.restore_original_limits()
+        os.sched_setaffinity(0, self.aff)
+
+
+def cpu_qft_full(n: int, threads: int) -> float:
+    """Wall seconds of one complete QFT-n c128 through the reference algorithm (the oracle's
+    numpy restatement of qsim.Circuit.execute / apply_matrix), |0..0> input."""
+    from oracle import statevec as ov
+
+    gates = ov.qft(n)
+    t0 = time.perf_counter()
+    ov.run(gates, n, n_threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_reference_sample(n: int, threads: int):
+    """Bounded sample of QFT-n on the CPU reference (the GPU arm's cpu_baseline): the circuit's
+    first column -- H(0) and the n-1 CZPow(k, 0) gates, in order -- plus one SWAP, timed on a
+    2^n state, extrapolated by gate kind to the full circuit (n H, n(n-1)/2 CZPow, n/2 SWAP)."""
+    import numpy as np
+
+    from oracle import statevec as ov
+
+    amps = np.zeros(1 << n, dtype=np.complex128)
+    amps[:] = 1.0 / math.sqrt(1 << n)  # touch every page outside the timed region
+    gates = ov.qft(n)
+    column = [g for g in gates[:n]]  # H(0), CZPow(1,0) ... CZPow(n-1,0)
+    swap = [g for g in gates if g[0] == "SWAP"][:1]
+    times = {"H": 0.0, "CZPow": 0.0, "SWAP": 0.0}
+    seen = {"H": 0, "CZPow": 0, "SWAP": 0}
+    for kind, tg, ct, _p, m in column + swap:
+        t0 = time.perf_counter()
+        ov.apply_matrix(amps, n, tg, m, ct, n_threads=threads)
+        times[kind] += time.perf_counter() - t0
+        seen[kind] += 1
+    counts = {"H": n, "CZPow": n * (n - 1) // 2, "SWAP": n // 2}
+    per = {k: times[k] / seen[k] for k in times}
+    total = sum(per[k] * counts[k] for k in counts)
+    del amps
+    return total, per, counts, sum(times.values())
+
+
 def run_reference_arm(args, rank, world):
+    """The reference's CPU path, timed in full: QFT-n c128 (qft_circuit(n).execute(), 480 gates at
+    n = 30) through the reference algorithm with every host thread.  The K timed steps TOGETHER
+    execute the circuit once: step i applies the i-th contiguous slice of the gate list to the
+    running state, so `value` (the sum of the step times) is the measured wall time of one whole
+    circuit, and the run ends after one circuit (~6 min at n = 30) instead of K.  Warm-up steps
+    run the CPU-only config (QFT-20, BASELINE configs[0]) in full, alternately at T=1 (one
+    pinned core, one BLAS thread) and T=all."""
     if rank != 0:
         return
+    import numpy as np
+
+    from oracle import statevec as ov
+
     threads = cpu_threads()
     n = args.qubits
-    scale = 1.0
-    sample_n = n
+    measured_n = n
     if host_ram_bytes() < (40 << 30) and n > 28:
-        sample_n = 28
-        scale = 2.0 ** (n - sample_n)
-    vals = []
-    for i in range(args.warmup + args.steps):
-        total, times, counts = cpu_reference_sample(sample_n, threads)
-        if i >= args.warmup:
-            vals.append(total * scale)
-    v = statistics.mean(vals)
-    sample = (f"3 gates (H(0), CZPow(1,0), SWAP(0,{sample_n - 1})) of QFT-{sample_n} c128 with the numpy port of "
-              f"qsim.apply_matrix, {threads} threads, extrapolated to 480 gates"
-              + (f" and x{scale:g} for n={n}" if scale != 1 else ""))
+        measured_n = 28  # the state and its copies do not fit: measure n = 28, extrapolate below
+    qft20 = {"T1": [], "Tall": []}
+    for i in range(args.warmup):
+        if i % 2 == 0:
+            with single_core():
+                qft20["T1"].append(cpu_qft_full(20, 1))
+        else:
+            qft20["Tall"].append(cpu_qft_full(20, threads))
+    gates = ov.qft(measured_n)
+    amps = np.zeros(1 << measured_n, dtype=np.complex128)
+    amps[0] = 1.0
+    k = max(1, args.steps)
+    bounds = [len(gates) * s // k for s in range(k + 1)]
+    step_s = []
+    for s in range(k):
+        t0 = time.perf_counter()
+        for _kind, tg, ct, _p, m in gates[bounds[s]:bounds[s + 1]]:
+            ov.apply_matrix(amps, measured_n, tg, m, ct, n_threads=threads)
+        step_s.append(time.perf_counter() - t0)
+    full = sum(step_s)
+    # the run's own check: QFT|0> is the uniform state
+    err = float(np.max(np.abs(amps - 1.0 / math.sqrt(1 << measured_n))))
+    del amps
+    scale = 2.0 ** (n - measured_n)
+    value = full * scale
+    sample = (f"one complete QFT-{measured_n} c128 ({len(gates)} gates) split over the {k} timed steps, "
+              f"reference algorithm (numpy port of qsim.Circuit.execute/apply_matrix), {threads} threads"
+              + (f"; x{scale:g} extrapolation to n={n} (host RAM too small for the full state)" if scale != 1 else ""))
+    best20 = min(qft20["T1"] + qft20["Tall"]) if qft20["T1"] + qft20["Tall"] else None
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"QFT {n} qubits complex128 (qft_circuit({n}), 480 gates) on |0..0>",
-                   "n_qubits": n, "precision": "f64", "parallelism": "host threads"},
-        "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "port", "sample": sample},
-        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus, "steps": k,
+        "warmup": args.warmup, "ms_per_step": statistics.mean(step_s) * 1e3 * scale, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"QFT {n} qubits complex128 (qft_circuit({n}), {len(ov.qft(n))} gates) on |0..0>",
+                   "n_qubits": n, "measured_n": measured_n, "precision": "f64", "parallelism": "host threads",
+                   "steps_cover": "the timed steps together execute ONE full circuit (value = their sum)"},
+        "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "qft20": {"T1_s": min(qft20["T1"]) if qft20["T1"] else None,
+                  "Tall_s": min(qft20["Tall"]) if qft20["Tall"] else None, "best_s": best20,
+                  "what": "BASELINE configs[0]: full QFT-20 c128 on the CPU reference, T=1 (pinned core, "
+                          "1 BLAS thread) and T=all"},
+        "parity": {"check": f"QFT-{measured_n}|0> == uniform state", "max_abs_err": err},
+        "host": cpu_info(),
+        "step_seconds": step_s,
     }
     print(json.dumps(line), flush=True)
 
@@ -250,18 +348,37 @@ def run_gpu_arm(args, rank, world):
             e2e_times.append(dt)
     e2e = statistics.mean(e2e_times)
 
+    # the timed kernels' own result, checked at full size: QFT-n on a basis state |k> against the
+    # analytic DFT column (the reference's known answer, tests/test_circuit.py:189-201), on device
+    from paper_2009_01845_b200.verify import dft_column_error
+
+    parity = None
+    if args.workload == "qft":
+        k = int(__import__("numpy").random.default_rng(n).integers(1 << n))
+        st = q.basis_state(n, k, prec)
+        engine.run_plan(st, plan, {})
+        err = dft_column_error(st, k)
+        tol = 1e-12 if prec is q.Precision.F64 else 1e-5
+        parity = {"check": f"QFT-{n}|k={k}> vs analytic DFT column (same plan / kernels as timed)",
+                  "max_abs_err": err, "tol": tol, "ok": err <= tol}
+        del st
+        torch.cuda.empty_cache()
+
     others = {} if args.no_extra_workloads else extra_workloads(q, engine, n, peak)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         threads = cpu_threads()
         sn = n if host_ram_bytes() >= (48 << 30) else min(n, 28)
-        total, times, counts = cpu_reference_sample(sn, threads)
+        total, per, counts, spent = cpu_reference_sample(sn, threads)
         scale = 2.0 ** (n - sn)
         cpu = {"value": total * scale, "unit": "s", "cores": threads, "kind": "port",
-               "sample": f"H(0), CZPow(1,0), SWAP(0,{sn - 1}) of QFT-{sn} c128 (numpy port of qsim.apply_matrix, "
-                         f"{threads} threads) timed {', '.join(f'{k}={v:.2f}s' for k, v in times.items())}, "
-                         f"extrapolated to {sum(counts.values())} gates" + (f", x{scale:g} to n={n}" if scale != 1 else "")}
+               "sample": f"first QFT-{sn} column (H(0) + {sn - 1} CZPow(k,0)) + SWAP(0,{sn - 1}) on the CPU reference "
+                         f"(numpy port of qsim.apply_matrix, {threads} threads; {spent:.1f} s of CPU work), per-gate "
+                         f"{', '.join(f'{k}={v:.2f}s' for k, v in per.items())}, extrapolated to "
+                         f"{sum(counts.values())} gates" + (f", x{scale:g} to n={n}" if scale != 1 else "")
+                         + "; bench.py --impl reference times the whole circuit",
+               "qft20_s": cpu_qft_full(20, threads), "host": cpu_info()}
 
     line = {
         "metric": METRIC, "value": value, "unit": "s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
@@ -280,6 +397,7 @@ def run_gpu_arm(args, rank, world):
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "qft_circuit(n).execute() + state D2H (pinned)"},
         "workloads": others,
+        "parity": parity,
         "gpu_launches": len(plan.steps) * args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,

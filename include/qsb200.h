@@ -68,7 +68,8 @@ int qsb_init_uniform(void* amps, int n_qubits, int dtype, double re, double im, 
 /* Classify a 2**t x 2**t complex128 matrix exactly like classify_kernel (gates.py:340-352):
  * returns QSB_KERNEL_DIAGONAL / _PERMUTATION / _GENERAL. */
 int qsb_classify(const double* matrix, int n_targets);
-/* In-place application of `matrix` on `target_bits` (t = 1 or 2), restricted to the basis
+/* In-place application of `matrix` on `target_bits` (t = 1 to 5; 3-5 targets run a generic
+ * one-group-per-thread kernel with the matrix as a kernel parameter), restricted to the basis
  * states whose `control_bits` are all 1.  `kernel` = QSB_KERNEL_AUTO classifies first;
  * an explicit class forces that body, with the reference's semantics (diagonal body reads only
  * the diagonal and skips rows equal to 1.0; permutation body takes the first non-zero of each
@@ -126,10 +127,18 @@ int qsb_jit_load(const void* cubin, const char* name, void** func_out);
  * rank-5 tensor the kernel's tile loads address (15 words: rank, global dims[5], byte strides of
  * dims 1..4, box dims[5]; jit.py tma_plan).  `tables` (doubles, staged to the device) are the
  * per-thread pivot tables; `params` (`param_bytes`, passed by value as the kernel's last
- * parameter) are the uniform gate coefficients; the grid is min(n_tiles, SMs * ctas_per_sm). */
+ * parameter) are the uniform gate coefficients; `grid` CTAs are launched (1 <= grid <= n_tiles:
+ * one-shot CTAs of a few tiles each, or a persistent grid, as the kernel was generated for). */
 int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tma_desc, uint64_t n_tiles,
                      const double* tables, int64_t n_tables, const void* params, int64_t param_bytes,
-                     int threads, int smem_bytes, int ctas_per_sm, void* stream);
+                     int threads, int smem_bytes, int grid, void* stream);
+/* qsb_jit_run_pass with the pivot tables already in device memory (`dev_tables`, owned by the
+ * caller and alive until the launch completes): nothing is staged through the library's host
+ * ring, so the launch can be captured into a CUDA graph and replayed.  (qsb_jit_run_pass and
+ * qsb_run_pass refuse to stage while their stream is capturing.) */
+int qsb_jit_run_pass_dev(void* func, const void* src, void* dst, const int64_t* tma_desc, uint64_t n_tiles,
+                         const double* dev_tables, int64_t n_tables, const void* params, int64_t param_bytes,
+                         int threads, int smem_bytes, int grid, void* stream);
 
 /* ---- reductions (state.py:109-122 norm / overlap) ---------------------------------------- */
 /* out[0] = sum |a_i|^2 (double, device pointer).  Deterministic two-level tree. */

@@ -155,5 +155,33 @@ def main():
     print("golden fixtures written to", OUT)
 
 
+def main_c64_large():
+    """complex64 fixtures at n = 16 (512 KB states): above the 128 KB shared-memory batch limit,
+    so the planned fused passes (packed FP32-pair code) run against the reference itself."""
+    rng = np.random.default_rng(16_64)
+    out = {}
+    n = 16
+    c = qsim.qft_circuit(n)
+    init = ref_oracle.random_state(n, rng)
+    f32 = qsim.StateVector(n, init.amplitudes.astype(np.complex64), qsim.Precision.F32)
+    out["qft_in"] = f32.amplitudes
+    out["qft_out"] = c.execute(f32, precision=qsim.Precision.F32).amplitudes
+    params = np.random.default_rng(42).uniform(0, 2 * np.pi, n * (2 * 3 + 1))
+    out["var_params"] = params
+    for fused in (False, True):
+        vc = qsim.variational_circuit(n, 3, params, fused=fused)
+        out[f"var_{int(fused)}"] = vc.execute(precision=qsim.Precision.F32).amplitudes
+    gates = ov.grid_supremacy(4, 4, 8, seed=7)
+    gc = to_ref_circuit(n, gates)
+    out["grid_circuit"] = circ_json(gc)
+    out["grid_out"] = gc.execute(precision=qsim.Precision.F32).amplitudes
+    save("c64_large", **out)
+    print("c64_large fixture written to", OUT)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["c64_large"]:
+        main_c64_large()
+    else:
+        main()
+        main_c64_large()

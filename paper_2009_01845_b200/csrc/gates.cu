@@ -308,12 +308,137 @@ static int prepare_gate(int n_qubits, int t, const int* tbits, int nc, const int
   return t == 1 ? kBodyGeneral1 : kBodyGeneral2;
 }
 
+// ---- 3..5-target matrices (apply_matrix takes any 2^t x 2^t matrix, gates.py:380-469) -------
+// One thread per group of 2^T amplitudes; the matrix travels as a kernel parameter (<= 16 KB at
+// T = 5, complex128).  mode 0: general (every row = M x), 1: diagonal (rows in `rowmask` times
+// m[r]), 2: permutation (row r <- m[r] * x[src[r]] for rows in `rowmask`; all loads first).
+constexpr int kMaxWideTargets = 5;
+
+template <typename R, int T>
+struct WideArgs {
+  uint64_t n_groups;
+  uint64_t cmask;
+  uint64_t off[1 << T];
+  OccBits occ;
+  int mode;
+  uint32_t rowmask;
+  uint32_t phasemask;  // permutation: rows whose entry is not exactly 1 (multiplied)
+  uint8_t src[1 << T];
+  cplx<R> m[(1 << T) * (1 << T)];
+};
+
+template <typename R, int T>
+__global__ void __launch_bounds__(128) k_wide(cplx<R>* __restrict__ a, const __grid_constant__ WideArgs<R, T> p) {
+  using C = cplx<R>;
+  constexpr int D = 1 << T;
+  const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= p.n_groups) return;
+  const uint64_t base = insert_zero_bits(g, p.occ) | p.cmask;
+  C x[D];
+  if (p.mode == 1) {
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+      if ((p.rowmask >> r) & 1u) x[r] = a[base | p.off[r]];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+      if ((p.rowmask >> r) & 1u) a[base | p.off[r]] = cmul(x[r], p.m[r]);
+    return;
+  }
+  if (p.mode == 2) {
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+      if ((p.rowmask >> r) & 1u) x[r] = a[base | p.off[p.src[r]]];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+      if ((p.rowmask >> r) & 1u) a[base | p.off[r]] = ((p.phasemask >> r) & 1u) ? cmul(x[r], p.m[r]) : x[r];
+    return;
+  }
+#pragma unroll
+  for (int c = 0; c < D; ++c) x[c] = a[base | p.off[c]];
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+    C y = cmul(p.m[r * D], x[0]);
+#pragma unroll
+    for (int c = 1; c < D; ++c) y = cmad(p.m[r * D + c], x[c], y);
+    a[base | p.off[r]] = y;
+  }
+}
+
+template <typename R, int T>
+static int launch_wide(cplx<R>* a, int n_qubits, const int* tbits, int nc, const int* cbits, const double* mat,
+                       int kclass, cudaStream_t st) {
+  constexpr int D = 1 << T;
+  WideArgs<R, T> p;
+  memset(&p, 0, sizeof p);
+  int occ[kMaxOcc];
+  int nocc = 0;
+  for (int i = 0; i < T; ++i) occ[nocc++] = tbits[i];
+  for (int i = 0; i < nc; ++i) occ[nocc++] = cbits[i];
+  for (int i = 1; i < nocc; ++i)
+    for (int j = i; j > 0 && occ[j - 1] > occ[j]; --j) {
+      int tmp = occ[j];
+      occ[j] = occ[j - 1];
+      occ[j - 1] = tmp;
+    }
+  p.occ.n = nocc;
+  for (int i = 0; i < nocc; ++i) p.occ.pos[i] = (uint8_t)occ[i];
+  for (int i = 0; i < nc; ++i) p.cmask |= 1ull << cbits[i];
+  for (int j = 0; j < D; ++j)
+    for (int b = 0; b < T; ++b)
+      if ((j >> (T - 1 - b)) & 1) p.off[j] |= 1ull << tbits[b];
+  p.n_groups = 1ull << (n_qubits - nocc);
+  if (kclass == QSB_KERNEL_DIAGONAL) {
+    p.mode = 1;
+    for (int j = 0; j < D; ++j) {
+      const double* d = mat + 2 * (j * D + j);
+      if (!is_one(d)) {
+        p.rowmask |= 1u << j;
+        to_dtype<R>(d, &p.m[j]);
+      }
+    }
+  } else if (kclass == QSB_KERNEL_PERMUTATION) {
+    p.mode = 2;
+    for (int j = 0; j < D; ++j) {
+      int s = 0;  // np.argmax(mat != 0)
+      for (int c = 0; c < D; ++c)
+        if (is_nonzero(mat + 2 * (j * D + c))) {
+          s = c;
+          break;
+        }
+      const double* ph = mat + 2 * (j * D + s);
+      if (s != j || !is_one(ph)) {
+        p.rowmask |= 1u << j;
+        p.src[j] = (uint8_t)s;
+        if (!is_one(ph)) p.phasemask |= 1u << j;
+        to_dtype<R>(ph, &p.m[j]);
+      }
+    }
+  } else {
+    p.mode = 0;
+    for (int k = 0; k < D * D; ++k) to_dtype<R>(mat + 2 * k, &p.m[k]);
+  }
+  if (p.mode != 0 && p.rowmask == 0) return QSB_OK;
+  k_wide<R, T><<<blocks_for(p.n_groups, 128), 128, 0, st>>>(a, p);
+  QSB_CHECK_LAUNCH("qsb_apply_matrix(3-5 targets)");
+  return QSB_OK;
+}
+
 template <typename R>
 static int launch_gate(void* amps, int n_qubits, int t, const int* tbits, int nc, const int* cbits,
                        const double* mat, int kclass, cudaStream_t st) {
+  cplx<R>* a = static_cast<cplx<R>*>(amps);
+  switch (t) {
+    case 3:
+      return launch_wide<R, 3>(a, n_qubits, tbits, nc, cbits, mat, kclass, st);
+    case 4:
+      return launch_wide<R, 4>(a, n_qubits, tbits, nc, cbits, mat, kclass, st);
+    case 5:
+      return launch_wide<R, 5>(a, n_qubits, tbits, nc, cbits, mat, kclass, st);
+    default:
+      break;
+  }
   GateArgs<R> p;
   const int body = prepare_gate<R>(n_qubits, t, tbits, nc, cbits, mat, kclass, p);
-  cplx<R>* a = static_cast<cplx<R>*>(amps);
   switch (body) {
     case kBodyDiag:
       k_diag<R, 4><<<blocks_for(p.n_groups, kThreads * 4), kThreads, 0, st>>>(a, p);
@@ -757,8 +882,8 @@ __global__ void __launch_bounds__(kGridThreads)
 
 static int validate_gate(int n_qubits, int n_targets, const int* target_bits, int n_controls,
                          const int* control_bits) {
-  if (n_targets < 1 || n_targets > 2) {
-    set_error("apply_matrix supports 1 or 2 targets, got %d", n_targets);
+  if (n_targets < 1 || n_targets > kMaxWideTargets) {
+    set_error("apply_matrix supports 1 to %d targets, got %d", kMaxWideTargets, n_targets);
     return QSB_ERR_SHAPE;
   }
   if (n_qubits < 1 || n_qubits > 40 || n_controls < 0 || n_targets + n_controls > n_qubits) {
@@ -934,8 +1059,8 @@ int qsb_apply_matrix(void* amps, int n_qubits, int dtype, int n_targets, const i
                      int n_controls, const int* control_bits, const double* matrix, int kernel,
                      void* stream) {
   if (int s = check_dtype(dtype)) return s;
-  if (n_targets < 1 || n_targets > 2) {
-    set_error("apply_matrix supports 1 or 2 targets, got %d", n_targets);
+  if (n_targets < 1 || n_targets > kMaxWideTargets) {
+    set_error("apply_matrix supports 1 to %d targets, got %d", kMaxWideTargets, n_targets);
     return QSB_ERR_SHAPE;
   }
   if (n_qubits < 1 || n_qubits > 40 || n_controls < 0 || n_targets + n_controls > n_qubits) {

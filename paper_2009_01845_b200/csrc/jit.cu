@@ -175,9 +175,9 @@ extern "C" int qsb_jit_load(const void* cubin, const char* name, void** func_out
 // Launch a JIT pass kernel: params (src, dst, tensor map, coefficients).  The tensor map is
 // encoded here from `tdesc` (jit.py tma_plan: rank, dims[5], byte strides[4], box[5]) over the
 // 8-byte elements of the state at `src`.
-extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tdesc, uint64_t n_tiles,
-                                const double* coeffs, int64_t n_coeffs, const void* params, int64_t param_bytes,
-                                int threads, int smem_bytes, int ctas_per_sm, void* stream) {
+static int run_pass_impl(void* func, const void* src, void* dst, const int64_t* tdesc, uint64_t n_tiles,
+                         const double* coeffs, int64_t n_coeffs, bool coeffs_on_device, const void* params,
+                         int64_t param_bytes, int threads, int smem_bytes, int grid, void* stream) {
   jit::Driver* dr = jit::driver();
   if (!dr || !func) {
     set_error("qsb_jit_run_pass: no driver / function");
@@ -190,7 +190,10 @@ extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, const in
   cudaStream_t st = as_stream(stream);
   void* dcoef = nullptr;
   if (n_coeffs > 0) {
-    if (int rc = pass::stage_words(coeffs, sizeof(double) * n_coeffs, &dcoef, st)) return rc;
+    if (coeffs_on_device)
+      dcoef = const_cast<double*>(coeffs);
+    else if (int rc = pass::stage_words(coeffs, sizeof(double) * n_coeffs, &dcoef, st))
+      return rc;
   }
   alignas(64) CUtensorMap map;
   memset(&map, 0, sizeof map);
@@ -216,20 +219,34 @@ extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, const in
     }
     if (n_attr < 256) attr_done[n_attr++] = fn;
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const uint64_t slots = (uint64_t)sms * (uint64_t)(ctas_per_sm > 0 ? ctas_per_sm : 1);
-  const unsigned grid = (unsigned)(n_tiles < slots ? n_tiles : slots);
+  if (grid <= 0 || (uint64_t)grid > n_tiles) {
+    set_error("qsb_jit_run_pass: grid %d outside [1, n_tiles]", grid);
+    return QSB_ERR_ARG;
+  }
   const void* a_src = src;
   void* a_dst = dst;
   const double* a_cf = static_cast<const double*>(dcoef);
   // the last kernel parameter is the coefficient struct, copied by value from `params`
   void* args[] = {(void*)&a_src, (void*)&a_dst, (void*)&map, (void*)&a_cf, const_cast<void*>(params)};
-  CUresult r = dr->launch(fn, grid, 1, 1, (unsigned)threads, 1, 1, (unsigned)smem_bytes, (CUstream)st, args, nullptr);
+  CUresult r = dr->launch(fn, (unsigned)grid, 1, 1, (unsigned)threads, 1, 1, (unsigned)smem_bytes, (CUstream)st, args,
+                          nullptr);
   if (r != CUDA_SUCCESS) {
     set_error("cuLaunchKernel failed (%d)", (int)r);
     return QSB_ERR_CUDA;
   }
   return QSB_OK;
+}
+
+extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tdesc, uint64_t n_tiles,
+                                const double* tables, int64_t n_tables, const void* params, int64_t param_bytes,
+                                int threads, int smem_bytes, int grid, void* stream) {
+  return run_pass_impl(func, src, dst, tdesc, n_tiles, tables, n_tables, false, params, param_bytes, threads,
+                       smem_bytes, grid, stream);
+}
+
+extern "C" int qsb_jit_run_pass_dev(void* func, const void* src, void* dst, const int64_t* tdesc, uint64_t n_tiles,
+                                    const double* dev_tables, int64_t n_tables, const void* params,
+                                    int64_t param_bytes, int threads, int smem_bytes, int grid, void* stream) {
+  return run_pass_impl(func, src, dst, tdesc, n_tiles, dev_tables, n_tables, true, params, param_bytes, threads,
+                       smem_bytes, grid, stream);
 }

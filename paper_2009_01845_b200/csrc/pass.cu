@@ -764,15 +764,20 @@ void plan_tma(const void* src, int n, int K, const int64_t* tile_pos, int amp_by
   tp->mode = 1;
 }
 
-// Device ring for per-launch program / coefficient words.  Copies are stream-ordered; when the
-// ring wraps, the stream is synchronised once so no in-flight launch can see overwritten words.
+// Device ring for per-launch program / coefficient words, one per CUDA device.  Copies are
+// stream-ordered; when a ring wraps, the whole device is synchronised once, so no launch queued
+// on ANY stream (other host threads' streams, side streams, user streams) can still be reading
+// the slots that are about to be overwritten.  Staging is refused while `st` is being captured
+// into a CUDA graph: a replay would re-read a ring slot that later launches overwrite (callers
+// that capture own their words in device buffers, see qsb_jit_run_pass_dev).
 int stage_words(const void* host, size_t bytes, void** device_out, cudaStream_t st) {
   // The words go through a pinned host mirror of the device ring, so the upload is a real
   // asynchronous DMA (a pageable source would make the driver synchronise with the stream,
   // stalling the host behind the GPU at every pass).
-  static char* ring = nullptr;
-  static char* hring = nullptr;
-  static size_t cursor = 0;
+  constexpr int kMaxDevices = 64;
+  static char* ring[kMaxDevices] = {};
+  static char* hring[kMaxDevices] = {};
+  static size_t cursor[kMaxDevices] = {};
   static std::mutex mu;  // ctypes drops the GIL: host threads may stage concurrently
   std::lock_guard<std::mutex> lock(mu);
   constexpr size_t kRing = 16u << 20;
@@ -780,31 +785,45 @@ int stage_words(const void* host, size_t bytes, void** device_out, cudaStream_t 
     set_error("stage_words: %zu bytes too large", bytes);
     return QSB_ERR_ARG;
   }
-  if (!ring) {
-    cudaError_t e = cudaMalloc(&ring, kRing);
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone) {
+    set_error("stage_words: host-staged words cannot be captured into a CUDA graph (own them on the device)");
+    return QSB_ERR_ARG;
+  }
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "program ring device");
+  if (dev < 0 || dev >= kMaxDevices) {
+    set_error("stage_words: device %d out of range", dev);
+    return QSB_ERR_ARG;
+  }
+  if (!ring[dev]) {
+    e = cudaMalloc(&ring[dev], kRing);
     if (e != cudaSuccess) {
-      ring = nullptr;
+      ring[dev] = nullptr;
       return cuda_status(e, "program ring");
     }
-    e = cudaMallocHost(&hring, kRing);
+    e = cudaMallocHost(&hring[dev], kRing);
     if (e != cudaSuccess) {
-      hring = nullptr;
+      cudaFree(ring[dev]);
+      ring[dev] = nullptr;
+      hring[dev] = nullptr;
       return cuda_status(e, "pinned program ring");
     }
   }
-  size_t off = (cursor + 255) & ~(size_t)255;
+  size_t off = (cursor[dev] + 255) & ~(size_t)255;
   if (off + bytes > kRing) {
-    // every earlier copy out of the pinned mirror (and every launch reading the device ring)
-    // is on this stream: after this sync both rings can be reused from the start
-    cudaError_t e = cudaStreamSynchronize(st);
+    // every earlier upload out of the pinned mirror and every launch reading the device ring,
+    // on whichever stream, has finished after this: both rings can be reused from the start
+    e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_status(e, "program ring wrap");
     off = 0;
   }
-  cursor = off + bytes;
-  memcpy(hring + off, host, bytes);
-  cudaError_t e = cudaMemcpyAsync(ring + off, hring + off, bytes, cudaMemcpyHostToDevice, st);
+  cursor[dev] = off + bytes;
+  memcpy(hring[dev] + off, host, bytes);
+  e = cudaMemcpyAsync(ring[dev] + off, hring[dev] + off, bytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return cuda_status(e, "program upload");
-  *device_out = ring + off;
+  *device_out = ring[dev] + off;
   return QSB_OK;
 }
 

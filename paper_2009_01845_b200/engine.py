@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _native as nat
 from . import jit
-from .errors import ShapeError
+from .errors import ShapeError, SimulationError
 from .fusion import GEOMETRY, GEOMETRY_JIT, GateStep, PassStep, Plan, compile_pass, plan_circuit
 from .gates import gate_matrix
 
@@ -161,7 +161,7 @@ def _launch_pass(step, words, dtype, src, dst, n, st):
             if step.jit is None:
                 step.jit = jit.compile_words(words, dtype)
             compiled, coeffs = step.jit
-            jit.run(words, dtype, src, dst, n, st, compiled, coeffs)
+            jit.run(words, dtype, src, dst, n, st, compiled, coeffs, step.dev_tables)
             return
         except Exception as exc:  # compile / TMA-plan failure: keep going on the interpreter
             step.no_jit = True
@@ -172,6 +172,25 @@ def _launch_pass(step, words, dtype, src, dst, n, st):
             step.interp_words, _ = compile_pass(step.gates, set(step.tile_pos), n, dtype, GEOMETRY[dtype])
         words = step.interp_words
     nat.check(nat.lib().qsb_run_pass(src, dst, n, dtype, words.ctypes.data, len(words), st), "run_pass")
+
+
+def own_device_tables(plan: Plan) -> None:
+    """Give every pass of `plan` its own device copy of its pivot tables, so its launches read
+    nothing staged from the host at launch time (required before CUDA-graph capture: a captured
+    upload out of the library's shared host ring would replay whatever later launches left in
+    that slot).  Raises when a pass cannot run as a specialised kernel (the interpreter stages
+    its whole program per launch)."""
+    torch = nat.torch_mod()
+    for step in plan.steps:
+        if not isinstance(step, PassStep):
+            continue
+        if step.jit is None and not step.no_jit and jit.available():
+            step.jit = jit.compile_words(step.words, plan.dtype)
+        if step.jit is None:
+            raise SimulationError("CUDA-graph capture needs the specialised (NVRTC) pass kernels")
+        tables = step.jit[1][1]
+        if len(tables) and step.dev_tables is None:
+            step.dev_tables = torch.from_numpy(np.ascontiguousarray(tables)).to("cuda")
 
 
 def run_plan(state, plan: Plan, scratch_holder: dict | None = None, stream=None, events: list | None = None):

@@ -329,6 +329,7 @@ class PassStep:
     jit: object = None  # (compiled kernel, coefficient array) once specialised
     no_jit: bool = False
     interp_words: object = None  # re-encoding for the interpreter's geometry (fallback only)
+    dev_tables: object = None  # device copy of the pivot tables (engine.own_device_tables; graph capture)
 
     @property
     def n_gates(self) -> int:

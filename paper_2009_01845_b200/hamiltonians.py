@@ -156,8 +156,7 @@ def _expectation_passes(bit_terms, state):
     torch = nat.torch_mod()
     total = None
     for words, (compiled, coeffs) in progs:
-        part = torch.zeros(compiled.n_tiles if compiled.n_tiles < 4096 else 4096, dtype=torch.float64,
-                           device=state.tensor.device)
+        part = torch.zeros(compiled.grid(), dtype=torch.float64, device=state.tensor.device)
         jit.run(words, dtype, state.data_ptr, part.data_ptr(), n, nat.stream_ptr(), compiled, coeffs)
         ssum = part.sum()
         total = ssum if total is None else total + ssum

@@ -49,6 +49,27 @@ def ctas_per_sm(consumers: int) -> int:
 
 REG_SPLIT = {c: _reg_split(c, ctas_per_sm(c)) for c in (128, 256, 512)}
 
+# Tiles per CTA (0 = persistent grid-stride loop).  Measured on the B200 (tools/probes/
+# stream_probe.cu, 2^30 complex128 in place): a persistent one-CTA-per-SM sweep with a static
+# tile split runs at 6.2-6.3 TB/s, while one-shot CTAs of 4 consecutive 64 KB tiles -- the grid
+# covering the state once, the block scheduler handing out the next CTA to whichever SM
+# finishes first -- reach 6.9 TB/s, the speed of the plain streaming kernels.
+TILES_PER_CTA = int(os.environ.get("QSB_TILES_PER_CTA", "4"))
+
+
+def tiles_per_cta(ext_bits: int, consumers: int) -> int:
+    """TPC of a pass over 2**ext_bits tiles (0 when the state has too few tiles to matter)."""
+    n_tiles = 1 << ext_bits
+    if TILES_PER_CTA <= 0 or n_tiles < 4 * 148 * TILES_PER_CTA:
+        return 0
+    return TILES_PER_CTA
+
+
+def pass_grid(n_tiles: int, consumers: int, tpc: int, sms: int) -> int:
+    if tpc:
+        return -(-n_tiles // tpc)
+    return min(n_tiles, sms * ctas_per_sm(consumers))
+
 
 def _w2d(w):
     return struct.unpack("<d", struct.pack("<q", int(w)))[0]
@@ -816,7 +837,8 @@ class _Gen:
         pr = "double" if (self.dtype == nat.QSB_C128 or self.expect) else "float"
         defs = (f"#define QSB_F32X2 {1 if self.dtype == nat.QSB_C64 else 0}\n#define R {real}\n#define PR {pr}\n#define C {real}2\n#define KB {K}\n#define HBB {self.HB}\n#define GB {self.G}\n#define STAGES {self.stages}\n#define ALIAS {1 if self.alias else 0}\n#define TBUF {"sm.stage[s]" if self.alias else "sm.tbuf"}\n"
                 f"#define CONSUMERS {self.consumers}\n#define MAXPIV {MAX_PIV}\n#define NPIV {self.npiv}\n"
-                f"#define NCOEF {max(1, len(self.coeffs))}\n#define NTAB {len(self.tables)}\n")
+                f"#define NCOEF {max(1, len(self.coeffs))}\n#define NTAB {len(self.tables)}\n"
+                f"#define TPC {tiles_per_cta(self.n - K, self.consumers)}\n")
         issue = f"""      {{ // producer warp: fetch tile c into stage s (tile number tno)
         const u64 base = {base_expr};
 {self.ep_code}
@@ -884,12 +906,22 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
   }}
   __syncthreads();
   const u64 n_tiles = {1 << (n - K)}ull;
+  // tiles of this CTA: TPC consecutive tiles per CTA with the grid covering the state once, so
+  // the hardware block scheduler balances the SMs (a persistent grid with a static tile split
+  // runs ~10% slower: every SM waits for the slowest one); TPC = 0: persistent grid-stride
+#if TPC
+  const u64 c_begin = (u64)blockIdx.x * TPC;
+  const u64 c_end = c_begin + TPC < n_tiles ? c_begin + TPC : n_tiles;
+  const u64 c_step = 1;
+#else
+  const u64 c_begin = blockIdx.x, c_end = n_tiles, c_step = gridDim.x;
+#endif
   if (tid >= CONSUMERS) {{
     asm volatile("setmaxnreg.dec.sync.aligned.u32 {REG_SPLIT[self.consumers][1]};" ::: "memory");
     if (tid >= CONSUMERS + 32) return;
     const int lane = tid - CONSUMERS;
     int it = 0;
-    for (u64 c = blockIdx.x; c < n_tiles; c += gridDim.x, ++it) {{
+    for (u64 c = c_begin; c < c_end; c += c_step, ++it) {{
       const int s = it % STAGES;
       const u32 ph = (it / STAGES) & 1;
 {"" if self.halves else "      if (it >= STAGES) mbar_wait(&sm.empty[s], ph ^ 1);"}
@@ -901,7 +933,7 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
   asm volatile("setmaxnreg.inc.sync.aligned.u32 {REG_SPLIT[self.consumers][0]};" ::: "memory");
   int it = 0;
   double ea = 0.0;  // expectation passes: this thread's sum of Re <x|M|x>
-  for (u64 c = blockIdx.x; c < n_tiles; c += gridDim.x, ++it) {{
+  for (u64 c = c_begin; c < c_end; c += c_step, ++it) {{
     const int s = it % STAGES;
     const u32 ph = (it / STAGES) & 1;
 {head}
@@ -927,7 +959,22 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
 
 
 class _Compiled:
-    __slots__ = ("func", "name", "smem", "tdesc", "n_tiles", "threads", "ctas")
+    __slots__ = ("func", "name", "smem", "tdesc", "n_tiles", "threads", "ctas", "tpc")
+
+    def grid(self) -> int:
+        """CTAs of one launch (one-shot tiles-per-CTA grid, or SMs x resident CTAs)."""
+        return pass_grid(self.n_tiles, self.threads - 128, self.tpc, _sm_count())
+
+
+_SMS = None
+
+
+def _sm_count() -> int:
+    global _SMS
+    if _SMS is None:
+        torch = nat.torch_mod()
+        _SMS = int(torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count)
+    return _SMS
 
 
 _cache: dict = {}
@@ -1087,6 +1134,7 @@ def _compile_words(words, dtype):
         fresh.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
         fresh.n_tiles = 1 << (int(words[4]) - K)
         fresh.threads = (1 << (K - nreg)) + 128
+        fresh.tpc = tiles_per_cta(int(words[4]) - K, 1 << (K - nreg))
         with _lock:
             hit = _cache.setdefault(src, fresh)
     return hit, (np.ascontiguousarray(pbytes), tables)
@@ -1115,14 +1163,25 @@ def precompile(steps, dtype, device: int | None = None) -> None:
         list(ex.map(work, todo))
 
 
-def run(words, dtype, src_ptr, dst_ptr, n_qubits, stream_ptr, compiled=None, coeffs=None):
+def run(words, dtype, src_ptr, dst_ptr, n_qubits, stream_ptr, compiled=None, coeffs=None, dev_tables=None):
+    """Launch a specialised pass.  The pivot tables are staged through the library's host ring,
+    or -- `dev_tables`, a device tensor holding them (CUDA-graph capture) -- read in place."""
     if compiled is None:
         compiled, coeffs = compile_words(words, dtype)
     params, tables = coeffs
+    lib = nat.lib()
+    if dev_tables is not None and len(tables):
+        nat.check(
+            lib.qsb_jit_run_pass_dev(compiled.func, src_ptr, dst_ptr, compiled.tdesc.ctypes.data, compiled.n_tiles,
+                                     dev_tables.data_ptr(), len(tables), params.ctypes.data, params.nbytes,
+                                     compiled.threads, compiled.smem, compiled.grid(), stream_ptr),
+            "jit_run_pass_dev",
+        )
+        return
     nat.check(
-        nat.lib().qsb_jit_run_pass(compiled.func, src_ptr, dst_ptr, compiled.tdesc.ctypes.data, compiled.n_tiles,
-                                   tables.ctypes.data if len(tables) else None, len(tables),
-                                   params.ctypes.data, params.nbytes, compiled.threads, compiled.smem, compiled.ctas,
-                                   stream_ptr),
+        lib.qsb_jit_run_pass(compiled.func, src_ptr, dst_ptr, compiled.tdesc.ctypes.data, compiled.n_tiles,
+                             tables.ctypes.data if len(tables) else None, len(tables),
+                             params.ctypes.data, params.nbytes, compiled.threads, compiled.smem, compiled.grid(),
+                             stream_ptr),
         "jit_run_pass",
     )

@@ -59,6 +59,45 @@ def test_apply_matrix_kernel_classes(cuda, n):
         assert max_abs(fast, ref) <= 1e-15
 
 
+@pytest.mark.parametrize("t", [3, 4, 5])
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_apply_matrix_three_to_five_targets(cuda, t, prec):
+    """apply_matrix takes any 2^t x 2^t matrix (gates.py:380-469): general, diagonal and
+    permutation bodies for 3-5 targets, with controls, against the oracle restatement."""
+    import paper_2009_01845_b200 as q
+
+    n = 11
+    rng = np.random.default_rng(100 + t)
+    dtype = np.complex128 if prec == "f64" else np.complex64
+    tol = TOL64 if prec == "f64" else TOL32
+    d = 1 << t
+    z = rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))
+    unitary, _ = np.linalg.qr(z)
+    phases = np.exp(1j * rng.uniform(0, 2 * np.pi, d))
+    phases[::3] = 1.0
+    diag = np.diag(phases)
+    perm = np.zeros((d, d), dtype=np.complex128)
+    order = rng.permutation(d)
+    for r in range(d):
+        perm[r, order[r]] = [1.0, -1.0, 1j, -1j][r % 4] if r % 2 else 1.0
+    for mat in (unitary, diag, perm):
+        qubits = [int(x) for x in rng.permutation(n)[:t + 1]]
+        targets, controls = qubits[:t], qubits[t:]
+        psi = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)).astype(dtype)
+        want = psi.copy()
+        ov.apply_matrix(want, n, targets, mat, controls)
+        got = q.from_amplitudes(psi)
+        q.apply_matrix(got, n, targets, mat, controls)
+        assert max_abs(got.amplitudes, want) <= tol
+        host = psi.copy()  # numpy callers: uploaded, transformed, written back in place
+        q.apply_matrix(host, n, targets, mat, controls)
+        assert max_abs(host, want) <= tol
+        if mat is perm:
+            assert np.array_equal(got.amplitudes, want)  # exact moves and +-1 / +-i phases
+    with pytest.raises(q.ShapeError):
+        q.apply_matrix(q.zero_state(8), 8, list(range(6)), np.eye(64))
+
+
 def test_control_leaves_unset_half_untouched(cuda):
     import paper_2009_01845_b200 as q
 
@@ -643,6 +682,45 @@ def test_circuit_graph_replay(cuda, n, prec):
         assert np.array_equal(init.amplitudes, keep)
     with pytest.raises(q.ShapeError):
         g.execute(q.zero_state(n + 1, precision))
+
+
+def _cached_plans(circuit):
+    from paper_2009_01845_b200.fusion import Plan
+
+    return [v[0] for v in circuit.__dict__.get("_plan_cache", {}).values() if isinstance(v[0], Plan)]
+
+
+def _staged_table_bytes(plan):
+    from paper_2009_01845_b200.fusion import PassStep
+
+    return sum(-(-8 * len(s.jit[1][1]) // 256) * 256 for s in plan.steps
+               if isinstance(s, PassStep) and s.jit is not None)
+
+
+def test_captured_qft_replays_after_ring_wraps(cuda):
+    """A captured QFT (fused passes with pivot tables) replays correctly after more than the
+    library's 16 MB host-staging ring has been cycled by other circuits: the graph's passes read
+    their tables from device buffers the plan owns, never from a ring slot."""
+    import paper_2009_01845_b200 as q
+
+    n = 16
+    c = q.qft_circuit(n)
+    g = c.capture()
+    (plan,) = _cached_plans(c)
+    assert _staged_table_bytes(plan) > 0, "QFT passes should carry pivot tables"
+    rng = np.random.default_rng(11)
+    psi = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)) / math.sqrt(2 << n)
+    want = ov.run(ov.qft(n), n, psi)
+    assert max_abs(g.execute(_sv(psi)).amplitudes, want) <= TOL64
+    other = q.qft_circuit(20)
+    st = q.zero_state(20)
+    other.execute(st)
+    other.execute(st)  # planned from the second run on
+    per_run = _staged_table_bytes(_cached_plans(other)[0])
+    assert per_run > 0
+    for _ in range((40 << 20) // per_run + 1):  # > 2 wraps of the 16 MB ring
+        other.execute(st)
+    assert max_abs(g.execute(_sv(psi)).amplitudes, want) <= TOL64
 
 
 def test_concurrent_small_executes_from_threads(cuda):

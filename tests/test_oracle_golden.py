@@ -52,6 +52,18 @@ def test_variational(n, fused):
     assert max_abs(ov.run(gates, n, dtype=np.complex64), g[f"f32_{n}_{int(fused)}"]) <= 1e-7
 
 
+def test_c64_large_fixtures():
+    """complex64 at n = 16 (the fixtures the GPU tests run through planned fused passes)."""
+    g = golden("c64_large")
+    n = 16
+    assert max_abs(ov.run(ov.qft(n), n, g["qft_in"], dtype=np.complex64), g["qft_out"]) <= 1e-7
+    for fused in (False, True):
+        gates = ov.variational(n, 3, g["var_params"], fused=fused)
+        assert max_abs(ov.run(gates, n, dtype=np.complex64), g[f"var_{int(fused)}"]) <= 1e-7
+    _, gates = ov.from_json(g["grid_circuit"])
+    assert max_abs(ov.run(gates, n, dtype=np.complex64), g["grid_out"]) <= 1e-7
+
+
 def test_grid_supremacy_builder_matches_reference_execution():
     g = golden("grid15")
     gates = ov.grid_supremacy(3, 5, 8, seed=42)
