@@ -208,6 +208,19 @@ int qsb_pack_half(const void* shard, int n_local_bits, int dtype, int bit, int h
                   uint64_t first, uint64_t count, void* staging, void* stream);
 int qsb_unpack_half(void* shard, int n_local_bits, int dtype, int bit, int half, uint64_t first,
                     uint64_t count, const void* staging, void* stream);
+/* Batched global<->local exchange of k qubits (one all-to-all instead of k pairwise
+ * reshuffles; the k-qubit generalisation of sharding.py:84-111).  A *part* of a shard is the
+ * set of amplitudes whose local bits `bits[0..k)` hold the pattern `part_bits` (a mask already
+ * placed at those bit positions); element e of a part is its e-th amplitude in index order.
+ * pack/unpack copy elements [first, first + count) of a part to / from a contiguous staging
+ * buffer (the per-peer send / receive chunks of the all-to-all). */
+int qsb_pack_part(const void* shard, int n_local_bits, int dtype, int k, const int* bits, uint64_t part_bits,
+                  uint64_t first, uint64_t count, void* staging, void* stream);
+int qsb_unpack_part(void* shard, int n_local_bits, int dtype, int k, const int* bits, uint64_t part_bits,
+                    uint64_t first, uint64_t count, const void* staging, void* stream);
+/* In-process form: swap part `a_bits` of shard a with part `b_bits` of shard b (a != b). */
+int qsb_exchange_parts(void* a, void* b, int n_local_bits, int dtype, int k, const int* bits, uint64_t a_bits,
+                       uint64_t b_bits, void* stream);
 
 #ifdef __cplusplus
 }

@@ -89,7 +89,7 @@ __version__ = "0.1.0"
 def __getattr__(name):
     # the sharded executor pulls in torch.distributed; import it lazily
     if name in ("ExecutionPlan", "ShardedState", "execute_sharded", "gather", "partition", "plan", "reshuffle",
-                "Reshuffle", "LocalSegment", "execute_distributed"):
+                "Reshuffle", "LocalSegment", "execute_distributed", "Exchange", "plan_batched"):
         from . import sharding
 
         return getattr(sharding, name)

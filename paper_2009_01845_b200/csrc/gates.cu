@@ -696,6 +696,42 @@ __global__ void k_unpack_half(cplx<R>* __restrict__ s, int bit, int half, uint64
   }
 }
 
+// k-qubit parts for the batched global<->local exchange: part `bits` of a shard = the
+// amplitudes whose local bits at `occ` (ascending) spell `bits` (already placed at those
+// positions).  Element e of a part is the e-th such amplitude in index order, so a part whose
+// bits are high positions is a few long contiguous runs.
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_pack_part(const cplx<R>* __restrict__ s, const OccBits occ,
+                                                        uint64_t bits, uint64_t first, uint64_t count,
+                                                        cplx<R>* __restrict__ out) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < count; e += stride)
+    out[e] = s[insert_zero_bits(first + e, occ) | bits];
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_unpack_part(cplx<R>* __restrict__ s, const OccBits occ,
+                                                          uint64_t bits, uint64_t first, uint64_t count,
+                                                          const cplx<R>* __restrict__ in) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < count; e += stride)
+    s[insert_zero_bits(first + e, occ) | bits] = in[e];
+}
+
+// in-process form: a's part `a_bits` <-> b's part `b_bits`
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_exchange_parts(cplx<R>* __restrict__ a, cplx<R>* __restrict__ b,
+                                                             const OccBits occ, uint64_t a_bits, uint64_t b_bits,
+                                                             uint64_t count) {
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e < count; e += stride) {
+    const uint64_t base = insert_zero_bits(e, occ);
+    const cplx<R> t = a[base | a_bits];
+    a[base | a_bits] = b[base | b_bits];
+    b[base | b_bits] = t;
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // bit-permuting copy (partition / gather) and half exchange between two shards
 // ------------------------------------------------------------------------------------------
@@ -1317,6 +1353,104 @@ int qsb_unpack_half(void* shard, int n_local_bits, int dtype, int bit, int half,
     k_unpack_half<float><<<stream_grid(count), kThreads, 0, st>>>(static_cast<float2*>(shard), bit, half, first,
                                                                   count, static_cast<const float2*>(staging));
   QSB_CHECK_LAUNCH("qsb_unpack_half");
+  return QSB_OK;
+}
+
+// k local bits (any order) -> sorted OccBits; the part's bit pattern at those positions
+static int part_args(int n_local_bits, int k, const int* bits, OccBits* occ, const char* where) {
+  if (k < 1 || k > 16 || k >= n_local_bits) {
+    set_error("%s: need 1 <= k <= 16 and k < n_local_bits (k=%d)", where, k);
+    return QSB_ERR_SHAPE;
+  }
+  uint64_t seen = 0;
+  for (int i = 0; i < k; ++i) {
+    if (bits[i] < 0 || bits[i] >= n_local_bits || ((seen >> bits[i]) & 1ull)) {
+      set_error("%s: bad or duplicate bit %d", where, bits[i]);
+      return QSB_ERR_SHAPE;
+    }
+    seen |= 1ull << bits[i];
+  }
+  occ->n = 0;
+  for (int b = 0; b < n_local_bits; ++b)
+    if ((seen >> b) & 1ull) occ->pos[occ->n++] = (uint8_t)b;
+  return QSB_OK;
+}
+
+static int check_part_bits(int k, const int* bits, uint64_t part, const char* where) {
+  uint64_t mask = 0;
+  for (int i = 0; i < k; ++i) mask |= 1ull << bits[i];
+  if (part & ~mask) {
+    set_error("%s: part bits 0x%llx outside the part positions", where, (unsigned long long)part);
+    return QSB_ERR_SHAPE;
+  }
+  return QSB_OK;
+}
+
+int qsb_pack_part(const void* shard, int n_local_bits, int dtype, int k, const int* bits, uint64_t part_bits,
+                  uint64_t first, uint64_t count, void* staging, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  OccBits occ;
+  if (int s = part_args(n_local_bits, k, bits, &occ, "qsb_pack_part")) return s;
+  if (int s = check_part_bits(k, bits, part_bits, "qsb_pack_part")) return s;
+  if (first + count > (1ull << (n_local_bits - k))) {
+    set_error("qsb_pack_part: range past the part");
+    return QSB_ERR_SHAPE;
+  }
+  if (count == 0) return QSB_OK;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    k_pack_part<double><<<stream_grid(count), kThreads, 0, st>>>(static_cast<const double2*>(shard), occ, part_bits,
+                                                                 first, count, static_cast<double2*>(staging));
+  else
+    k_pack_part<float><<<stream_grid(count), kThreads, 0, st>>>(static_cast<const float2*>(shard), occ, part_bits,
+                                                                first, count, static_cast<float2*>(staging));
+  QSB_CHECK_LAUNCH("qsb_pack_part");
+  return QSB_OK;
+}
+
+int qsb_unpack_part(void* shard, int n_local_bits, int dtype, int k, const int* bits, uint64_t part_bits,
+                    uint64_t first, uint64_t count, const void* staging, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  OccBits occ;
+  if (int s = part_args(n_local_bits, k, bits, &occ, "qsb_unpack_part")) return s;
+  if (int s = check_part_bits(k, bits, part_bits, "qsb_unpack_part")) return s;
+  if (first + count > (1ull << (n_local_bits - k))) {
+    set_error("qsb_unpack_part: range past the part");
+    return QSB_ERR_SHAPE;
+  }
+  if (count == 0) return QSB_OK;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    k_unpack_part<double><<<stream_grid(count), kThreads, 0, st>>>(static_cast<double2*>(shard), occ, part_bits,
+                                                                   first, count, static_cast<const double2*>(staging));
+  else
+    k_unpack_part<float><<<stream_grid(count), kThreads, 0, st>>>(static_cast<float2*>(shard), occ, part_bits,
+                                                                  first, count, static_cast<const float2*>(staging));
+  QSB_CHECK_LAUNCH("qsb_unpack_part");
+  return QSB_OK;
+}
+
+int qsb_exchange_parts(void* a, void* b, int n_local_bits, int dtype, int k, const int* bits, uint64_t a_bits,
+                       uint64_t b_bits, void* stream) {
+  if (int s = check_dtype(dtype)) return s;
+  OccBits occ;
+  if (int s = part_args(n_local_bits, k, bits, &occ, "qsb_exchange_parts")) return s;
+  if (int s = check_part_bits(k, bits, a_bits, "qsb_exchange_parts")) return s;
+  if (int s = check_part_bits(k, bits, b_bits, "qsb_exchange_parts")) return s;
+  if (a == b && a_bits == b_bits) return QSB_OK;
+  if (a == b) {
+    set_error("qsb_exchange_parts: a part cannot be exchanged within one shard");
+    return QSB_ERR_ARG;
+  }
+  const uint64_t count = 1ull << (n_local_bits - k);
+  cudaStream_t st = as_stream(stream);
+  if (dtype == QSB_C128)
+    k_exchange_parts<double><<<stream_grid(count), kThreads, 0, st>>>(static_cast<double2*>(a), static_cast<double2*>(b),
+                                                                      occ, a_bits, b_bits, count);
+  else
+    k_exchange_parts<float><<<stream_grid(count), kThreads, 0, st>>>(static_cast<float2*>(a), static_cast<float2*>(b),
+                                                                     occ, a_bits, b_bits, count);
+  QSB_CHECK_LAUNCH("qsb_exchange_parts");
   return QSB_OK;
 }
 

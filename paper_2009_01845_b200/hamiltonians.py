@@ -87,6 +87,7 @@ def build_x(n_qubits: int, form: Form = Form.TROTTER):
     if n_qubits < 2:
         raise ShapeError("Trotter form needs at least 2 qubits")
     ground = lambda precision=Precision.F64: plus_state(n_qubits, precision)  # noqa: E731
+    ground.is_plus_state = True  # lets the sharded evolution build |+>^n shard by shard
     return TrotterHamiltonian(n_qubits, [((i,), -_PX) for i in range(n_qubits)], ground_state=ground)
 
 

@@ -54,7 +54,7 @@ REG_SPLIT = {c: _reg_split(c, ctas_per_sm(c)) for c in (128, 256, 512)}
 # tile split runs at 6.2-6.3 TB/s, while one-shot CTAs of 4 consecutive 64 KB tiles -- the grid
 # covering the state once, the block scheduler handing out the next CTA to whichever SM
 # finishes first -- reach 6.9 TB/s, the speed of the plain streaming kernels.
-TILES_PER_CTA = int(os.environ.get("QSB_TILES_PER_CTA", "4"))
+TILES_PER_CTA = int(os.environ.get("QSB_TILES_PER_CTA", "16"))
 
 
 def tiles_per_cta(ext_bits: int, consumers: int) -> int:

@@ -59,10 +59,26 @@ class ExecutionPlan:
     n_shards: int
     global_qubits: tuple
     steps: list = field(default_factory=list)
+    # uncontrolled SWAPs are label swaps (plan_batched); the reference plan moves their data
+    relabel_swaps: bool = False
 
     @property
     def n_reshuffles(self) -> int:
         return sum(1 for s in self.steps if isinstance(s, Reshuffle))
+
+    @property
+    def n_exchanges(self) -> int:
+        """Data-moving steps: reshuffles plus batched exchanges."""
+        return sum(1 for s in self.steps if isinstance(s, (Reshuffle, Exchange)))
+
+    @property
+    def swapped_qubits(self) -> int:
+        return sum(1 if isinstance(s, Reshuffle) else s.k for s in self.steps if isinstance(s, (Reshuffle, Exchange)))
+
+    def shard_fraction_moved(self) -> float:
+        """Fraction of one shard every rank sends over the whole plan."""
+        return sum(0.5 if isinstance(s, Reshuffle) else 1.0 - 2.0 ** -s.k
+                   for s in self.steps if isinstance(s, (Reshuffle, Exchange)))
 
 
 def _kind(spec):
@@ -136,6 +152,200 @@ def plan(circuit: Circuit, n_shards: int, global_qubits=None) -> ExecutionPlan:
     return ExecutionPlan(n, n_shards, global_qubits, steps)
 
 
+@dataclass
+class Exchange:
+    """Swap k global qubits with k local qubits in one all-to-all (pairs: (global, local));
+    the batched form of k Reshuffles: (1 - 2^-k) of every shard moves once instead of half a
+    shard k times."""
+
+    pairs: tuple
+
+    @property
+    def k(self) -> int:
+        return len(self.pairs)
+
+
+def _is_free_swap(spec) -> bool:
+    return _kind(spec) is GateKind.SWAP and not spec.controls
+
+
+def _required_local_batched(spec) -> tuple:
+    """Targets that must be local when global controls are shard filters, every diagonal gate
+    is applied shard-locally (any kind, not only CZ/CZPow) and uncontrolled SWAPs are label
+    swaps."""
+    kind = _kind(spec)
+    if kind in (GateKind.CZ, GateKind.CZPOW, GateKind.Z, GateKind.RZ) or _is_free_swap(spec):
+        return ()
+    if kind is GateKind.CNOT:
+        return (spec.targets[1],)
+    m = gate_matrix(spec)
+    if not np.count_nonzero(m - np.diag(np.diagonal(m))):
+        return ()
+    return tuple(spec.targets)
+
+
+def _diag_qubits(spec) -> set:
+    """Qubits on which the gate acts diagonally (controls; every target of a diagonal gate):
+    two gates commute when every qubit they share is diagonal for both."""
+    kind = _kind(spec)
+    ctrl = set(spec.controls)
+    if kind in (GateKind.CZ, GateKind.CZPOW, GateKind.Z, GateKind.RZ):
+        return ctrl | set(spec.targets)
+    if kind is GateKind.SWAP:
+        return ctrl
+    m = gate_matrix(spec)
+    if not np.count_nonzero(m - np.diag(np.diagonal(m))):
+        return ctrl | set(spec.targets)
+    if kind is GateKind.CNOT:
+        return ctrl | {spec.targets[0]}
+    return ctrl
+
+
+def _gate_dag(queue):
+    """Predecessor lists of the commutation DAG: gate j waits for gate i < j when they share a
+    qubit on which at least one of them is not diagonal."""
+    preds = [set() for _ in queue]
+    last_nd: dict = {}  # qubit -> last gate non-diagonal on it
+    diag_since: dict = {}  # qubit -> gates diagonal on it since then
+    for j, spec in enumerate(queue):
+        dq = _diag_qubits(spec)
+        for q in set(spec.targets) | set(spec.controls):
+            if q in last_nd:
+                preds[j].add(last_nd[q])
+            if q in dq:
+                diag_since.setdefault(q, []).append(j)
+            else:
+                preds[j].update(diag_since.pop(q, ()))
+                last_nd[q] = j
+        preds[j].discard(j)
+    return preds
+
+
+def plan_batched(circuit: Circuit, n_shards: int, global_qubits=None, local_order=None) -> ExecutionPlan:
+    """Exchange-minimising schedule for the resident multi-GPU path.
+
+    Locality rules of plan() (sharding.py:141-149) widened to every diagonal gate, with
+    uncontrolled SWAPs as free relabels.  Gates run in any order their commutation DAG allows
+    (disjoint supports, or shared qubits that both act on diagonally): every gate whose
+    qubits are local runs as soon as its predecessors have.  When only blocked gates remain,
+    ONE exchange installs a new global set: the g qubits (outside the blocked gate's targets)
+    whose first use lies deepest in the remaining DAG -- Belady on sets over DAG depth, which
+    maximises how much runs before the next exchange -- keeping every current global whose
+    first use is at or past that horizon, so k is as small as the horizon allows.  Among equal
+    candidates, locals at higher bit positions enter (long contiguous runs for pack/unpack).
+    `local_order`: the current local qubits in slot order (defaults to significance order)."""
+    import heapq
+
+    n = circuit.n_qubits
+    if n_shards < 2 or n_shards & (n_shards - 1):
+        raise ShapeError(f"n_shards must be a power of two >= 2, got {n_shards}")
+    if n_shards > 1 << (n - 1):
+        raise CapacityError(f"{n_shards} shards exceed the cap of {1 << (n - 1)} for {n} qubits")
+    g = n_shards.bit_length() - 1
+    queue = circuit.queue
+    need = [_required_local_batched(s) for s in queue]
+    for pos, req in enumerate(need):
+        if len(req) > n - g:
+            raise CapacityError(
+                f"gate at position {pos} needs {len(req)} local qubits but only {n - g} exist with {n_shards} shards")
+    if global_qubits is None:
+        count = [0] * n
+        for req in need:
+            for q in req:
+                count[q] += 1
+        order = sorted(range(n), key=lambda q: (count[q], -q))
+        global_qubits = tuple(sorted(order[:g]))
+    else:
+        global_qubits = tuple(global_qubits)
+        if len(global_qubits) != g or len(set(global_qubits)) != g:
+            raise ShapeError(f"{n_shards} shards need {g} distinct global qubits, got {global_qubits}")
+    preds = _gate_dag(queue)
+    succ = [[] for _ in queue]
+    for j, ps in enumerate(preds):
+        for i in ps:
+            succ[i].append(j)
+    indeg = [len(ps) for ps in preds]
+    done = [False] * len(queue)
+    glob = list(global_qubits)
+    loc = list(local_order) if local_order is not None else [q for q in range(n) if q not in global_qubits]
+    ready = [j for j in range(len(queue)) if not indeg[j]]
+    heapq.heapify(ready)
+    blocked: list = []
+    steps, seg = [], []
+    remaining = len(queue)
+    while remaining:
+        gset = set(glob)
+        progressed = False
+        while ready:
+            j = heapq.heappop(ready)
+            if any(q in gset for q in need[j]):
+                blocked.append(j)
+                continue
+            progressed = True
+            done[j] = True
+            remaining -= 1
+            seg.append(j)
+            if _is_free_swap(queue[j]):
+                a, b = queue[j].targets
+                for lst in (glob, loc):
+                    for i, q in enumerate(lst):
+                        if q == a:
+                            lst[i] = b
+                        elif q == b:
+                            lst[i] = a
+                gset = set(glob)
+            for k in succ[j]:
+                indeg[k] -= 1
+                if not indeg[k]:
+                    heapq.heappush(ready, k)
+        if not remaining:
+            break
+        if progressed and blocked:
+            # a relabel may have unblocked some of them
+            for j in blocked:
+                heapq.heappush(ready, j)
+            blocked = []
+            if any(not any(q in set(glob) for q in need[j]) for j in ready):
+                continue
+            blocked = [heapq.heappop(ready) for _ in range(len(ready))]
+        # only blocked gates are ready: one exchange
+        if seg:
+            steps.append(LocalSegment(seg))
+            seg = []
+        first = min(blocked)
+        rs = set(need[first])
+        # depth of every remaining gate from the current frontier; first use of each qubit
+        depth = {}
+        nu = {q: math.inf for q in range(n)}
+        for j in range(len(queue)):  # queue order is a topological order of the DAG
+            if done[j]:
+                continue
+            d = 0
+            for i in preds[j]:
+                if not done[i]:
+                    d = max(d, depth[i] + 1)
+            depth[j] = d
+            for q in need[j]:
+                if d < nu[q]:
+                    nu[q] = d
+        cand = {q: nu[q] for q in range(n) if q not in rs}
+        horizon = sorted(cand.values(), reverse=True)[g - 1]
+        keep = [q for q in glob if q not in rs and cand[q] >= horizon]
+        outs = [q for q in glob if q not in keep]
+        pool = sorted((q for q in loc if q not in rs and cand[q] >= horizon), key=lambda q: (-cand[q], loc.index(q)))
+        ins = pool[:len(outs)]
+        for a, b in zip(outs, ins):
+            ja, mb = glob.index(a), loc.index(b)
+            glob[ja], loc[mb] = b, a
+        steps.append(Exchange(tuple(zip(outs, ins))))
+        for j in blocked:
+            heapq.heappush(ready, j)
+        blocked = []
+    if seg:
+        steps.append(LocalSegment(seg))
+    return ExecutionPlan(n, n_shards, global_qubits, steps, relabel_swaps=True)
+
+
 # ------------------------------------------------------------------------------------------
 # device backend (the product path) -- tests inject a CPU stand-in with the same methods
 # ------------------------------------------------------------------------------------------
@@ -193,6 +403,21 @@ class CudaBackend:
     def unpack(self, shard, n_local, bit, half, first, count, staging):
         nat.check(nat.lib().qsb_unpack_half(shard.data_ptr(), n_local, self.dtype, bit, half, first, count,
                                             staging.data_ptr(), nat.stream_ptr()), "unpack_half")
+
+    def exchange_parts(self, a, b, n_local, bits, a_bits, b_bits):
+        pb = np.ascontiguousarray(bits, dtype=np.int32)
+        nat.check(nat.lib().qsb_exchange_parts(a.data_ptr(), b.data_ptr(), n_local, self.dtype, len(bits), pb.ctypes.data,
+                                               a_bits, b_bits, nat.stream_ptr()), "exchange_parts")
+
+    def pack_part(self, shard, n_local, bits, part_bits, first, count, staging):
+        pb = np.ascontiguousarray(bits, dtype=np.int32)
+        nat.check(nat.lib().qsb_pack_part(shard.data_ptr(), n_local, self.dtype, len(bits), pb.ctypes.data, part_bits,
+                                          first, count, staging.data_ptr(), nat.stream_ptr()), "pack_part")
+
+    def unpack_part(self, shard, n_local, bits, part_bits, first, count, staging):
+        pb = np.ascontiguousarray(bits, dtype=np.int32)
+        nat.check(nat.lib().qsb_unpack_part(shard.data_ptr(), n_local, self.dtype, len(bits), pb.ctypes.data, part_bits,
+                                            first, count, staging.data_ptr(), nat.stream_ptr()), "unpack_part")
 
     def permute(self, src, n_bits, dst_bit):
         out = self.empty(src.numel())
@@ -267,6 +492,16 @@ class TorchComm:
         after the transfer without blocking the host; gloo: wait() blocks)."""
         dist = self.dist
         ops = [dist.P2POp(dist.isend, send, peer, self.group), dist.P2POp(dist.irecv, recv, peer, self.group)]
+        return dist.batch_isend_irecv(ops)
+
+    def ialltoall(self, triples):
+        """Start paired sends/receives with several peers as one group ((send, recv, peer) per
+        peer); NCCL runs the group as an all-to-all among those ranks."""
+        dist = self.dist
+        ops = []
+        for send, recv, peer in triples:
+            ops.append(dist.P2POp(dist.isend, send, peer, self.group))
+            ops.append(dist.P2POp(dist.irecv, recv, peer, self.group))
         return dist.batch_isend_irecv(ops)
 
     def all_gather(self, t):
@@ -453,14 +688,119 @@ def reshuffle(sharded: ShardedState, global_qubit: int, local_qubit: int):
     sharded.local_qubits = tuple(lc)
 
 
+def _part_bits(value, bits):
+    """Local index pattern with bit i of `value` at local bit bits[i]."""
+    out = 0
+    for i, b in enumerate(bits):
+        out |= ((value >> i) & 1) << b
+    return out
+
+
+def exchange(sharded: ShardedState, pairs) -> None:
+    """Swap the roles of k global and k local qubits in place with ONE all-to-all (pairs:
+    (global, local)); equal to k reshuffles (sharding.py:84-111) up to the order of the qubits'
+    slots.  Shard s with swapped-global bits sJ = a trades its part whose swapped-local bits
+    spell u with the part spelling a of the shard whose swapped-global bits are u: every rank
+    sends (1 - 2^-k) of its shard, to 2^k - 1 peers at once, and each part comes back into
+    the slots it left (in place, chunked staging)."""
+    pairs = tuple(pairs)
+    if not pairs:
+        return
+    k = len(pairs)
+    g, nl = sharded.n_global, sharded.n_local
+    gl, lc = list(sharded.global_qubits), list(sharded.local_qubits)
+    jbits = [sharded.shard_bit(a) for a, _ in pairs]
+    pbits = [sharded.local_bit(b) for _, b in pairs]
+    if len(set(jbits)) != k or len(set(pbits)) != k:
+        raise ShapeError(f"exchange pairs {pairs} repeat a qubit")
+    backend, comm = sharded.backend, sharded.comm
+
+    def s_val(s):
+        return sum(((s >> j) & 1) << i for i, j in enumerate(jbits))
+
+    def with_val(s, v):
+        for i, j in enumerate(jbits):
+            s = (s & ~(1 << j)) | (((v >> i) & 1) << j)
+        return s
+
+    if isinstance(comm, LocalComm):
+        for s in range(1 << g):
+            a = s_val(s)
+            for u in range(a + 1, 1 << k):
+                t = with_val(s, u)
+                backend.exchange_parts(sharded.shards[s], sharded.shards[t], nl, pbits,
+                                       _part_bits(u, pbits), _part_bits(a, pbits))
+    else:
+        _exchange_parts_dist(sharded, k, pbits, s_val, with_val)
+    for (a, b), j, p in zip(pairs, jbits, pbits):
+        gl[g - 1 - j] = b
+        lc[nl - 1 - p] = a
+    sharded.global_qubits = tuple(gl)
+    sharded.local_qubits = tuple(lc)
+
+
+def _exchange_parts_dist(sharded, k, pbits, s_val, with_val):
+    """All-to-all among the 2^k ranks that share the other global bits: every chunk round
+    packs one chunk of each outgoing part, posts all sends and receives as one batched group
+    (NCCL: a grouped send/recv = all-to-all), and unpacks the previous round's chunks into the
+    parts they came for (double-buffered; stream-ordered under NCCL)."""
+    nl = sharded.n_local
+    backend, comm = sharded.backend, sharded.comm
+    part = 1 << (nl - k)
+    itemsize = sharded.precision.itemsize
+    for s, buf in list(sharded.shards.items()):
+        a = s_val(s)
+        peers = [(u, sharded.owner[with_val(s, u)]) for u in range(1 << k) if u != a]
+        chunk = max(1, min(part, comm.CHUNK_BYTES // itemsize // len(peers)))
+        send = [[backend.empty(chunk) for _ in peers] for _ in range(2)]
+        recv = [[backend.empty(chunk) for _ in peers] for _ in range(2)]
+        inflight = [None, None]
+
+        def drain(bi):
+            works, first, cnt = inflight[bi]
+            for w in works:
+                w.wait()
+            for pi, (u, _) in enumerate(peers):
+                backend.unpack_part(buf, nl, pbits, _part_bits(u, pbits), first, cnt, recv[bi][pi])
+            inflight[bi] = None
+
+        for c, first in enumerate(range(0, part, chunk)):
+            bi = c & 1
+            if inflight[bi] is not None:
+                drain(bi)
+            cnt = min(chunk, part - first)
+            for pi, (u, _) in enumerate(peers):
+                backend.pack_part(buf, nl, pbits, _part_bits(u, pbits), first, cnt, send[bi][pi])
+            if not comm.stream_ordered:
+                _sync_stream()
+            works = comm.ialltoall([(send[bi][pi][:cnt], recv[bi][pi][:cnt], peer)
+                                    for pi, (_, peer) in enumerate(peers)])
+            inflight[bi] = (works, first, cnt)
+        for bi in (0, 1):
+            if inflight[bi] is not None:
+                drain(bi)
+
+
 # ------------------------------------------------------------------------------------------
 # runner
 # ------------------------------------------------------------------------------------------
 class _Runner:
-    def __init__(self, sharded: ShardedState, cache: dict | None = None):
+    def __init__(self, sharded: ShardedState, cache: dict | None = None, relabel_swaps: bool = False):
         self.sh = sharded
         self.pending = {s: [] for s in sharded.shards}
         self.cache: dict = {} if cache is None else cache
+        self.relabel_swaps = relabel_swaps
+
+    def _relabel(self, a, b):
+        """Uncontrolled SWAP as a label swap: the data stays, the two qubits trade slots
+        (queued gates are already in bit terms, so nothing is flushed)."""
+        sh = self.sh
+
+        def sw(t):
+            return tuple(b if q == a else a if q == b else q for q in t)
+
+        sh.global_qubits = sw(sh.global_qubits)
+        sh.local_qubits = sw(sh.local_qubits)
 
     def flush(self):
         sh = self.sh
@@ -477,6 +817,9 @@ class _Runner:
         kind = _kind(spec)
         targets, controls = tuple(spec.targets), tuple(spec.controls)
         glob = set(sh.global_qubits)
+        if kind is GateKind.SWAP and not controls and self.relabel_swaps:
+            self._relabel(*targets)
+            return
         if kind is GateKind.SWAP and not controls and (set(targets) & glob):
             self.flush()
             self._swap(targets)
@@ -606,36 +949,46 @@ def run_sharded(circuit: Circuit, n_shards: int, initial: StateVector | None = N
                 cache: dict | None = None, exec_plan: ExecutionPlan | None = None) -> ShardedState:
     """Plan + execute; returns the ShardedState (no gather).  `cache` keeps the per-shard fused
     plans (and their compiled kernels) across calls with the same circuit."""
-    exec_plan = exec_plan or plan(circuit, n_shards, global_qubits)
+    exec_plan = exec_plan or _default_plan(circuit, n_shards, global_qubits)
     comm = comm or LocalComm()
     backend = backend or CudaBackend(precision if initial is None else initial.precision)
     prec = precision if initial is None else initial.precision
     sh = _make_sharded(initial, exec_plan.global_qubits, comm, backend, prec, circuit.n_qubits)
-    runner = _Runner(sh, cache)
+    _run_steps(sh, circuit, exec_plan, cache)
+    return sh
+
+
+# QSB_SHARD_PLANNER=reference selects the reference's one-qubit Belady schedule (sharding.py:
+# 152-216; reshuffle counts equal the reference's); the default is the batched schedule.
+SHARD_PLANNER = os.environ.get("QSB_SHARD_PLANNER", "batched")
+
+
+def _default_plan(circuit, n_shards, global_qubits=None, local_order=None):
+    if SHARD_PLANNER == "reference":
+        return plan(circuit, n_shards, global_qubits)
+    return plan_batched(circuit, n_shards, global_qubits, local_order)
+
+
+def _run_steps(sh, circuit, exec_plan, cache):
+    runner = _Runner(sh, cache, relabel_swaps=exec_plan.relabel_swaps)
     for step in exec_plan.steps:
         if isinstance(step, Reshuffle):
             runner.flush()
             reshuffle(sh, step.global_qubit, step.local_qubit)
+        elif isinstance(step, Exchange):
+            runner.flush()
+            exchange(sh, step.pairs)
         else:
             for pos in step.positions:
                 runner.apply(circuit.queue[pos], pos)
     runner.flush()
-    return sh
 
 
 def apply_sharded(sharded: ShardedState, circuit: Circuit, cache: dict | None = None) -> ShardedState:
     """Run `circuit` on an existing sharded state in place: planned from its current global
     qubits, the state stays sharded (no partition / gather around the circuit)."""
-    exec_plan = plan(circuit, 1 << sharded.n_global, sharded.global_qubits)
-    runner = _Runner(sharded, cache)
-    for step in exec_plan.steps:
-        if isinstance(step, Reshuffle):
-            runner.flush()
-            reshuffle(sharded, step.global_qubit, step.local_qubit)
-        else:
-            for pos in step.positions:
-                runner.apply(circuit.queue[pos], pos)
-    runner.flush()
+    exec_plan = _default_plan(circuit, 1 << sharded.n_global, sharded.global_qubits, sharded.local_qubits)
+    _run_steps(sharded, circuit, exec_plan, cache)
     return sharded
 
 
@@ -705,6 +1058,47 @@ def expectation_sharded(h, sharded: ShardedState) -> float:
             reshuffle(sharded, q, cand)
         total += local_sum(rest)
     return total
+
+
+def _shard_vdot(a, b, precision) -> complex:
+    from .state import _scalar_buffer
+
+    out = _scalar_buffer(2)
+    nat.check(nat.lib().qsb_vdot(a.data_ptr(), b.data_ptr(), a.numel(), precision.qsb_dtype, out.data_ptr(),
+                                 nat.stream_ptr()), "shard vdot")
+    re, im = out.tolist()
+    return complex(re, im)
+
+
+def norm_sharded(sharded: ShardedState) -> float:
+    """Euclidean norm of a sharded state (state.py:109-111): per-shard device sums of |x|^2,
+    summed over ranks; no gather."""
+    acc = 0.0
+    for t in sharded.shards.values():
+        acc += _shard_vdot(t, t, sharded.precision).real
+    return math.sqrt(_allreduce_sum(sharded.comm, acc))
+
+
+def overlap_sharded(target, sharded: ShardedState) -> complex:
+    """<target|psi> of a sharded state (state.py:114-122) without gathering psi.  `target`: a
+    ShardedState of the same qubits (both are brought to the canonical layout) or a StateVector
+    (partitioned into psi's canonical layout)."""
+    if target.n_qubits != sharded.n_qubits:
+        raise ShapeError(f"qubit counts differ: {target.n_qubits} vs {sharded.n_qubits}")
+    if target.precision is not sharded.precision:
+        raise ValueError("cannot mix f32 and f64 states in one operation")
+    canonicalize(sharded)
+    if isinstance(target, ShardedState):
+        canonicalize(target)
+        tgt = target
+    else:
+        tgt = partition(target, sharded.global_qubits, sharded.comm, sharded.backend)
+    re = im = 0.0
+    for s_id, t in sharded.shards.items():
+        v = _shard_vdot(tgt.shards[s_id], t, sharded.precision)
+        re += v.real
+        im += v.imag
+    return complex(_allreduce_sum(sharded.comm, re), _allreduce_sum(sharded.comm, im))
 
 
 def canonicalize(sharded: ShardedState) -> None:
@@ -830,7 +1224,7 @@ def execute_distributed(circuit: Circuit, precision: Precision = Precision.F64, 
     return run_sharded(circuit, comm.world, None, precision, global_qubits, comm)
 
 
-__all__ = ["ExecutionPlan", "LocalSegment", "Reshuffle", "ShardedState", "apply_sharded", "canonicalize",
-           "execute_distributed", "execute_sharded", "expectation_sharded", "gather", "partition", "plan", "reshuffle",
+__all__ = ["Exchange", "ExecutionPlan", "LocalSegment", "Reshuffle", "exchange", "plan_batched", "ShardedState", "apply_sharded", "canonicalize",
+           "execute_distributed", "execute_sharded", "expectation_sharded", "gather", "norm_sharded", "overlap_sharded", "partition", "plan", "reshuffle",
            "sample_sharded", "uniform_sharded"]
 _ = (_check_cap, zero_state, diag_terms, NGate)

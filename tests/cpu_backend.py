@@ -58,6 +58,30 @@ class CpuBackend:
         idx = torch.from_numpy(self._half_index(n_local, bit, half)[first:first + count])
         shard[idx] = staging[:count]
 
+    @staticmethod
+    def _part_index(n_local, bits, part_bits):
+        occ = sorted(bits)
+        e = np.arange(1 << (n_local - len(bits)), dtype=np.int64)
+        for p in occ:  # open a zero bit at each position, ascending (gates.py:355-360)
+            low = e & ((1 << p) - 1)
+            e = ((e ^ low) << 1) | low
+        return e | part_bits
+
+    def exchange_parts(self, a, b, n_local, bits, a_bits, b_bits):
+        ia = torch.from_numpy(self._part_index(n_local, bits, a_bits))
+        ib = torch.from_numpy(self._part_index(n_local, bits, b_bits))
+        tmp = a[ia].clone()
+        a[ia] = b[ib]
+        b[ib] = tmp
+
+    def pack_part(self, shard, n_local, bits, part_bits, first, count, staging):
+        idx = torch.from_numpy(self._part_index(n_local, bits, part_bits)[first:first + count])
+        staging[:count] = shard[idx]
+
+    def unpack_part(self, shard, n_local, bits, part_bits, first, count, staging):
+        idx = torch.from_numpy(self._part_index(n_local, bits, part_bits)[first:first + count])
+        shard[idx] = staging[:count]
+
     def permute(self, src, n_bits, dst_bit):
         i = np.arange(1 << n_bits, dtype=np.int64)
         j = np.zeros_like(i)

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4])
 def test_distributed_ranks_on_one_gpu(cuda, world):
     env = dict(os.environ, QSB_EXCHANGE_CHUNK_BYTES=str(1 << 15))
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone", "--nnodes=1",

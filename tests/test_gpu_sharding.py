@@ -157,3 +157,31 @@ def test_cli_evolve_sharded_energy(cuda, capsys):
     assert cli.main(["evolve", "--nqubits", "10", "--dt", "0.1", "--T", "1.0", "--shards", "4"]) == 0
     four = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
     assert abs(one["final_energy"] - four["final_energy"]) <= 1e-10
+
+
+@pytest.mark.parametrize("window", [1, 3, None])
+def test_resident_evolution_callbacks_and_windows(cuda, window):
+    """Callbacks during a resident sharded evolution (evaluated at t = 0 and after every step
+    without a gather, as evolution.py:339-347 does on the full state) and windows of several
+    Trotter steps scheduled together: the state, the energies and the overlaps equal the 1-GPU
+    evolution's."""
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200 import sharding as sd
+
+    n, shards = 12, 8
+    h0, h1 = q.build_x(n), q.build_tfim(n, 1.0)
+    cfg = q.EvolutionConfig(q.Solver.TROTTER, 0.1, 0.75)  # 7 full steps + a remainder step
+    target = q.uniform_state(n)
+    cb1 = [q.EnergyCallback(h1), q.OverlapCallback(target)]
+    want = q.adiabatic_evolve(h0, h1, q.Schedule.linear(), cfg, callbacks=cb1)
+    if window == 1:
+        cb2 = [q.EnergyCallback(h1), q.OverlapCallback(target)]
+        sh = q.adiabatic_evolve_sharded(h0, h1, q.Schedule.linear(), cfg, n_shards=shards, callbacks=cb2)
+        for a, b in zip(cb1, cb2):
+            assert len(a.records) == len(b.records) == 9
+            assert np.max(np.abs(np.array(a.records) - np.array(b.records))) <= 1e-10
+    else:
+        sh = q.adiabatic_evolve_sharded(h0, h1, q.Schedule.linear(), cfg, n_shards=shards, window=window)
+    assert abs(sd.norm_sharded(sh) - 1.0) <= 1e-12
+    assert abs(sd.overlap_sharded(target, sh) - q.overlap(target, want)) <= 1e-12
+    assert max_abs(sd.gather(sh).amplitudes, want.amplitudes) <= 1e-12

@@ -98,9 +98,76 @@ def test_plan_rules():
     assert (moves[0].global_qubit, moves[0].local_qubit) == (3, 2)
 
 
-# ------------------------------------------------------------------ in-process runner on CPU
+def _trotter(n, steps):
+    from paper_2009_01845_b200 import build_tfim, build_x, combine
+    from paper_2009_01845_b200.evolution import trotter_step_circuit
+
+    c = Circuit(n)
+    for k in range(steps):
+        s = (k + 0.5) / steps
+        c.add(list(trotter_step_circuit(combine(build_x(n), 1 - s, build_tfim(n, 1.0), s), 0.05).queue))
+    return c
+
+
+def _check_batched_plan(c, shards):
+    """Replay a batched plan: every gate runs exactly once, after its DAG predecessors, with its
+    required qubits local; exchanges pair current globals with current locals."""
+    p = sd.plan_batched(c, shards)
+    g = shards.bit_length() - 1
+    glob, loc = list(p.global_qubits), [q for q in range(c.n_qubits) if q not in p.global_qubits]
+    preds = sd._gate_dag(c.queue)
+    seen = set()
+    for st in p.steps:
+        if isinstance(st, sd.Exchange):
+            assert 1 <= st.k <= g
+            for a, b in st.pairs:
+                assert a in glob and b in loc
+                glob[glob.index(a)], loc[loc.index(b)] = b, a
+            continue
+        for pos in st.positions:
+            assert pos not in seen and preds[pos] <= seen
+            assert not set(sd._required_local_batched(c.queue[pos])) & set(glob)
+            spec = c.queue[pos]
+            if sd._is_free_swap(spec):
+                a, b = spec.targets
+                for lst in (glob, loc):
+                    for i, x in enumerate(lst):
+                        lst[i] = b if x == a else a if x == b else x
+            seen.add(pos)
+    assert seen == set(range(len(c.queue)))
+    return p
+
+
 @pytest.mark.parametrize("shards", [2, 4, 8])
-def test_local_runner_qft_and_random(shards):
+def test_batched_plan_valid_and_fewer_exchanges(shards):
+    """The all-to-all schedule never needs more data-moving steps (or bytes) than the
+    reference's one-qubit Belady plan, and at 8 shards a TFIM Trotter step needs one exchange
+    where the reference needs 15 ('Communication vs compute')."""
+    from paper_2009_01845_b200 import random_grid_circuit, variational_circuit
+
+    rng = np.random.default_rng(5)
+    cases = [qft_circuit(12), random_grid_circuit(3, 4, 8, 42), _trotter(12, 2),
+             variational_circuit(12, 3, rng.uniform(0, 6, 12 * 7), fused=True), random_circuit(10, 60, 9)]
+    for c in cases:
+        bat = _check_batched_plan(c, shards)
+        ref = sd.plan(c, shards)
+        assert bat.n_exchanges <= ref.n_reshuffles
+        assert bat.shard_fraction_moved() <= ref.shard_fraction_moved() + 1e-12
+    if shards == 8:
+        one = _trotter(34, 1)
+        assert sd.plan(one, 8).n_reshuffles == 15
+        assert _check_batched_plan(one, 8).n_exchanges == 1
+
+
+# ------------------------------------------------------------------ in-process runner on CPU
+@pytest.fixture(params=["batched", "reference"])
+def planner(request, monkeypatch):
+    monkeypatch.setattr(sd, "SHARD_PLANNER", request.param)
+    return request.param
+
+
+@pytest.mark.parametrize("shards", [2, 4, 8])
+def test_local_runner_qft_and_random(shards, planner):
     n = 8
     assert max_abs(run_cpu(qft_circuit(n), shards), oracle_of(qft_circuit(n))) <= 1e-12
     for seed in range(6):
@@ -109,7 +176,7 @@ def test_local_runner_qft_and_random(shards):
         assert max_abs(run_cpu(c, shards, psi), oracle_of(c, psi)) <= 1e-12
 
 
-def test_local_runner_special_cases():
+def test_local_runner_special_cases(planner):
     n = 5
     psi = rand_state(n, 3)
     cases = [
@@ -119,6 +186,8 @@ def test_local_runner_special_cases():
         (Circuit(n).add([X(2, controls=(0, 1)), RY(3, 0.7, controls=(1,))]), (0, 1)),
         (Circuit(n).add([CZ(0, 1), CZPow(0, 1, 1.3, controls=(2,))]), (0, 1)),  # all-global phases
         (Circuit(n).add([H(0), H(1), H(2), H(0), H(1), H(2)]), (0,)),  # forced reshuffles
+        (Circuit(n).add([H(0), H(1), H(2), H(3), H(4), H(0), H(1)]), (0, 1, 2)),  # 3-qubit exchanges
+        (Circuit(n).add([SWAP(0, 4), H(0), SWAP(1, 3), RY(1, 0.3), SWAP(0, 1), H(4)]), (0, 1)),  # relabels
     ]
     for c, globs in cases:
         shards = 1 << len(globs)
@@ -134,9 +203,10 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, planner="batched"):
     import torch.distributed as dist
 
+    sd.SHARD_PLANNER = planner
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -173,11 +243,11 @@ def _worker(rank, world, port, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_distributed_gloo(world, tmp_path):
+@pytest.mark.parametrize("world,planner", [(2, "batched"), (4, "batched"), (4, "reference")])
+def test_distributed_gloo(world, planner, tmp_path):
     import torch.multiprocessing as mp
 
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), planner), nprocs=world, join=True)
     for r in range(world):
         res = json.load(open(tmp_path / f"r{r}.json"))
         for name, err in res.items():

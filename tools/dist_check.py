@@ -30,6 +30,14 @@ class HostStagedComm(sd.TorchComm):
         recv.copy_(hr)
         return []
 
+    def ialltoall(self, triples):
+        staged = [(send.cpu(), torch.empty(send.shape, dtype=send.dtype), recv, peer) for send, recv, peer in triples]
+        for w in super().ialltoall([(hs, hr, peer) for hs, hr, _, peer in staged]):
+            w.wait()
+        for _, hr, recv, _ in staged:
+            recv.copy_(hr)
+        return []
+
     def all_gather(self, t):
         return [x.cuda() for x in super().all_gather(t.cpu())]
 
