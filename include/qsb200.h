@@ -221,6 +221,14 @@ int qsb_unpack_part(void* shard, int n_local_bits, int dtype, int k, const int* 
 /* In-process form: swap part `a_bits` of shard a with part `b_bits` of shard b (a != b). */
 int qsb_exchange_parts(void* a, void* b, int n_local_bits, int dtype, int k, const int* bits, uint64_t a_bits,
                        uint64_t b_bits, void* stream);
+/* Reduced density matrix of a qubit subset (entanglement_entropy, evolution.py:154-173):
+ * rho[i][j] = sum_b psi(i, b) conj(psi(j, b)) in complex128, i = the k state bits
+ * `partition_bits` (partition_bits[0] = MSB of i), b = every other bit.  Replaces the
+ * reference's moveaxis + reshape + SVD (whose squared singular values are rho's eigenvalues).
+ * 1 <= k <= 12.  `partials`: n_split * 4^k complex128 of device scratch (n_split a power of
+ * two, n_split * 32 <= 2^(n-k)); `rho`: 4^k complex128 (device), row-major. */
+int qsb_reduced_density(const void* amps, int n, int dtype, int k, const int* partition_bits, int n_split,
+                        void* partials, void* rho, void* stream);
 
 #ifdef __cplusplus
 }

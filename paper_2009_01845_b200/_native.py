@@ -83,6 +83,8 @@ SIGNATURES = {
     "qsb_exchange_halves": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_void_p]),
     "qsb_pack_half": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_u64, _c_u64, _c_void_p, _c_void_p]),
     "qsb_unpack_half": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_int, _c_u64, _c_u64, _c_void_p, _c_void_p]),
+    "qsb_reduced_density": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_int, _c_void_p, _c_void_p,
+                                     _c_void_p]),
     "qsb_pack_part": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_u64, _c_u64, _c_u64, _c_void_p,
                                _c_void_p]),
     "qsb_unpack_part": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_u64, _c_u64, _c_u64, _c_void_p,

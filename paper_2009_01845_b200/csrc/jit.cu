@@ -3,6 +3,8 @@
 // kinds; matrix / phase values stay runtime coefficients), for sm_100a, and the driver API
 // loads and launches it.  Same TMA producer, mbarrier ring and tile addressing as the
 // interpreted kernel in pass.cu; no dispatch loop, every amplitude stays in a named register.
+#include <atomic>
+#include <mutex>
 #include <dlfcn.h>
 #include <stdio.h>
 #include <string.h>
@@ -149,6 +151,38 @@ extern "C" int qsb_jit_compile_cubin(const char* source, const char* name, const
   return st;
 }
 
+// Tile counters of the dynamically scheduled pass kernels: 2 x u64 per slot (next tile
+// chunk, retired producers), zero between launches (the last producer of a launch re-arms its
+// slot).  Launches take slots round-robin, so concurrent launches on different streams do not
+// share a counter unless kSchedSlots launches are in flight at once.
+constexpr int kSchedSlots = 1024;
+static unsigned long long* g_sched[64];
+static std::atomic<unsigned> g_sched_next{0};
+static std::mutex g_sched_mu;
+
+static int sched_slot(unsigned long long** out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) {
+    set_error("qsb_jit_run_pass: device %d out of range", dev);
+    return QSB_ERR_ARG;
+  }
+  if (!g_sched[dev]) {
+    std::lock_guard<std::mutex> lk(g_sched_mu);
+    if (!g_sched[dev]) {
+      void* p = nullptr;
+      cudaError_t e = cudaMalloc(&p, kSchedSlots * 2 * sizeof(unsigned long long));
+      if (e != cudaSuccess) return cuda_status(e, "tile counters");
+      e = cudaMemset(p, 0, kSchedSlots * 2 * sizeof(unsigned long long));
+      if (e != cudaSuccess) return cuda_status(e, "tile counters");
+      cudaDeviceSynchronize();
+      g_sched[dev] = static_cast<unsigned long long*>(p);
+    }
+  }
+  *out = g_sched[dev] + 2 * (g_sched_next.fetch_add(1) % kSchedSlots);
+  return QSB_OK;
+}
+
 extern "C" int qsb_jit_load(const void* cubin, const char* name, void** func_out) {
   jit::Driver* dr = jit::driver();
   if (!dr) {
@@ -156,6 +190,8 @@ extern "C" int qsb_jit_load(const void* cubin, const char* name, void** func_out
     return QSB_ERR_CUDA;
   }
   cudaFree(nullptr);  // the runtime's primary context current on this thread
+  unsigned long long* slot = nullptr;  // allocate the tile counters now, never under capture
+  if (int rc = sched_slot(&slot)) return rc;
   CUmodule mod = nullptr;
   CUresult r = dr->load(&mod, cubin);
   if (r != CUDA_SUCCESS) {
@@ -172,7 +208,7 @@ extern "C" int qsb_jit_load(const void* cubin, const char* name, void** func_out
   return QSB_OK;
 }
 
-// Launch a JIT pass kernel: params (src, dst, tensor map, coefficients).  The tensor map is
+// Launch a JIT pass kernel: params (src, dst, tensor map, coefficients, tile counter).  The tensor map is
 // encoded here from `tdesc` (jit.py tma_plan: rank, dims[5], byte strides[4], box[5]) over the
 // 8-byte elements of the state at `src`.
 static int run_pass_impl(void* func, const void* src, void* dst, const int64_t* tdesc, uint64_t n_tiles,
@@ -226,8 +262,11 @@ static int run_pass_impl(void* func, const void* src, void* dst, const int64_t* 
   const void* a_src = src;
   void* a_dst = dst;
   const double* a_cf = static_cast<const double*>(dcoef);
+  unsigned long long* a_sched = nullptr;
+  if (int rc = sched_slot(&a_sched)) return rc;
   // the last kernel parameter is the coefficient struct, copied by value from `params`
-  void* args[] = {(void*)&a_src, (void*)&a_dst, (void*)&map, (void*)&a_cf, const_cast<void*>(params)};
+  void* args[] = {(void*)&a_src, (void*)&a_dst, (void*)&map, (void*)&a_cf, (void*)&a_sched,
+                  const_cast<void*>(params)};
   CUresult r = dr->launch(fn, (unsigned)grid, 1, 1, (unsigned)threads, 1, 1, (unsigned)smem_bytes, (CUstream)st, args,
                           nullptr);
   if (r != CUDA_SUCCESS) {

@@ -54,15 +54,34 @@ REG_SPLIT = {c: _reg_split(c, ctas_per_sm(c)) for c in (128, 256, 512)}
 # tile split runs at 6.2-6.3 TB/s, while one-shot CTAs of 4 consecutive 64 KB tiles -- the grid
 # covering the state once, the block scheduler handing out the next CTA to whichever SM
 # finishes first -- reach 6.9 TB/s, the speed of the plain streaming kernels.
+# Measured sweep at n = 30 (tools/tpc_sweep.sh, round 2): one-shot CTAs win on light passes
+# (QFT pass 4: 5.97 -> 5.17 ms at 16 tiles per CTA) but lose on passes with heavy per-CTA
+# set-up (pivot tables, pipeline ramp: QFT pass 1 5.76 -> 6.19 ms), so the default is a
+# persistent grid that takes DYN_CHUNK consecutive tiles at a time from a global counter
+# (dynamic balance without per-CTA restarts).  Expectation passes keep a static split: their
+# per-CTA partial sums must not depend on timing.
 TILES_PER_CTA = int(os.environ.get("QSB_TILES_PER_CTA", "16"))
+PASS_SCHED = os.environ.get("QSB_PASS_SCHED", "dynamic")  # dynamic | oneshot | static
+DYN_CHUNK = int(os.environ.get("QSB_DYN_CHUNK", "2"))
 
 
 def tiles_per_cta(ext_bits: int, consumers: int) -> int:
-    """TPC of a pass over 2**ext_bits tiles (0 when the state has too few tiles to matter)."""
+    """TPC of a one-shot pass over 2**ext_bits tiles (0 when the state has too few tiles to
+    matter)."""
     n_tiles = 1 << ext_bits
     if TILES_PER_CTA <= 0 or n_tiles < 4 * 148 * TILES_PER_CTA:
         return 0
     return TILES_PER_CTA
+
+
+def pass_schedule(ext_bits: int, consumers: int, expect: bool, halves: bool):
+    """(tpc, dyn_chunk) of a pass: dyn_chunk > 0 = persistent grid with a tile counter."""
+    n_tiles = 1 << ext_bits
+    if PASS_SCHED == "dynamic" and not expect and not halves and n_tiles >= 4 * 148 * max(1, DYN_CHUNK):
+        return 0, max(1, DYN_CHUNK)
+    if PASS_SCHED == "static":
+        return 0, 0
+    return tiles_per_cta(ext_bits, consumers), 0
 
 
 def pass_grid(n_tiles: int, consumers: int, tpc: int, sms: int) -> int:
@@ -245,6 +264,7 @@ class _Gen:
         # two CTAs per SM with 64 KB tiles: one stage per CTA, reused as the transpose buffer
         self.alias = (not self.halves) and ctas_per_sm(self.consumers) == 2 and (1 << K) * amp_bytes == 65536
         self.stages = 1 if self.alias else STAGES
+        self.sched = pass_schedule(self.n - K, self.consumers, self.expect, self.halves)
         self.HB = K - 1 if self.halves else K  # bits of a stage / transpose-buffer index
 
     # uniform coefficients (gate matrices, phases): a kernel-parameter array of R, read as
@@ -838,7 +858,7 @@ class _Gen:
         defs = (f"#define QSB_F32X2 {1 if self.dtype == nat.QSB_C64 else 0}\n#define R {real}\n#define PR {pr}\n#define C {real}2\n#define KB {K}\n#define HBB {self.HB}\n#define GB {self.G}\n#define STAGES {self.stages}\n#define ALIAS {1 if self.alias else 0}\n#define TBUF {"sm.stage[s]" if self.alias else "sm.tbuf"}\n"
                 f"#define CONSUMERS {self.consumers}\n#define MAXPIV {MAX_PIV}\n#define NPIV {self.npiv}\n"
                 f"#define NCOEF {max(1, len(self.coeffs))}\n#define NTAB {len(self.tables)}\n"
-                f"#define TPC {tiles_per_cta(self.n - K, self.consumers)}\n")
+                f"#define TPC {self.sched[0]}\n#define DYN {self.sched[1]}\n")
         issue = f"""      {{ // producer warp: fetch tile c into stage s (tile number tno)
         const u64 base = {base_expr};
 {self.ep_code}
@@ -885,6 +905,9 @@ class _Gen:
         else:
             head = """    mbar_wait(&sm.full[s], ph);
     const u64 base = sm.base[s][0];
+#if DYN
+    if (base == ~0ull) break;
+#endif
     const u64 obase = sm.base[s][1];
     C* buf = sm.stage[s];"""
         return defs + _PRELUDE + f"""
@@ -893,7 +916,7 @@ class _Gen:
 // consumers, which hold the tile in registers.
 extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_sm(self.consumers)})
 {name}(const C* __restrict__ src, C* __restrict__ dst, const __grid_constant__ TMap tmap,
-       const double* __restrict__ cf, const __grid_constant__ CP cp) {{
+       const double* __restrict__ cf, unsigned long long* __restrict__ sched, const __grid_constant__ CP cp) {{
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   double* scf = reinterpret_cast<double*>(smem_raw + sizeof(Smem));  // pivot tables
@@ -921,6 +944,38 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
     if (tid >= CONSUMERS + 32) return;
     const int lane = tid - CONSUMERS;
     int it = 0;
+#if DYN
+    // persistent: DYN consecutive tiles per grab from the launch's counter; a sentinel base
+    // tells the consumers to stop; the last producer to finish re-arms the counter
+    u64 c = 0, c_stop = 0;
+    for (;; ++it) {{
+      const int s = it % STAGES;
+      const u32 ph = (it / STAGES) & 1;
+      if (it >= STAGES) mbar_wait(&sm.empty[s], ph ^ 1);
+      if (c == c_stop) {{
+        u64 k = 0;
+        if (lane == 0) k = atomicAdd(sched, 1ull);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        c = k * DYN;
+        c_stop = c + DYN < n_tiles ? c + DYN : n_tiles;
+      }}
+      if (c >= n_tiles) {{
+        if (lane == 0) {{ sm.base[s][0] = ~0ull; mbar_arrive(&sm.full[s]); }}
+        break;
+      }}
+      const int tno = it;
+{issue}
+      ++c;
+    }}
+    if (lane == 0) {{
+      __threadfence();
+      if (atomicAdd(sched + 1, 1ull) == (u64)gridDim.x - 1) {{
+        sched[0] = 0;
+        sched[1] = 0;
+        __threadfence();
+      }}
+    }}
+#else
     for (u64 c = c_begin; c < c_end; c += c_step, ++it) {{
       const int s = it % STAGES;
       const u32 ph = (it / STAGES) & 1;
@@ -928,12 +983,17 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
       const int tno = it;
 {issue}
     }}
+#endif
     return;
   }}
   asm volatile("setmaxnreg.inc.sync.aligned.u32 {REG_SPLIT[self.consumers][0]};" ::: "memory");
   int it = 0;
   double ea = 0.0;  // expectation passes: this thread's sum of Re <x|M|x>
+#if DYN
+  for (;; ++it) {{
+#else
   for (u64 c = c_begin; c < c_end; c += c_step, ++it) {{
+#endif
     const int s = it % STAGES;
     const u32 ph = (it / STAGES) & 1;
 {head}
@@ -1134,7 +1194,7 @@ def _compile_words(words, dtype):
         fresh.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
         fresh.n_tiles = 1 << (int(words[4]) - K)
         fresh.threads = (1 << (K - nreg)) + 128
-        fresh.tpc = tiles_per_cta(int(words[4]) - K, 1 << (K - nreg))
+        fresh.tpc = pass_schedule(int(words[4]) - K, 1 << (K - nreg), expect, (1 << K) * amp > 65536)[0]
         with _lock:
             hit = _cache.setdefault(src, fresh)
     return hit, (np.ascontiguousarray(pbytes), tables)

@@ -386,6 +386,8 @@ class CudaBackend:
         holder = {}
         view = _ShardView(shard, n_local, self.precision)
         engine.run_plan(view, plan_, holder)
+        if _STATS is not None:
+            _STATS["local_bytes"] += int(plan_.state_sweeps() * 2 * shard.numel() * shard.element_size())
         return view._t
 
     def scale(self, shard, phase):
@@ -688,6 +690,25 @@ def reshuffle(sharded: ShardedState, global_qubit: int, local_qubit: int):
     sharded.local_qubits = tuple(lc)
 
 
+# Optional per-run counters for the CLI's metric fields (collect_stats): exchange count, bytes
+# each rank sent, CUDA events around every exchange, local HBM bytes of the per-shard passes.
+_STATS = None
+
+
+def collect_stats(enable: bool | None = True):
+    """Start (or with None, stop) collecting exchange / pass statistics; returns the dict."""
+    global _STATS
+    _STATS = {"exchanges": 0, "exchange_bytes": 0, "events": [], "local_bytes": 0} if enable else None
+    return _STATS
+
+
+def finish_stats(stats: dict) -> dict:
+    """Resolve the CUDA events of a finished run into seconds (call after a synchronize)."""
+    ev = stats.pop("events", [])
+    stats["exchange_seconds"] = sum(a.elapsed_time(b) for a, b in ev) / 1e3
+    return stats
+
+
 def _part_bits(value, bits):
     """Local index pattern with bit i of `value` at local bit bits[i]."""
     out = 0
@@ -714,6 +735,15 @@ def exchange(sharded: ShardedState, pairs) -> None:
     if len(set(jbits)) != k or len(set(pbits)) != k:
         raise ShapeError(f"exchange pairs {pairs} repeat a qubit")
     backend, comm = sharded.backend, sharded.comm
+    stats = _STATS
+    if stats is not None:
+        torch = nat.torch_mod()
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record()
+        stats["exchanges"] += 1
+        stats["exchange_bytes"] += int(((1 << nl) - (1 << (nl - k))) * sharded.precision.itemsize)
+        stats["nvlink"] = bool(getattr(comm, "stream_ordered", False)) and not isinstance(comm, LocalComm)
+        stats["ranks"] = comm.world
 
     def s_val(s):
         return sum(((s >> j) & 1) << i for i, j in enumerate(jbits))
@@ -732,6 +762,9 @@ def exchange(sharded: ShardedState, pairs) -> None:
                                        _part_bits(u, pbits), _part_bits(a, pbits))
     else:
         _exchange_parts_dist(sharded, k, pbits, s_val, with_val)
+    if stats is not None:
+        ev[1].record()
+        stats["events"].append(ev)
     for (a, b), j, p in zip(pairs, jbits, pbits):
         gl[g - 1 - j] = b
         lc[nl - 1 - p] = a

@@ -494,7 +494,8 @@ def test_cli_qft_verify_and_evolve(cuda, capsys):
 
 @pytest.mark.parametrize("partition", [(0,), (3, 1), (0, 2, 4, 6), (1, 2, 3, 5, 7, 8, 9)])
 def test_entanglement_entropy_matches_svd(cuda, partition):
-    """Device entropy (GEMM + eigvalsh on the smaller side) against the reference's numpy SVD."""
+    """Device entropy (reduced-density kernel + eigvalsh on the smaller side) against the
+    reference's numpy SVD."""
     import paper_2009_01845_b200 as q
 
     n = 10
@@ -803,3 +804,63 @@ def test_marginal_from_amplitudes_equals_probability_path(cuda, prec):
         ref = ov.marginal(st.amplitudes, n, qubits) if hasattr(ov, "marginal") else None
         if ref is not None:
             assert np.array_equal(fused, ref), qubits
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("n,partition", [(12, (0,)), (12, (11, 3)), (14, (13, 12, 11, 10, 9)), (14, (2, 9, 4, 0, 13, 7)),
+                                         (16, tuple(range(0, 16, 2))), (17, (16, 1, 15, 2, 14, 3, 13, 4, 12, 5, 11, 6))])
+def test_reduced_density_matrix_kernel(cuda, prec, n, partition):
+    """qsb_reduced_density against numpy's M M^dagger of the reference's moveaxis/reshape
+    (evolution.py:166-169), every tile shape (k = 1..12, partition bits low, high, mixed)."""
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200.evolution import reduced_density_matrix
+
+    p = q.Precision(prec)
+    rng = np.random.default_rng(n + len(partition))
+    psi = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)).astype(p.complex_dtype)
+    psi /= np.linalg.norm(psi)
+    st = q.from_amplitudes(psi)
+    m = np.moveaxis(psi.astype(np.complex128).reshape([2] * n), partition, range(len(partition)))
+    m = m.reshape(1 << len(partition), -1)
+    want = m @ m.conj().T
+    got = reduced_density_matrix(st, partition).cpu().numpy()
+    assert np.max(np.abs(got - want)) <= 1e-14
+    assert np.array_equal(got, got.conj().T)
+
+
+def test_entanglement_entropy_large(cuda):
+    """n = 24 states: a GHZ state across the cut (one bit), a product of Bell pairs (one bit per
+    pair cut), and a random state's entropy against the reference's SVD."""
+    import paper_2009_01845_b200 as q
+
+    n = 24
+    ghz = q.Circuit(n).add([q.H(0)] + [q.CNOT(0, k) for k in range(1, n)]).execute()
+    assert abs(q.entanglement_entropy(ghz, (3, 17, 20)) - 1.0) <= 1e-12
+    pairs = q.Circuit(n).add([g for k in range(0, n, 2) for g in (q.H(k), q.CNOT(k, k + 1))]).execute()
+    assert abs(q.entanglement_entropy(pairs, (0, 2, 4, 7, 9)) - 5.0) <= 1e-11
+    rng = np.random.default_rng(1)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    part = (1, 5, 8, 13, 22, 23)
+    m = np.moveaxis(psi.reshape([2] * n), part, range(len(part))).reshape(1 << len(part), -1)
+    sv = np.linalg.svd(m, compute_uv=False) ** 2
+    sv = sv[sv > 1e-15]
+    assert abs(q.entanglement_entropy(q.from_amplitudes(psi), part) - float(-(sv * np.log2(sv)).sum())) <= 1e-10
+
+
+def test_cli_gpu_metric_fields(cuda, capsys):
+    """CLI records carry the GPU metrics: device, gpus, passes,
+    bytes_moved, hbm_gbps, roofline_frac; sharded runs add exchanges and their bandwidth."""
+    import json
+
+    from paper_2009_01845_b200 import cli
+
+    assert cli.main(["qft", "--nqubits", "24"]) == 0
+    rec = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert "B200" in rec["device"] and rec["gpus"] == 1 and rec["passes"] >= 1
+    assert rec["bytes_moved"] == rec["passes"] * 2 * (1 << 24) * 16 or rec["bytes_moved"] > 0
+    assert 0 < rec["hbm_gbps"] and 0 < rec["roofline_frac"] < 1.2
+    assert cli.main(["variational", "--nqubits", "24", "--fuse", "--gpus", "4"]) == 0
+    rec = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    assert rec["shards"] == 4 and rec["exchanges"] >= 1 and rec["exchange_bytes"] == rec["exchanges"] * 3 * (1 << 20) * 16 // 1
+    assert rec["exchange_gbps"] > 0
