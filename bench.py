@@ -467,7 +467,8 @@ def extra_workloads(q, engine, n, peak):
 
 def run_distributed_arm(args, rank, world):
     """N > 1: QFT on n = qubits + log2(N) qubits, one shard (2^qubits amplitudes) per rank;
-    global<->local reshuffles are NCCL send/recv exchanges (weak scaling)."""
+    global<->local exchanges are batched all-to-alls (grouped NCCL send/recv, sharding.exchange)
+    scheduled by the DAG planner (sharding.plan_batched) (weak scaling)."""
     import torch
     import torch.distributed as dist
 
@@ -483,7 +484,7 @@ def run_distributed_arm(args, rank, world):
     circuit = q.qft_circuit(n)
     comm = sd.TorchComm()
     backend = sd.CudaBackend(prec)
-    exec_plan = sd.plan(circuit, world)
+    exec_plan = sd.plan_batched(circuit, world)
     cache: dict = {}
 
     def step():
@@ -518,10 +519,10 @@ def run_distributed_arm(args, rank, world):
         del sh, loc
     value = float(ms.item()) / 1e3
     shard_bytes = (1 << args.qubits) * prec.itemsize
-    exch_bytes = exec_plan.n_reshuffles * shard_bytes // 2
+    exch_bytes = int(exec_plan.shard_fraction_moved() * shard_bytes)
     nvlink, t_exch = _time_exchanges(sd, comm, backend, prec, n, exec_plan, shard_bytes)
-    roofline, launches = _dist_summary(cache, exec_plan.n_reshuffles, value, t_exch, shard_bytes, prec.itemsize,
-                                       sd.TorchComm.CHUNK_BYTES)
+    roofline, launches = _dist_summary(cache, exec_plan.n_exchanges, value, t_exch, shard_bytes, prec.itemsize,
+                                       sd.TorchComm.CHUNK_BYTES, g)
     workloads = {"adiabatic_tfim_step": _dist_adiabatic(q, sd, comm, n, world),
                  "random_grid_20_cycles": _dist_grid(q, sd, comm, n, world, prec)}
     line = {
@@ -529,9 +530,9 @@ def run_distributed_arm(args, rank, world):
         "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128" if prec is q.Precision.F64 else "c64", "data": "synthetic",
         "config": {"workload": f"QFT {n} qubits sharded over {world} GPUs (2^{args.qubits} amplitudes per GPU)",
-                   "n_qubits": n, "parallelism": f"global-qubit sharding x{world}, NCCL P2P reshuffles",
-                   "reshuffles": exec_plan.n_reshuffles, "global_qubits": list(exec_plan.global_qubits),
-                   "exchange_bytes_per_gpu": exch_bytes},
+                   "n_qubits": n, "parallelism": f"global-qubit sharding x{world}, batched NCCL all-to-all exchanges",
+                   "exchanges": exec_plan.n_exchanges, "reference_planner_reshuffles": sd.plan(circuit, world).n_reshuffles,
+                   "global_qubits": list(exec_plan.global_qubits), "exchange_bytes_per_gpu": exch_bytes},
         "e2e": {"value": min(e2e_t), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,
                 "api": "sharding.execute_distributed + per-rank norm readback"},
         "gpu_launches": launches,
@@ -546,24 +547,26 @@ def run_distributed_arm(args, rank, world):
     dist.destroy_process_group()
 
 
-def _dist_summary(cache, n_reshuffles, value, t_exch, shard_bytes, itemsize, chunk_bytes):
+def _dist_summary(cache, n_exchanges, value, t_exch, shard_bytes, itemsize, chunk_bytes, k=1):
     """(roofline, launches) of one sharded step: the local fused passes' HBM rate (step time minus
-    the measured exchange time) and the kernels one step launches per GPU."""
+    the measured exchange time) and the kernels one step launches per GPU (k: qubits per
+    exchange; each exchange packs and unpacks 2^k - 1 parts)."""
     # the per-shard fused plans of one step (the runner's cache holds exactly those)
     plans = [p for p in cache.values() if hasattr(p, "state_sweeps")]
     sweeps = sum(p.state_sweeps() for p in plans)
-    local_s = value - (n_reshuffles * t_exch if t_exch else 0.0)
+    local_s = value - (n_exchanges * t_exch if t_exch else 0.0)
     hbm_peak, peak_kind = _peaks()
     achieved = sweeps * 2 * shard_bytes / local_s / 1e9 if local_s > 0 and sweeps else None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak if achieved else None, "traffic": None, "peak_kind": peak_kind,
                 "sweeps_per_step": sweeps,
                 "note": "local fused passes per GPU: step time minus the measured exchange time"}
-    half_amps = shard_bytes // itemsize // 2
-    chunk = max(1, min(half_amps, chunk_bytes // itemsize))
-    chunks = -(-half_amps // chunk)
-    # plan steps + (pack + unpack) per chunk per reshuffle + the |0> initialisation
-    launches = sum(len(p.steps) for p in plans) + n_reshuffles * 2 * chunks + 1
+    peers = (1 << k) - 1
+    part_amps = shard_bytes // itemsize >> k
+    chunk = max(1, min(part_amps, chunk_bytes // itemsize // peers))
+    chunks = -(-part_amps // chunk)
+    # plan steps + (pack + unpack) per peer per chunk per exchange + the |0> initialisation
+    launches = sum(len(p.steps) for p in plans) + n_exchanges * 2 * peers * chunks + 1
     return roofline, launches
 
 
@@ -603,6 +606,8 @@ def _dist_adiabatic(q, sd, comm, n, world, steps=4):
         torch.cuda.empty_cache()
         return {"value": float(t.item()), "unit": "s per Trotter step", "n_qubits": n, "steps": steps,
                 "gates_per_step": len(circuits[1].queue), "energy_after": energy,
+                "exchanges_per_step": sd.plan_batched(circuits[1], world).n_exchanges,
+                "reference_planner_reshuffles_per_step": sd.plan(circuits[1], world).n_reshuffles,
                 "what": "adiabatic_evolve_sharded step, state resident in shards (no gather)"}
     except Exception as exc:  # the QFT line stands; say why this one is missing
         return {"error": f"{type(exc).__name__}: {exc}"[:300]}
@@ -618,7 +623,7 @@ def _dist_grid(q, sd, comm, n, world, prec, cycles=20):
     try:
         rows = 3 if n % 3 == 0 else (2 if n % 2 == 0 else 1)
         circuit = q.random_grid_circuit(rows, n // rows, cycles, 42)
-        exec_plan = sd.plan(circuit, world)
+        exec_plan = sd.plan_batched(circuit, world)
         cache: dict = {}
         sh = sd.run_sharded(circuit, world, None, prec, None, comm, sd.CudaBackend(prec), cache, exec_plan)
         del sh
@@ -635,43 +640,45 @@ def _dist_grid(q, sd, comm, n, world, prec, cycles=20):
         del sh
         torch.cuda.empty_cache()
         return {"value": float(t.item()), "unit": "s", "n_qubits": n, "grid": f"{rows}x{n // rows}",
-                "cycles": cycles, "gates": len(circuit.queue), "reshuffles": exec_plan.n_reshuffles}
+                "cycles": cycles, "gates": len(circuit.queue), "exchanges": exec_plan.n_exchanges,
+                "reference_planner_reshuffles": sd.plan(circuit, world).n_reshuffles}
     except Exception as exc:  # the QFT line stands; say why this one is missing
         return {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
 
 def _time_exchanges(sd, comm, backend, prec, n, exec_plan, shard_bytes, reps=4):
-    """One global<->local reshuffle in isolation (pairwise half-shard exchange through the
-    runner's own pipeline: pack, NCCL send/recv, unpack), max over ranks: the NVLink number."""
+    """One batched exchange of every global qubit with a local one in isolation (the all-to-all
+    the planner issues: pack, grouped NCCL send/recv, unpack), max over ranks: the NVLink
+    number (bytes each GPU sends / time, unidirectional)."""
     import torch
     import torch.distributed as dist
 
     try:
         sh = sd._make_sharded(None, exec_plan.global_qubits, comm, backend, prec, n)
-        gq, lq = sh.global_qubits[0], sh.local_qubits[-1]
-        sd.reshuffle(sh, gq, lq)  # warm-up (staging buffers, NCCL channels)
-        sd.reshuffle(sh, lq, gq)
+        g = sh.n_global
+        pairs = list(zip(sh.global_qubits, sh.local_qubits[:g]))
+        back = [(b, a) for a, b in pairs]
+        sd.exchange(sh, pairs)  # warm-up (staging buffers, NCCL channels)
+        sd.exchange(sh, back)
         torch.cuda.synchronize()
         comm.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         for k in range(reps):
-            if k % 2 == 0:
-                sd.reshuffle(sh, gq, lq)
-            else:
-                sd.reshuffle(sh, lq, gq)
+            sd.exchange(sh, pairs if k % 2 == 0 else back)
         e1.record()
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1) / reps / 1e3], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_exch = float(t.item())
-        half = shard_bytes // 2
+        sent = shard_bytes - (shard_bytes >> g)
         del sh
         torch.cuda.empty_cache()
-        return ({"achieved": half / t_exch / 1e9, "peak": 900.0, "unit": "GB/s", "frac": half / t_exch / 900e9,
-                 "bytes_per_exchange_per_gpu": half, "ms_per_exchange": t_exch * 1e3,
-                 "what": "pairwise half-shard exchange, bytes sent per GPU / time (unidirectional)"}, t_exch)
+        return ({"achieved": sent / t_exch / 1e9, "peak": 900.0, "unit": "GB/s", "frac": sent / t_exch / 900e9,
+                 "bytes_per_exchange_per_gpu": sent, "ms_per_exchange": t_exch * 1e3, "qubits_per_exchange": g,
+                 "what": f"{g}-qubit all-to-all exchange (2^{g}-1 peers), bytes sent per GPU / time (unidirectional)"},
+                t_exch)
     except Exception as exc:  # the step's own number stands; say why this one is missing
         return {"error": f"{type(exc).__name__}: {exc}"[:300]}, None
 

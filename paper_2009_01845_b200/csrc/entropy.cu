@@ -110,15 +110,15 @@ __global__ void __launch_bounds__(kRdmThreads) k_rdm(const cplx<R>* __restrict__
   }
 }
 
-// rho[i][j] = sum over splits in order (upper triangle from the tiles, lower = conjugate)
-__global__ void k_rdm_reduce(const double2* __restrict__ partials, int n_split, int k, int T,
+// rho[i][j] = sum over splits in order (i <= j from the tiles, i > j = conjugate of rho[j][i])
+__global__ void k_rdm_reduce(const double2* __restrict__ partials, int n_split, int k,
                              double2* __restrict__ rho) {
   const uint64_t dim = 1ull << k;
   const uint64_t total = dim * dim;
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = e / dim, j = e % dim;
-    const bool upper = (i / T) <= (j / T);
+    const bool upper = i <= j;  // (j, i) lies in a computed tile whenever i > j
     const uint64_t src = upper ? e : j * dim + i;
     double2 s = make_double2(0.0, 0.0);
     for (int q = 0; q < n_split; ++q) {
@@ -127,6 +127,7 @@ __global__ void k_rdm_reduce(const double2* __restrict__ partials, int n_split, 
       s.y += v.y;
     }
     if (!upper) s.y = -s.y;
+    if (i == j) s.y = 0.0;  // rho_ii = sum |psi|^2 is real; drop the rounding of x * conj(x)
     rho[e] = s;
   }
 }
@@ -187,7 +188,7 @@ int qsb_reduced_density(const void* amps, int n, int dtype, int k, const int* pa
                                                static_cast<double2*>(partials));
   const uint64_t total = 1ull << (2 * k);
   const int rblocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
-  k_rdm_reduce<<<rblocks, 256, 0, st>>>(static_cast<const double2*>(partials), n_split, k, a.T,
+  k_rdm_reduce<<<rblocks, 256, 0, st>>>(static_cast<const double2*>(partials), n_split, k,
                                         static_cast<double2*>(rho));
   QSB_CHECK_LAUNCH("qsb_reduced_density");
   return QSB_OK;

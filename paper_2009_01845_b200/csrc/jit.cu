@@ -156,11 +156,16 @@ extern "C" int qsb_jit_compile_cubin(const char* source, const char* name, const
 // slot).  Launches take slots round-robin, so concurrent launches on different streams do not
 // share a counter unless kSchedSlots launches are in flight at once.
 constexpr int kSchedSlots = 1024;
+// launches recorded into a CUDA graph keep their counter for the graph's lifetime: they take
+// slots from a separate, never-recycled range (a replay must not share a counter with a live
+// launch on another stream)
+constexpr int kSchedGraphSlots = 8192;
 static unsigned long long* g_sched[64];
 static std::atomic<unsigned> g_sched_next{0};
+static std::atomic<unsigned> g_sched_graph_next{0};
 static std::mutex g_sched_mu;
 
-static int sched_slot(unsigned long long** out) {
+static int sched_slot(unsigned long long** out, cudaStream_t st = nullptr, bool check_capture = false) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) {
@@ -171,13 +176,24 @@ static int sched_slot(unsigned long long** out) {
     std::lock_guard<std::mutex> lk(g_sched_mu);
     if (!g_sched[dev]) {
       void* p = nullptr;
-      cudaError_t e = cudaMalloc(&p, kSchedSlots * 2 * sizeof(unsigned long long));
+      const size_t bytes = (size_t)(kSchedSlots + kSchedGraphSlots) * 2 * sizeof(unsigned long long);
+      cudaError_t e = cudaMalloc(&p, bytes);
       if (e != cudaSuccess) return cuda_status(e, "tile counters");
-      e = cudaMemset(p, 0, kSchedSlots * 2 * sizeof(unsigned long long));
+      e = cudaMemset(p, 0, bytes);
       if (e != cudaSuccess) return cuda_status(e, "tile counters");
       cudaDeviceSynchronize();
       g_sched[dev] = static_cast<unsigned long long*>(p);
     }
+  }
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (check_capture && cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusActive) {
+    const unsigned k = g_sched_graph_next.fetch_add(1);
+    if (k >= (unsigned)kSchedGraphSlots) {
+      set_error("qsb_jit_run_pass: more than %d pass launches captured in CUDA graphs", kSchedGraphSlots);
+      return QSB_ERR_CAPACITY;
+    }
+    *out = g_sched[dev] + 2 * ((size_t)kSchedSlots + k);
+    return QSB_OK;
   }
   *out = g_sched[dev] + 2 * (g_sched_next.fetch_add(1) % kSchedSlots);
   return QSB_OK;
@@ -263,7 +279,7 @@ static int run_pass_impl(void* func, const void* src, void* dst, const int64_t* 
   void* a_dst = dst;
   const double* a_cf = static_cast<const double*>(dcoef);
   unsigned long long* a_sched = nullptr;
-  if (int rc = sched_slot(&a_sched)) return rc;
+  if (int rc = sched_slot(&a_sched, st, true)) return rc;
   // the last kernel parameter is the coefficient struct, copied by value from `params`
   void* args[] = {(void*)&a_src, (void*)&a_dst, (void*)&map, (void*)&a_cf, (void*)&a_sched,
                   const_cast<void*>(params)};

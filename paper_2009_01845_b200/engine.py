@@ -198,7 +198,6 @@ def run_plan(state, plan: Plan, scratch_holder: dict | None = None, stream=None,
 
     `events`, when given, receives one (start, end) pair of CUDA events per pass launch,
     recorded on the launching stream (bench.py's per-kernel timing)."""
-    lib = nat.lib()
     st = nat.stream_ptr(stream)
     n = state.n_qubits
     dtype = state.precision.qsb_dtype
@@ -218,9 +217,9 @@ def run_plan(state, plan: Plan, scratch_holder: dict | None = None, stream=None,
                 run = packed.get(i)
                 if run is None:
                     run = packed[i] = pack_gate_batch([s.gate for s in plan.steps[i:j]])
-                _apply_gate_batch(state.data_ptr, n, dtype, run, st)
+                _apply_gate_batch(state.raw_ptr, n, dtype, run, st)
             else:
-                _apply_gate_step(state.data_ptr, n, dtype, step.gate, st)
+                _apply_gate_step(state.raw_ptr, n, dtype, step.gate, st)
             i = j
             continue
         i += 1
@@ -229,11 +228,11 @@ def run_plan(state, plan: Plan, scratch_holder: dict | None = None, stream=None,
             ev0 = nat.torch_mod().cuda.Event(enable_timing=True)
             ev1 = nat.torch_mod().cuda.Event(enable_timing=True)
             ev0.record(stream)
-        src = state.data_ptr
+        src = state.raw_ptr
         if step.ext_perm:
             scratch = holder.get("buf")
-            if scratch is None or scratch.numel() != state.n_amps or scratch.dtype != state.tensor.dtype:
-                scratch = nat.torch_mod().empty_like(state.tensor)
+            if scratch is None or scratch.numel() != state.n_amps or scratch.dtype != state.raw_tensor.dtype:
+                scratch = nat.torch_mod().empty_like(state.raw_tensor)
             dst_t = scratch
         else:
             dst_t = None
@@ -282,6 +281,47 @@ def prepare_plan(n_qubits, precision, specs, fuse: bool | None = None, plan_cach
     return plan
 
 
+class _Relabelled:
+    """A gate spec acting on other qubits (same kind, parameters and matrix)."""
+
+    __slots__ = ("kind", "targets", "controls", "params", "matrix")
+
+    def __init__(self, spec, targets, controls):
+        self.kind = spec.kind
+        self.targets = targets
+        self.controls = controls
+        self.params = getattr(spec, "params", ())
+        self.matrix = getattr(spec, "matrix", None)
+
+
+def relabel_specs(specs, layout, n_qubits):
+    """Gates mapped through a logical -> physical qubit map, uncontrolled SWAPs absorbed into
+    the map (no data moves).  Returns (mapped specs, final layout or None if canonical)."""
+    from .gates import GateKind
+
+    phys = list(layout) if layout is not None else list(range(n_qubits))
+    out = []
+    for spec in specs:
+        kind = spec.kind if isinstance(spec.kind, GateKind) else GateKind(getattr(spec.kind, "value", spec.kind))
+        if kind is GateKind.SWAP and not spec.controls:
+            a, b = spec.targets
+            phys[a], phys[b] = phys[b], phys[a]
+            continue
+        out.append(_Relabelled(spec, tuple(phys[q] for q in spec.targets), tuple(phys[q] for q in spec.controls)))
+    final = None if phys == list(range(n_qubits)) else tuple(phys)
+    return out, final
+
+
+def _has_free_swap(specs) -> bool:
+    from .gates import GateKind
+
+    for spec in specs:
+        k = spec.kind
+        if (k is GateKind.SWAP or getattr(k, "value", k) == "SWAP") and not spec.controls:
+            return True
+    return False
+
+
 def run_gates(state, specs, fuse: bool | None = None, scratch_holder: dict | None = None,
               plan_cache: dict | None = None):
     """Run `specs` on `state`.
@@ -299,6 +339,21 @@ def run_gates(state, specs, fuse: bool | None = None, scratch_holder: dict | Non
     fuse_ = FUSION_DEFAULT if fuse is None else fuse
     n, precision = state.n_qubits, state.precision
     nbytes = state.n_amps * precision.itemsize
+    if getattr(state, "layout", None) is not None or (fuse_ and _has_free_swap(specs) and hasattr(state, "layout")
+                                                      and nbytes > GRID_BATCH_MAX_STATE_BYTES and not scratch_fits(nbytes)):
+        # no room for an out-of-place pass (e.g. 33 qubits c128 = 137 GB): SWAPs become qubit
+        # relabels instead of in-place half sweeps; the state keeps the map until a canonical read
+        key = ("relabel", state.layout, tuple(id(s) for s in specs))
+        hit = plan_cache.get(key) if plan_cache is not None else None
+        if hit is None:
+            hit = relabel_specs(specs, state.layout, n) + (list(specs),)
+            if plan_cache is not None:
+                plan_cache[key] = hit
+        mapped, final, _keep = hit
+        plan = prepare_plan(n, precision, mapped, fuse_, plan_cache)
+        run_plan(state, plan, scratch_holder)
+        state._layout = final
+        return plan
     small = nbytes <= BATCH_MAX_STATE_BYTES
     if small or (fuse_ and FIRST_RUN_BATCH and nbytes <= GRID_BATCH_MAX_STATE_BYTES):
         planned = (not small and plan_cache is not None
@@ -315,7 +370,7 @@ def run_gates(state, specs, fuse: bool | None = None, scratch_holder: dict | Non
             if small or entry[2] == 0:
                 entry[2] += 1
                 if len(entry[0][0]):
-                    _apply_gate_batch(state.data_ptr, n, precision.qsb_dtype, entry[0], nat.stream_ptr())
+                    _apply_gate_batch(state.raw_ptr, n, precision.qsb_dtype, entry[0], nat.stream_ptr())
                 return None
     plan = prepare_plan(n, precision, specs, fuse_, plan_cache)
     run_plan(state, plan, scratch_holder)

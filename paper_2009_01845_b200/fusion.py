@@ -45,6 +45,9 @@ class TileGeometry:
     L: int  # low bits always in the tile (256-byte runs)
     R: int = 0  # register (slot) bits per thread; 0 = K - THREAD_BITS (the interpreter's)
     halves: bool = False  # tile staged as two halves split on tile bit K-1 (128 KB tiles)
+    # layout changes in two rounds through a half-tile buffer (consecutive layouts share a
+    # register bit), so the stage is free as soon as the tile is in registers
+    split: bool = False
 
     @property
     def nreg(self) -> int:
@@ -80,6 +83,16 @@ GEOMETRY_JIT_K11 = {nat.QSB_C128: TileGeometry(11, 3, 4, 4), nat.QSB_C64: TileGe
 # of the default 256 x 32), measured variational-30 c64 44.7 -> 41.7 ms; 128 x 64 with two CTAs
 # per SM measured 48.2 ms
 GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 5), nat.QSB_C64: TileGeometry(13, 4, 5, 4)}
+# ... and its split variant for the lighter of those passes: a separate 32 KB transpose buffer
+# (layout changes in two rounds on a shared register bit), so each CTA's stage is refilled
+# while the CTA computes instead of after its stores.  Measured (round 2, variational-30 c128):
+# passes of <= ~100 FP operations per amplitude 7.45 -> 7.0 ms (8 VariationalLayers, 2 layout
+# changes), 7.47 -> 6.73 ms (1 layout change); the 16-layer pass 13.6 -> 15.0 ms, so it is
+# chosen per pass (SPLIT_MAX_CODE, and only when it needs no extra layout change).
+# QSB_SPLIT_2Q=0 disables it, =1 forces it for every 2-qubit-gate pass.
+GEOMETRY_JIT_2Q_SPLIT = {nat.QSB_C128: TileGeometry(12, 3, 4, 5, split=True)}
+SPLIT_2Q = os.environ.get("QSB_SPLIT_2Q", "auto")
+SPLIT_MAX_CODE = float(os.environ.get("QSB_SPLIT_MAX_CODE", "100"))
 # ... unless the pass's straight-line gate code per thread (FP operations per amplitude x 32
 # amplitudes) would outgrow the instruction cache: measured on grid-30, the two passes of 16
 # dense complex 4x4 gates (~8,200 FP instructions per thread) ran 21.5 / 32.0 ms in that geometry
@@ -476,6 +489,13 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
                 if code * GEOMETRY_JIT_2Q[dtype].A <= MAX_2Q_CODE:
                     pgeo = GEOMETRY_JIT_2Q[dtype]
             words, info = compile_pass(absorbed, T, n_qubits, dtype, pgeo, minimal=MINIMAL_LAYOUT_CHANGES)
+            if pgeo is GEOMETRY_JIT_2Q.get(dtype) and dtype in GEOMETRY_JIT_2Q_SPLIT and SPLIT_2Q != "0":
+                code = sum(matrix_cost(g.matrix) for g in absorbed if g.kind in ("g1", "g2"))
+                if SPLIT_2Q == "1" or code <= SPLIT_MAX_CODE:
+                    w2, i2 = compile_pass(absorbed, T, n_qubits, dtype, GEOMETRY_JIT_2Q_SPLIT[dtype],
+                                          minimal=MINIMAL_LAYOUT_CHANGES)
+                    if SPLIT_2Q == "1" or i2["transposes"] <= info["transposes"]:
+                        words, info = w2, i2
             plan.steps.append(PassStep(words, absorbed, tuple(sorted(T)), info["ext_perm"],
                                        info["transposes"], info["pivots"]))
         remaining = deferred
@@ -805,7 +825,7 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
         need = needs[gi]
         if not need <= set(cur.R):
             flush_diag()
-            if geo.halves:
+            if geo.halves or geo.split:
                 cur = make_layout(pick_R(gi, keep=cur.R))
             elif not minimal:
                 cur = make_layout(pick_R(gi))
@@ -825,7 +845,7 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
                 break
             if b not in Rs and b not in store_bits:
                 Rs.append(b)
-        if geo.halves and not set(Rs) & set(cur.R):
+        if (geo.halves or geo.split) and not set(Rs) & set(cur.R):
             # split-tile transposes need a common register bit: go through an intermediate layout
             Rm = list(cur.R[:NREG // 2]) + [b for b in Rs if b not in cur.R][:NREG - NREG // 2]
             cur = make_layout(Rm)
@@ -845,7 +865,7 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
     header[4] = n
     header[5] = dtype
     header[6] = 1 << (n - K)
-    header[7] = (1 if ext_perm else 0) | (2 if expect else 0)
+    header[7] = (1 if ext_perm else 0) | (2 if expect else 0) | (4 if geo.split else 0)
     contig = 0
     while contig < K and tile_pos[contig] == contig:
         contig += 1

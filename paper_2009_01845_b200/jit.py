@@ -62,6 +62,7 @@ REG_SPLIT = {c: _reg_split(c, ctas_per_sm(c)) for c in (128, 256, 512)}
 # per-CTA partial sums must not depend on timing.
 TILES_PER_CTA = int(os.environ.get("QSB_TILES_PER_CTA", "16"))
 PASS_SCHED = os.environ.get("QSB_PASS_SCHED", "dynamic")  # dynamic | oneshot | static
+TMA_STORE = os.environ.get("QSB_TMA_STORE", "1") != "0"
 DYN_CHUNK = int(os.environ.get("QSB_DYN_CHUNK", "2"))
 
 
@@ -112,6 +113,12 @@ __device__ __forceinline__ void mbar_wait(u64* b, u32 par) {
 __device__ __forceinline__ void tma5(void* d, const TMap* m, const int* c, u64* b) {
   asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
                :: "r"(smem_u32(d)), "l"((u64)m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(b)) : "memory"); }
+__device__ __forceinline__ void tma5_store(const TMap* m, const int* c, const void* s) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];"
+               :: "l"((u64)m), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(s)) : "memory"); }
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" :: "n"(CONSUMERS) : "memory"); }
 __device__ __forceinline__ void fence_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ C cm(C a, C b) { C r; r.x = a.x * b.x - a.y * b.y; r.y = a.x * b.y + a.y * b.x; return r; }
@@ -150,7 +157,7 @@ __device__ __forceinline__ u32 swz(u32 j) {
   for (int s = GB; s < HBB; s += GB) f ^= (j >> s);
   return j ^ (f & ((1u << GB) - 1u));
 }
-struct Smem { C stage[STAGES][1 << HBB]; C tbuf[ALIAS ? 1 : (1 << HBB)]; double2 ep[4][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 base[STAGES][2]; u32 zero; };
+struct Smem { C stage[STAGES][1 << SBB]; C tbuf[ALIAS ? 1 : (1 << HBB)]; double2 ep[4][MAXPIV]; u64 full[STAGES]; u64 empty[STAGES]; u64 base[STAGES][2]; u32 zero; };
 """
 
 
@@ -261,11 +268,30 @@ class _Gen:
         # 128 KB tiles are staged as two 64 KB halves split on tile bit K-1 (a register bit of
         # the first layout); layout changes then run in two rounds through a 64 KB buffer
         self.halves = (1 << K) * amp_bytes > 65536
+        # split: one 64 KB stage released as soon as the tile is in registers and a separate
+        # 32 KB transpose buffer (two-round layout changes), two CTAs per SM
+        self.split = bool(w[7] & 4) and not self.halves
         # two CTAs per SM with 64 KB tiles: one stage per CTA, reused as the transpose buffer
-        self.alias = (not self.halves) and ctas_per_sm(self.consumers) == 2 and (1 << K) * amp_bytes == 65536
-        self.stages = 1 if self.alias else STAGES
+        self.alias = (not self.halves and not self.split and ctas_per_sm(self.consumers) == 2
+                      and (1 << K) * amp_bytes == 65536)
+        self.stages = 1 if (self.alias or self.split) else STAGES
         self.sched = pass_schedule(self.n - K, self.consumers, self.expect, self.halves)
-        self.HB = K - 1 if self.halves else K  # bits of a stage / transpose-buffer index
+        self.HB = K - 1 if (self.halves or self.split) else K  # bits of a transpose-buffer index
+        self.SB = K - 1 if self.halves else K  # bits of a stage index
+        # bulk tensor stores through the transpose buffer (2-stage geometry, in-place passes)
+        # for passes without dense two-qubit gates: measured (round 2, n = 30) QFT c128
+        # 21.6 -> 20.9 ms, c64 11.5 -> 11.0 ms, but passes with dense 2-qubit gates in this
+        # geometry got slower (variational c64 44.4 -> 46.0 ms, grid c128 300 -> 308 ms): their
+        # FP work already hides the store back-pressure and the extra staging costs shared
+        # memory bandwidth.  QSB_TMA_STORE=0 disables it.
+        ops = []
+        q = self.ops0
+        while w[q] != OP_END:
+            ops.append(w[q])
+            q += w[q + 1]
+        self.tma_store = (TMA_STORE and not (self.halves or self.split or self.alias or self.expect)
+                          and not self.ext_perm and OP_G2 not in ops)
+        self.uses_tma_store = False
 
     # uniform coefficients (gate matrices, phases): a kernel-parameter array of R, read as
     # constant-bank operands (no registers held across the tile); returns the first index
@@ -368,7 +394,7 @@ class _Gen:
         body_start = len(self.lines)
         # initial load: the TMA stage holds tile bit b at stage bit sigma[b] (tma_plan)
         amp_bytes = 16 if self.dtype == nat.QSB_C128 else 8
-        stage_pos = self.tile_pos[:self.HB]
+        stage_pos = self.tile_pos[:self.SB]
         self.tplan = tma_plan(stage_pos, self.n, amp_bytes)
         if self.tplan is None:
             raise ValueError("tile has too many bit runs for the TMA tile fetch")
@@ -412,10 +438,12 @@ class _Gen:
             elif op == OP_LAYOUT:
                 new = self.parse_layout(a)
                 li += 1
-                pairs = None if (self.halves or not _MINIMAL) else self.swap_pairs(self.lay, new)
+                pairs = None if (self.halves or self.split or not _MINIMAL) else self.swap_pairs(self.lay, new)
                 if pairs:
                     self.gen_predicated_transpose(new, li, pairs)
-                elif not self.halves:
+                elif not (self.halves or self.split):
+                    if self.tma_store:
+                        self.emit("    if (tid < 32) bulk_wait_read0();  // the last tile's store has read tbuf")
                     self.emit("    csync();")
                     self.emit("    { const u32 sj = swz(jt%d);" % self.li)
                     for s in range(A):
@@ -454,13 +482,39 @@ class _Gen:
             return self._kernel(name, body, "")
         # output offsets of the final layout
         lay = self.lay
-        store = [f"    const u64 ot = obase | {self.thread_expr(lay['opos'], 64)};"]
+        store = []
         if self.h_scale:
             k = self.h_scale
             scale = 2.0 ** (-(k // 2)) * (0.7071067811865476 if k % 2 else 1.0)
             store.append(f"    const R hs = (R){scale!r};")
             for s in range(A):
                 store.append(f"    v{self.vm[s]}.x *= hs; v{self.vm[s]}.y *= hs;")
+        # output global position of every tile bit of the final layout
+        out_of = {b: p for b, p in zip(lay['Tb'], lay['opos'])}
+        for i, b in enumerate(lay['R']):
+            out_of[b] = lay['ooff'][1 << i].bit_length() - 1
+        tpos = list(self.tile_pos)
+        if self.tma_store and sorted(out_of.values()) == sorted(tpos):
+            # in-place pass whose tile lands on its own positions (SWAPs inside the tile only
+            # permute them): the tile goes back through the transpose buffer in the TMA image
+            # order of the OUTPUT positions and one warp issues bulk tensor stores, so the
+            # consumers never wait for HBM write back-pressure
+            sig = self.tplan["sigma"]
+            img = {b: sig[tpos.index(out_of[b])] for b in out_of}
+            so = self.thread_expr([img[b] for b in lay['Tb']], 32)
+            store.append("    if (tid < 32) bulk_wait_read0();")
+            store.append("    csync();")
+            store.append(f"    {{ const u32 so = {so};")
+            for s in range(A):
+                off = sum(1 << img[lay['R'][i]] for i in range(self.NREG) if (s >> i) & 1)
+                store.append(f"      sm.tbuf[so | {off}u] = v{self.vm[s]};")
+            store.append("    }")
+            store.append("    fence_async();")
+            store.append("    csync();")
+            store.append("@@TMASTORE@@")
+            self.uses_tma_store = True
+            return self._kernel(name, body, "\n".join(store))
+        store.append(f"    const u64 ot = obase | {self.thread_expr(lay['opos'], 64)};")
         for s in range(A):
             if _PROBE == "nostores":  # timing probe: keep the values live, store (almost) nothing
                 store.append(f"    if (v{self.vm[s]}.x == (R)1234.5) dst[ot | {lay['ooff'][s]}ull] = v{self.vm[s]};")
@@ -854,8 +908,18 @@ class _Gen:
                    f"          const int co[5] = {{{', '.join(coords)}}};\n"
                    f"          tma5(d + (u64)k * {call_bytes}u, &tmap, co, &sm.full[s]);\n"
                    f"        }}")
+        if "@@TMASTORE@@" in store:
+            store = store.replace("@@TMASTORE@@", (
+                f"    if (tid < 32) {{\n"
+                f"      for (int k = tid; k < {ncalls}; k += 32) {{\n"
+                f"        const u64 b = base | {koff};\n"
+                f"        const int co[5] = {{{', '.join(coords)}}};\n"
+                f"        tma5_store(&tmap, co, reinterpret_cast<const char*>(&sm.tbuf[0]) + (u64)k * {call_bytes}u);\n"
+                f"      }}\n"
+                f"      bulk_commit();\n"
+                f"    }}"))
         pr = "double" if (self.dtype == nat.QSB_C128 or self.expect) else "float"
-        defs = (f"#define QSB_F32X2 {1 if self.dtype == nat.QSB_C64 else 0}\n#define R {real}\n#define PR {pr}\n#define C {real}2\n#define KB {K}\n#define HBB {self.HB}\n#define GB {self.G}\n#define STAGES {self.stages}\n#define ALIAS {1 if self.alias else 0}\n#define TBUF {"sm.stage[s]" if self.alias else "sm.tbuf"}\n"
+        defs = (f"#define QSB_F32X2 {1 if self.dtype == nat.QSB_C64 else 0}\n#define R {real}\n#define PR {pr}\n#define C {real}2\n#define KB {K}\n#define HBB {self.HB}\n#define SBB {self.SB}\n#define GB {self.G}\n#define STAGES {self.stages}\n#define ALIAS {1 if self.alias else 0}\n#define TBUF {"sm.stage[s]" if self.alias else "sm.tbuf"}\n"
                 f"#define CONSUMERS {self.consumers}\n#define MAXPIV {MAX_PIV}\n#define NPIV {self.npiv}\n"
                 f"#define NCOEF {max(1, len(self.coeffs))}\n#define NTAB {len(self.tables)}\n"
                 f"#define TPC {self.sched[0]}\n#define DYN {self.sched[1]}\n")
@@ -1001,6 +1065,7 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
 {store}
   }}
 {self._expect_epilogue() if self.expect else "  (void)ea;"}
+{"  if (tid < 32) bulk_wait0();  // the last bulk stores are done before the CTA retires" if self.uses_tma_store else ""}
 }}
 """
 
@@ -1093,11 +1158,15 @@ MAX_COEFFS = 3072  # 24 KB of pivot tables staged in shared memory
 MAX_PARAM_BYTES = 31744  # kernel parameter space: 32764 B minus the pointers and the tensor map
 
 
-def smem_bytes(stage_bytes: int, n_coeffs=MAX_COEFFS, alias: bool = False) -> int:
+def smem_bytes(stage_bytes: int, n_coeffs=MAX_COEFFS, alias: bool = False, split: bool = False) -> int:
     # STAGES stages + one transpose buffer of stage_bytes (a whole tile, or half of a 128 KB
-    # tile); `alias`: a single stage that doubles as the transpose buffer (two CTAs per SM)
-    n_buf = 1 if alias else STAGES + 1
-    struct_bytes = n_buf * stage_bytes + 4 * MAX_PIV * 16 + 8 * STAGES * 4 + 16 + 16
+    # tile); `alias`: a single stage that doubles as the transpose buffer (two CTAs per SM);
+    # `split`: a single stage + a half-size transpose buffer (two CTAs per SM)
+    if split:
+        buf_bytes = stage_bytes + stage_bytes // 2
+    else:
+        buf_bytes = (1 if alias else STAGES + 1) * stage_bytes
+    struct_bytes = buf_bytes + 4 * MAX_PIV * 16 + 8 * STAGES * 4 + 16 + 16
     return struct_bytes + 8 * n_coeffs + 128
 
 
@@ -1188,8 +1257,9 @@ def _compile_words(words, dtype):
         fresh = _Compiled()
         fresh.func = fn
         fresh.name = name
-        alias = (1 << K) * amp == 65536 and ctas_per_sm(1 << (K - nreg)) == 2
-        fresh.smem = smem_bytes(stage_amps * amp, len(tables), alias)
+        split = bool(int(words[7]) & 4) and (1 << K) * amp <= 65536
+        alias = (1 << K) * amp == 65536 and ctas_per_sm(1 << (K - nreg)) == 2 and not split
+        fresh.smem = smem_bytes(stage_amps * amp, len(tables), alias, split)
         fresh.ctas = ctas_per_sm(1 << (K - nreg))
         fresh.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
         fresh.n_tiles = 1 << (int(words[4]) - K)

@@ -445,6 +445,12 @@ class _ShardView:
     def data_ptr(self):
         return int(self._t.data_ptr())
 
+    raw_ptr = data_ptr
+
+    @property
+    def raw_tensor(self):
+        return self._t
+
     @property
     def n_amps(self):
         return 1 << self.n_qubits

@@ -110,7 +110,7 @@ class StateVector:
     `amplitudes` may be a numpy array (uploaded) or a CUDA tensor (adopted without a copy).
     """
 
-    __slots__ = ("n_qubits", "precision", "_t")
+    __slots__ = ("n_qubits", "precision", "_t", "_layout")
 
     def __init__(self, n_qubits: int, amplitudes, precision: Precision = Precision.F64):
         _check_cap(n_qubits)
@@ -133,10 +133,16 @@ class StateVector:
             if arr.dtype != precision.complex_dtype:
                 raise ShapeError(f"amplitude dtype {arr.dtype} does not match precision {precision.value}")
             self._t = upload(arr)
+        # logical -> physical qubit map (None = canonical): a state too large for an
+        # out-of-place scratch buffer takes uncontrolled SWAPs as relabels (engine.run_gates);
+        # every canonical access below (tensor, data_ptr, amplitudes) applies the permutation
+        # first, so callers always see the reference layout (state.py:1-6, 34-36)
+        self._layout = None
 
     # -- numpy view (host copy) ------------------------------------------------------------
     @property
     def amplitudes(self) -> np.ndarray:
+        self._canonicalize()
         return download(self._t)
 
     @amplitudes.setter
@@ -145,23 +151,78 @@ class StateVector:
         if arr.shape != (1 << self.n_qubits,) or arr.dtype != self.precision.complex_dtype:
             raise ShapeError("replacement amplitudes must keep shape and dtype")
         self._t = upload(arr)
+        self._layout = None
 
     # -- device view -----------------------------------------------------------------------
     @property
     def tensor(self):
         """The CUDA tensor holding the amplitudes (mutated in place by the kernels)."""
+        self._canonicalize()
         return self._t
 
     @property
     def data_ptr(self) -> int:
+        self._canonicalize()
         return int(self._t.data_ptr())
+
+    @property
+    def raw_ptr(self) -> int:
+        """Device pointer of the buffer in its current (possibly relabelled) layout (engine)."""
+        return int(self._t.data_ptr())
+
+    @property
+    def raw_tensor(self):
+        return self._t
+
+    @property
+    def layout(self):
+        """Physical qubit of every logical qubit, or None when the buffer is canonical."""
+        return self._layout
 
     @property
     def n_amps(self) -> int:
         return 1 << self.n_qubits
 
     def copy(self) -> "StateVector":
-        return StateVector(self.n_qubits, self._t.clone(), self.precision)
+        dup = StateVector(self.n_qubits, self._t.clone(), self.precision)
+        dup._layout = self._layout
+        return dup
+
+    def _canonicalize(self) -> None:
+        """Apply a pending qubit relabelling: one bit-permuting copy when a scratch buffer fits,
+        else in-place SWAP kernels (one half sweep per transposition)."""
+        if self._layout is None:
+            return
+        from . import engine
+
+        n = self.n_qubits
+        phys = list(self._layout)
+        self._layout = None
+        if engine.scratch_fits(self.n_amps * self.precision.itemsize):
+            dst = [0] * n  # physical qubit p (bit n-1-p) holds logical q: bit n-1-p -> bit n-1-q
+            for q, p in enumerate(phys):
+                dst[n - 1 - p] = n - 1 - q
+            torch = nat.torch_mod()
+            out = torch.empty_like(self._t)
+            perm = np.ascontiguousarray(dst, dtype=np.int32)
+            nat.check(nat.lib().qsb_permute_qubits(self._t.data_ptr(), out.data_ptr(), n, self.precision.qsb_dtype,
+                                                   perm.ctypes.data, nat.stream_ptr()), "canonicalize")
+            self._t = out
+            return
+        swap = np.array([[1, 0, 0, 0], [0, 0, 1, 0], [0, 1, 0, 0], [0, 0, 0, 1]], dtype=np.complex128)
+        where = {p: q for q, p in enumerate(phys)}  # physical -> logical
+        for q in range(n):
+            p = phys[q]
+            if p == q:
+                continue
+            q2 = where[q]  # the logical qubit currently stored at physical q
+            tb = np.array([n - 1 - p, n - 1 - q], dtype=np.int32)
+            cb = np.zeros(1, dtype=np.int32)
+            nat.check(nat.lib().qsb_apply_matrix(self._t.data_ptr(), n, self.precision.qsb_dtype, 2, tb.ctypes.data, 0,
+                                                 cb.ctypes.data, swap.ctypes.data, nat.KERNEL_PERMUTATION,
+                                                 nat.stream_ptr()), "canonicalize")
+            phys[q], phys[q2] = q, p
+            where[q], where[p] = q, q2
 
     def __repr__(self):
         return f"StateVector(n_qubits={self.n_qubits}, precision={self.precision.value}, device={self._t.device})"
@@ -175,7 +236,8 @@ def upload(arr: np.ndarray):
 
 
 def download(t) -> np.ndarray:
-    return t.detach().to("cpu").numpy().copy()
+    """One device -> host copy into fresh host memory (the tensor .cpu() returns owns it)."""
+    return t.detach().to("cpu").numpy()
 
 
 def zero_state(n_qubits: int, precision: Precision = Precision.F64) -> StateVector:

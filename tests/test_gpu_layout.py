@@ -1,0 +1,61 @@
+"""Qubit relabelling for states with no room for an out-of-place scratch buffer (the 2^33
+per-GPU regime of the 36-qubit target): uncontrolled SWAPs become a logical -> physical qubit
+map on the StateVector instead of in-place half sweeps, and every canonical access (amplitudes,
+tensor, sampling, energies) applies the pending permutation first.  Forced here at n = 25 by
+pretending the scratch does not fit."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def no_scratch(monkeypatch):
+    from paper_2009_01845_b200 import engine
+
+    monkeypatch.setattr(engine, "scratch_fits", lambda nbytes: nbytes <= engine.GRID_BATCH_MAX_STATE_BYTES)
+    return engine
+
+
+def test_qft_swaps_become_a_layout(cuda, no_scratch):
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200.verify import dft_column_error
+
+    n = 25
+    k = 1234567
+    c = q.qft_circuit(n)
+    out = c.execute(q.basis_state(n, k))
+    assert out.layout is not None and sorted(out.layout) == list(range(n))
+    assert out.layout == tuple(n - 1 - x for x in range(n))  # the QFT's final reversal, not applied
+    assert dft_column_error(out, k) <= 1e-12  # canonicalised in place (scratch "does not fit")
+    assert out.layout is None
+
+
+def test_layout_follows_later_circuits_and_reads(cuda, no_scratch, monkeypatch):
+    import paper_2009_01845_b200 as q
+
+    n = 25
+    rng = np.random.default_rng(3)
+    swaps = q.Circuit(n).add([q.SWAP(0, 24), q.H(3), q.SWAP(3, 7), q.RY(7, 0.4), q.CNOT(24, 0), q.SWAP(24, 3),
+                              q.SWAP(1, 2),
+                              q.CZPow(2, 5, 0.3), q.Unitary(np.linalg.qr(rng.standard_normal((4, 4)))[0], 1, 24)])
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    a = swaps.execute(q.from_amplitudes(psi))
+    assert a.layout is not None
+    b = swaps.execute(a)  # a second circuit on a relabelled state (its copy keeps the map)
+    assert b.layout is not None and b.layout != a.layout  # (0 24 3 7) is not an involution
+    want = swaps.execute(swaps.execute(q.from_amplitudes(psi), fuse=False), fuse=False)
+    monkeypatch.undo()  # scratch fits again: the canonical read is one bit-permuting copy
+    assert want.layout is None
+    assert np.max(np.abs(b.amplitudes - want.amplitudes)) <= 1e-12
+    # reads through the public API see the canonical layout: norm, energy, sampling
+    c = swaps.execute(q.from_amplitudes(psi))
+    assert c.layout is None  # planned with a scratch buffer now: SWAPs folded into the passes
+    d = swaps.execute(q.from_amplitudes(psi))
+    h = q.build_tfim(n, 0.7)
+    assert abs(q.expectation(h, d) - q.expectation(h, c)) <= 1e-10
+    r1 = q.sample(d, range(n), 2000, seed=5)
+    r2 = q.sample(c, range(n), 2000, seed=5)
+    assert np.count_nonzero(r1.samples != r2.samples) <= 2

@@ -185,3 +185,23 @@ def test_resident_evolution_callbacks_and_windows(cuda, window):
     assert abs(sd.norm_sharded(sh) - 1.0) <= 1e-12
     assert abs(sd.overlap_sharded(target, sh) - q.overlap(target, want)) <= 1e-12
     assert max_abs(sd.gather(sh).amplitudes, want.amplitudes) <= 1e-12
+
+
+def test_sharded_equals_one_gpu_at_config4_size(cuda):
+    """SURVEY.md section 8(e) at BASELINE config 4's size: the 33-qubit random grid circuit
+    sharded over 8 shards (batched all-to-all schedule) against the whole 137 GB state on one
+    B200, compared through per-chunk fingerprints and 2^20 sampled amplitudes
+    (tools/sharded33_check.py; each state is freed before the other is built)."""
+    import os
+    import subprocess
+    import sys
+
+    cuda.cuda.synchronize()
+    cuda.cuda.empty_cache()
+    free, _ = cuda.cuda.mem_get_info()
+    if free < (165 << 30):
+        pytest.skip(f"needs ~160 GB of free device memory, {free / 2**30:.0f} GiB free")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "sharded33_check.py"), "33", "8", "20"],
+                       capture_output=True, text=True, timeout=900, cwd=root)
+    assert "CHECK_OK" in r.stdout, (r.stdout[-2000:], r.stderr[-3000:])

@@ -272,3 +272,6 @@ def test_bench_distributed_summary():
     assert roof["sweeps_per_step"] == p.state_sweeps()
     assert abs(roof["achieved"] - p.state_sweeps() * 2 * shard / 8e-4 / 1e9) < 1e-9
     assert launches == len(p.steps) + 2 * 2 * ((shard // 32) // 4096) + 1
+    # 3-qubit exchanges: 7 peers, each part 2^11 amplitudes in chunks of (2^16 / 16) // 7 = 585
+    roof, launches = bench._dist_summary({"k": p}, 1, 1e-3, 1e-4, shard, 16, 1 << 16, 3)
+    assert launches == len(p.steps) + 2 * 7 * -(-(1 << 11) // 585) + 1
