@@ -580,6 +580,11 @@ def _order_thread_bits(cands, geo, prefer, natural=False):
 # (variational-30 c128 100 -> 146 ms, QFT-30 22.6 -> 23.6 ms) -- the kept lane assignment loses
 # the conflict-free swizzle and predicated half-warp accesses save no wavefronts -- so off.
 MINIMAL_LAYOUT_CHANGES = os.environ.get("QSB_MINIMAL_LAYOUT", "0") == "1"
+# QSB_TMA_STORE_LAYOUT=1: final layouts chosen for conflict-free staging of the jit's bulk tensor
+# stores instead of the coalesced-register-store rule.  Measured round 2 (QFT-30 pass 4): bank
+# conflicts 162 M -> 33 M but shared-memory wavefronts 762 M -> 901 M, 5.07 -> 5.18 ms (c128)
+# and 2.57 -> 2.84 ms (c64), so off by default
+TMA_STORE_LAYOUT = os.environ.get("QSB_TMA_STORE_LAYOUT", "0") == "1"
 
 
 # Gates of a pass are re-ordered within their dependencies so that each register layout serves as
@@ -837,8 +842,27 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
         words += _gate_op(kind, g, pt, pc, cur, tidx)
         gi += 1
     flush_diag()
+    # bulk tensor stores (jit: in-place passes without dense 2-qubit gates in the two-stage
+    # geometry) write the tile through shared memory in the TMA image order of the output
+    # positions: lanes 0..G-1 on the tile bits stored to output bits 0..G-1 make those writes
+    # bank-conflict free; no other lane constraint (the bulk store is coalesced by construction)
+    tma_store = (TMA_STORE_LAYOUT and not expect and not ext_perm and not geo.halves and not geo.split
+                 and geo.thread_bits > 7 and not any(ev[0] == "g2" for ev in events))
+    if tma_store:
+        want = sorted((b for b in range(K) if out_pos[b] < geo.G), key=lambda b: out_pos[b])
+        if set(cur.Tb[:geo.G]) != set(want):
+            Rs = [b for b in cur.R if b not in want]
+            for b in sorted(range(K), key=lambda b: -b):
+                if len(Rs) >= NREG:
+                    break
+                if b not in Rs and b not in want:
+                    Rs.append(b)
+            rest = [b for b in range(K) if b not in Rs and b not in want]
+            cur = _Layout(Rs, want + rest)
+            words += layout_words(cur)
+            n_trans += 1
     # store layout: lanes must cover the tile bits that land on the low output bits
-    if not expect and not store_bits <= set(cur.Tb[:5]):
+    elif not expect and not store_bits <= set(cur.Tb[:5]):
         Rs = [b for b in cur.R if b not in store_bits]
         for b in sorted(range(K), key=lambda b: -b):
             if len(Rs) >= NREG:
