@@ -240,6 +240,36 @@ def tma_plan(tile_pos, n, amp_bytes, max_iter=MAX_TMA_ITER_BITS):
                 box_amps=1 << len(box_bits))
 
 
+def parity_quadratic(z: int, s1: int, pairs) -> int:
+    """Q(z) = |z & s1| + sum_d |z & (z >> d) & m_d|  (mod 2): the sign bit of amplitude z under
+    Z gates on the bits of s1 and CZ gates on the bit pairs (b, b + d), b in m_d."""
+    t = bin(z & s1).count("1")
+    for d, m in pairs:
+        t += bin(z & (z >> d) & m).count("1")
+    return t & 1
+
+
+def parity_sign_plan(s1: int, pairs, goff, nreg: int):
+    """Compile-time part of a parity op for one register layout: C = the slots' own signs
+    Q(goff[s]) as a bit mask, and per register bit i the cross-term mask K_i (sign contribution
+    |x & K_i| mod 2 of the runtime bits x) with M_i = the slots that have bit i.  At run time
+    W = C ^ (Q(x) ? all : 0) ^ XOR_i (|x & K_i| odd ? M_i : 0); bit s of W is Q(x | goff[s])."""
+    A = 1 << nreg
+    C = sum(parity_quadratic(goff[sl], s1, pairs) << sl for sl in range(A))
+    cross = []
+    for i in range(nreg):
+        p_i = goff[1 << i].bit_length() - 1
+        K = 0
+        for d, m in pairs:
+            if (m >> p_i) & 1:
+                K |= 1 << (p_i + d)
+            if p_i >= d and (m >> (p_i - d)) & 1:
+                K |= 1 << (p_i - d)
+        if K:
+            cross.append((K, sum(1 << sl for sl in range(A) if (sl >> i) & 1)))
+    return C, cross
+
+
 class _Gen:
     def __init__(self, words, dtype):
         self.w = [int(x) for x in words]
@@ -862,18 +892,27 @@ class _Gen:
         self.emit("    }")
 
     def gen_parity(self, a):
-        w, A = self.w, self.A
+        """Sign flips of a batch of -1-phase diagonal gates (Z: single bits s1; CZ: bit pairs (b,
+        b + d) for the bits b of mask m_d): the sign of amplitude gi is the GF(2) quadratic form
+        Q(gi) = |gi & s1| + sum_d |gi & (gi >> d) & m_d|  (mod 2).  With gi = x | z, x = the
+        tile-external and thread bits (runtime), z = the slot's register bits (compile-time),
+        Q(x | z) = Q(x) + Q(z) + sum_i z_i L_i(x) with L_i(x) = |x & K_i| (mod 2) the bilinear
+        cross terms of register bit i.  So one 32-bit sign word per thread and tile -- a few
+        popcounts -- replaces per-amplitude 64-bit popcounts, and each amplitude costs one bit
+        test and its negation."""
+        w, A, NREG = self.w, self.A, self.NREG
         s1, nd = w[a], w[a + 1]
         pairs = [(w[a + 2 + 2 * q], w[a + 3 + 2 * q]) for q in range(nd)]
-        self.emit("    { // parity")
-        for s in range(A):
-            gi = f"(base | gt{self.li} | {self.lay['goff'][s]}ull)"
-            terms = []
-            if s1:
-                terms.append(f"__popcll(gi & {s1}ull)")
-            for d, m in pairs:
-                terms.append(f"__popcll(gi & (gi >> {d}) & {m}ull)")
-            self.emit(f"      {{ const u64 gi = {gi}; if (({' + '.join(terms)}) & 1) {{ v{self.vm[s]}.x = -v{self.vm[s]}.x; v{self.vm[s]}.y = -v{self.vm[s]}.y; }} }}")
+        C, cross = parity_sign_plan(s1, pairs, self.lay['goff'], NREG)
+        full = (1 << A) - 1
+        qx = " + ".join([f"__popcll(x & {s1}ull)"] + [f"__popcll(x & (x >> {d}) & {m}ull)" for d, m in pairs])
+        self.emit("    { // parity (sign word)")
+        self.emit(f"      const u64 x = base | gt{self.li};")
+        self.emit(f"      u32 W = {C}u ^ ((({qx}) & 1) ? {full}u : 0u);")
+        for K, Mi in cross:
+            self.emit(f"      if (__popcll(x & {K}ull) & 1) W ^= {Mi}u;")
+        for sl in range(A):
+            self.emit(f"      if (W & {1 << sl}u) {{ v{self.vm[sl]}.x = -v{self.vm[sl]}.x; v{self.vm[sl]}.y = -v{self.vm[sl]}.y; }}")
         self.emit("    }")
 
     def gen_term(self, a):

@@ -51,3 +51,31 @@ def test_structure_sharing_across_angles():
         sa, _, ca = jit.generate(a.words, nat.QSB_C128)
         sb, _, cb = jit.generate(b.words, nat.QSB_C128)
         assert sa == sb and not np.array_equal(ca, cb)
+
+
+def test_parity_sign_word_equals_quadratic_form():
+    """The jit's per-thread sign word for -1-phase diagonal batches (jit.parity_sign_plan) gives
+    every slot the sign Q(x | goff[s]) of the direct per-amplitude quadratic form."""
+    rng = np.random.default_rng(11)
+    for trial in range(200):
+        n = int(rng.integers(8, 34))
+        nreg = int(rng.integers(2, 6))
+        pos = rng.permutation(n)
+        regs = sorted(int(p) for p in pos[:nreg])
+        rest = [int(p) for p in pos[nreg:]]
+        goff = [sum(1 << regs[i] for i in range(nreg) if (sl >> i) & 1) for sl in range(1 << nreg)]
+        s1 = int(sum(1 << int(b) for b in rng.choice(n, size=int(rng.integers(0, 4)), replace=False)))
+        pairs = []
+        for d in sorted(set(int(x) for x in rng.integers(1, n, size=int(rng.integers(0, 4))))):
+            m = int(sum(1 << int(b) for b in range(n - d) if rng.random() < 0.3))
+            if m:
+                pairs.append((d, m))
+        C, cross = jit.parity_sign_plan(s1, pairs, goff, nreg)
+        for _ in range(8):
+            x = sum(1 << p for p in rest if rng.random() < 0.5)
+            W = C ^ (((1 << (1 << nreg)) - 1) if jit.parity_quadratic(x, s1, pairs) else 0)
+            for K, M in cross:
+                if bin(x & K).count("1") & 1:
+                    W ^= M
+            for sl in range(1 << nreg):
+                assert (W >> sl) & 1 == jit.parity_quadratic(x | goff[sl], s1, pairs), (trial, sl)
