@@ -91,6 +91,11 @@ GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 5), nat.QSB_C64: TileGeo
 # chosen per pass (SPLIT_MAX_CODE, and only when it needs no extra layout change).
 # QSB_SPLIT_2Q=0 disables it, =1 forces it for every 2-qubit-gate pass.
 GEOMETRY_JIT_2Q_SPLIT = {nat.QSB_C128: TileGeometry(12, 3, 4, 5, split=True)}
+if os.environ.get("QSB_2Q_GEOMETRY", "") == "s3":
+    # experiment: 256 consumers x 16 amplitudes, one CTA per SM, three 64 KB stages + the split
+    # 32 KB transpose buffer (half the straight-line code per thread, three tiles in flight)
+    GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 4, split=True), nat.QSB_C64: GEOMETRY_JIT_2Q[nat.QSB_C64]}
+    GEOMETRY_JIT_2Q_SPLIT = {}
 SPLIT_2Q = os.environ.get("QSB_SPLIT_2Q", "auto")
 SPLIT_MAX_CODE = float(os.environ.get("QSB_SPLIT_MAX_CODE", "100"))
 # ... unless the pass's straight-line gate code per thread (FP operations per amplitude x 32

@@ -304,7 +304,9 @@ class _Gen:
         # two CTAs per SM with 64 KB tiles: one stage per CTA, reused as the transpose buffer
         self.alias = (not self.halves and not self.split and ctas_per_sm(self.consumers) == 2
                       and (1 << K) * amp_bytes == 65536)
-        self.stages = 1 if (self.alias or self.split) else STAGES
+        # split geometry: one stage per CTA at two CTAs per SM; three stages (3 x 64 KB + the
+        # 32 KB transpose buffer) at one CTA per SM
+        self.stages = 1 if self.alias else (split_stages(self.consumers) if self.split else STAGES)
         self.sched = pass_schedule(self.n - K, self.consumers, self.expect, self.halves)
         self.HB = K - 1 if (self.halves or self.split) else K  # bits of a transpose-buffer index
         self.SB = K - 1 if self.halves else K  # bits of a stage index
@@ -912,7 +914,16 @@ class _Gen:
         for K, Mi in cross:
             self.emit(f"      if (__popcll(x & {K}ull) & 1) W ^= {Mi}u;")
         for sl in range(A):
-            self.emit(f"      if (W & {1 << sl}u) {{ v{self.vm[sl]}.x = -v{self.vm[sl]}.x; v{self.vm[sl]}.y = -v{self.vm[sl]}.y; }}")
+            v = f"v{self.vm[sl]}"
+            if self.dtype == nat.QSB_C128:
+                # flip the sign bits of both high words with a mask built from bit sl of W (no
+                # predicate, no select: three integer ops per amplitude)
+                sh = f"(W << {31 - sl})" if sl < 31 else "W"
+                self.emit(f"      {{ const int m = (int)({sh} & 0x80000000u); "
+                          f"{v}.x = __hiloint2double(__double2hiint({v}.x) ^ m, __double2loint({v}.x)); "
+                          f"{v}.y = __hiloint2double(__double2hiint({v}.y) ^ m, __double2loint({v}.y)); }}")
+            else:
+                self.emit(f"      if (W & {1 << sl}u) {{ {v}.x = -{v}.x; {v}.y = -{v}.y; }}")
         self.emit("    }")
 
     def gen_term(self, a):
@@ -1197,15 +1208,20 @@ MAX_COEFFS = 3072  # 24 KB of pivot tables staged in shared memory
 MAX_PARAM_BYTES = 31744  # kernel parameter space: 32764 B minus the pointers and the tensor map
 
 
-def smem_bytes(stage_bytes: int, n_coeffs=MAX_COEFFS, alias: bool = False, split: bool = False) -> int:
+def split_stages(consumers: int) -> int:
+    return 1 if ctas_per_sm(consumers) == 2 else 3
+
+
+def smem_bytes(stage_bytes: int, n_coeffs=MAX_COEFFS, alias: bool = False, split: bool = False,
+               consumers: int = 128) -> int:
     # STAGES stages + one transpose buffer of stage_bytes (a whole tile, or half of a 128 KB
     # tile); `alias`: a single stage that doubles as the transpose buffer (two CTAs per SM);
-    # `split`: a single stage + a half-size transpose buffer (two CTAs per SM)
+    # `split`: split_stages() stages + a half-size transpose buffer
     if split:
-        buf_bytes = stage_bytes + stage_bytes // 2
+        buf_bytes = split_stages(consumers) * stage_bytes + stage_bytes // 2
     else:
         buf_bytes = (1 if alias else STAGES + 1) * stage_bytes
-    struct_bytes = buf_bytes + 4 * MAX_PIV * 16 + 8 * STAGES * 4 + 16 + 16
+    struct_bytes = buf_bytes + 4 * MAX_PIV * 16 + 8 * 3 * 4 + 16 + 16
     return struct_bytes + 8 * n_coeffs + 128
 
 
@@ -1298,7 +1314,7 @@ def _compile_words(words, dtype):
         fresh.name = name
         split = bool(int(words[7]) & 4) and (1 << K) * amp <= 65536
         alias = (1 << K) * amp == 65536 and ctas_per_sm(1 << (K - nreg)) == 2 and not split
-        fresh.smem = smem_bytes(stage_amps * amp, len(tables), alias, split)
+        fresh.smem = smem_bytes(stage_amps * amp, len(tables), alias, split, 1 << (K - nreg))
         fresh.ctas = ctas_per_sm(1 << (K - nreg))
         fresh.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
         fresh.n_tiles = 1 << (int(words[4]) - K)
