@@ -33,6 +33,15 @@ sys.path.insert(0, ROOT)
 METRIC = "circuit wall-seconds & achieved HBM GB/s (QFT/variational, c128) at 1/2/4/8 B200"
 
 
+def _local_device() -> int:
+    """This rank's GPU (LOCAL_RANK; modulo the visible devices for validation runs that put
+    several ranks on one GPU)."""
+    import torch
+
+    n = max(1, torch.cuda.device_count())
+    return int(os.environ.get("LOCAL_RANK", 0)) % n
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -282,7 +291,7 @@ def run_gpu_arm(args, rank, world):
     from paper_2009_01845_b200 import engine
     from paper_2009_01845_b200.fusion import PassStep
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(_local_device())
     if world > 1:
         return run_distributed_arm(args, rank, world)
 
@@ -301,7 +310,7 @@ def run_gpu_arm(args, rank, world):
     evs: list = []
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk:
+    with ClockSampler(_local_device()) as clk:
         t0.record()
         for _ in range(args.steps):
             engine.run_plan(state, plan, holder, events=evs)
@@ -475,14 +484,20 @@ def run_distributed_arm(args, rank, world):
     import paper_2009_01845_b200 as q
     from paper_2009_01845_b200 import sharding as sd
 
+    # QSB_BENCH_DIST_BACKEND=gloo: a validation run of this arm with several ranks sharing one GPU
+    # (NCCL refuses that): transfers staged through host memory, numbers not representative
+    backend_name = os.environ.get("QSB_BENCH_DIST_BACKEND", "nccl")
     if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
+        if backend_name == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", _local_device()))
+        else:
+            dist.init_process_group(backend_name)
     g = world.bit_length() - 1
     n = args.qubits + g
     prec = q.Precision.F64 if args.precision == "f64" else q.Precision.F32
     q.set_max_qubits(max(n, q.max_qubits()))
     circuit = q.qft_circuit(n)
-    comm = sd.TorchComm()
+    comm = sd.TorchComm() if backend_name == "nccl" else sd.HostStagedComm()
     backend = sd.CudaBackend(prec)
     exec_plan = sd.plan_batched(circuit, world)
     cache: dict = {}
@@ -497,7 +512,7 @@ def run_distributed_arm(args, rank, world):
     comm.barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk:
+    with ClockSampler(_local_device()) as clk:
         t0.record()
         for _ in range(args.steps):
             sh = step()
@@ -530,7 +545,8 @@ def run_distributed_arm(args, rank, world):
         "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128" if prec is q.Precision.F64 else "c64", "data": "synthetic",
         "config": {"workload": f"QFT {n} qubits sharded over {world} GPUs (2^{args.qubits} amplitudes per GPU)",
-                   "n_qubits": n, "parallelism": f"global-qubit sharding x{world}, batched NCCL all-to-all exchanges",
+                   "n_qubits": n, "parallelism": f"global-qubit sharding x{world}, batched NCCL all-to-all exchanges"
+                   + ("" if backend_name == "nccl" else f" (VALIDATION RUN: {backend_name}, host-staged, ranks sharing GPUs)"),
                    "exchanges": exec_plan.n_exchanges, "reference_planner_reshuffles": sd.plan(circuit, world).n_reshuffles,
                    "global_qubits": list(exec_plan.global_qubits), "exchange_bytes_per_gpu": exch_bytes},
         "e2e": {"value": min(e2e_t), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,

@@ -91,6 +91,9 @@ GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 5), nat.QSB_C64: TileGeo
 # chosen per pass (SPLIT_MAX_CODE, and only when it needs no extra layout change).
 # QSB_SPLIT_2Q=0 disables it, =1 forces it for every 2-qubit-gate pass.
 GEOMETRY_JIT_2Q_SPLIT = {nat.QSB_C128: TileGeometry(12, 3, 4, 5, split=True)}
+if os.environ.get("QSB_2Q_GEOMETRY", "") == "c64s3":
+    # experiment: complex64 512 x 16 with three 64 KB stages + the split 32 KB transpose buffer
+    GEOMETRY_JIT_2Q = {nat.QSB_C128: GEOMETRY_JIT_2Q[nat.QSB_C128], nat.QSB_C64: TileGeometry(13, 4, 5, 4, split=True)}
 if os.environ.get("QSB_2Q_GEOMETRY", "") == "s3":
     # experiment: 256 consumers x 16 amplitudes, one CTA per SM, three 64 KB stages + the split
     # 32 KB transpose buffer (half the straight-line code per thread, three tiles in flight)

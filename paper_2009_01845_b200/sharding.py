@@ -521,6 +521,33 @@ class TorchComm:
         self.dist.barrier(group=self.group)
 
 
+class HostStagedComm(TorchComm):
+    """TorchComm over a backend that cannot move CUDA tensors (gloo): every transfer is staged
+    through host memory.  A validation transport only (several ranks sharing one GPU, where
+    NCCL refuses to run); the compute stays on the device and the exchange pipeline is the same
+    code as under NCCL, with host synchronisation instead of stream ordering."""
+
+    stream_ordered = False
+
+    def isendrecv(self, send, recv, peer):
+        return self.ialltoall([(send, recv, peer)])
+
+    def ialltoall(self, triples):
+        torch = nat.torch_mod()
+        staged = [(send.cpu(), torch.empty(send.shape, dtype=send.dtype), recv, peer) for send, recv, peer in triples]
+        for w in super().ialltoall([(hs, hr, peer) for hs, hr, _, peer in staged]):
+            w.wait()
+        for _, hr, recv, _ in staged:
+            recv.copy_(hr)
+        return []
+
+    def all_gather(self, t):
+        return [x.to(t.device) for x in super().all_gather(t.cpu())]
+
+    def barrier(self):
+        self.dist.barrier(group=self.group)
+
+
 # ------------------------------------------------------------------------------------------
 # sharded state
 # ------------------------------------------------------------------------------------------
@@ -1263,7 +1290,7 @@ def execute_distributed(circuit: Circuit, precision: Precision = Precision.F64, 
     return run_sharded(circuit, comm.world, None, precision, global_qubits, comm)
 
 
-__all__ = ["Exchange", "ExecutionPlan", "LocalSegment", "Reshuffle", "exchange", "plan_batched", "ShardedState", "apply_sharded", "canonicalize",
+__all__ = ["Exchange", "ExecutionPlan", "HostStagedComm", "LocalSegment", "Reshuffle", "exchange", "plan_batched", "ShardedState", "apply_sharded", "canonicalize",
            "execute_distributed", "execute_sharded", "expectation_sharded", "gather", "norm_sharded", "overlap_sharded", "partition", "plan", "reshuffle",
            "sample_sharded", "uniform_sharded"]
 _ = (_check_cap, zero_state, diag_terms, NGate)

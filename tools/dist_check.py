@@ -19,27 +19,7 @@ os.environ.setdefault("QSB_EXCHANGE_CHUNK_BYTES", str(1 << 16))
 sd.TorchComm.CHUNK_BYTES = int(os.environ["QSB_EXCHANGE_CHUNK_BYTES"])
 
 
-class HostStagedComm(sd.TorchComm):
-    """gloo cannot move CUDA tensors: stage each chunk through host memory (check only)."""
-
-    def isendrecv(self, send, recv, peer):
-        hs = send.cpu()
-        hr = torch.empty_like(hs)
-        for w in super().isendrecv(hs, hr, peer):
-            w.wait()
-        recv.copy_(hr)
-        return []
-
-    def ialltoall(self, triples):
-        staged = [(send.cpu(), torch.empty(send.shape, dtype=send.dtype), recv, peer) for send, recv, peer in triples]
-        for w in super().ialltoall([(hs, hr, peer) for hs, hr, _, peer in staged]):
-            w.wait()
-        for _, hr, recv, _ in staged:
-            recv.copy_(hr)
-        return []
-
-    def all_gather(self, t):
-        return [x.cuda() for x in super().all_gather(t.cpu())]
+HostStagedComm = sd.HostStagedComm
 
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 18
