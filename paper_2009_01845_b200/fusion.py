@@ -205,15 +205,22 @@ def _entry_cost(z) -> float:
 
 
 def matrix_cost(m: np.ndarray) -> float:
-    """FP ops per amplitude of applying `m` (sum of entry costs / dimension; vectorised form of
-    _entry_cost)."""
-    z = np.asarray(m, dtype=np.complex128).reshape(-1)
-    re, im = z.real, z.imag
-    nz = z != 0
-    unit = (im == 0) & (np.abs(re) == 1)
-    half = (re == 0) | (im == 0)
-    cost = np.where(~nz, 0.0, np.where(unit, 1.0, np.where(half, 2.0, 4.0)))
-    return float(cost.sum()) / m.shape[0]
+    """FP ops per amplitude of applying `m` (sum of entry costs / dimension, _entry_cost per
+    entry; a plain loop: the matrices are at most 4 x 4 and numpy's per-call overhead dominated
+    host planning)."""
+    a = np.asarray(m, dtype=np.complex128)
+    total = 0.0
+    for z in a.reshape(-1).tolist():
+        if z == 0:
+            continue
+        re, im = z.real, z.imag
+        if im == 0 and (re == 1 or re == -1):
+            total += 1.0
+        elif re == 0 or im == 0:
+            total += 2.0
+        else:
+            total += 4.0
+    return total / a.shape[0]
 
 
 def _embed_1q(u: np.ndarray, pos: int) -> np.ndarray:

@@ -294,6 +294,13 @@ class _Gen:
         self.h_scale = 0  # deferred 1/sqrt(2) factors of uncontrolled Hadamard butterflies
         self.vm = list(range(self.A))  # slot of the current layout -> register variable v<i>
         self.n_cops = 0  # ops with coefficient reads emitted so far
+        # coefficient-only mode (structure templates): no source text, only the parameter /
+        # table vectors, the word positions read as doubles and the value-dependent structure
+        # decisions (entry classes, Hadamard detection, unit pivot factors) -- together with
+        # the other words they determine the source exactly (compile_words' template cache)
+        self.quiet = False
+        self.dpos: set = set()
+        self.trace: list = []
         amp_bytes = 16 if dtype == nat.QSB_C128 else 8
         # 128 KB tiles are staged as two 64 KB halves split on tile bit K-1 (a register bit of
         # the first layout); layout changes then run in two rounds through a 64 KB buffer
@@ -339,7 +346,13 @@ class _Gen:
         return k
 
     def emit(self, s):
-        self.lines.append(s)
+        if not self.quiet:
+            self.lines.append(s)
+
+    def d(self, i):
+        """Word i read as a double (a coefficient: recorded for the structure key)."""
+        self.dpos.add(i)
+        return _w2d(self.w[i])
 
     # ---- layouts ------------------------------------------------------------------------
     def parse_layout(self, a):
@@ -409,7 +422,7 @@ class _Gen:
             for slot, ne, a in tables:
                 vals = [float(ne)] + [float(w[a + 5 + 3 * k]) for k in range(ne)]
                 for k in range(ne):
-                    vals += [_w2d(w[a + 6 + 3 * k]), _w2d(w[a + 7 + 3 * k])]
+                    vals += [self.d(a + 6 + 3 * k), self.d(a + 7 + 3 * k)]
                 offs[slot] = self.tf(vals)
             offtab = self.tf([float(o) for o in offs])
             ep.append("        if (lane < NPIV) {")
@@ -467,6 +480,10 @@ class _Gen:
                 new = self.parse_layout(a)
                 li += 1
                 self.set_layout(new, li)
+            elif op == OP_LAYOUT and self.quiet:
+                li += 1
+                self.lay = self.parse_layout(a)  # layout changes carry no coefficients
+                self.li = li
             elif op == OP_LAYOUT:
                 new = self.parse_layout(a)
                 li += 1
@@ -509,6 +526,8 @@ class _Gen:
                 self.emit("#undef ZO")
                 self.n_cops += 1
             q += ln
+        if self.quiet:
+            return ""
         body = "\n".join(self.lines[body_start:])
         if self.expect:
             return self._kernel(name, body, "")
@@ -561,11 +580,11 @@ class _Gen:
         w, A = self.w, self.A
         if op == OP_G1:
             slots_bits = [w[a]]
-            m = [_w2d(x) for x in w[a + 6:a + 14]]
+            m = [self.d(i) for i in range(a + 6, a + 14)]
             d = 2
         else:
             slots_bits = [w[a], w[a + 1]]  # ih, il
-            m = [_w2d(x) for x in w[a + 7:a + 39]]
+            m = [self.d(i) for i in range(a + 7, a + 39)]
             d = 4
         M = [[complex(m[2 * (r * d + c)], m[2 * (r * d + c) + 1]) for c in range(d)] for r in range(d)]
         diag = [(r, M[r][r].real) for r in range(d) if M[r][r].real != 0.0]
@@ -576,8 +595,11 @@ class _Gen:
                 bi = M[c][r].imag - M[r][c].imag
                 if ar != 0.0 or bi != 0.0:
                     offs.append((r, c, ar, bi))
+        self.trace.append(("expect", tuple(r for r, _ in diag), tuple((r, c, ar != 0.0, bi != 0.0) for r, c, ar, bi in offs)))
         dci = self.cf([v for _, v in diag]) if diag else 0
         oci = self.cf([x for _, _, ar, bi in offs for x in (ar, bi)]) if offs else 0
+        if self.quiet:
+            return
         mask = sum(1 << b for b in slots_bits)
         self.emit(f"    {{ // expectation term on slot bits {slots_bits}")
         for s in range(A):
@@ -603,8 +625,9 @@ class _Gen:
         self.emit("    }")
 
     def gen_scale(self, a):
-        w = self.w
-        ci = self.cf([_w2d(w[a]), _w2d(w[a + 1])])
+        ci = self.cf([self.d(a), self.d(a + 1)])
+        if self.quiet:
+            return
         self.emit(f"    {{ const C ph = PZ({ci});")
         for s in range(self.A):
             self.emit(f"      v{self.vm[s]} = cm(v{self.vm[s]}, ph);")
@@ -703,12 +726,16 @@ class _Gen:
     def gen_g1(self, a):
         w, A = self.w, self.A
         ib, kind, gmask, gval, rmask, rval = w[a:a + 6]
-        m = [_w2d(x) for x in w[a + 6:a + 14]]
+        m = [self.d(i) for i in range(a + 6, a + 14)]
         hh = 0.7071067811865475
-        if kind == 1 and not gmask and not rmask and m[0] == hh and m[2] == hh and m[4] == hh and m[6] == -hh \
-                and not any(m[1::2]):
+        is_h = (kind == 1 and not gmask and not rmask and m[0] == hh and m[2] == hh and m[4] == hh and m[6] == -hh
+                and not any(m[1::2]))
+        self.trace.append(("h", is_h))
+        if is_h:
             # uncontrolled Hadamard: sum/difference butterfly, the 1/sqrt(2) is applied once at the store
             self.h_scale += 1
+            if self.quiet:
+                return
             self.emit(f"    {{ // H butterfly slot bit {ib}")
             for s in range(A):
                 if s & (1 << ib):
@@ -761,6 +788,7 @@ class _Gen:
                 out.append(("i", self.cf([z.imag])))
             else:
                 out.append(("c", self.cf([z.real, z.imag])))
+        self.trace.append(("m", tuple(e[0] for e in out)))
         return out
 
     def emit_matvec_f32x2(self, coef, slots):
@@ -795,6 +823,8 @@ class _Gen:
     def emit_matvec(self, coef, slots):
         """y = M x over the amplitudes in `slots` (matrix row/col index = position in `slots`),
         skipping zero entries; one FMA chain per output component."""
+        if self.quiet:
+            return
         if self.dtype == nat.QSB_C64:
             return self.emit_matvec_f32x2(coef, slots)
         d = len(slots)
@@ -841,7 +871,7 @@ class _Gen:
     def gen_g2(self, a):
         w, A = self.w, self.A
         ih, il, kind, gmask, gval, rmask, rval = w[a:a + 7]
-        m = [_w2d(x) for x in w[a + 7:a + 39]]
+        m = [self.d(i) for i in range(a + 7, a + 39)]
         self.emit(f"    {{ // G2 slot bits {ih},{il}")
         if gmask:
             self.emit(f"    if (((base | gt{self.li}) & {gmask}ull) == {gval}ull) {{")
@@ -862,14 +892,18 @@ class _Gen:
         ta_w = w[a + 5 + 3 * ne:a + 5 + 3 * ne + 32]
         tb_w = w[a + 5 + 3 * ne + 32:a + 5 + 3 * ne + 32 + 2 * nb]
         rt_w = w[a + 5 + 3 * ne + 32 + 2 * nb:a + 5 + 3 * ne + 32 + 2 * nb + 2 * A]
-        ta = [complex(_w2d(ta_w[2 * k]), _w2d(ta_w[2 * k + 1])) for k in range(16)]
-        tb = [complex(_w2d(tb_w[2 * k]), _w2d(tb_w[2 * k + 1])) for k in range(nb)]
-        rt = [complex(_w2d(rt_w[2 * k]), _w2d(rt_w[2 * k + 1])) for k in range(A)]
+        o_ta = a + 5 + 3 * ne
+        o_tb = o_ta + 32
+        o_rt = o_tb + 2 * nb
+        ta = [complex(self.d(o_ta + 2 * k), self.d(o_ta + 2 * k + 1)) for k in range(16)]
+        tb = [complex(self.d(o_tb + 2 * k), self.d(o_tb + 2 * k + 1)) for k in range(nb)]
+        rt = [complex(self.d(o_rt + 2 * k), self.d(o_rt + 2 * k + 1)) for k in range(A)]
         self.emit(f"    {{ // pivot {slot}")
         if ptype == 1:
             self.emit(f"    if (((base | gt{self.li}) & {pval}ull) != 0ull) {{")
         ta_all_one = all(z == 1 for z in ta)
         tb_all_one = all(z == 1 for z in tb)
+        self.trace.append(("pivot", ta_all_one, tb_all_one, tuple(bool(use_rt and rt[s] != 1) for s in range(A))))
         self.emit(f"      double2 fd = sm.ep[it & 3][{slot}];")
         if not ta_all_one:
             ci = self.tf([x for z in ta for x in (z.real, z.imag)])
@@ -902,6 +936,8 @@ class _Gen:
         cross terms of register bit i.  So one 32-bit sign word per thread and tile -- a few
         popcounts -- replaces per-amplitude 64-bit popcounts, and each amplitude costs one bit
         test and its negation."""
+        if self.quiet:
+            return  # integer words only: no coefficients
         w, A, NREG = self.w, self.A, self.NREG
         s1, nd = w[a], w[a + 1]
         pairs = [(w[a + 2 + 2 * q], w[a + 3 + 2 * q]) for q in range(nd)]
@@ -929,7 +965,9 @@ class _Gen:
     def gen_term(self, a):
         w, A = self.w, self.A
         mask, val = w[a], w[a + 1]
-        ci = self.cf([_w2d(w[a + 2]), _w2d(w[a + 3])])
+        ci = self.cf([self.d(a + 2), self.d(a + 3)])
+        if self.quiet:
+            return
         self.emit(f"    {{ const C ph = PZ({ci});")
         for s in range(A):
             gi = f"(base | gt{self.li} | {self.lay['goff'][s]}ull)"
@@ -1192,11 +1230,35 @@ def available() -> bool:
 def generate_full(words, dtype):
     """(source, kernel name, parameter coefficients, table coefficients, TMA plan) for a pass
     program (CPU-only)."""
+    src, name, coeffs, tables, tplan, _key = _generate(words, dtype)
+    return src, name, coeffs, tables, tplan
+
+
+def _structure_key(g, words, dtype):
+    masked = np.array(words, dtype=np.int64)
+    if g.dpos:
+        masked[np.fromiter(g.dpos, dtype=np.int64)] = 0
+    return (int(dtype), masked.tobytes(), tuple(g.trace))
+
+
+def _generate(words, dtype):
     g = _Gen(words, dtype)
     body_probe = g.generate("KNAME")
     name = "qsb_pass_" + hashlib.sha1(body_probe.encode()).hexdigest()[:16]
     src = body_probe.replace("KNAME", name)
-    return src, name, np.array(g.coeffs, dtype=np.float64), np.array(g.tables, dtype=np.float64), g.tplan
+    return (src, name, np.array(g.coeffs, dtype=np.float64), np.array(g.tables, dtype=np.float64), g.tplan,
+            _structure_key(g, words, dtype))
+
+
+def coefficients_only(words, dtype):
+    """(structure key, parameter coefficients, table coefficients) without generating source:
+    two programs with the same key compile to the same kernel (the key holds every word that is
+    not a coefficient plus every value-dependent structure decision), so a pass whose structure
+    was seen before -- every step of a time-dependent Trotter evolution -- only needs these."""
+    g = _Gen(words, dtype)
+    g.quiet = True
+    g.generate("KNAME")
+    return _structure_key(g, words, dtype), np.array(g.coeffs, dtype=np.float64), np.array(g.tables, dtype=np.float64)
 
 
 def generate(words, dtype):
@@ -1277,13 +1339,37 @@ _WORDS_CACHE: dict = {}  # (dtype, program bytes) -> compile_words result: rebui
 _WORDS_CACHE_MAX = 256
 
 
+# compiled kernels by structure key (coefficients_only): a program whose structure was seen
+# before only needs its coefficient vectors, not its source (time-dependent evolutions: every
+# step has new coefficients, the same structure)
+_STRUCT_CACHE: dict = {}
+
+
+def _param_bytes(params, words, dtype):
+    expect = bool(int(words[7]) & 2)
+    pbytes = params.astype(np.float64 if (dtype == nat.QSB_C128 or expect) else np.float32)
+    if pbytes.nbytes > MAX_PARAM_BYTES:
+        raise RuntimeError(f"{pbytes.nbytes} bytes of gate coefficients exceed the kernel parameter space")
+    if len(pbytes) == 0:
+        pbytes = np.zeros(1, dtype=pbytes.dtype)
+    return np.ascontiguousarray(pbytes)
+
+
 def compile_words(words, dtype):
     wkey = (int(dtype), np.asarray(words, dtype=np.int64).tobytes())
     with _lock:
         done = _WORDS_CACHE.get(wkey)
     if done is not None:
         return done
-    out = _compile_words(words, dtype)
+    out = None
+    if _STRUCT_CACHE:
+        key, params, tables = coefficients_only(words, dtype)
+        with _lock:
+            hit = _STRUCT_CACHE.get(key)
+        if hit is not None and len(tables) <= MAX_COEFFS:
+            out = (hit, (_param_bytes(params, words, dtype), tables))
+    if out is None:
+        out = _compile_words(words, dtype)
     with _lock:
         if len(_WORDS_CACHE) >= _WORDS_CACHE_MAX:
             _WORDS_CACHE.pop(next(iter(_WORDS_CACHE)))
@@ -1292,15 +1378,11 @@ def compile_words(words, dtype):
 
 
 def _compile_words(words, dtype):
-    src, name, params, tables, tplan = generate_full(words, dtype)
+    src, name, params, tables, tplan, skey = _generate(words, dtype)
     if len(tables) > MAX_COEFFS:
         raise RuntimeError(f"{len(tables)} table entries exceed the shared-memory budget")
+    pbytes = _param_bytes(params, words, dtype)
     expect = bool(int(words[7]) & 2)
-    pbytes = params.astype(np.float64 if (dtype == nat.QSB_C128 or expect) else np.float32)
-    if pbytes.nbytes > MAX_PARAM_BYTES:
-        raise RuntimeError(f"{pbytes.nbytes} bytes of gate coefficients exceed the kernel parameter space")
-    if len(pbytes) == 0:
-        pbytes = np.zeros(1, dtype=pbytes.dtype)
     with _lock:
         hit = _cache.get(src)
     if hit is None:
@@ -1322,7 +1404,11 @@ def _compile_words(words, dtype):
         fresh.tpc = pass_schedule(int(words[4]) - K, 1 << (K - nreg), expect, (1 << K) * amp > 65536)[0]
         with _lock:
             hit = _cache.setdefault(src, fresh)
-    return hit, (np.ascontiguousarray(pbytes), tables)
+    with _lock:
+        if len(_STRUCT_CACHE) >= 4096:
+            _STRUCT_CACHE.pop(next(iter(_STRUCT_CACHE)))
+        _STRUCT_CACHE[skey] = hit
+    return hit, (pbytes, tables)
 
 
 def precompile(steps, dtype, device: int | None = None) -> None:

@@ -10,7 +10,7 @@ import pytest
 from oracle import statevec as ov
 from plan_helpers import spec_tuples_to_specs
 from paper_2009_01845_b200 import _native as nat, jit, qft_circuit, variational_circuit
-from paper_2009_01845_b200.fusion import PassStep, plan_circuit
+from paper_2009_01845_b200.fusion import GEOMETRY_JIT, PassStep, plan_circuit
 
 
 def _compile(src, tmp_path):
@@ -79,3 +79,36 @@ def test_parity_sign_word_equals_quadratic_form():
                     W ^= M
             for sl in range(1 << nreg):
                 assert (W >> sl) & 1 == jit.parity_quadratic(x | goff[sl], s1, pairs), (trial, sl)
+
+
+def test_structure_key_determines_source():
+    """jit.coefficients_only: programs with equal structure keys generate identical kernel
+    sources, and the coefficient-only pass yields exactly the full generator's coefficients --
+    so compile_words may reuse a compiled kernel by key (time-dependent Trotter steps)."""
+    from paper_2009_01845_b200 import build_tfim, build_x, combine, random_grid_circuit, trotter_step_circuit
+
+    n = 18
+    seen = {}
+    progs = []
+    for s in (0.2, 0.5, 0.9):
+        h = combine(build_x(n), 1 - s, build_tfim(n, 1.0), s)
+        progs.append(trotter_step_circuit(h, 0.05).queue)
+    rng = np.random.default_rng(4)
+    for seed in (1, 2):
+        progs.append(random_grid_circuit(3, 6, 4, seed).queue)
+        progs.append(variational_circuit(n, 2, rng.uniform(0, 6, n * 5), fused=True).queue)
+    progs.append(qft_circuit(n).queue)
+    for dtype in (nat.QSB_C128, nat.QSB_C64):
+        for queue in progs:
+            plan = plan_circuit(queue, n, dtype, geometry=GEOMETRY_JIT[dtype])
+            for st in plan.steps:
+                if not isinstance(st, PassStep):
+                    continue
+                src, _name, cf, tab, _tp, key = jit._generate(st.words, dtype)
+                k2, cf2, tab2 = jit.coefficients_only(st.words, dtype)
+                assert k2 == key and np.array_equal(cf, cf2) and np.array_equal(tab, tab2)
+                if key in seen:
+                    assert seen[key] == src
+                seen[key] = src
+    # the Trotter steps at different field ratios share their kernels
+    assert len(seen) < sum(1 for q_ in progs for _ in q_)
