@@ -34,9 +34,25 @@ def _free_bytes() -> int:
 _SCRATCH_ASSUMED = 256 << 20
 
 
+# (time, free bytes, torch-reserved bytes) of the last cudaMemGetInfo: reused for 0.5 s while
+# this process's reserved memory has not moved by more than 256 MB
+_FREE_CACHE = [0.0, 0, 0]
+
+
 def scratch_fits(nbytes: int) -> bool:
-    """Whether an out-of-place pass may allocate a scratch state of `nbytes` (plus headroom)."""
-    return nbytes <= _SCRATCH_ASSUMED or _free_bytes() > nbytes + (512 << 20)
+    """Whether an out-of-place pass may allocate a scratch state of `nbytes` (plus headroom).
+    The free-memory query (~2 ms) is cached briefly: a time-dependent evolution asks several
+    times per step."""
+    if nbytes <= _SCRATCH_ASSUMED:
+        return True
+    import time
+
+    torch = nat.torch_mod()
+    now = time.monotonic()
+    reserved = int(torch.cuda.memory_reserved())
+    if now - _FREE_CACHE[0] > 0.5 or abs(reserved - _FREE_CACHE[2]) > (256 << 20):
+        _FREE_CACHE[:] = [now, _free_bytes(), reserved]
+    return _FREE_CACHE[1] > nbytes + (512 << 20)
 
 
 def default_geometry(dtype: int):

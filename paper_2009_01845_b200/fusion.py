@@ -223,9 +223,17 @@ def matrix_cost(m: np.ndarray) -> float:
     return total / a.shape[0]
 
 
+_EYE2 = np.eye(2, dtype=np.complex128)
+
+
+def _kron2(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """np.kron of two 2x2 matrices (a = MSB factor) without np.kron's per-call overhead."""
+    return (np.asarray(a)[:, None, :, None] * np.asarray(b)[None, :, None, :]).reshape(4, 4)
+
+
 def _embed_1q(u: np.ndarray, pos: int) -> np.ndarray:
     """4x4 of a single-qubit matrix on target `pos` (0 = matrix MSB) of a two-qubit gate."""
-    return np.kron(u, np.eye(2)) if pos == 0 else np.kron(np.eye(2), u)
+    return _kron2(u, _EYE2) if pos == 0 else _kron2(_EYE2, u)
 
 
 def merge_1q_runs(gates: list) -> list:
@@ -269,7 +277,7 @@ def sandwich_diagonals(gates: list) -> list:
     for i, d in enumerate(out):
         if not alive[i] or d.kind not in ("diag", "g2") or d.controls or len(d.targets) != 2:
             continue
-        parts, pre, post = [], [np.eye(2), np.eye(2)], [np.eye(2), np.eye(2)]
+        parts, pre, post = [], [_EYE2, _EYE2], [_EYE2, _EYE2]
         for pos, t in enumerate(d.targets):
             bit = 1 << t
             for step, slot in ((-1, pre), (1, post)):
@@ -281,7 +289,7 @@ def sandwich_diagonals(gates: list) -> list:
             continue
         core = np.diag(d.matrix) if d.kind == "diag" else d.matrix
         core_cost = 0.0 if d.kind == "diag" else matrix_cost(d.matrix)
-        merged = np.kron(post[0], post[1]) @ core @ np.kron(pre[0], pre[1])
+        merged = _kron2(post[0], post[1]) @ core @ _kron2(pre[0], pre[1])
         if matrix_cost(merged) < core_cost + sum(matrix_cost(out[k].matrix) for k in parts) - 1e-9:
             out[i] = NGate("g2", d.targets, (), merged, _bits(d.targets), d.smask, d.index)
             for k in parts:
@@ -777,18 +785,23 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
     words = []
     n_trans = 0
 
+    def slot_offsets(bits):
+        # offsets of all A slots: slot s = OR of bits[i] for the set bits i of s (built by doubling)
+        offs = [0]
+        for b in bits:
+            v = 1 << b
+            offs += [o | v for o in offs]
+        return offs
+
     def layout_words(lay):
         w = [OP_LAYOUT, 0]
         w += lay.R
         w += lay.Tb
-        for s in range(A):
-            w.append(sum(1 << tile_pos[lay.R[i]] for i in range(NREG) if (s >> i) & 1))
+        w += slot_offsets([tile_pos[b] for b in lay.R])
         w += [tile_pos[b] for b in lay.Tb]
-        for s in range(A):
-            w.append(sum(1 << out_pos[lay.R[i]] for i in range(NREG) if (s >> i) & 1))
+        w += slot_offsets([out_pos[b] for b in lay.R])
         w += [out_pos[b] for b in lay.Tb]
-        for s in range(A):
-            w.append(sum(1 << lay.R[i] for i in range(NREG) if (s >> i) & 1))
+        w += slot_offsets(list(lay.R))
         w[1] = len(w)
         return w
 

@@ -1418,6 +1418,25 @@ def precompile(steps, dtype, device: int | None = None) -> None:
     todo = [s for s in steps if getattr(s, "jit", None) is None and not getattr(s, "no_jit", False)]
     if len(todo) < 2 or not available():
         return
+    if _STRUCT_CACHE:
+        # passes whose structure is compiled already only need their coefficients: inline
+        # (a thread pool per call costs more than that), the rest compile concurrently
+        rest = []
+        for st in todo:
+            try:
+                key, params, tables = coefficients_only(st.words, dtype)
+            except Exception:
+                rest.append(st)
+                continue
+            with _lock:
+                hit = _STRUCT_CACHE.get(key)
+            if hit is not None and len(tables) <= MAX_COEFFS:
+                st.jit = (hit, (_param_bytes(params, st.words, dtype), tables))
+            else:
+                rest.append(st)
+        todo = rest
+        if len(todo) < 2:
+            return
     torch = nat.torch_mod()
     dev = torch.cuda.current_device() if device is None else device
 
