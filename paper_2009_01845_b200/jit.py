@@ -63,6 +63,12 @@ REG_SPLIT = {c: _reg_split(c, ctas_per_sm(c)) for c in (128, 256, 512)}
 TILES_PER_CTA = int(os.environ.get("QSB_TILES_PER_CTA", "16"))
 PASS_SCHED = os.environ.get("QSB_PASS_SCHED", "dynamic")  # dynamic | oneshot | static
 TMA_STORE = os.environ.get("QSB_TMA_STORE", "1") != "0"
+# Immediate coefficient offsets (constant-bank operands, no per-op zero pin): complex64 passes
+# (measured round 2: variational-30 c64 42.0 -> 38.0 ms, QFT-30 c64 11.0 -> 10.5 ms, no spills)
+# and, with QSB_IMMEDIATE_C128=1, complex128 passes without dense 2-qubit gates (measured on the
+# QFT-30 passes: 20.87 -> 20.95 ms, so off; the variational passes would spill 296 bytes)
+IMMEDIATE_C64 = os.environ.get("QSB_IMMEDIATE_C64", "1") == "1"
+IMMEDIATE_C128 = os.environ.get("QSB_IMMEDIATE_C128", "0") == "1"
 DYN_CHUNK = int(os.environ.get("QSB_DYN_CHUNK", "2"))
 
 
@@ -330,6 +336,8 @@ class _Gen:
             q += w[q + 1]
         self.tma_store = (TMA_STORE and not (self.halves or self.split or self.alias or self.expect)
                           and not self.ext_perm and OP_G2 not in ops)
+        self.immediate = (IMMEDIATE_C64 if dtype == nat.QSB_C64
+                          else (IMMEDIATE_C128 and OP_G2 not in ops and not self.expect))
         self.uses_tma_store = False
 
     # uniform coefficients (gate matrices, phases): a kernel-parameter array of R, read as
@@ -518,10 +526,15 @@ class _Gen:
                 # this op's coefficient reads are indexed by zo<k>; zo<k+1> is loaded now so the
                 # next op's coefficients can be fetched while this op computes
                 k = self.n_cops
-                if k == 0:
-                    self.emit("    const int zo0 = zpin(&sm.zero);")
-                self.emit(f"    const int zo{k + 1} = zpin(&sm.zero);")
-                self.emit(f"#define ZO zo{k}")
+                if self.immediate:
+                    # immediate coefficient offsets (constant-bank operands); the zero-pin
+                    # guard below keeps ptxas from hoisting every coefficient into registers
+                    self.emit("#define ZO 0")
+                else:
+                    if k == 0:
+                        self.emit("    const int zo0 = zpin(&sm.zero);")
+                    self.emit(f"    const int zo{k + 1} = zpin(&sm.zero);")
+                    self.emit(f"#define ZO zo{k}")
                 gen(a)
                 self.emit("#undef ZO")
                 self.n_cops += 1
