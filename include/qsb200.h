@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define QSB_ABI_VERSION 3
+#define QSB_ABI_VERSION 4
 
 typedef enum { QSB_C64 = 0, QSB_C128 = 1 } qsb_dtype;
 
@@ -125,18 +125,21 @@ int qsb_jit_compile_cubin(const char* source, const char* name, const char* nvrt
 int qsb_jit_load(const void* cubin, const char* name, void** func_out);
 /* Launch a specialised pass kernel over `n_tiles` tiles.  `tma_desc` describes the state as the
  * rank-5 tensor the kernel's tile loads address (15 words: rank, global dims[5], byte strides of
- * dims 1..4, box dims[5]; jit.py tma_plan).  `tables` (doubles, staged to the device) are the
+ * dims 1..4, box dims[5]; jit.py tma_plan); `tma_desc_out` (NULL: the same) the tensor the bulk
+ * tile stores address over `dst` (out-of-place passes whose output tile bits sit elsewhere).  `tables` (doubles, staged to the device) are the
  * per-thread pivot tables; `params` (`param_bytes`, passed by value as the kernel's last
  * parameter) are the uniform gate coefficients; `grid` CTAs are launched (1 <= grid <= n_tiles:
  * one-shot CTAs of a few tiles each, or a persistent grid, as the kernel was generated for). */
-int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tma_desc, uint64_t n_tiles,
+int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tma_desc, const int64_t* tma_desc_out,
+                     uint64_t n_tiles,
                      const double* tables, int64_t n_tables, const void* params, int64_t param_bytes,
                      int threads, int smem_bytes, int grid, void* stream);
 /* qsb_jit_run_pass with the pivot tables already in device memory (`dev_tables`, owned by the
  * caller and alive until the launch completes): nothing is staged through the library's host
  * ring, so the launch can be captured into a CUDA graph and replayed.  (qsb_jit_run_pass and
  * qsb_run_pass refuse to stage while their stream is capturing.) */
-int qsb_jit_run_pass_dev(void* func, const void* src, void* dst, const int64_t* tma_desc, uint64_t n_tiles,
+int qsb_jit_run_pass_dev(void* func, const void* src, void* dst, const int64_t* tma_desc,
+                         const int64_t* tma_desc_out, uint64_t n_tiles,
                          const double* dev_tables, int64_t n_tables, const void* params, int64_t param_bytes,
                          int threads, int smem_bytes, int grid, void* stream);
 

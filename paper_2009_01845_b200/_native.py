@@ -71,13 +71,13 @@ SIGNATURES = {
     "qsb_jit_load": (_c_int, [_c_void_p, ctypes.c_char_p, _c_void_p]),
     "qsb_jit_run_pass": (
         _c_int,
-        [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_u64, _c_void_p, _c_i64, _c_void_p, _c_i64, _c_int, _c_int,
-         _c_int, _c_void_p],
+        [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_u64, _c_void_p, _c_i64, _c_void_p, _c_i64, _c_int,
+         _c_int, _c_int, _c_void_p],
     ),
     "qsb_jit_run_pass_dev": (
         _c_int,
-        [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_u64, _c_void_p, _c_i64, _c_void_p, _c_i64, _c_int, _c_int,
-         _c_int, _c_void_p],
+        [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_u64, _c_void_p, _c_i64, _c_void_p, _c_i64, _c_int,
+         _c_int, _c_int, _c_void_p],
     ),
     "qsb_permute_qubits": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_int, _c_void_p, _c_void_p]),
     "qsb_exchange_halves": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_int, _c_int, _c_void_p]),

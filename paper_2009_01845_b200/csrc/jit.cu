@@ -227,7 +227,20 @@ extern "C" int qsb_jit_load(const void* cubin, const char* name, void** func_out
 // Launch a JIT pass kernel: params (src, dst, tensor map, coefficients, tile counter).  The tensor map is
 // encoded here from `tdesc` (jit.py tma_plan: rank, dims[5], byte strides[4], box[5]) over the
 // 8-byte elements of the state at `src`.
-static int run_pass_impl(void* func, const void* src, void* dst, const int64_t* tdesc, uint64_t n_tiles,
+static int encode_desc(CUtensorMap* map, void* base, const int64_t* tdesc) {
+  cuuint64_t gdim[5], gstride[4];
+  cuuint32_t box[5], estride[5];
+  for (int d = 0; d < 5; ++d) {
+    gdim[d] = (cuuint64_t)tdesc[1 + d];
+    box[d] = (cuuint32_t)tdesc[10 + d];
+    estride[d] = 1;
+    if (d < 4) gstride[d] = (cuuint64_t)tdesc[6 + d];
+  }
+  return pass::encode_tensor_map(map, base, gdim, gstride, box, estride);
+}
+
+static int run_pass_impl(void* func, const void* src, void* dst, const int64_t* tdesc, const int64_t* tdesc_out,
+                         uint64_t n_tiles,
                          const double* coeffs, int64_t n_coeffs, bool coeffs_on_device, const void* params,
                          int64_t param_bytes, int threads, int smem_bytes, int grid, void* stream) {
   jit::Driver* dr = jit::driver();
@@ -235,7 +248,7 @@ static int run_pass_impl(void* func, const void* src, void* dst, const int64_t* 
     set_error("qsb_jit_run_pass: no driver / function");
     return QSB_ERR_CUDA;
   }
-  if (!tdesc || tdesc[0] != 5 || n_tiles == 0 || !params || param_bytes <= 0 || param_bytes > 32000) {
+  if (!tdesc || tdesc[0] != 5 || n_tiles == 0 || !params || param_bytes <= 0 || param_bytes > 31616) {
     set_error("qsb_jit_run_pass: bad tile descriptor");
     return QSB_ERR_ARG;
   }
@@ -248,16 +261,19 @@ static int run_pass_impl(void* func, const void* src, void* dst, const int64_t* 
       return rc;
   }
   alignas(64) CUtensorMap map;
+  alignas(64) CUtensorMap map_o;
   memset(&map, 0, sizeof map);
-  cuuint64_t gdim[5], gstride[4];
-  cuuint32_t box[5], estride[5];
-  for (int d = 0; d < 5; ++d) {
-    gdim[d] = (cuuint64_t)tdesc[1 + d];
-    box[d] = (cuuint32_t)tdesc[10 + d];
-    estride[d] = 1;
-    if (d < 4) gstride[d] = (cuuint64_t)tdesc[6 + d];
+  if (int rc = encode_desc(&map, const_cast<void*>(src), tdesc)) return rc;
+  if (tdesc_out) {
+    if (tdesc_out[0] != 5) {
+      set_error("qsb_jit_run_pass: bad output tile descriptor");
+      return QSB_ERR_ARG;
+    }
+    memset(&map_o, 0, sizeof map_o);
+    if (int rc = encode_desc(&map_o, dst, tdesc_out)) return rc;
+  } else {
+    map_o = map;
   }
-  if (int rc = pass::encode_tensor_map(&map, const_cast<void*>(src), gdim, gstride, box, estride)) return rc;
   CUfunction fn = reinterpret_cast<CUfunction>(func);
   static CUfunction attr_done[256];
   static int n_attr = 0;
@@ -281,7 +297,7 @@ static int run_pass_impl(void* func, const void* src, void* dst, const int64_t* 
   unsigned long long* a_sched = nullptr;
   if (int rc = sched_slot(&a_sched, st, true)) return rc;
   // the last kernel parameter is the coefficient struct, copied by value from `params`
-  void* args[] = {(void*)&a_src, (void*)&a_dst, (void*)&map, (void*)&a_cf, (void*)&a_sched,
+  void* args[] = {(void*)&a_src, (void*)&a_dst, (void*)&map, (void*)&map_o, (void*)&a_cf, (void*)&a_sched,
                   const_cast<void*>(params)};
   CUresult r = dr->launch(fn, (unsigned)grid, 1, 1, (unsigned)threads, 1, 1, (unsigned)smem_bytes, (CUstream)st, args,
                           nullptr);
@@ -292,16 +308,18 @@ static int run_pass_impl(void* func, const void* src, void* dst, const int64_t* 
   return QSB_OK;
 }
 
-extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tdesc, uint64_t n_tiles,
-                                const double* tables, int64_t n_tables, const void* params, int64_t param_bytes,
-                                int threads, int smem_bytes, int grid, void* stream) {
-  return run_pass_impl(func, src, dst, tdesc, n_tiles, tables, n_tables, false, params, param_bytes, threads,
-                       smem_bytes, grid, stream);
+extern "C" int qsb_jit_run_pass(void* func, const void* src, void* dst, const int64_t* tdesc,
+                                const int64_t* tdesc_out, uint64_t n_tiles, const double* tables, int64_t n_tables,
+                                const void* params, int64_t param_bytes, int threads, int smem_bytes, int grid,
+                                void* stream) {
+  return run_pass_impl(func, src, dst, tdesc, tdesc_out, n_tiles, tables, n_tables, false, params, param_bytes,
+                       threads, smem_bytes, grid, stream);
 }
 
-extern "C" int qsb_jit_run_pass_dev(void* func, const void* src, void* dst, const int64_t* tdesc, uint64_t n_tiles,
-                                    const double* dev_tables, int64_t n_tables, const void* params,
-                                    int64_t param_bytes, int threads, int smem_bytes, int grid, void* stream) {
-  return run_pass_impl(func, src, dst, tdesc, n_tiles, dev_tables, n_tables, true, params, param_bytes, threads,
-                       smem_bytes, grid, stream);
+extern "C" int qsb_jit_run_pass_dev(void* func, const void* src, void* dst, const int64_t* tdesc,
+                                    const int64_t* tdesc_out, uint64_t n_tiles, const double* dev_tables,
+                                    int64_t n_tables, const void* params, int64_t param_bytes, int threads,
+                                    int smem_bytes, int grid, void* stream) {
+  return run_pass_impl(func, src, dst, tdesc, tdesc_out, n_tiles, dev_tables, n_tables, true, params, param_bytes,
+                       threads, smem_bytes, grid, stream);
 }

@@ -323,19 +323,24 @@ class _Gen:
         self.sched = pass_schedule(self.n - K, self.consumers, self.expect, self.halves)
         self.HB = K - 1 if (self.halves or self.split) else K  # bits of a transpose-buffer index
         self.SB = K - 1 if self.halves else K  # bits of a stage index
-        # bulk tensor stores through the transpose buffer (2-stage geometry, in-place passes)
-        # for passes without dense two-qubit gates: measured (round 2, n = 30) QFT c128
-        # 21.6 -> 20.9 ms, c64 11.5 -> 11.0 ms, but passes with dense 2-qubit gates in this
-        # geometry got slower (variational c64 44.4 -> 46.0 ms, grid c128 300 -> 308 ms): their
-        # FP work already hides the store back-pressure and the extra staging costs shared
-        # memory bandwidth.  QSB_TMA_STORE=0 disables it.
+        # bulk tensor stores through the transpose buffer (2-stage geometry) for passes without
+        # dense two-qubit gates: measured (round 2, n = 30) QFT c128 21.6 -> 20.9 ms, c64 11.5 ->
+        # 11.0 ms, but passes with dense 2-qubit gates in this geometry got slower (variational
+        # c64 44.4 -> 46.0 ms, grid c128 300 -> 308 ms): their FP work already hides the store
+        # back-pressure and the extra staging costs shared memory bandwidth.  Out-of-place
+        # passes store through a second tensor map over the destination.  QSB_TMA_STORE=0
+        # disables it.
         ops = []
         q = self.ops0
         while w[q] != OP_END:
             ops.append(w[q])
             q += w[q + 1]
-        self.tma_store = (TMA_STORE and not (self.halves or self.split or self.alias or self.expect)
-                          and not self.ext_perm and OP_G2 not in ops)
+        self.tma_store_ok = (TMA_STORE and not (self.halves or self.split or self.alias or self.expect)
+                             and OP_G2 not in ops)
+        # the bulk-store path needs the transpose buffer free of an in-flight store before a
+        # layout change writes it (set once the store plan is known, see the store section)
+        self.tma_store = self.tma_store_ok
+        self.oplan = None
         self.immediate = (IMMEDIATE_C64 if dtype == nat.QSB_C64
                           else (IMMEDIATE_C128 and OP_G2 not in ops and not self.expect))
         self.uses_tma_store = False
@@ -558,13 +563,22 @@ class _Gen:
         for i, b in enumerate(lay['R']):
             out_of[b] = lay['ooff'][1 << i].bit_length() - 1
         tpos = list(self.tile_pos)
-        if self.tma_store and sorted(out_of.values()) == sorted(tpos):
-            # in-place pass whose tile lands on its own positions (SWAPs inside the tile only
-            # permute them): the tile goes back through the transpose buffer in the TMA image
-            # order of the OUTPUT positions and one warp issues bulk tensor stores, so the
-            # consumers never wait for HBM write back-pressure
-            sig = self.tplan["sigma"]
-            img = {b: sig[tpos.index(out_of[b])] for b in out_of}
+        opos = sorted(out_of.values())
+        if self.tma_store_ok:
+            if opos == sorted(tpos):
+                self.oplan = self.tplan  # the tile lands on its own positions: one tensor map
+            else:
+                # out of place, tile bits landing on other positions (SWAPs across the tile
+                # boundary): a second tensor map over the destination, planned for the output
+                # positions
+                amp_bytes = 16 if self.dtype == nat.QSB_C128 else 8
+                self.oplan = tma_plan(opos, self.n, amp_bytes)
+        if self.oplan is not None:
+            # the tile goes back through the transpose buffer in the TMA image order of its
+            # OUTPUT positions and one warp issues bulk tensor stores, so the consumers never
+            # wait for HBM write back-pressure
+            sig = self.oplan["sigma"]
+            img = {b: sig[opos.index(out_of[b])] for b in out_of}
             so = self.thread_expr([img[b] for b in lay['Tb']], 32)
             store.append("    if (tid < 32) bulk_wait_read0();")
             store.append("    csync();")
@@ -1010,12 +1024,20 @@ class _Gen:
                    f"          tma5(d + (u64)k * {call_bytes}u, &tmap, co, &sm.full[s]);\n"
                    f"        }}")
         if "@@TMASTORE@@" in store:
+            op_ = self.oplan
+            o_ncalls = 1 << len(op_["iter_pos"])
+            o_koff = " | ".join(f"((u64)((k >> {j}) & 1) << {b})" for j, b in enumerate(op_["iter_pos"])) or "0ull"
+            o_coords = ["0" if bx else f"(int)((b >> {lo}) & {(1 << nb) - 1}ull)" for lo, nb, bx in op_["dims"]]
+            o_coords += ["0"] * (5 - len(o_coords))
+            o_bytes = op_["box_amps"] * (16 if self.dtype == nat.QSB_C128 else 8)
+            # in place: the loads' map (over src = dst); out of place: a map over dst
+            o_map = "tmap" if (op_ is tp and not self.ext_perm) else "tmap_o"
             store = store.replace("@@TMASTORE@@", (
                 f"    if (tid < 32) {{\n"
-                f"      for (int k = tid; k < {ncalls}; k += 32) {{\n"
-                f"        const u64 b = base | {koff};\n"
-                f"        const int co[5] = {{{', '.join(coords)}}};\n"
-                f"        tma5_store(&tmap, co, reinterpret_cast<const char*>(&sm.tbuf[0]) + (u64)k * {call_bytes}u);\n"
+                f"      for (int k = tid; k < {o_ncalls}; k += 32) {{\n"
+                f"        const u64 b = obase | {o_koff};\n"
+                f"        const int co[5] = {{{', '.join(o_coords)}}};\n"
+                f"        tma5_store(&{o_map}, co, reinterpret_cast<const char*>(&sm.tbuf[0]) + (u64)k * {o_bytes}u);\n"
                 f"      }}\n"
                 f"      bulk_commit();\n"
                 f"    }}"))
@@ -1081,7 +1103,8 @@ class _Gen:
 // consumers, which hold the tile in registers.
 extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_sm(self.consumers)})
 {name}(const C* __restrict__ src, C* __restrict__ dst, const __grid_constant__ TMap tmap,
-       const double* __restrict__ cf, unsigned long long* __restrict__ sched, const __grid_constant__ CP cp) {{
+       const __grid_constant__ TMap tmap_o, const double* __restrict__ cf, unsigned long long* __restrict__ sched,
+       const __grid_constant__ CP cp) {{
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   double* scf = reinterpret_cast<double*>(smem_raw + sizeof(Smem));  // pivot tables
@@ -1185,7 +1208,7 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
 
 
 class _Compiled:
-    __slots__ = ("func", "name", "smem", "tdesc", "n_tiles", "threads", "ctas", "tpc")
+    __slots__ = ("func", "name", "smem", "tdesc", "tdesc_out", "n_tiles", "threads", "ctas", "tpc")
 
     def grid(self) -> int:
         """CTAs of one launch (one-shot tiles-per-CTA grid, or SMs x resident CTAs)."""
@@ -1259,7 +1282,10 @@ def _generate(words, dtype):
     body_probe = g.generate("KNAME")
     name = "qsb_pass_" + hashlib.sha1(body_probe.encode()).hexdigest()[:16]
     src = body_probe.replace("KNAME", name)
-    return (src, name, np.array(g.coeffs, dtype=np.float64), np.array(g.tables, dtype=np.float64), g.tplan,
+    tplan = dict(g.tplan)
+    # tensor map of the bulk stores when it differs from the loads' (out-of-place passes)
+    tplan["tdesc_out"] = g.oplan["tdesc"] if (g.oplan is not None and (g.oplan is not g.tplan or g.ext_perm)) else None
+    return (src, name, np.array(g.coeffs, dtype=np.float64), np.array(g.tables, dtype=np.float64), tplan,
             _structure_key(g, words, dtype))
 
 
@@ -1280,7 +1306,7 @@ def generate(words, dtype):
 
 
 MAX_COEFFS = 3072  # 24 KB of pivot tables staged in shared memory
-MAX_PARAM_BYTES = 31744  # kernel parameter space: 32764 B minus the pointers and the tensor map
+MAX_PARAM_BYTES = 31616  # kernel parameter space: 32764 B minus the pointers and the two tensor maps
 
 
 def split_stages(consumers: int) -> int:
@@ -1412,6 +1438,7 @@ def _compile_words(words, dtype):
         fresh.smem = smem_bytes(stage_amps * amp, len(tables), alias, split, 1 << (K - nreg))
         fresh.ctas = ctas_per_sm(1 << (K - nreg))
         fresh.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
+        fresh.tdesc_out = None if tplan.get("tdesc_out") is None else np.array(tplan["tdesc_out"], dtype=np.int64)
         fresh.n_tiles = 1 << (int(words[4]) - K)
         fresh.threads = (1 << (K - nreg)) + 128
         fresh.tpc = pass_schedule(int(words[4]) - K, 1 << (K - nreg), expect, (1 << K) * amp > 65536)[0]
@@ -1473,16 +1500,17 @@ def run(words, dtype, src_ptr, dst_ptr, n_qubits, stream_ptr, compiled=None, coe
         compiled, coeffs = compile_words(words, dtype)
     params, tables = coeffs
     lib = nat.lib()
+    tdo = None if compiled.tdesc_out is None else compiled.tdesc_out.ctypes.data
     if dev_tables is not None and len(tables):
         nat.check(
-            lib.qsb_jit_run_pass_dev(compiled.func, src_ptr, dst_ptr, compiled.tdesc.ctypes.data, compiled.n_tiles,
+            lib.qsb_jit_run_pass_dev(compiled.func, src_ptr, dst_ptr, compiled.tdesc.ctypes.data, tdo, compiled.n_tiles,
                                      dev_tables.data_ptr(), len(tables), params.ctypes.data, params.nbytes,
                                      compiled.threads, compiled.smem, compiled.grid(), stream_ptr),
             "jit_run_pass_dev",
         )
         return
     nat.check(
-        lib.qsb_jit_run_pass(compiled.func, src_ptr, dst_ptr, compiled.tdesc.ctypes.data, compiled.n_tiles,
+        lib.qsb_jit_run_pass(compiled.func, src_ptr, dst_ptr, compiled.tdesc.ctypes.data, tdo, compiled.n_tiles,
                              tables.ctypes.data if len(tables) else None, len(tables),
                              params.ctypes.data, params.nbytes, compiled.threads, compiled.smem, compiled.grid(),
                              stream_ptr),
