@@ -48,6 +48,8 @@ class TileGeometry:
     # layout changes in two rounds through a half-tile buffer (consecutive layouts share a
     # register bit), so the stage is free as soon as the tile is in registers
     split: bool = False
+    # two consumer groups per CTA taking alternate tiles, gate math handed back and forth
+    pingpong: bool = False
 
     @property
     def nreg(self) -> int:
@@ -91,6 +93,14 @@ GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 5), nat.QSB_C64: TileGeo
 # chosen per pass (SPLIT_MAX_CODE, and only when it needs no extra layout change).
 # QSB_SPLIT_2Q=0 disables it, =1 forces it for every 2-qubit-gate pass.
 GEOMETRY_JIT_2Q_SPLIT = {nat.QSB_C128: TileGeometry(12, 3, 4, 5, split=True)}
+# QSB_PINGPONG=1: one CTA with two 128-thread consumer groups taking alternate tiles and handing
+# the gate-math turn back and forth (named barriers, FA3-style).  Correct, but measured slower
+# (round 2, n = 30: variational c128 74.9 -> 86.5 ms, Trotter step 50.3 -> 56.1 ms): one
+# group's four warps cannot keep the FP64 pipes busy alone, so serialising the math loses more
+# than the overlap with the other group's loads gains.
+if os.environ.get("QSB_PINGPONG", "0") == "1":
+    GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 5, pingpong=True), nat.QSB_C64: GEOMETRY_JIT_2Q[nat.QSB_C64]}
+    GEOMETRY_JIT_2Q_SPLIT = {}
 if os.environ.get("QSB_2Q_GEOMETRY", "") == "c64s3":
     # experiment: complex64 512 x 16 with three 64 KB stages + the split 32 KB transpose buffer
     GEOMETRY_JIT_2Q = {nat.QSB_C128: GEOMETRY_JIT_2Q[nat.QSB_C128], nat.QSB_C64: TileGeometry(13, 4, 5, 4, split=True)}
@@ -107,6 +117,11 @@ SPLIT_MAX_CODE = float(os.environ.get("QSB_SPLIT_MAX_CODE", "100"))
 # and 19.0 / 20.0 ms in the default one, while variational's 16 real 4x4 gates (~4,100) and the
 # grid's 10-gate passes (~5,100) are faster in it
 MAX_2Q_CODE = int(os.environ.get("QSB_MAX_2Q_CODE", "6500"))
+# QSB_BALANCE_DIAGONALS=1: spread the trailing diagonals of diagonal-heavy plans evenly over the
+# passes.  Measured slower (round 2, QFT-30 c128: passes 212/149/92/27 gates 20.8 ms -> 155/156/
+# 142/27 gates 23.2 ms): a deferred cross-tile phase costs more in the later passes (more
+# pivots, tile-external partners) than in the first, so it is off.
+BALANCE_DIAGONALS = os.environ.get("QSB_BALANCE_DIAGONALS", "0") == "1"
 _GEO_ENV = os.environ.get("QSB_JIT_GEOMETRY", "")
 if _GEO_ENV == "wide":
     GEOMETRY_JIT = GEOMETRY_JIT_WIDE
@@ -493,9 +508,64 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
         plan.steps = [GateStep(g) for g in gates]
         return plan
     gates = merge_single_qubit(sandwich_diagonals(merge_1q_runs(gates)))
+    plan = _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, None)
+    if BALANCE_DIAGONALS:
+        # diagonal-heavy plans (the QFT: 204 / 141 / 84 / 21 diagonal gates in its four passes
+        # at n = 30) keep their early passes compute-bound; the trailing diagonals of a pass
+        # (nothing later in it acts non-diagonally on their qubits) may run in any later pass
+        # that precedes their next non-diagonal use, so spread them evenly
+        passes = [st for st in plan.steps if isinstance(st, PassStep)]
+        counts = [sum(1 for g in st.gates if g.kind == "diag") for st in passes]
+        if len(passes) >= 3 and max(counts) > 1.5 * (sum(counts) / len(counts)) + 8:
+            # passes that cannot pass diagonals on (their qubits are used right after) end up
+            # above the budget: try a few budgets and keep the plan with the lowest maximum
+            mean = sum(counts) / len(counts)
+            best, best_max = plan, max(counts)
+            for f in (1.0, 1.1, 1.2, 1.35, 1.5):
+                budget = int(mean * f + 0.5)
+                if budget >= best_max:
+                    break
+                alt = _plan_passes(Plan(n_qubits, dtype), gates, n_qubits, dtype, geo, allow_ext_perm, budget)
+                if alt.n_passes != plan.n_passes or alt.state_sweeps() > plan.state_sweeps() + 1e-9:
+                    continue
+                m = max(sum(1 for g in st.gates if g.kind == "diag") for st in alt.steps if isinstance(st, PassStep))
+                if m < best_max:
+                    best, best_max = alt, m
+            plan = best
+    return plan
+
+
+def _defer_trailing_diagonals(absorbed, deferred, budget):
+    """Move the trailing diagonal gates of a pass beyond `budget` diagonals (latest first) to the
+    head of the deferred list.  A trailing diagonal has no later gate of the pass acting
+    non-diagonally on its qubits, and it commutes with every deferred gate that preceded it (the
+    absorption rule), so running it at the start of the next passes is exact reordering."""
+    diags = [i for i, g in enumerate(absorbed) if g.kind == "diag"]
+    excess = len(diags) - budget
+    if excess <= 0:
+        return absorbed, deferred
+    later_nondiag = 0
+    move = set()
+    for i in range(len(absorbed) - 1, -1, -1):
+        g = absorbed[i]
+        if g.kind == "diag":
+            if not (g.smask & later_nondiag) and len(move) < excess:
+                move.add(i)
+        else:
+            later_nondiag |= g.tmask
+    if not move:
+        return absorbed, deferred
+    kept = [g for i, g in enumerate(absorbed) if i not in move]
+    moved = [g for i, g in enumerate(absorbed) if i in move]
+    return kept, moved + list(deferred)
+
+
+def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget):
     remaining = gates
     while remaining:
         absorbed, deferred, T = _select_pass_best(remaining, n_qubits, geo, allow_ext_perm)
+        if diag_budget is not None:
+            absorbed, deferred = _defer_trailing_diagonals(absorbed, deferred, diag_budget)
         if not absorbed:  # cannot happen with K >= L + 2, but never loop forever
             absorbed, deferred = [remaining[0]], remaining[1:]
             plan.steps.append(GateStep(absorbed[0]))
@@ -917,7 +987,7 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
     header[4] = n
     header[5] = dtype
     header[6] = 1 << (n - K)
-    header[7] = (1 if ext_perm else 0) | (2 if expect else 0) | (4 if geo.split else 0)
+    header[7] = (1 if ext_perm else 0) | (2 if expect else 0) | (4 if geo.split else 0) | (8 if geo.pingpong else 0)
     contig = 0
     while contig < K and tile_pos[contig] == contig:
         contig += 1

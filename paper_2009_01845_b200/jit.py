@@ -125,7 +125,16 @@ __device__ __forceinline__ void tma5_store(const TMap* m, const int* c, const vo
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" :: "n"(CONSUMERS) : "memory"); }
+__device__ __forceinline__ void csync_all() { asm volatile("bar.sync 1, %0;" :: "n"(CONSUMERS) : "memory"); }
+// ping-pong: barrier 1 + g syncs consumer group g; barrier 3 + g is group g's gate-math turn
+__device__ __forceinline__ void csync_grp(int g) { asm volatile("bar.sync %0, %1;" :: "r"(1 + g), "n"(CONSUMERS) : "memory"); }
+__device__ __forceinline__ void pp_sync(int g) { asm volatile("bar.sync %0, %1;" :: "r"(3 + g), "n"(2 * CONSUMERS) : "memory"); }
+__device__ __forceinline__ void pp_arrive(int g) { asm volatile("bar.arrive %0, %1;" :: "r"(3 + g), "n"(2 * CONSUMERS) : "memory"); }
+#if PINGPONG
+#define csync() csync_grp(grp)
+#else
+#define csync() csync_all()
+#endif
 __device__ __forceinline__ void fence_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ C cm(C a, C b) { C r; r.x = a.x * b.x - a.y * b.y; r.y = a.x * b.y + a.y * b.x; return r; }
 __device__ __forceinline__ double2 dm(double2 a, double2 b) {
@@ -314,12 +323,19 @@ class _Gen:
         # split: one 64 KB stage released as soon as the tile is in registers and a separate
         # 32 KB transpose buffer (two-round layout changes), two CTAs per SM
         self.split = bool(w[7] & 4) and not self.halves
+        # ping-pong: two consumer groups of CONSUMERS threads in one CTA, each with its own
+        # stage (doubling as its transpose buffer), taking alternate tiles; a pair of named
+        # barriers hands the gate-math turn back and forth, so one group's FP work always
+        # overlaps the other's tile load / stores instead of both computing (and both waiting)
+        # at the same time as two independent CTAs drift into doing
+        self.pingpong = bool(w[7] & 8) and not self.halves and not self.split
+        self.groups = 2 if self.pingpong else 1
         # two CTAs per SM with 64 KB tiles: one stage per CTA, reused as the transpose buffer
-        self.alias = (not self.halves and not self.split and ctas_per_sm(self.consumers) == 2
+        self.alias = (not self.halves and not self.split and (ctas_per_sm(self.consumers) == 2 or self.pingpong)
                       and (1 << K) * amp_bytes == 65536)
         # split geometry: one stage per CTA at two CTAs per SM; three stages (3 x 64 KB + the
         # 32 KB transpose buffer) at one CTA per SM
-        self.stages = 1 if self.alias else (split_stages(self.consumers) if self.split else STAGES)
+        self.stages = 2 if self.pingpong else (1 if self.alias else (split_stages(self.consumers) if self.split else STAGES))
         self.sched = pass_schedule(self.n - K, self.consumers, self.expect, self.halves)
         self.HB = K - 1 if (self.halves or self.split) else K  # bits of a transpose-buffer index
         self.SB = K - 1 if self.halves else K  # bits of a stage index
@@ -1043,7 +1059,8 @@ class _Gen:
                 f"    }}"))
         pr = "double" if (self.dtype == nat.QSB_C128 or self.expect) else "float"
         defs = (f"#define QSB_F32X2 {1 if self.dtype == nat.QSB_C64 else 0}\n#define R {real}\n#define PR {pr}\n#define C {real}2\n#define KB {K}\n#define HBB {self.HB}\n#define SBB {self.SB}\n#define GB {self.G}\n#define STAGES {self.stages}\n#define ALIAS {1 if self.alias else 0}\n#define TBUF {"sm.stage[s]" if self.alias else "sm.tbuf"}\n"
-                f"#define CONSUMERS {self.consumers}\n#define MAXPIV {MAX_PIV}\n#define NPIV {self.npiv}\n"
+                f"#define CONSUMERS {self.consumers}\n#define CONSUMERS_ALL {self.consumers * self.groups}\n"
+                f"#define PINGPONG {1 if self.pingpong else 0}\n#define MAXPIV {MAX_PIV}\n#define NPIV {self.npiv}\n"
                 f"#define NCOEF {max(1, len(self.coeffs))}\n#define NTAB {len(self.tables)}\n"
                 f"#define TPC {self.sched[0]}\n#define DYN {self.sched[1]}\n")
         issue = f"""      {{ // producer warp: fetch tile c into stage s (tile number tno)
@@ -1080,7 +1097,11 @@ class _Gen:
 {produce}
       }}""")
             issue = "\n".join(halves_code)
-        body = body.replace("@@REFILL@@", "")
+        if self.pingpong:
+            body = body.replace("@@REFILL@@", "    pp_sync(grp);  // my turn for the gate math")
+            body += "\n    pp_arrive(1 - grp);  // the other group's turn"
+        else:
+            body = body.replace("@@REFILL@@", "")
         if self.alias:
             body = body.replace("@@RELEASE@@", "")
             body += "\n    csync();  // every thread is done with the stage (loads and transposes)\n" \
@@ -1092,7 +1113,7 @@ class _Gen:
         else:
             head = """    mbar_wait(&sm.full[s], ph);
     const u64 base = sm.base[s][0];
-#if DYN
+#if DYN || PINGPONG
     if (base == ~0ull) break;
 #endif
     const u64 obase = sm.base[s][1];
@@ -1101,7 +1122,7 @@ class _Gen:
 // {self.consumers} consumer threads + one producer warpgroup (one active warp: TMA tile fetches and
 // per-tile pivot factors, STAGES tiles ahead); setmaxnreg moves the producers' registers to the
 // consumers, which hold the tile in registers.
-extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_sm(self.consumers)})
+extern "C" __global__ void __launch_bounds__({self.consumers * self.groups + 128}, {1 if self.pingpong else ctas_per_sm(self.consumers)})
 {name}(const C* __restrict__ src, C* __restrict__ dst, const __grid_constant__ TMap tmap,
        const __grid_constant__ TMap tmap_o, const double* __restrict__ cf, unsigned long long* __restrict__ sched,
        const __grid_constant__ CP cp) {{
@@ -1109,7 +1130,7 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
   Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
   double* scf = reinterpret_cast<double*>(smem_raw + sizeof(Smem));  // pivot tables
   const int tid = threadIdx.x;
-  for (int i = tid; i < NTAB; i += {self.consumers + 128}) scf[i] = cf[i];
+  for (int i = tid; i < NTAB; i += {self.consumers * self.groups + 128}) scf[i] = cf[i];
   if (tid == 0) {{
     for (int s = 0; s < STAGES; ++s) {{ mbar_init(&sm.full[s], 1); mbar_init(&sm.empty[s], CONSUMERS); }}
     sm.zero = 0;
@@ -1127,10 +1148,10 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
 #else
   const u64 c_begin = blockIdx.x, c_end = n_tiles, c_step = gridDim.x;
 #endif
-  if (tid >= CONSUMERS) {{
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 {REG_SPLIT[self.consumers][1]};" ::: "memory");
-    if (tid >= CONSUMERS + 32) return;
-    const int lane = tid - CONSUMERS;
+  if (tid >= CONSUMERS_ALL) {{
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 {REG_SPLIT[self.consumers * self.groups][1]};" ::: "memory");
+    if (tid >= CONSUMERS_ALL + 32) return;
+    const int lane = tid - CONSUMERS_ALL;
     int it = 0;
 #if DYN
     // persistent: DYN consecutive tiles per grab from the launch's counter; a sentinel base
@@ -1149,6 +1170,13 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
       }}
       if (c >= n_tiles) {{
         if (lane == 0) {{ sm.base[s][0] = ~0ull; mbar_arrive(&sm.full[s]); }}
+#if PINGPONG
+        {{  // the other consumer group's next stage gets a sentinel too
+          const int s2 = (it + 1) % STAGES;
+          if (it + 1 >= STAGES) mbar_wait(&sm.empty[s2], (((it + 1) / STAGES) & 1) ^ 1);
+          if (lane == 0) {{ sm.base[s2][0] = ~0ull; mbar_arrive(&sm.full[s2]); }}
+        }}
+#endif
         break;
       }}
       const int tno = it;
@@ -1171,16 +1199,31 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
       const int tno = it;
 {issue}
     }}
+#if PINGPONG
+    for (int e = 0; e < 2; ++e, ++it) {{  // both consumer groups stop on a sentinel
+      const int s = it % STAGES;
+      if (it >= STAGES) mbar_wait(&sm.empty[s], ((it / STAGES) & 1) ^ 1);
+      if (lane == 0) {{ sm.base[s][0] = ~0ull; mbar_arrive(&sm.full[s]); }}
+    }}
+#endif
 #endif
     return;
   }}
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 {REG_SPLIT[self.consumers][0]};" ::: "memory");
-  int it = 0;
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 {REG_SPLIT[self.consumers * self.groups][0]};" ::: "memory");
   double ea = 0.0;  // expectation passes: this thread's sum of Re <x|M|x>
+#if PINGPONG
+  {{
+  const int grp = threadIdx.x / CONSUMERS;  // consumer group: takes producer iterations it = grp (mod 2)
+  const int tid = threadIdx.x % CONSUMERS;
+  if (grp == 1) pp_arrive(0);  // group 0 has the first gate-math turn
+  for (int it = grp;; it += 2) {{
+#else
+  int it = 0;
 #if DYN
   for (;; ++it) {{
 #else
   for (u64 c = c_begin; c < c_end; c += c_step, ++it) {{
+#endif
 #endif
     const int s = it % STAGES;
     const u32 ph = (it / STAGES) & 1;
@@ -1188,6 +1231,9 @@ extern "C" __global__ void __launch_bounds__({self.consumers + 128}, {ctas_per_s
 {body}
 {store}
   }}
+#if PINGPONG
+  }}
+#endif
 {self._expect_epilogue() if self.expect else "  (void)ea;"}
 {"  if (tid < 32) bulk_wait0();  // the last bulk stores are done before the CTA retires" if self.uses_tma_store else ""}
 }}
@@ -1314,11 +1360,13 @@ def split_stages(consumers: int) -> int:
 
 
 def smem_bytes(stage_bytes: int, n_coeffs=MAX_COEFFS, alias: bool = False, split: bool = False,
-               consumers: int = 128) -> int:
+               consumers: int = 128, pingpong: bool = False) -> int:
     # STAGES stages + one transpose buffer of stage_bytes (a whole tile, or half of a 128 KB
     # tile); `alias`: a single stage that doubles as the transpose buffer (two CTAs per SM);
     # `split`: split_stages() stages + a half-size transpose buffer
-    if split:
+    if pingpong:
+        buf_bytes = 2 * stage_bytes  # one stage per consumer group, each its group's transpose buffer
+    elif split:
         buf_bytes = split_stages(consumers) * stage_bytes + stage_bytes // 2
     else:
         buf_bytes = (1 if alias else STAGES + 1) * stage_bytes
@@ -1434,13 +1482,14 @@ def _compile_words(words, dtype):
         fresh.func = fn
         fresh.name = name
         split = bool(int(words[7]) & 4) and (1 << K) * amp <= 65536
-        alias = (1 << K) * amp == 65536 and ctas_per_sm(1 << (K - nreg)) == 2 and not split
-        fresh.smem = smem_bytes(stage_amps * amp, len(tables), alias, split, 1 << (K - nreg))
-        fresh.ctas = ctas_per_sm(1 << (K - nreg))
+        pingpong = bool(int(words[7]) & 8) and (1 << K) * amp == 65536 and not split
+        alias = (1 << K) * amp == 65536 and ctas_per_sm(1 << (K - nreg)) == 2 and not split and not pingpong
+        fresh.smem = smem_bytes(stage_amps * amp, len(tables), alias, split, 1 << (K - nreg), pingpong)
+        fresh.ctas = 1 if pingpong else ctas_per_sm(1 << (K - nreg))
         fresh.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
         fresh.tdesc_out = None if tplan.get("tdesc_out") is None else np.array(tplan["tdesc_out"], dtype=np.int64)
         fresh.n_tiles = 1 << (int(words[4]) - K)
-        fresh.threads = (1 << (K - nreg)) + 128
+        fresh.threads = (1 << (K - nreg)) * (2 if pingpong else 1) + 128
         fresh.tpc = pass_schedule(int(words[4]) - K, 1 << (K - nreg), expect, (1 << K) * amp > 65536)[0]
         with _lock:
             hit = _cache.setdefault(src, fresh)
