@@ -752,6 +752,68 @@ __global__ void __launch_bounds__(kThreads) k_permute(const cplx<R>* __restrict_
   }
 }
 
+// Tiled form (both sides coalesced): a tile is the 2^T elements spanned by the bit set S = the
+// low source bits {0..t-1} plus the source bits that land on destination bits {0..t-1}; the
+// remaining bits pick the tile.  A CTA reads its tile with the low source bits varying
+// fastest into shared memory, then writes it with the low destination bits varying fastest.
+constexpr int kPermTileBits = 10;
+struct TilePerm {
+  int n, T, E;                    // index bits, tile bits, tile-selecting bits
+  uint8_t src_s[kPermTileBits];   // source position of tile bit j (ascending)
+  uint8_t dst_s[kPermTileBits];   // destination position of the j-th destination tile bit (ascending)
+  uint8_t pi[kPermTileBits];      // destination tile bit j carries source tile bit pi[j]
+  uint8_t src_e[64], dst_e[64];   // tile-selecting bit k: source / destination position
+};
+
+template <typename R>
+__global__ void __launch_bounds__(kThreads) k_permute_tiled(const cplx<R>* __restrict__ src,
+                                                            cplx<R>* __restrict__ dst, uint64_t n_tiles,
+                                                            const TilePerm p) {
+  constexpr int kPer = (1 << kPermTileBits) / kThreads;  // elements per thread and tile (4)
+  __shared__ cplx<R> tile[1 << kPermTileBits];
+  const int size = 1 << p.T;
+  // this thread's tile elements: source offsets (read phase) and destination offsets plus the
+  // tile slot they come from (write phase), computed once for every tile
+  uint64_t soff[kPer], doff[kPer];
+  int sslot[kPer], dslot[kPer];
+#pragma unroll
+  for (int k = 0; k < kPer; ++k) {
+    const int e = threadIdx.x + k * kThreads;
+    uint64_t si = 0, di = 0;
+    int eo = 0;
+    for (int j = 0; j < p.T; ++j) {
+      si |= (uint64_t)((e >> j) & 1) << p.src_s[j];
+      const int b = (e >> j) & 1;  // as destination tile index f = e
+      eo |= b << p.pi[j];
+      di |= (uint64_t)b << p.dst_s[j];
+    }
+    soff[k] = si;
+    sslot[k] = e ^ ((e >> 5) & 7);  // xor: spread the 8 x 16 B rows of a later column read
+    doff[k] = di;
+    dslot[k] = eo ^ ((eo >> 5) & 7);
+  }
+  for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    uint64_t sb = 0, db = 0;
+    for (int k = 0; k < p.E; ++k) {
+      const uint64_t b = (t >> k) & 1ull;
+      sb |= b << p.src_e[k];
+      db |= b << p.dst_e[k];
+    }
+    cplx<R> v[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (threadIdx.x + k * kThreads < size) v[k] = src[sb | soff[k]];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (threadIdx.x + k * kThreads < size) tile[sslot[k]] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPer; ++k)
+      if (threadIdx.x + k * kThreads < size) dst[db | doff[k]] = tile[dslot[k]];
+    __syncthreads();
+  }
+}
+
 // swap a's half with bit=1 and b's half with bit=0 (sharding.py:100-111 _exchange_halves)
 template <typename R>
 __global__ void __launch_bounds__(kThreads) k_exchange_halves(cplx<R>* __restrict__ a, cplx<R>* __restrict__ b,
@@ -1278,6 +1340,7 @@ int qsb_permute_qubits(const void* src, void* dst, int n_bits, int dtype, const 
   BitPerm p;
   p.n = n_bits;
   uint64_t seen = 0;
+  int src_of[64];
   for (int b = 0; b < n_bits; ++b) {
     if (dst_bit[b] < 0 || dst_bit[b] >= n_bits || ((seen >> dst_bit[b]) & 1ull)) {
       set_error("qsb_permute_qubits: not a permutation");
@@ -1285,9 +1348,55 @@ int qsb_permute_qubits(const void* src, void* dst, int n_bits, int dtype, const 
     }
     seen |= 1ull << dst_bit[b];
     p.dst_bit[b] = (uint8_t)dst_bit[b];
+    src_of[dst_bit[b]] = b;
   }
   const uint64_t total = 1ull << n_bits;
   cudaStream_t st = as_stream(stream);
+  // tile set: low source bits 0..t-1 and the sources of destination bits 0..t-1, as many as fit
+  uint64_t S = 0;
+  int t = 0;
+  while (t < n_bits) {
+    const uint64_t add = (1ull << t) | (1ull << src_of[t]);
+    if (__builtin_popcountll(S | add) > kPermTileBits) break;
+    S |= add;
+    ++t;
+  }
+  if (t >= 4 && n_bits > kPermTileBits) {
+    TilePerm tp;
+    tp.n = n_bits;
+    tp.T = 0;
+    tp.E = 0;
+    int idx_of[64];
+    for (int b = 0; b < n_bits; ++b) {
+      if ((S >> b) & 1ull) {
+        idx_of[b] = tp.T;
+        tp.src_s[tp.T++] = (uint8_t)b;
+      } else {
+        tp.src_e[tp.E] = (uint8_t)b;
+        tp.dst_e[tp.E++] = (uint8_t)dst_bit[b];
+      }
+    }
+    // destination tile bits in ascending destination order, each with its source tile bit
+    int j = 0;
+    for (int d = 0; d < n_bits; ++d) {
+      const int b = src_of[d];
+      if ((S >> b) & 1ull) {
+        tp.dst_s[j] = (uint8_t)d;
+        tp.pi[j] = (uint8_t)idx_of[b];
+        ++j;
+      }
+    }
+    const uint64_t n_tiles = total >> tp.T;
+    const int grid = (int)(n_tiles < 148ull * 16ull ? n_tiles : 148ull * 16ull);
+    if (dtype == QSB_C128)
+      k_permute_tiled<double><<<grid, kThreads, 0, st>>>(static_cast<const double2*>(src), static_cast<double2*>(dst),
+                                                         n_tiles, tp);
+    else
+      k_permute_tiled<float><<<grid, kThreads, 0, st>>>(static_cast<const float2*>(src), static_cast<float2*>(dst),
+                                                        n_tiles, tp);
+    QSB_CHECK_LAUNCH("qsb_permute_qubits");
+    return QSB_OK;
+  }
   if (dtype == QSB_C128)
     k_permute<double><<<stream_grid(total), kThreads, 0, st>>>(static_cast<const double2*>(src),
                                                                static_cast<double2*>(dst), total, p);

@@ -113,3 +113,23 @@ def test_stream_ordered_exchange_threads(cuda, world):
         for r in range(world):
             for got, want in zip(res[r], wants):
                 assert max_abs(got, want) <= 1e-12, (planner, r)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_permute_qubits_tiled_and_plain(cuda, prec):
+    """qsb_permute_qubits (tiled through shared memory when the permutation leaves room for a
+    2^10-element tile, plain otherwise) against numpy's bit permutation, random and reversal
+    permutations, n = 6 .. 21."""
+    torch = cuda
+    from paper_2009_01845_b200 import Precision
+    from paper_2009_01845_b200.sharding import CudaBackend
+
+    p = Precision(prec)
+    dev, cpu = CudaBackend(p), CpuBackend(p)
+    rng = np.random.default_rng(17)
+    for n in (6, 11, 14, 21):
+        a = _rand(n, n, torch, p.complex_dtype)
+        for perm in (list(range(n))[::-1], [int(x) for x in rng.permutation(n)], list(range(n))):
+            got = dev.permute(a.cuda(), n, perm).cpu()
+            want = cpu.permute(a, n, perm)
+            assert torch.equal(got, want), (n, perm)
