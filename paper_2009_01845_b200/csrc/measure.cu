@@ -786,7 +786,10 @@ __global__ void __launch_bounds__(kMT, 3) k_materialize2(const double* __restric
                                                       const double* __restrict__ block_start,
                                                       const double* __restrict__ serial_val,
                                                       const double* __restrict__ total,
-                                                      double* __restrict__ c_out, int normalize) {
+                                                      double* __restrict__ c_out, int normalize,
+                                                      const unsigned char* __restrict__ only) {
+  // only != nullptr: materialise just the blocks flagged there (the blocks that hold a draw)
+  if (only && !only[blockIdx.x]) return;
   __shared__ double sh[kMT * kRow];
   __shared__ double wsum[kMT / 32];
   __shared__ unsigned int usum[kMT / 32];
@@ -1069,10 +1072,36 @@ extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cu
   return qsb_cumsum(probs, n, cum, scratch, scratch_bytes, 1, stream);
 }
 
+struct CumsumCtx {
+  uint64_t n, nb;
+  double margin;
+  double* bpre;
+  unsigned int* base;
+  double* bstart;
+  double* sval;
+  double* d_total;
+};
+
+static int cumsum_phases(const double* probs, uint64_t n, void* scratch, size_t scratch_bytes, cudaStream_t st,
+                         CumsumCtx* ctx);
+
 extern "C" int qsb_cumsum(const double* probs, uint64_t n, double* cum, void* scratch, size_t scratch_bytes,
                           int normalize, void* stream) {
   cudaStream_t st = as_stream(stream);
   if (n == 0) return QSB_OK;
+  CumsumCtx c;
+  if (int rc = cumsum_phases(probs, n, scratch, scratch_bytes, st, &c)) return rc;
+  // E: every c_i, divided by c_{n-1}
+  k_materialize2<<<(int)c.nb, kMT, 0, st>>>(probs, n, c.margin, c.bpre, c.base, c.bstart, c.sval, c.d_total, cum,
+                                            normalize, nullptr);
+  QSB_CHECK_LAUNCH("qsb_cumsum");
+  return QSB_OK;
+}
+
+// phases A-D of the exact cumsum: block classification, serial points, block head pieces and
+// the stitch -- everything but the per-element values (k_materialize2)
+static int cumsum_phases(const double* probs, uint64_t n, void* scratch, size_t scratch_bytes, cudaStream_t st,
+                         CumsumCtx* ctx) {
   if (scratch_bytes < qsb_cumsum_scratch_bytes(n)) {
     set_error("qsb_cumsum: scratch too small");
     return QSB_ERR_ARG;
@@ -1149,9 +1178,15 @@ extern "C" int qsb_cumsum(const double* probs, uint64_t n, double* cum, void* sc
   k_stitch_serial<<<1, 1, 0, st>>>(probs, ns, sidx, after, runp, sval, rstart);
   k_block_starts<<<(int)((nb + kMT - 1) / kMT), kMT, 0, st>>>(runp, nb, rstart, bstart);
   k_total2<<<1, 1, 0, st>>>(head, cnt, nb, bstart, after, sval, ns, d_total);
-  // E: every c_i, divided by c_{n-1}
-  k_materialize2<<<(int)nb, kMT, 0, st>>>(probs, n, margin, bpre, base, bstart, sval, d_total, cum, normalize);
   QSB_CHECK_LAUNCH("qsb_cumsum");
+  ctx->n = n;
+  ctx->nb = nb;
+  ctx->margin = margin;
+  ctx->bpre = bpre;
+  ctx->base = base;
+  ctx->bstart = bstart;
+  ctx->sval = sval;
+  ctx->d_total = d_total;
   return QSB_OK;
 }
 
@@ -1161,6 +1196,120 @@ extern "C" int qsb_cumsum_serial(const double* probs, uint64_t n, double* cum, v
   cudaStream_t st = as_stream(stream);
   k_cumsum_serial<<<1, 1, 0, st>>>(probs, n, cum);
   QSB_CHECK_LAUNCH("qsb_cumsum_serial");
+  return QSB_OK;
+}
+
+// ---- sampling without materialising the whole CDF ---------------------------------------------
+// A draw u lands in block b when the normalised value of block b-1's last element is <= u and
+// block b's is > u; those values are the (exact) block starts of the stitch divided by the total,
+// the same division k_materialize2 applies, so only the blocks that hold a draw are materialised
+// and searched.  Samples are bit-identical to qsb_cumsum_normalized + qsb_sample.
+namespace qsb {
+__global__ void k_block_ends(const double* __restrict__ bstart, uint64_t nb, const double* __restrict__ total,
+                             double* __restrict__ ends) {
+  const uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  ends[b] = (b + 1 < nb) ? __ddiv_rn(bstart[b + 1], *total) : 2.0;  // every u < 1
+}
+
+__global__ void __launch_bounds__(kMT) k_draw_blocks(const double* __restrict__ ends, uint64_t nb, uint64_t s_hi,
+                                                     uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, uint64_t n_shots,
+                                                     unsigned int* __restrict__ shot_block,
+                                                     unsigned char* __restrict__ flags) {
+  const uint64_t t = (uint64_t)blockIdx.x * kMT + threadIdx.x;
+  const uint64_t first = t * kShotsPerThread;
+  if (first >= n_shots) return;
+  const u128 inc = ((u128)i_hi << 64) | i_lo;
+  u128 s = pcg_advance(((u128)s_hi << 64) | s_lo, inc, first);
+  const u128 mult = pcg_mult();
+  for (int k = 0; k < kShotsPerThread; ++k) {
+    const uint64_t shot = first + k;
+    if (shot >= n_shots) break;
+    s = s * mult + inc;
+    const double u = (double)(pcg_out(s) >> 11) * (1.0 / 9007199254740992.0);
+    uint64_t lo = 0, hi = nb;  // first block whose last value exceeds u
+    while (lo < hi) {
+      const uint64_t mid = lo + ((hi - lo) >> 1);
+      if (ends[mid] <= u)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    shot_block[shot] = (unsigned int)lo;
+    flags[lo] = 1;
+  }
+}
+
+__global__ void __launch_bounds__(kMT) k_draw_final(const double* __restrict__ cum, uint64_t n, uint64_t s_hi,
+                                                    uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, uint64_t n_shots,
+                                                    const unsigned int* __restrict__ shot_block,
+                                                    long long* __restrict__ out, uint64_t clip_max) {
+  const uint64_t t = (uint64_t)blockIdx.x * kMT + threadIdx.x;
+  const uint64_t first = t * kShotsPerThread;
+  if (first >= n_shots) return;
+  const u128 inc = ((u128)i_hi << 64) | i_lo;
+  u128 s = pcg_advance(((u128)s_hi << 64) | s_lo, inc, first);
+  const u128 mult = pcg_mult();
+  for (int k = 0; k < kShotsPerThread; ++k) {
+    const uint64_t shot = first + k;
+    if (shot >= n_shots) break;
+    s = s * mult + inc;
+    const double u = (double)(pcg_out(s) >> 11) * (1.0 / 9007199254740992.0);
+    const uint64_t b0 = (uint64_t)shot_block[shot] * kScanBlock;
+    uint64_t lo = b0, hi = b0 + kScanBlock < n ? b0 + kScanBlock : n;
+    while (lo < hi) {  // every element before the block is <= u, the block's last one is not
+      const uint64_t mid = lo + ((hi - lo) >> 1);
+      if (cum[mid] <= u)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    out[shot] = (long long)(lo > clip_max ? clip_max : lo);
+  }
+}
+}  // namespace qsb
+
+extern "C" size_t qsb_sample_exact_scratch_bytes(uint64_t n, uint64_t n_shots) {
+  const uint64_t nb = (n + kScanBlock - 1) / kScanBlock;
+  size_t b = (qsb_cumsum_scratch_bytes(n) + 255) & ~(size_t)255;
+  b += ((nb * sizeof(double) + 255) & ~(size_t)255);        // block ends
+  b += ((nb + 255) & ~(size_t)255);                          // block flags
+  b += ((n_shots * sizeof(unsigned int) + 255) & ~(size_t)255);  // block of every shot
+  return b;
+}
+
+extern "C" int qsb_sample_exact(const double* probs, uint64_t n, double* cum, void* scratch, size_t scratch_bytes,
+                                uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, uint64_t n_shots,
+                                int64_t* samples, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  if (n == 0 || n_shots == 0) {
+    set_error("qsb_sample_exact: empty distribution or no shots");
+    return QSB_ERR_ARG;
+  }
+  if (n_shots > 0xffffffffull || scratch_bytes < qsb_sample_exact_scratch_bytes(n, n_shots)) {
+    set_error("qsb_sample_exact: scratch too small or too many shots");
+    return QSB_ERR_ARG;
+  }
+  const size_t cs = (qsb_cumsum_scratch_bytes(n) + 255) & ~(size_t)255;
+  CumsumCtx c;
+  if (int rc = cumsum_phases(probs, n, scratch, cs, st, &c)) return rc;
+  char* w = static_cast<char*>(scratch) + cs;
+  double* ends = reinterpret_cast<double*>(w);
+  w += (c.nb * sizeof(double) + 255) & ~(size_t)255;
+  unsigned char* flags = reinterpret_cast<unsigned char*>(w);
+  w += (c.nb + 255) & ~(size_t)255;
+  unsigned int* shot_block = reinterpret_cast<unsigned int*>(w);
+  cudaError_t e = cudaMemsetAsync(flags, 0, c.nb, st);
+  if (e != cudaSuccess) return cuda_status(e, "block flags");
+  k_block_ends<<<(int)((c.nb + kMT - 1) / kMT), kMT, 0, st>>>(c.bstart, c.nb, c.d_total, ends);
+  const uint64_t threads = (n_shots + kShotsPerThread - 1) / kShotsPerThread;
+  const int grid = (int)((threads + kMT - 1) / kMT);
+  k_draw_blocks<<<grid, kMT, 0, st>>>(ends, c.nb, s_hi, s_lo, i_hi, i_lo, n_shots, shot_block, flags);
+  k_materialize2<<<(int)c.nb, kMT, 0, st>>>(probs, n, c.margin, c.bpre, c.base, c.bstart, c.sval, c.d_total, cum, 1,
+                                            flags);
+  k_draw_final<<<grid, kMT, 0, st>>>(cum, n, s_hi, s_lo, i_hi, i_lo, n_shots, shot_block,
+                                      reinterpret_cast<long long*>(samples), n - 1);
+  QSB_CHECK_LAUNCH("qsb_sample_exact");
   return QSB_OK;
 }
 

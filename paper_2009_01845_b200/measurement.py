@@ -13,6 +13,8 @@ on the device with jump-ahead).
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -163,10 +165,38 @@ def sample(state, qubits, n_shots: int, seed: int, registers: dict | None = None
             raise ShapeError(f"register {name!r} references unmeasured qubits {sorted(missing)}")
         regs[name] = tuple(reg)
     probs = device_marginal(state, qubits)
-    cum = device_cdf(probs)
-    del probs
-    samples = device_sample(cum, n_shots, seed).cpu().numpy()
+    if SPARSE_CDF and probs.numel() >= SPARSE_CDF_MIN and n_shots <= probs.numel() // 4096:
+        samples = device_sample_exact(probs, n_shots, seed).cpu().numpy()
+    else:
+        cum = device_cdf(probs)
+        del probs
+        samples = device_sample(cum, n_shots, seed).cpu().numpy()
     return MeasurementResult(int(n_shots), qubits, samples, int(seed), regs)
+
+
+# sample() materialises only the CDF blocks that hold a draw (qsb_sample_exact) for marginals of
+# at least SPARSE_CDF_MIN outcomes and at most one shot per 4096-outcome block (measured at 2^30
+# outcomes: 1e5 shots 31.6 -> 24.2 ms; 1e6 shots touch nearly every block and are faster with
+# the full CDF, 32.2 vs 35.0 ms); QSB_SPARSE_CDF=0: always the full CDF
+SPARSE_CDF = os.environ.get("QSB_SPARSE_CDF", "1") != "0"
+SPARSE_CDF_MIN = 1 << 16
+
+
+def device_sample_exact(probs, n_shots: int, seed: int):
+    """The draws of sample() straight from the probabilities: the exact scan's block
+    boundaries route every draw to its 4096-element block, and only those blocks are
+    materialised and searched (bit-identical to device_cdf + device_sample)."""
+    torch = nat.torch_mod()
+    lib = nat.lib()
+    n = probs.numel()
+    cum = torch.empty_like(probs)
+    nbytes = int(lib.qsb_sample_exact_scratch_bytes(n, int(n_shots)))
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device=probs.device)
+    out = torch.empty(int(n_shots), dtype=torch.int64, device=probs.device)
+    sh, sl, ih, il = pcg64_seed_state(seed)
+    nat.check(lib.qsb_sample_exact(probs.data_ptr(), n, cum.data_ptr(), scratch.data_ptr(), nbytes, sh, sl, ih, il,
+                                   int(n_shots), out.data_ptr(), nat.stream_ptr()), "sample_exact")
+    return out
 
 
 def collapse(state, qubits, outcome: int) -> float:
