@@ -50,6 +50,7 @@ class TileGeometry:
     split: bool = False
     # two consumer groups per CTA taking alternate tiles, gate math handed back and forth
     pingpong: bool = False
+    two_ctas: bool = False  # two CTAs per SM even with 256 consumers (one stage each, aliased)
 
     @property
     def nreg(self) -> int:
@@ -101,6 +102,10 @@ GEOMETRY_JIT_2Q_SPLIT = {nat.QSB_C128: TileGeometry(12, 3, 4, 5, split=True)}
 if os.environ.get("QSB_PINGPONG", "0") == "1":
     GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 5, pingpong=True), nat.QSB_C64: GEOMETRY_JIT_2Q[nat.QSB_C64]}
     GEOMETRY_JIT_2Q_SPLIT = {}
+if os.environ.get("QSB_2Q_GEOMETRY", "") == "x2s16":
+    # experiment: c128 256 consumers x 16 amplitudes with two CTAs per SM (one aliased stage each)
+    GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 4, two_ctas=True), nat.QSB_C64: GEOMETRY_JIT_2Q[nat.QSB_C64]}
+    GEOMETRY_JIT_2Q_SPLIT = {}
 if os.environ.get("QSB_2Q_GEOMETRY", "") == "c64s3":
     # experiment: complex64 512 x 16 with three 64 KB stages + the split 32 KB transpose buffer
     GEOMETRY_JIT_2Q = {nat.QSB_C128: GEOMETRY_JIT_2Q[nat.QSB_C128], nat.QSB_C64: TileGeometry(13, 4, 5, 4, split=True)}
@@ -110,6 +115,11 @@ if os.environ.get("QSB_2Q_GEOMETRY", "") == "s3":
     GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 4, split=True), nat.QSB_C64: GEOMETRY_JIT_2Q[nat.QSB_C64]}
     GEOMETRY_JIT_2Q_SPLIT = {}
 SPLIT_2Q = os.environ.get("QSB_SPLIT_2Q", "auto")
+# ... and the 256 x 16 two-CTA variant for the heavier ones (measured round 2, n = 30: variational
+# passes of 21 / 32 / 25 gates 10.0 / 13.1 / 9.8 -> 9.6 / 12.2 / 9.6 ms, Trotter 9-gate passes
+# 10.0 -> 9.4 ms; lighter passes are faster split).  QSB_X2_2Q=0 disables it.
+GEOMETRY_JIT_2Q_X2 = {nat.QSB_C128: TileGeometry(12, 3, 4, 4, two_ctas=True)}
+X2_2Q = os.environ.get("QSB_X2_2Q", "1") != "0"
 SPLIT_MAX_CODE = float(os.environ.get("QSB_SPLIT_MAX_CODE", "100"))
 # ... unless the pass's straight-line gate code per thread (FP operations per amplitude x 32
 # amplitudes) would outgrow the instruction cache: measured on grid-30, the two passes of 16
@@ -584,11 +594,21 @@ def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget)
             words, info = compile_pass(absorbed, T, n_qubits, dtype, pgeo, minimal=MINIMAL_LAYOUT_CHANGES)
             if pgeo is GEOMETRY_JIT_2Q.get(dtype) and dtype in GEOMETRY_JIT_2Q_SPLIT and SPLIT_2Q != "0":
                 code = sum(matrix_cost(g.matrix) for g in absorbed if g.kind in ("g1", "g2"))
+                chosen = False
                 if SPLIT_2Q == "1" or code <= SPLIT_MAX_CODE:
                     w2, i2 = compile_pass(absorbed, T, n_qubits, dtype, GEOMETRY_JIT_2Q_SPLIT[dtype],
                                           minimal=MINIMAL_LAYOUT_CHANGES)
                     if SPLIT_2Q == "1" or i2["transposes"] <= info["transposes"]:
                         words, info = w2, i2
+                        chosen = True
+                if not chosen and dtype in GEOMETRY_JIT_2Q_X2 and X2_2Q:
+                    # heavier passes: 256 consumers x 16 amplitudes at two CTAs per SM (half the
+                    # straight-line code per thread, twice the warps) unless it needs more layout
+                    # changes
+                    w3, i3 = compile_pass(absorbed, T, n_qubits, dtype, GEOMETRY_JIT_2Q_X2[dtype],
+                                          minimal=MINIMAL_LAYOUT_CHANGES)
+                    if i3["transposes"] <= info["transposes"]:
+                        words, info = w3, i3
             plan.steps.append(PassStep(words, absorbed, tuple(sorted(T)), info["ext_perm"],
                                        info["transposes"], info["pivots"]))
         remaining = deferred
@@ -987,7 +1007,8 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
     header[4] = n
     header[5] = dtype
     header[6] = 1 << (n - K)
-    header[7] = (1 if ext_perm else 0) | (2 if expect else 0) | (4 if geo.split else 0) | (8 if geo.pingpong else 0)
+    header[7] = ((1 if ext_perm else 0) | (2 if expect else 0) | (4 if geo.split else 0) | (8 if geo.pingpong else 0)
+                 | (16 if geo.two_ctas else 0))
     contig = 0
     while contig < K and tile_pos[contig] == contig:
         contig += 1

@@ -36,7 +36,7 @@ def _reg_split(consumers: int, ctas: int = 1):
     threads = consumers + 128
     per = min(255, 65536 // (threads * ctas)) // 8 * 8
     pool = per * threads
-    prod = 40 if consumers <= 256 else 24
+    prod = 40 if (consumers <= 256 and not (consumers == 256 and ctas == 2)) else 24
     cons = min(248, (pool - 128 * prod) // consumers // 8 * 8)
     return cons, prod
 
@@ -330,8 +330,11 @@ class _Gen:
         # at the same time as two independent CTAs drift into doing
         self.pingpong = bool(w[7] & 8) and not self.halves and not self.split
         self.groups = 2 if self.pingpong else 1
+        # resident CTAs per SM: 2 for 128-consumer kernels, or (header flag 16) for 256 consumers
+        self.ctas = 1 if self.pingpong else (2 if (ctas_per_sm(self.consumers) == 2 or (w[7] & 16)) else 1)
+        self.regs = _reg_split(self.consumers * self.groups, self.ctas)
         # two CTAs per SM with 64 KB tiles: one stage per CTA, reused as the transpose buffer
-        self.alias = (not self.halves and not self.split and (ctas_per_sm(self.consumers) == 2 or self.pingpong)
+        self.alias = (not self.halves and not self.split and (self.ctas == 2 or self.pingpong)
                       and (1 << K) * amp_bytes == 65536)
         # split geometry: one stage per CTA at two CTAs per SM; three stages (3 x 64 KB + the
         # 32 KB transpose buffer) at one CTA per SM
@@ -1122,7 +1125,7 @@ class _Gen:
 // {self.consumers} consumer threads + one producer warpgroup (one active warp: TMA tile fetches and
 // per-tile pivot factors, STAGES tiles ahead); setmaxnreg moves the producers' registers to the
 // consumers, which hold the tile in registers.
-extern "C" __global__ void __launch_bounds__({self.consumers * self.groups + 128}, {1 if self.pingpong else ctas_per_sm(self.consumers)})
+extern "C" __global__ void __launch_bounds__({self.consumers * self.groups + 128}, {self.ctas})
 {name}(const C* __restrict__ src, C* __restrict__ dst, const __grid_constant__ TMap tmap,
        const __grid_constant__ TMap tmap_o, const double* __restrict__ cf, unsigned long long* __restrict__ sched,
        const __grid_constant__ CP cp) {{
@@ -1149,7 +1152,7 @@ extern "C" __global__ void __launch_bounds__({self.consumers * self.groups + 128
   const u64 c_begin = blockIdx.x, c_end = n_tiles, c_step = gridDim.x;
 #endif
   if (tid >= CONSUMERS_ALL) {{
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 {REG_SPLIT[self.consumers * self.groups][1]};" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 {self.regs[1]};" ::: "memory");
     if (tid >= CONSUMERS_ALL + 32) return;
     const int lane = tid - CONSUMERS_ALL;
     int it = 0;
@@ -1209,7 +1212,7 @@ extern "C" __global__ void __launch_bounds__({self.consumers * self.groups + 128
 #endif
     return;
   }}
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 {REG_SPLIT[self.consumers * self.groups][0]};" ::: "memory");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 {self.regs[0]};" ::: "memory");
   double ea = 0.0;  // expectation passes: this thread's sum of Re <x|M|x>
 #if PINGPONG
   {{
@@ -1258,7 +1261,9 @@ class _Compiled:
 
     def grid(self) -> int:
         """CTAs of one launch (one-shot tiles-per-CTA grid, or SMs x resident CTAs)."""
-        return pass_grid(self.n_tiles, self.threads - 128, self.tpc, _sm_count())
+        if self.tpc:
+            return pass_grid(self.n_tiles, self.threads - 128, self.tpc, _sm_count())
+        return min(self.n_tiles, _sm_count() * self.ctas)
 
 
 _SMS = None
@@ -1483,9 +1488,10 @@ def _compile_words(words, dtype):
         fresh.name = name
         split = bool(int(words[7]) & 4) and (1 << K) * amp <= 65536
         pingpong = bool(int(words[7]) & 8) and (1 << K) * amp == 65536 and not split
-        alias = (1 << K) * amp == 65536 and ctas_per_sm(1 << (K - nreg)) == 2 and not split and not pingpong
+        two = (ctas_per_sm(1 << (K - nreg)) == 2 or bool(int(words[7]) & 16)) and not pingpong
+        alias = (1 << K) * amp == 65536 and two and not split
         fresh.smem = smem_bytes(stage_amps * amp, len(tables), alias, split, 1 << (K - nreg), pingpong)
-        fresh.ctas = 1 if pingpong else ctas_per_sm(1 << (K - nreg))
+        fresh.ctas = 2 if two else 1
         fresh.tdesc = np.array(tplan["tdesc"], dtype=np.int64)
         fresh.tdesc_out = None if tplan.get("tdesc_out") is None else np.array(tplan["tdesc_out"], dtype=np.int64)
         fresh.n_tiles = 1 << (int(words[4]) - K)
