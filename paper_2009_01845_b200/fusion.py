@@ -120,6 +120,9 @@ SPLIT_2Q = os.environ.get("QSB_SPLIT_2Q", "auto")
 # 10.0 -> 9.4 ms; lighter passes are faster split).  QSB_X2_2Q=0 disables it.
 GEOMETRY_JIT_2Q_X2 = {nat.QSB_C128: TileGeometry(12, 3, 4, 4, two_ctas=True)}
 X2_2Q = os.environ.get("QSB_X2_2Q", "1") != "0"
+# passes whose gate code is too big for 32 amplitudes per thread (the grid's 16-gate passes) also
+# run 256 x 16 at two CTAs per SM instead of one CTA with two stages (20.4 / 23.4 -> 19.5 / 22.4 ms)
+X2_BIG = os.environ.get("QSB_X2_BIG", "1") != "0"
 SPLIT_MAX_CODE = float(os.environ.get("QSB_SPLIT_MAX_CODE", "100"))
 # ... unless the pass's straight-line gate code per thread (FP operations per amplitude x 32
 # amplitudes) would outgrow the instruction cache: measured on grid-30, the two passes of 16
@@ -591,6 +594,8 @@ def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget)
                 code = sum(matrix_cost(g.matrix) for g in absorbed if g.kind in ("g1", "g2"))
                 if code * GEOMETRY_JIT_2Q[dtype].A <= MAX_2Q_CODE:
                     pgeo = GEOMETRY_JIT_2Q[dtype]
+                elif X2_BIG and dtype in GEOMETRY_JIT_2Q_X2:
+                    pgeo = GEOMETRY_JIT_2Q_X2[dtype]
             words, info = compile_pass(absorbed, T, n_qubits, dtype, pgeo, minimal=MINIMAL_LAYOUT_CHANGES)
             if pgeo is GEOMETRY_JIT_2Q.get(dtype) and dtype in GEOMETRY_JIT_2Q_SPLIT and SPLIT_2Q != "0":
                 code = sum(matrix_cost(g.matrix) for g in absorbed if g.kind in ("g1", "g2"))
