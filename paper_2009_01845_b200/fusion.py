@@ -106,6 +106,11 @@ if os.environ.get("QSB_2Q_GEOMETRY", "") == "x2s16":
     # experiment: c128 256 consumers x 16 amplitudes with two CTAs per SM (one aliased stage each)
     GEOMETRY_JIT_2Q = {nat.QSB_C128: TileGeometry(12, 3, 4, 4, two_ctas=True), nat.QSB_C64: GEOMETRY_JIT_2Q[nat.QSB_C64]}
     GEOMETRY_JIT_2Q_SPLIT = {}
+if os.environ.get("QSB_C64_2Q", "") == "x2_256":
+    # experiment: complex64 256 consumers x 32 amplitudes at two CTAs per SM
+    GEOMETRY_JIT_2Q = {nat.QSB_C128: GEOMETRY_JIT_2Q[nat.QSB_C128], nat.QSB_C64: TileGeometry(13, 4, 5, 5, two_ctas=True)}
+if os.environ.get("QSB_C64_2Q", "") == "x2_512":
+    GEOMETRY_JIT_2Q = {nat.QSB_C128: GEOMETRY_JIT_2Q[nat.QSB_C128], nat.QSB_C64: TileGeometry(13, 4, 5, 4, two_ctas=True)}
 if os.environ.get("QSB_2Q_GEOMETRY", "") == "c64s3":
     # experiment: complex64 512 x 16 with three 64 KB stages + the split 32 KB transpose buffer
     GEOMETRY_JIT_2Q = {nat.QSB_C128: GEOMETRY_JIT_2Q[nat.QSB_C128], nat.QSB_C64: TileGeometry(13, 4, 5, 4, split=True)}
@@ -118,11 +123,13 @@ SPLIT_2Q = os.environ.get("QSB_SPLIT_2Q", "auto")
 # ... and the 256 x 16 two-CTA variant for the heavier ones (measured round 2, n = 30: variational
 # passes of 21 / 32 / 25 gates 10.0 / 13.1 / 9.8 -> 9.6 / 12.2 / 9.6 ms, Trotter 9-gate passes
 # 10.0 -> 9.4 ms; lighter passes are faster split).  QSB_X2_2Q=0 disables it.
-GEOMETRY_JIT_2Q_X2 = {nat.QSB_C128: TileGeometry(12, 3, 4, 4, two_ctas=True)}
+GEOMETRY_JIT_2Q_X2 = {nat.QSB_C128: TileGeometry(12, 3, 4, 4, two_ctas=True),
+                      nat.QSB_C64: TileGeometry(13, 4, 5, 5, two_ctas=True)}
 X2_2Q = os.environ.get("QSB_X2_2Q", "1") != "0"
 # passes whose gate code is too big for 32 amplitudes per thread (the grid's 16-gate passes) also
 # run 256 x 16 at two CTAs per SM instead of one CTA with two stages (20.4 / 23.4 -> 19.5 / 22.4 ms)
 X2_BIG = os.environ.get("QSB_X2_BIG", "1") != "0"
+X2_C64 = os.environ.get("QSB_X2_C64", "0") == "1"
 SPLIT_MAX_CODE = float(os.environ.get("QSB_SPLIT_MAX_CODE", "100"))
 # ... unless the pass's straight-line gate code per thread (FP operations per amplitude x 32
 # amplitudes) would outgrow the instruction cache: measured on grid-30, the two passes of 16
@@ -597,6 +604,19 @@ def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget)
                 elif X2_BIG and dtype in GEOMETRY_JIT_2Q_X2:
                     pgeo = GEOMETRY_JIT_2Q_X2[dtype]
             words, info = compile_pass(absorbed, T, n_qubits, dtype, pgeo, minimal=MINIMAL_LAYOUT_CHANGES)
+            if (pgeo is GEOMETRY_JIT_2Q.get(dtype) and dtype == nat.QSB_C64 and X2_C64
+                    and dtype in GEOMETRY_JIT_2Q_X2):
+                # complex64: 256 x 32 at two CTAs per SM when it saves a layout change, or for the
+                # heaviest passes (measured variational-30 c64: 32-gate pass 6.22 -> 5.72 ms,
+                # a 16-gate pass with one layout change fewer 3.55 -> 3.24 ms).  Off by default:
+                # at n = 18-24 whole variational layers fit one pass and ptxas needs minutes for
+                # the 32-amplitude straight-line kernel (QSB_X2_C64=1 enables it)
+                code = sum(matrix_cost(g.matrix) for g in absorbed if g.kind in ("g1", "g2"))
+                w3, i3 = compile_pass(absorbed, T, n_qubits, dtype, GEOMETRY_JIT_2Q_X2[dtype],
+                                      minimal=MINIMAL_LAYOUT_CHANGES)
+                if i3["transposes"] < info["transposes"] or (i3["transposes"] == info["transposes"]
+                                                             and code > SPLIT_MAX_CODE):
+                    words, info = w3, i3
             if pgeo is GEOMETRY_JIT_2Q.get(dtype) and dtype in GEOMETRY_JIT_2Q_SPLIT and SPLIT_2Q != "0":
                 code = sum(matrix_cost(g.matrix) for g in absorbed if g.kind in ("g1", "g2"))
                 chosen = False
