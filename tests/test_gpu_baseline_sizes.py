@@ -141,3 +141,26 @@ def test_c64_large_fixtures_through_planned_passes(cuda, mode):
             assert max_abs(got, want) <= TOL32
         plan = c.plan(f32)
         assert any(isinstance(s, PassStep) for s in plan.steps)
+
+
+def test_evolve_step_windows_equal_single_steps(cuda, monkeypatch):
+    """evolve() without callbacks runs consecutive Trotter steps as one circuit
+    (evolution.STEP_WINDOW); planned fused passes then cross the step boundaries.  The result
+    equals stepping one circuit at a time (the reference's loop, evolution.py:339-347) to 1e-12,
+    for a time-independent H and for the time-dependent adiabatic schedule (with its remainder
+    step)."""
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200 import engine, evolution
+
+    monkeypatch.setattr(engine, "FIRST_RUN_BATCH", False)
+    n = 22
+    h = q.combine(q.build_x(n), 0.4, q.build_tfim(n, 1.0), 0.6)
+    cfg = q.EvolutionConfig(q.Solver.TROTTER, 0.05, 0.33)  # 6 full steps + a remainder
+    psi0 = q.uniform_state(n)
+    outs = {}
+    for w in (1, 4):
+        monkeypatch.setattr(evolution, "STEP_WINDOW", w)
+        outs[w] = (q.evolve(h, psi0, cfg).tensor,
+                   q.adiabatic_evolve(q.build_x(n), q.build_tfim(n, 1.0), q.Schedule.linear(), cfg).tensor)
+    assert _device_max_abs_diff(outs[1][0], outs[4][0]) <= TOL64
+    assert _device_max_abs_diff(outs[1][1], outs[4][1]) <= TOL64
