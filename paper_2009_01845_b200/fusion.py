@@ -368,6 +368,30 @@ def merge_single_qubit(gates: list) -> list:
     return [g for g, a in zip(out, alive) if a]
 
 
+def merge_2q_runs(gates: list) -> list:
+    """Consecutive uncontrolled two-qubit gates on the same bit pair (no other gate on either
+    bit in between) become their product when that is cheaper: the trailing half step of one
+    Trotter step and the leading half step of the next (with the single-qubit layer between
+    them folded in by merge_single_qubit) are one 4x4 when evolve() plans steps together."""
+    out = list(gates)
+    alive = [True] * len(out)
+    for i, g in enumerate(out):
+        if not alive[i] or g.kind != "g2" or g.controls:
+            continue
+        j = next((k for k in range(i + 1, len(out)) if alive[k] and out[k].smask & g.smask), None)
+        if j is None:
+            continue
+        h = out[j]
+        if h.kind != "g2" or h.controls or set(h.targets) != set(g.targets):
+            continue
+        gm = g.matrix if h.targets == g.targets else g.matrix[np.ix_([0, 2, 1, 3], [0, 2, 1, 3])]
+        m = h.matrix @ gm
+        if matrix_cost(m) < matrix_cost(h.matrix) + matrix_cost(g.matrix) - 1e-9:
+            out[j] = NGate("g2", h.targets, (), m, h.tmask, h.smask, h.index)
+            alive[i] = False
+    return [g for g, a in zip(out, alive) if a]
+
+
 def diag_terms(g: NGate):
     """(mask, value, phase) rows of a diagonal gate: exactly the rows the reference multiplies
     (diag entry != 1.0), restricted to the control subspace."""
@@ -527,7 +551,7 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
     if not fuse or n_qubits < geo.K + 1:
         plan.steps = [GateStep(g) for g in gates]
         return plan
-    gates = merge_single_qubit(sandwich_diagonals(merge_1q_runs(gates)))
+    gates = merge_2q_runs(merge_single_qubit(sandwich_diagonals(merge_1q_runs(gates))))
     plan = _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, None)
     if BALANCE_DIAGONALS:
         # diagonal-heavy plans (the QFT: 204 / 141 / 84 / 21 diagonal gates in its four passes

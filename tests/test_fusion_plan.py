@@ -230,3 +230,34 @@ def test_reordered_layouts_keep_the_state_and_cut_transposes():
     t_on = sum(s.n_transposes for s in on.steps if isinstance(s, PassStep))
     t_off = sum(s.n_transposes for s in off.steps if isinstance(s, PassStep))
     assert t_on <= 0.6 * t_off, (t_on, t_off)
+
+
+@pytest.mark.parametrize("dtype,tol", [(C128, 1e-12), (C64, 1e-5)])
+def test_consecutive_trotter_steps_merge_two_qubit_runs(dtype, tol):
+    """Several Trotter steps planned as one circuit: the trailing half step of each step and the
+    leading half step of the next (X layer in between) become one 4x4 per bit pair; also for a
+    pair given in the opposite target order."""
+    from paper_2009_01845_b200.fusion import GEOMETRY_JIT, merge_2q_runs, normalize
+
+    n = 16
+    rng = np.random.default_rng(6)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    npd = np.complex128 if dtype == C128 else np.complex64
+    step = ov.trotter_step(ov.combine(ov.x_terms(n), 0.3, ov.tfim_terms(n, 1.0), 0.7), 0.1)
+    gates = step * 3
+    specs = spec_tuples_to_specs(gates)
+    plan = plan_circuit(specs, n, dtype, geometry=GEOMETRY_JIT[dtype])
+    assert max_abs(emulate_plan(plan, psi, npd), ov.run(gates, n, psi)) <= tol
+    single = plan_circuit(spec_tuples_to_specs(step), n, dtype, geometry=GEOMETRY_JIT[dtype])
+    g2 = lambda p: sum(g.kind == "g2" for s in p.steps if isinstance(s, PassStep) for g in s.gates)  # noqa: E731
+    assert g2(plan) < 3 * g2(single)
+    # reversed target order on the second gate of a pair
+    a, _ = np.linalg.qr(rng.standard_normal((4, 4)) + 1j * rng.standard_normal((4, 4)))
+    b, _ = np.linalg.qr(rng.standard_normal((4, 4)) + 1j * rng.standard_normal((4, 4)))
+    pair = [("Unitary", (3, 7), (), (), a), ("Unitary", (7, 3), (), (), b)]
+    ng = [normalize(s, n, i) for i, s in enumerate(spec_tuples_to_specs(pair))]
+    merged = merge_2q_runs(ng)
+    assert len(merged) == 1
+    plan = plan_circuit(spec_tuples_to_specs(pair), n, dtype, geometry=GEOMETRY_JIT[dtype])
+    assert max_abs(emulate_plan(plan, psi, npd), ov.run(pair, n, psi)) <= tol
