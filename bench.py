@@ -519,6 +519,23 @@ def _big_state_workloads(q, engine, n, peak):
                                  "effective_gbs": gbs, "hbm_frac": gbs / peak,
                                  "swaps": "relabelled (qubit map kept on the state)",
                                  "canonical_read_s": b.elapsed_time(c) / 1e3}}
+        # BASELINE config 4's circuit (grid 3x11, 20 cycles) and config 5's TFIM Trotter steps
+        # (four per circuit, as evolve() plans them) at the same 137 GB per GPU, in place
+        step = q.trotter_step_circuit(q.combine(q.build_x(n), 0.5, q.build_tfim(n, 1.0), 0.5), 0.05)
+        for name, circ, per in ((f"trotter_tfim_4steps_{n}_c128", q.Circuit(n).add([g for _ in range(4) for g in step.queue]), 4),
+                                (f"random_grid_3x{n // 3}_20cycles_{n}_c128", q.random_grid_circuit(3, n // 3, 20, 42), 1)):
+            plan = engine.plan_for_state(st, circ.queue)
+            engine.run_plan(st, plan, holder)
+            torch.cuda.synchronize()
+            a.record()
+            engine.run_plan(st, plan, holder)
+            b.record()
+            torch.cuda.synchronize()
+            sec = a.elapsed_time(b) / 1e3
+            sweeps = plan.state_sweeps()
+            gbs = sweeps * 2 * need / sec / 1e9
+            res[name] = {"seconds": sec / per, "per": "Trotter step" if per > 1 else "circuit", "passes": plan.n_passes,
+                         "state_sweeps": sweeps / per, "effective_gbs": gbs, "hbm_frac": gbs / peak}
         del st, holder, cache
         torch.cuda.empty_cache()
         return res
