@@ -182,6 +182,9 @@ class NGate:
     tmask: int
     smask: int
     index: int = -1  # position in the source queue
+    # matrix (g1 / g2) or diagonal (diag) as a function of the source gates' matrices: how a
+    # plan template (PlanTemplate) recomputes it for a circuit of the same structure
+    build: object = None
 
     def touched_fraction(self) -> float:
         """Share of the state a stand-alone single-gate kernel reads+writes."""
@@ -198,17 +201,36 @@ _SWAP = np.array([[1, 0, 0, 0], [0, 0, 1, 0], [0, 1, 0, 0], [0, 0, 0, 1]], dtype
 _XMAT = np.array([[0, 1], [1, 0]], dtype=np.complex128)
 
 
-def normalize(spec, n_qubits: int, index: int = -1) -> NGate | None:
-    """GateSpec (or duck-typed reference GateSpec) -> NGate; None for exact identities."""
-    m = gate_matrix(spec)
+# Real or imaginary parts below this magnitude are rounding noise of the host matrix algebra
+# (1e-17 .. 5e-16 where the step exponentials and gate products are exactly zero) and are
+# planned as exact zeros: the kernels skip them, and a time-dependent circuit's structure does
+# not flip between steps with the noise.  The dropped terms change an amplitude by at most
+# ~1e-15 of its norm per gate, far inside the 1e-12 parity bound.  QSB_SNAP_TINY=0 disables.
+SNAP_TINY = float(os.environ.get("QSB_SNAP_TINY", "1e-15"))
+
+
+def _snap(m):
+    m = np.array(m, dtype=np.complex128)
+    if SNAP_TINY > 0:
+        v = m.reshape(-1).view(np.float64)
+        v[np.abs(v) < SNAP_TINY] = 0.0
+    return m
+
+
+def normalize(spec, n_qubits: int, index: int = -1, m=None) -> NGate | None:
+    """GateSpec (or duck-typed reference GateSpec) -> NGate; None for exact identities.  `m`:
+    the spec's gate matrix (as plan_circuit snaps it) when the caller has it already."""
+    if m is None:
+        m = _snap(gate_matrix(spec))
     tb = tuple(n_qubits - 1 - int(q) for q in spec.targets)
     cb = tuple(n_qubits - 1 - int(q) for q in spec.controls)
     support = _bits(tb + cb)
+    i = index
     if classify_kernel(m) is KernelClass.DIAGONAL:
         d = np.ascontiguousarray(np.diagonal(m))
         if np.all(d == 1.0):
             return None  # the reference's diagonal body finds no rows and returns
-        return NGate("diag", tb, cb, d, 0, support, index)
+        return NGate("diag", tb, cb, d, 0, support, index, lambda M: np.ascontiguousarray(np.diagonal(M[i])))
     if len(tb) == 2:
         if not cb and np.array_equal(m, _SWAP):
             return NGate("swap", tb, (), None, support, support, index)
@@ -222,10 +244,51 @@ def normalize(spec, n_qubits: int, index: int = -1) -> NGate | None:
             if classify_kernel(u) is KernelClass.DIAGONAL:
                 d = np.ones(4, dtype=np.complex128)
                 d[2:] = np.diagonal(u)
-                return NGate("diag", tb, cb, d, 0, support, index)
-            return NGate("g1", (tb[1],), cb + (tb[0],), u, 1 << tb[1], support, index)
-        return NGate("g2", tb, cb, np.ascontiguousarray(m), _bits(tb), support, index)
-    return NGate("g1", tb, cb, np.ascontiguousarray(m), _bits(tb), support, index)
+                return NGate("diag", tb, cb, d, 0, support, index,
+                             lambda M: np.concatenate((np.ones(2, dtype=np.complex128), np.diagonal(M[i])[2:])))
+            return NGate("g1", (tb[1],), cb + (tb[0],), u, 1 << tb[1], support, index,
+                         lambda M: np.ascontiguousarray(M[i][2:, 2:]))
+        return NGate("g2", tb, cb, np.ascontiguousarray(m), _bits(tb), support, index, lambda M: M[i])
+    return NGate("g1", tb, cb, np.ascontiguousarray(m), _bits(tb), support, index, lambda M: M[i])
+
+
+def _product_build(*parts):
+    """build of a product of gate factors: each part is a build, a constant matrix, or
+    ('kron', part, part) / ('embed', part, pos) / ('diag', part)."""
+
+    def ev(p, M):
+        if isinstance(p, tuple):
+            if p[0] == "kron":
+                return _kron2(ev(p[1], M), ev(p[2], M))
+            if p[0] == "embed":
+                return _embed_1q(ev(p[1], M), p[2])
+            if p[0] == "diag":
+                return np.diag(ev(p[1], M))
+            if p[0] == "perm":
+                return ev(p[1], M)[np.ix_(_PERM2, _PERM2)]
+        if callable(p):
+            return p(M)
+        return p
+
+    def known(p):
+        if isinstance(p, tuple):
+            return all(known(x) for x in p[1:] if not isinstance(x, int))
+        return p is not None
+
+    if not all(known(p) for p in parts):
+        return None
+    flat = list(parts)
+
+    def build(M):
+        out = ev(flat[0], M)
+        for p in flat[1:]:
+            out = out @ ev(p, M)
+        return _snap(out)
+
+    return build
+
+
+_PERM2 = [0, 2, 1, 3]
 
 
 def _entry_cost(z) -> float:
@@ -285,9 +348,9 @@ def merge_1q_runs(gates: list) -> list:
             continue
         h = out[j]
         if h.kind == "g1" and not h.controls and h.targets == g.targets:
-            m = h.matrix @ g.matrix
+            m = _snap(h.matrix @ g.matrix)
             if matrix_cost(m) < matrix_cost(h.matrix) + matrix_cost(g.matrix) - 1e-9:
-                out[j] = NGate("g1", h.targets, (), m, h.tmask, h.smask, h.index)
+                out[j] = NGate("g1", h.targets, (), m, h.tmask, h.smask, h.index, _product_build(h.build, g.build))
                 alive[i] = False
     return [g for g, a in zip(out, alive) if a]
 
@@ -313,26 +376,30 @@ def sandwich_diagonals(gates: list) -> list:
         if not alive[i] or d.kind not in ("diag", "g2") or d.controls or len(d.targets) != 2:
             continue
         parts, pre, post = [], [_EYE2, _EYE2], [_EYE2, _EYE2]
+        pre_b, post_b = [_EYE2, _EYE2], [_EYE2, _EYE2]
         for pos, t in enumerate(d.targets):
             bit = 1 << t
-            for step, slot in ((-1, pre), (1, post)):
+            for step, slot, slot_b in ((-1, pre, pre_b), (1, post, post_b)):
                 k = neighbour(i, bit, step)
                 if k is not None and out[k].kind == "g1" and not out[k].controls and out[k].targets == (t,):
                     parts.append(k)
                     slot[pos] = out[k].matrix
+                    slot_b[pos] = out[k].build
         if not parts:
             continue
         core = np.diag(d.matrix) if d.kind == "diag" else d.matrix
         core_cost = 0.0 if d.kind == "diag" else matrix_cost(d.matrix)
-        merged = _kron2(post[0], post[1]) @ core @ _kron2(pre[0], pre[1])
+        merged = _snap(_kron2(post[0], post[1]) @ core @ _kron2(pre[0], pre[1]))
         if matrix_cost(merged) < core_cost + sum(matrix_cost(out[k].matrix) for k in parts) - 1e-9:
-            out[i] = NGate("g2", d.targets, (), merged, _bits(d.targets), d.smask, d.index)
+            core_b = ("diag", d.build) if d.kind == "diag" else d.build
+            out[i] = NGate("g2", d.targets, (), merged, _bits(d.targets), d.smask, d.index,
+                           _product_build(("kron", post_b[0], post_b[1]), core_b, ("kron", pre_b[0], pre_b[1])))
             for k in parts:
                 alive[k] = False
     return [g for g, a in zip(out, alive) if a]
 
 
-def merge_single_qubit(gates: list) -> list:
+def merge_single_qubit(gates: list, slack: float = 0.0) -> list:
     """Fold uncontrolled single-qubit gates into the neighbouring two-qubit gate on the same bit
     when the product is cheaper to apply than the two separately (entry-structure cost model:
     e.g. the X rotation of a Trotter ZZ + hX term's first qubit keeps its 8-entry block structure;
@@ -352,18 +419,20 @@ def merge_single_qubit(gates: list) -> list:
         j = next((k for k in range(i + 1, len(out)) if alive[k] and out[k].smask & bit), None)
         if j is not None and out[j].kind == "g2" and not out[j].controls and q in out[j].targets:
             h = out[j]
-            merged = h.matrix @ _embed_1q(u, h.targets.index(q))
-            if matrix_cost(merged) < matrix_cost(h.matrix) + matrix_cost(u) - 1e-9:
-                out[j] = NGate("g2", h.targets, (), merged, h.tmask, h.smask, h.index)
+            merged = _snap(h.matrix @ _embed_1q(u, h.targets.index(q)))
+            if matrix_cost(merged) < matrix_cost(h.matrix) + matrix_cost(u) + slack - 1e-9:
+                out[j] = NGate("g2", h.targets, (), merged, h.tmask, h.smask, h.index,
+                               _product_build(h.build, ("embed", g.build, h.targets.index(q))))
                 alive[i] = False
                 continue
         # backward: the previous gate touching q
         k = next((k for k in range(i - 1, -1, -1) if alive[k] and out[k].smask & bit), None)
         if k is not None and out[k].kind == "g2" and not out[k].controls and q in out[k].targets:
             h = out[k]
-            merged = _embed_1q(u, h.targets.index(q)) @ h.matrix
-            if matrix_cost(merged) < matrix_cost(h.matrix) + matrix_cost(u) - 1e-9:
-                out[k] = NGate("g2", h.targets, (), merged, h.tmask, h.smask, h.index)
+            merged = _snap(_embed_1q(u, h.targets.index(q)) @ h.matrix)
+            if matrix_cost(merged) < matrix_cost(h.matrix) + matrix_cost(u) + slack - 1e-9:
+                out[k] = NGate("g2", h.targets, (), merged, h.tmask, h.smask, h.index,
+                               _product_build(("embed", g.build, h.targets.index(q)), h.build))
                 alive[i] = False
     return [g for g, a in zip(out, alive) if a]
 
@@ -384,10 +453,12 @@ def merge_2q_runs(gates: list) -> list:
         h = out[j]
         if h.kind != "g2" or h.controls or set(h.targets) != set(g.targets):
             continue
-        gm = g.matrix if h.targets == g.targets else g.matrix[np.ix_([0, 2, 1, 3], [0, 2, 1, 3])]
-        m = h.matrix @ gm
+        same = h.targets == g.targets
+        gm = g.matrix if same else g.matrix[np.ix_(_PERM2, _PERM2)]
+        m = _snap(h.matrix @ gm)
         if matrix_cost(m) < matrix_cost(h.matrix) + matrix_cost(g.matrix) - 1e-9:
-            out[j] = NGate("g2", h.targets, (), m, h.tmask, h.smask, h.index)
+            out[j] = NGate("g2", h.targets, (), m, h.tmask, h.smask, h.index,
+                           _product_build(h.build, g.build if same else ("perm", g.build)))
             alive[i] = False
     return [g for g, a in zip(out, alive) if a]
 
@@ -425,6 +496,7 @@ class PassStep:
     no_jit: bool = False
     interp_words: object = None  # re-encoding for the interpreter's geometry (fallback only)
     dev_tables: object = None  # device copy of the pivot tables (engine.own_device_tables; graph capture)
+    tpl: object = None  # (geometry, dense-gate matrix word positions, has diagonals): PlanTemplate
 
     @property
     def n_gates(self) -> int:
@@ -537,22 +609,169 @@ def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool, lazy_1q: bool = F
     return absorbed, deferred, T
 
 
+# ------------------------------------------------------------------------------------------
+# plan templates: a circuit with the structure of one planned before -- the same qubits and
+# controls gate by gate, and the same class (0, +-1, +-1/sqrt 2, rounding noise, other) for the
+# real and imaginary part of every matrix entry: the values the planner's and the kernel
+# generator's structure decisions test -- e.g. each step of a time-dependent Trotter evolution,
+# reuses that plan: merged matrices are recomputed from the recorded products (NGate.build), and
+# each pass's program gets the new matrix words patched in (passes with diagonal terms, whose
+# words hold derived phase products, are re-encoded with the recorded tile and geometry).  An
+# exact 0 where the template held rounding noise (1e-17 from the step exponentials in one step,
+# 0 in the next) fits too: that entry's code multiplies by whatever is there.  Anything else
+# that changes class -- an exact identity where the template had a rotation, which a fresh plan
+# drops -- plans from scratch, and the new plan becomes the newest template for that gate
+# layout.  QSB_PLAN_TEMPLATES=0 disables.
+# ------------------------------------------------------------------------------------------
+PLAN_TEMPLATES = os.environ.get("QSB_PLAN_TEMPLATES", "1") != "0"
+_TEMPLATES: dict = {}
+_TEMPLATES_MAX = 64
+_HH = 0.7071067811865475
+_GENERIC = 5
+_TINY = 6
+TEMPLATE_STATS = {"hits": 0, "misses": 0, "rejected": 0}
+
+
+def _entry_classes(m) -> np.ndarray:
+    """Class of every real and imaginary part of a matrix (uint8): 0, 1, -1, 1/sqrt 2,
+    -1/sqrt 2 -> 0..4, rounding-noise size (0 < |x| <= 1e-12) -> _TINY, anything else ->
+    _GENERIC."""
+    v = np.ascontiguousarray(m, dtype=np.complex128).reshape(-1).view(np.float64)
+    out = np.full(v.shape[0], _GENERIC, np.uint8)
+    out[np.abs(v) <= 1e-12] = _TINY
+    out[v == 0.0] = 0
+    out[v == 1.0] = 1
+    out[v == -1.0] = 2
+    out[v == _HH] = 3
+    out[v == -_HH] = 4
+    return out
+
+
+def _planner_switches():
+    """Module switches the planner reads (part of a template's key: tests and experiments flip
+    them at run time)."""
+    return (SNAP_TINY, MERGE_SLACKS, FP_PER_SWEEP, BALANCE_DIAGONALS, REORDER_GATES, SEED_GATES, MINIMAL_LAYOUT_CHANGES, TMA_STORE_LAYOUT, SPLIT_2Q,
+            SPLIT_MAX_CODE, MAX_2Q_CODE, X2_2Q, X2_BIG, X2_C64, id(GEOMETRY_JIT), id(GEOMETRY_JIT_2Q),
+            id(GEOMETRY_JIT_2Q_SPLIT), id(GEOMETRY_JIT_2Q_X2))
+
+
+def _compatible(old: np.ndarray, new: np.ndarray) -> bool:
+    """New entries fit a template's: the same class, or an exact 0 where the template held
+    rounding noise (its code multiplies by whatever is there)."""
+    return old.shape == new.shape and bool(np.all((new == old) | ((old == _TINY) & (new == 0))))
+
+
+class PlanTemplate:
+    def __init__(self, plan: Plan, leaf_classes: np.ndarray):
+        self.plan = plan
+        self.leaf_classes = leaf_classes
+        self.classes = {}  # id(gate) -> entry classes of its matrix in the template
+        for st in plan.steps:
+            for g in (st.gates if isinstance(st, PassStep) else [st.gate]):
+                if g.kind != "swap" and g.matrix is not None:
+                    self.classes[id(g)] = _entry_classes(g.matrix)
+
+    def _rebuilt(self, g: NGate, M):
+        if g.kind == "swap":
+            return g
+        if g.build is None:
+            return None
+        m = _snap(g.build(M))
+        if m.shape != g.matrix.shape or not _compatible(self.classes[id(g)], _entry_classes(m)):
+            return None
+        return NGate(g.kind, g.targets, g.controls, m, g.tmask, g.smask, g.index, g.build)
+
+    def instantiate(self, M) -> Plan | None:
+        """The template's plan for the gate matrices M (None: a special entry changed)."""
+        src = self.plan
+        out = Plan(src.n_qubits, src.dtype)
+        for st in src.steps:
+            if isinstance(st, GateStep):
+                g = self._rebuilt(st.gate, M)
+                if g is None:
+                    return None
+                out.steps.append(GateStep(g))
+                continue
+            gates = []
+            for g in st.gates:
+                h = self._rebuilt(g, M)
+                if h is None:
+                    return None
+                gates.append(h)
+            geo, mpos, has_diag = st.tpl
+            if has_diag:
+                words, info = compile_pass(gates, set(st.tile_pos), src.n_qubits, src.dtype, geo,
+                                           minimal=MINIMAL_LAYOUT_CHANGES)
+                mp = info["mpos"]
+            else:
+                words = st.words.copy()
+                where = {id(g): k for k, g in enumerate(st.gates)}
+                mp = []
+                for pos, g_old, swapped in mpos:
+                    g = gates[where[id(g_old)]]
+                    m = g.matrix[np.ix_(_PERM2, _PERM2)] if swapped else g.matrix
+                    v = np.ascontiguousarray(m, dtype=np.complex128).reshape(-1).view(np.int64)
+                    words[pos:pos + v.shape[0]] = v
+                    mp.append((pos, g, swapped))
+            out.steps.append(PassStep(words, gates, st.tile_pos, st.ext_perm, st.n_transposes, st.n_pivots,
+                                      tpl=(geo, mp, has_diag)))
+        return out
+
+
 def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, fuse: bool = True,
                  geometry: TileGeometry | None = None) -> Plan:
     """Plan a gate list into PassSteps (fused) and GateSteps (stand-alone kernels).  `geometry`
     defaults to the interpreter's (GEOMETRY); the specialised kernels use GEOMETRY_JIT."""
     geo = geometry or GEOMETRY[dtype]
+    use_tpl = (PLAN_TEMPLATES and fuse and n_qubits >= geo.K + 1 and len(specs) > 0
+               and not any(isinstance(spec, NGate) for spec in specs))
+    mats = key = leaf = None
+    if use_tpl:
+        mats = [_snap(gate_matrix(spec)) for spec in specs]
+        key = (n_qubits, dtype, geo, allow_ext_perm, _planner_switches(),
+               tuple((tuple(int(q) for q in spec.targets), tuple(int(q) for q in spec.controls), m.shape[0])
+                     for spec, m in zip(specs, mats)))
+        leaf = _entry_classes(np.concatenate([np.asarray(m, dtype=np.complex128).reshape(-1) for m in mats]))
+        for tpl in _TEMPLATES.get(key, ()):
+            if not _compatible(tpl.leaf_classes, leaf):
+                continue
+            plan = tpl.instantiate(mats)
+            if plan is not None:
+                TEMPLATE_STATS["hits"] += 1
+                return plan
+            TEMPLATE_STATS["rejected"] += 1
+        TEMPLATE_STATS["misses"] += 1
     gates = []
     for i, spec in enumerate(specs):
-        g = spec if isinstance(spec, NGate) else normalize(spec, n_qubits, i)
+        if isinstance(spec, NGate):
+            g = spec
+        else:
+            g = normalize(spec, n_qubits, i, mats[i] if mats is not None else None)
         if g is not None:
             gates.append(g)
     plan = Plan(n_qubits, dtype)
     if not fuse or n_qubits < geo.K + 1:
         plan.steps = [GateStep(g) for g in gates]
         return plan
-    gates = merge_2q_runs(merge_single_qubit(sandwich_diagonals(merge_1q_runs(gates))))
-    plan = _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, None)
+    base = sandwich_diagonals(merge_1q_runs(gates))
+    best = None
+    seen = set()
+    for slack in MERGE_SLACKS:
+        # folding a single-qubit gate into a 2-qubit neighbour that gets a little dearer can
+        # let two 2-qubit gates on the same pair meet and merge (consecutive Trotter steps: 383
+        # -> 315 FMAs per amplitude per step at n = 30), or just cost more: each variant is
+        # planned and the one with the lowest estimated time kept
+        cand = merge_2q_runs(merge_single_qubit(base, slack))
+        sig = tuple((g.kind, g.targets, g.controls, round(matrix_cost(g.matrix), 6) if g.kind in ("g1", "g2") else 0)
+                    for g in cand)
+        if sig in seen:
+            continue
+        seen.add(sig)
+        alt = _plan_passes(Plan(n_qubits, dtype), cand, n_qubits, dtype, geo, allow_ext_perm, None)
+        est = plan_estimate(alt)
+        if best is None or est < best[0] - 1e-9:
+            best = (est, alt, cand)
+    _, plan, gates = best
     if BALANCE_DIAGONALS:
         # diagonal-heavy plans (the QFT: 204 / 141 / 84 / 21 diagonal gates in its four passes
         # at n = 30) keep their early passes compute-bound; the trailing diagonals of a pass
@@ -576,7 +795,47 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
                 if m < best_max:
                     best, best_max = alt, m
             plan = best
+    if use_tpl:
+        if len(_TEMPLATES) >= _TEMPLATES_MAX and key not in _TEMPLATES:
+            _TEMPLATES.pop(next(iter(_TEMPLATES)))
+        # newest first; a few per gate layout (e.g. the first steps of an adiabatic schedule,
+        # where a zero coefficient makes gates exact identities)
+        _TEMPLATES[key] = [PlanTemplate(plan, leaf)] + _TEMPLATES.get(key, [])[:3]
     return plan
+
+
+# merge_single_qubit cost slacks tried by plan_circuit (QSB_MERGE_SLACKS, comma separated)
+MERGE_SLACKS = tuple(float(x) for x in os.environ.get("QSB_MERGE_SLACKS", "0,4,8").split(",") if x.strip())
+# Pass time model (in state sweeps), fitted to per-pass device times of the n = 30 complex128
+# Trotter / variational / grid passes (tools/variant_sweep.py, round 2): the longer of one sweep
+# and 0.15 + (FP work per amplitude) / FP_PER_SWEEP (~75: B200 copy bandwidth over the FP64
+# FMA rate at the ~0.75 the dense-gate passes reach; complex64 has twice the FP32 rate and half
+# the bytes, so the same), and at least 1 + (runs - 5) / 4 for a tile of more than five runs of
+# contiguous state bits (the rank-5 TMA box covers five; the rest become separate loads -- a
+# tile of nine runs measured two sweeps)
+FP_PER_SWEEP = float(os.environ.get("QSB_FP_PER_SWEEP", "75"))
+
+
+def _tile_runs(tile_pos) -> int:
+    runs, prev = 0, -2
+    for p in sorted(tile_pos):
+        if p != prev + 1:
+            runs += 1
+        prev = p
+    return runs
+
+
+def plan_estimate(plan: Plan) -> float:
+    """Estimated time of a plan in state sweeps (see FP_PER_SWEEP); a stand-alone gate costs its
+    touched fraction."""
+    t = 0.0
+    for st in plan.steps:
+        if isinstance(st, PassStep):
+            fp = sum(matrix_cost(g.matrix) for g in st.gates if g.kind in ("g1", "g2"))
+            t += max(1.0 + max(0, _tile_runs(st.tile_pos) - 5) / 4.0, 0.15 + fp / FP_PER_SWEEP)
+        else:
+            t += st.gate.touched_fraction()
+    return t
 
 
 def _defer_trailing_diagonals(absorbed, deferred, budget):
@@ -628,6 +887,7 @@ def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget)
                 elif X2_BIG and dtype in GEOMETRY_JIT_2Q_X2:
                     pgeo = GEOMETRY_JIT_2Q_X2[dtype]
             words, info = compile_pass(absorbed, T, n_qubits, dtype, pgeo, minimal=MINIMAL_LAYOUT_CHANGES)
+            used_geo = pgeo
             if (pgeo is GEOMETRY_JIT_2Q.get(dtype) and dtype == nat.QSB_C64 and X2_C64
                     and dtype in GEOMETRY_JIT_2Q_X2):
                 # complex64: 256 x 32 at two CTAs per SM when it saves a layout change, or for the
@@ -640,7 +900,7 @@ def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget)
                                       minimal=MINIMAL_LAYOUT_CHANGES)
                 if i3["transposes"] < info["transposes"] or (i3["transposes"] == info["transposes"]
                                                              and code > SPLIT_MAX_CODE):
-                    words, info = w3, i3
+                    words, info, used_geo = w3, i3, GEOMETRY_JIT_2Q_X2[dtype]
             if pgeo is GEOMETRY_JIT_2Q.get(dtype) and dtype in GEOMETRY_JIT_2Q_SPLIT and SPLIT_2Q != "0":
                 code = sum(matrix_cost(g.matrix) for g in absorbed if g.kind in ("g1", "g2"))
                 chosen = False
@@ -648,7 +908,7 @@ def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget)
                     w2, i2 = compile_pass(absorbed, T, n_qubits, dtype, GEOMETRY_JIT_2Q_SPLIT[dtype],
                                           minimal=MINIMAL_LAYOUT_CHANGES)
                     if SPLIT_2Q == "1" or i2["transposes"] <= info["transposes"]:
-                        words, info = w2, i2
+                        words, info, used_geo = w2, i2, GEOMETRY_JIT_2Q_SPLIT[dtype]
                         chosen = True
                 if not chosen and dtype in GEOMETRY_JIT_2Q_X2 and X2_2Q:
                     # heavier passes: 256 consumers x 16 amplitudes at two CTAs per SM (half the
@@ -657,9 +917,10 @@ def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget)
                     w3, i3 = compile_pass(absorbed, T, n_qubits, dtype, GEOMETRY_JIT_2Q_X2[dtype],
                                           minimal=MINIMAL_LAYOUT_CHANGES)
                     if i3["transposes"] <= info["transposes"]:
-                        words, info = w3, i3
+                        words, info, used_geo = w3, i3, GEOMETRY_JIT_2Q_X2[dtype]
             plan.steps.append(PassStep(words, absorbed, tuple(sorted(T)), info["ext_perm"],
-                                       info["transposes"], info["pivots"]))
+                                       info["transposes"], info["pivots"],
+                                       tpl=(used_geo, info["mpos"], info["has_diag"])))
         remaining = deferred
     return plan
 
@@ -978,6 +1239,7 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
 
     pivot_count = 0
     pending_diag = []
+    mpos = []  # (word index, gate, rows/columns exchanged) of every dense gate matrix
 
     def flush_diag():
         nonlocal pivot_count
@@ -1006,7 +1268,9 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
             words += layout_words(cur)
             n_trans += 1
         flush_diag()
-        words += _gate_op(kind, g, pt, pc, cur, tidx)
+        op, swapped = _gate_op(kind, g, pt, pc, cur, tidx)
+        mpos.append((len(words) + (8 if kind == "g1" else 9), g, swapped))
+        words += op
         gi += 1
     flush_diag()
     # bulk tensor stores (jit: in-place passes without dense 2-qubit gates in the two-stage
@@ -1069,7 +1333,10 @@ def compile_pass(absorbed, T, n, dtype, geo: TileGeometry | None = None, minimal
     if len(prog) > MAX_PROG_WORDS or pivot_count > MAX_PIVOTS:
         raise _TooLarge()
     arr = np.array(prog, dtype=np.int64)
-    return arr, {"ext_perm": ext_perm, "transposes": n_trans, "pivots": pivot_count}
+    base = len(prog) - len(words)
+    return arr, {"ext_perm": ext_perm, "transposes": n_trans, "pivots": pivot_count,
+                 "mpos": [(base + w, g, sw) for w, g, sw in mpos],
+                 "has_diag": any(ev[0] == "diag" for ev in events)}
 
 
 class _TooLarge(Exception):
@@ -1085,7 +1352,10 @@ def _matrix_words(m):
 
 
 def _gate_op(kind, g, pt, pc, lay, tidx):
+    """Program words of a dense gate, and whether its 4x4 was re-ordered (row / column bits
+    exchanged so that row bit 1 is the higher register slot)."""
     gmask = rmask = 0
+    swapped = False
     for c in pc:
         if c in tidx and tidx[c] in lay.R:
             rmask |= 1 << lay.slot_of(tidx[c])
@@ -1108,12 +1378,12 @@ def _gate_op(kind, g, pt, pc, lay, tidx):
             ih, il, mm = i0, i1, m
         else:
             # exchange the two row/column bits so that row bit 1 <-> the higher slot
-            perm = [0, 2, 1, 3]
-            ih, il, mm = i1, i0, m[np.ix_(perm, perm)]
+            ih, il, mm = i1, i0, m[np.ix_(_PERM2, _PERM2)]
+            swapped = True
         gk = G_REAL if not np.any(mm.imag) else G_COMPLEX
         w = [OP_G2, 0, ih, il, gk, gmask, gmask, rmask, rmask] + _matrix_words(mm)
     w[1] = len(w)
-    return w
+    return w, swapped
 
 
 def _compile_diag(terms, lay, tile_pos, tidx, geo, slot0):

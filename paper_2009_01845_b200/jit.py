@@ -101,6 +101,18 @@ def _w2d(w):
     return struct.unpack("<d", struct.pack("<q", int(w)))[0]
 
 
+class _Tagged(float):
+    """A coefficient word read as a double, remembering its word position (recipe recording:
+    arithmetic on it yields a plain float, which the recipe check below then catches)."""
+
+    __slots__ = ("p",)
+
+    def __new__(cls, value, pos):
+        x = float.__new__(cls, value)
+        x.p = pos
+        return x
+
+
 _PRELUDE = r"""
 typedef unsigned long long u64;
 typedef unsigned int u32;
@@ -316,6 +328,11 @@ class _Gen:
         self.quiet = False
         self.dpos: set = set()
         self.trace: list = []
+        # recipe recording (coefficient_recipe): the word position each coefficient is read
+        # from (-1: a constant of the structure)
+        self.record = False
+        self.csrc: list = []
+        self.tsrc: list = []
         amp_bytes = 16 if dtype == nat.QSB_C128 else 8
         # 128 KB tiles are staged as two 64 KB halves split on tile bit K-1 (a register bit of
         # the first layout); layout changes then run in two rounds through a 64 KB buffer
@@ -368,12 +385,16 @@ class _Gen:
     # constant-bank operands (no registers held across the tile); returns the first index
     def cf(self, values):
         k = len(self.coeffs)
+        if self.record:
+            self.csrc.extend(v.p if type(v) is _Tagged else -1 for v in values)
         self.coeffs.extend(float(v) for v in values)
         return k
 
     # per-thread-indexed tables (pivot factor tables): doubles staged in shared memory
     def tf(self, values):
         k = len(self.tables)
+        if self.record:
+            self.tsrc.extend(v.p if type(v) is _Tagged else -1 for v in values)
         self.tables.extend(float(v) for v in values)
         return k
 
@@ -384,6 +405,8 @@ class _Gen:
     def d(self, i):
         """Word i read as a double (a coefficient: recorded for the structure key)."""
         self.dpos.add(i)
+        if self.record:
+            return _Tagged(_w2d(self.w[i]), i)
         return _w2d(self.w[i])
 
     # ---- layouts ------------------------------------------------------------------------
@@ -806,7 +829,7 @@ class _Gen:
                 self.emit(f"      {{ const C x = v{self.vm[s]}; v{self.vm[s]} = v{self.vm[t]}; v{self.vm[t]} = x; }}")
         else:
             mat = [complex(m[2 * k], m[2 * k + 1]) for k in range(4)]
-            coef = self.matrix_coeffs(mat, 2)
+            coef = self.matrix_coeffs(mat, 2, m)
             for s in range(A):
                 if s & (1 << ib) or (s & rmask) != rval:
                     continue
@@ -815,13 +838,15 @@ class _Gen:
             self.emit("    }")
         self.emit("    }")
 
-    def matrix_coeffs(self, mat, d):
+    def matrix_coeffs(self, mat, d, parts=None):
         """Per-entry structure of a d x d gate matrix: ('z',) exact zero (skipped), ('1',)/('-1',)
         exact +-1 (no multiply), ('r', k) real, ('i', k) imaginary, ('c', k) complex -- k indexes
         the parameter array.  The structure is part of the kernel source (so e.g. every fSim or
         every Trotter ZZ+X term shares one kernel), the values are runtime coefficients."""
         out = []
-        for z in mat:
+        for k, z in enumerate(mat):
+            # the real / imaginary words themselves when given (recipe recording keeps their positions)
+            re, im = (parts[2 * k], parts[2 * k + 1]) if parts is not None else (z.real, z.imag)
             if z == 0:
                 out.append(("z",))
             elif z == 1:
@@ -829,11 +854,11 @@ class _Gen:
             elif z == -1:
                 out.append(("-1",))
             elif z.imag == 0:
-                out.append(("r", self.cf([z.real])))
+                out.append(("r", self.cf([re])))
             elif z.real == 0:
-                out.append(("i", self.cf([z.imag])))
+                out.append(("i", self.cf([im])))
             else:
-                out.append(("c", self.cf([z.real, z.imag])))
+                out.append(("c", self.cf([re, im])))
         self.trace.append(("m", tuple(e[0] for e in out)))
         return out
 
@@ -922,7 +947,7 @@ class _Gen:
         if gmask:
             self.emit(f"    if (((base | gt{self.li}) & {gmask}ull) == {gval}ull) {{")
         mat = [complex(m[2 * k], m[2 * k + 1]) for k in range(16)]
-        coef = self.matrix_coeffs(mat, 4)
+        coef = self.matrix_coeffs(mat, 4, m)
         for s in range(A):
             if s & ((1 << ih) | (1 << il)) or (s & rmask) != rval:
                 continue
@@ -941,9 +966,12 @@ class _Gen:
         o_ta = a + 5 + 3 * ne
         o_tb = o_ta + 32
         o_rt = o_tb + 2 * nb
-        ta = [complex(self.d(o_ta + 2 * k), self.d(o_ta + 2 * k + 1)) for k in range(16)]
-        tb = [complex(self.d(o_tb + 2 * k), self.d(o_tb + 2 * k + 1)) for k in range(nb)]
-        rt = [complex(self.d(o_rt + 2 * k), self.d(o_rt + 2 * k + 1)) for k in range(A)]
+        ta_p = [self.d(o_ta + k) for k in range(32)]
+        tb_p = [self.d(o_tb + k) for k in range(2 * nb)]
+        rt_p = [self.d(o_rt + k) for k in range(2 * A)]
+        ta = [complex(ta_p[2 * k], ta_p[2 * k + 1]) for k in range(16)]
+        tb = [complex(tb_p[2 * k], tb_p[2 * k + 1]) for k in range(nb)]
+        rt = [complex(rt_p[2 * k], rt_p[2 * k + 1]) for k in range(A)]
         self.emit(f"    {{ // pivot {slot}")
         if ptype == 1:
             self.emit(f"    if (((base | gt{self.li}) & {pval}ull) != 0ull) {{")
@@ -952,16 +980,16 @@ class _Gen:
         self.trace.append(("pivot", ta_all_one, tb_all_one, tuple(bool(use_rt and rt[s] != 1) for s in range(A))))
         self.emit(f"      double2 fd = sm.ep[it & 3][{slot}];")
         if not ta_all_one:
-            ci = self.tf([x for z in ta for x in (z.real, z.imag)])
+            ci = self.tf(ta_p)
             self.emit(f"      fd = dm(fd, cfz(scf, {ci} + 2 * (tid & 15)));")
         if not tb_all_one:
-            ci = self.tf([x for z in tb for x in (z.real, z.imag)])
+            ci = self.tf(tb_p)
             self.emit(f"      fd = dm(fd, cfz(scf, {ci} + 2 * (tid >> 4)));")
         self.emit("      const C f = toC(fd);")
         # which slots carry a register-partner factor (structure: RT entry != 1 from a partner bit)
         rt_ci = None
         if use_rt:
-            rt_ci = self.cf([x for z in rt for x in (z.real, z.imag)])
+            rt_ci = self.cf(rt_p)
         for s in range(A):
             if ptype == 0 and not (s >> pval) & 1:
                 continue
@@ -1351,6 +1379,127 @@ def coefficients_only(words, dtype):
     return _structure_key(g, words, dtype), np.array(g.coeffs, dtype=np.float64), np.array(g.tables, dtype=np.float64)
 
 
+# Coefficient recipes: for a structure seen before, the parameter and table vectors are plain
+# reads of the program's coefficient words (plus structural constants), so a recipe -- the word
+# position of every coefficient -- replaces the coefficient-only generator run (which walks the
+# whole program: ~0.5 ms per pass).  A recipe is recorded with position-tagged reads and kept
+# only if it reproduces a quiet generator run on a perturbed copy of the program (any derived
+# value would differ); it matches a program with the same words outside the coefficient
+# positions whose coefficients keep their value classes (0, +-1, +-1/sqrt 2, rounding noise,
+# other), except that recorded noise may be an exact 0 now.  QSB_COEFF_RECIPES=0 disables.
+RECIPES = os.environ.get("QSB_COEFF_RECIPES", "1") != "0"
+_RECIPES: dict = {}
+_RECIPES_MAX = 4096
+_HH = 0.7071067811865475
+RECIPE_STATS = {"hits": 0, "built": 0, "refused": 0}
+
+
+def _value_classes(v) -> np.ndarray:
+    """0, 1, -1, 1/sqrt 2, -1/sqrt 2 -> 0..4, anything else 5 (the values the generator's
+    structure decisions test)."""
+    out = np.full(v.shape[0], 5, np.uint8)
+    out[np.abs(v) <= 1e-12] = 6  # rounding noise
+    out[v == 0.0] = 0
+    out[v == 1.0] = 1
+    out[v == -1.0] = 2
+    out[v == _HH] = 3
+    out[v == -_HH] = 4
+    return out
+
+
+class _Recipe:
+    __slots__ = ("dpos", "masked", "cls", "p_src", "p_const", "t_src", "t_const", "skey")
+
+
+def _recipe_prekey(w, dtype):
+    return (int(dtype), int(w.shape[0]), w[:H_TILEPOS + int(w[2])].tobytes())
+
+
+def _recipe_lookup(w, dtype):
+    with _lock:
+        cands = list(_RECIPES.get(_recipe_prekey(w, dtype), ()))
+    for r in cands:
+        m = w.copy()
+        m[r.dpos] = 0
+        if m.tobytes() != r.masked:
+            continue
+        # every coefficient keeps its class (the kernel specialised on 0, +-1, ...), except that
+        # rounding noise in the recorded program may be an exact 0 now (multiplied as a value)
+        cls = _value_classes(w[r.dpos].view(np.float64))
+        if np.all((cls == r.cls) | ((r.cls == 6) & (cls == 0))):
+            return r
+    return None
+
+
+def _recipe_apply(r, w):
+    v = w.view(np.float64)
+    p = r.p_const.copy()
+    sel = r.p_src >= 0
+    p[sel] = v[r.p_src[sel]]
+    t = r.t_const.copy()
+    sel = r.t_src >= 0
+    t[sel] = v[r.t_src[sel]]
+    return p, t
+
+
+def _recipe_build(words, dtype):
+    """Record and check the recipe of a program (None when its coefficients are not plain
+    reads, e.g. expectation passes)."""
+    w = np.array(words, dtype=np.int64)
+    if int(w[7]) & 2:
+        return None
+    g = _Gen(w, dtype)
+    g.quiet = True
+    g.record = True
+    g.generate("KNAME")
+    r = _Recipe()
+    r.dpos = np.array(sorted(g.dpos), dtype=np.int64)
+    m = w.copy()
+    m[r.dpos] = 0
+    r.masked = m.tobytes()
+    vals = w[r.dpos].view(np.float64)
+    r.cls = _value_classes(vals)
+    r.p_src = np.array(g.csrc, dtype=np.int64)
+    r.p_const = np.array(g.coeffs, dtype=np.float64)
+    r.t_src = np.array(g.tsrc, dtype=np.int64)
+    r.t_const = np.array(g.tables, dtype=np.float64)
+    r.skey = _structure_key(g, w, dtype)
+    # check on a perturbed program: every coefficient of class "other" scaled by (1 + 2^-20)
+    w2 = w.copy()
+    f = w2.view(np.float64)
+    other = (r.cls == 5) | (r.cls == 6)
+    f[r.dpos[other]] *= 1.0 + 2.0 ** -20
+    g2 = _Gen(w2, dtype)
+    g2.quiet = True
+    g2.generate("KNAME")
+    p2, t2 = _recipe_apply(r, w2)
+    p1, t1 = _recipe_apply(r, w)
+    ok = (_structure_key(g2, w2, dtype) == r.skey and np.array_equal(p2, np.array(g2.coeffs, dtype=np.float64))
+          and np.array_equal(t2, np.array(g2.tables, dtype=np.float64))
+          and np.array_equal(p1, r.p_const) and np.array_equal(t1, r.t_const))
+    with _lock:
+        if not ok:
+            RECIPE_STATS["refused"] += 1
+            return None
+        RECIPE_STATS["built"] += 1
+        if sum(len(v) for v in _RECIPES.values()) >= _RECIPES_MAX:
+            _RECIPES.clear()
+        _RECIPES.setdefault(_recipe_prekey(w, dtype), []).append(r)
+    return r
+
+
+def fast_coefficients(words, dtype):
+    """coefficients_only through a matching recipe when there is one."""
+    if RECIPES:
+        w = np.asarray(words, dtype=np.int64)
+        r = _recipe_lookup(w, dtype)
+        if r is not None:
+            RECIPE_STATS["hits"] += 1
+            p, t = _recipe_apply(r, w)
+            return r.skey, p, t
+    return coefficients_only(words, dtype)
+
+
 def generate(words, dtype):
     """(source, kernel name, parameter coefficients) for a pass program (CPU-only, tests)."""
     return generate_full(words, dtype)[:3]
@@ -1455,7 +1604,7 @@ def compile_words(words, dtype):
         return done
     out = None
     if _STRUCT_CACHE:
-        key, params, tables = coefficients_only(words, dtype)
+        key, params, tables = fast_coefficients(words, dtype)
         with _lock:
             hit = _STRUCT_CACHE.get(key)
         if hit is not None and len(tables) <= MAX_COEFFS:
@@ -1503,6 +1652,11 @@ def _compile_words(words, dtype):
         if len(_STRUCT_CACHE) >= 4096:
             _STRUCT_CACHE.pop(next(iter(_STRUCT_CACHE)))
         _STRUCT_CACHE[skey] = hit
+    if RECIPES:
+        try:
+            _recipe_build(words, dtype)
+        except Exception:  # an optimisation only
+            pass
     return hit, (pbytes, tables)
 
 
@@ -1519,7 +1673,7 @@ def precompile(steps, dtype, device: int | None = None) -> None:
         rest = []
         for st in todo:
             try:
-                key, params, tables = coefficients_only(st.words, dtype)
+                key, params, tables = fast_coefficients(st.words, dtype)
             except Exception:
                 rest.append(st)
                 continue

@@ -250,8 +250,13 @@ def test_consecutive_trotter_steps_merge_two_qubit_runs(dtype, tol):
     plan = plan_circuit(specs, n, dtype, geometry=GEOMETRY_JIT[dtype])
     assert max_abs(emulate_plan(plan, psi, npd), ov.run(gates, n, psi)) <= tol
     single = plan_circuit(spec_tuples_to_specs(step), n, dtype, geometry=GEOMETRY_JIT[dtype])
-    g2 = lambda p: sum(g.kind == "g2" for s in p.steps if isinstance(s, PassStep) for g in s.gates)  # noqa: E731
-    assert g2(plan) < 3 * g2(single)
+    from paper_2009_01845_b200.fusion import matrix_cost
+
+    def fp(p):
+        return sum(matrix_cost(g.matrix) for s in p.steps if isinstance(s, PassStep) for g in s.gates
+                   if g.kind in ("g1", "g2"))
+
+    assert fp(plan) < 3 * fp(single)  # the step boundaries merge
     # reversed target order on the second gate of a pair
     a, _ = np.linalg.qr(rng.standard_normal((4, 4)) + 1j * rng.standard_normal((4, 4)))
     b, _ = np.linalg.qr(rng.standard_normal((4, 4)) + 1j * rng.standard_normal((4, 4)))
@@ -261,3 +266,69 @@ def test_consecutive_trotter_steps_merge_two_qubit_runs(dtype, tol):
     assert len(merged) == 1
     plan = plan_circuit(spec_tuples_to_specs(pair), n, dtype, geometry=GEOMETRY_JIT[dtype])
     assert max_abs(emulate_plan(plan, psi, npd), ov.run(pair, n, psi)) <= tol
+
+
+@pytest.mark.parametrize("dtype,tol", [(C128, 1e-12), (C64, 1e-5)])
+def test_plan_templates_reuse_structure_with_new_coefficients(dtype, tol, monkeypatch):
+    """A circuit with the structure of one planned before (time-dependent Trotter steps,
+    phase circuits with new angles, variational layers with new parameters) is planned from the
+    template -- merged matrices rebuilt, matrix words patched, diagonal passes re-encoded -- and
+    the plan still computes the circuit; a template entry that was special (here an exact
+    identity gate) but no longer is forces a fresh plan."""
+    from paper_2009_01845_b200 import fusion
+    from paper_2009_01845_b200.fusion import GEOMETRY_JIT
+
+    monkeypatch.setattr(fusion, "_TEMPLATES", {})
+    monkeypatch.setattr(fusion, "PLAN_TEMPLATES", True)
+    n = 15
+    rng = np.random.default_rng(12)
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    npd = np.complex128 if dtype == C128 else np.complex64
+
+    def trotter(s):
+        return ov.trotter_step(ov.combine(ov.x_terms(n), 1 - s, ov.tfim_terms(n, 1.0), s), 0.1) * 2
+
+    def phases(seed):
+        r = np.random.default_rng(seed)
+        out = []
+        for q in range(n - 1):
+            out.append(ov.gate("H", (q,)))
+            out.append(ov.gate("CZPow", (q, q + 1), (), (float(r.uniform(0.1, 0.9)),)))
+            out.append(ov.gate("RZ", (q,), (), (float(r.uniform(0.1, 3)),)))
+        return out
+
+    def layers(seed):
+        r = np.random.default_rng(seed)
+        out = []
+        for _ in range(3):
+            for q in range(n):
+                out.append(ov.gate("RY", (q,), (), (float(r.uniform(0, 6)),)))
+            for q in range(0, n - 1, 2):
+                out.append(ov.gate("CZ", (q, q + 1)))
+        return out
+
+    for family, args in ((trotter, (0.3, 0.45, 0.8)), (phases, (1, 2)), (layers, (3, 4))):
+        for k, a in enumerate(args):
+            gates = family(a)
+            before = dict(fusion.TEMPLATE_STATS)
+            plan = plan_circuit(spec_tuples_to_specs(gates), n, dtype, geometry=GEOMETRY_JIT[dtype])
+            if k > 0:
+                assert fusion.TEMPLATE_STATS["hits"] == before["hits"] + 1
+            assert max_abs(emulate_plan(plan, psi, npd), ov.run(gates, n, psi)) <= tol
+    # s = 0 (the ZZ terms vanish, the term exponentials become exact identities): planned afresh
+    before = dict(fusion.TEMPLATE_STATS)
+    gates = trotter(0.0)
+    plan = plan_circuit(spec_tuples_to_specs(gates), n, dtype, geometry=GEOMETRY_JIT[dtype])
+    assert fusion.TEMPLATE_STATS["hits"] == before["hits"]
+    assert max_abs(emulate_plan(plan, psi, npd), ov.run(gates, n, psi)) <= tol
+    # ... and a template whose rotations were exact identities (dropped) does not serve the same
+    # circuit with non-zero angles
+    fusion._TEMPLATES.clear()
+    zero = [ov.gate(g[0], g[1], g[2], (0.0,) if g[0] == "RY" else g[3]) for g in layers(3)]
+    plan_circuit(spec_tuples_to_specs(zero), n, dtype, geometry=GEOMETRY_JIT[dtype])
+    before = dict(fusion.TEMPLATE_STATS)
+    gates = layers(4)
+    plan = plan_circuit(spec_tuples_to_specs(gates), n, dtype, geometry=GEOMETRY_JIT[dtype])
+    assert fusion.TEMPLATE_STATS["hits"] == before["hits"]
+    assert max_abs(emulate_plan(plan, psi, npd), ov.run(gates, n, psi)) <= tol

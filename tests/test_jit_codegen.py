@@ -112,3 +112,64 @@ def test_structure_key_determines_source():
                 seen[key] = src
     # the Trotter steps at different field ratios share their kernels
     assert len(seen) < sum(1 for q_ in progs for _ in q_)
+
+
+def test_coefficient_recipes_equal_the_generator(monkeypatch):
+    """jit coefficient recipes: after one program of a structure has been recorded, another
+    program of that structure (new coefficients) gets exactly the coefficient-only generator's
+    structure key, parameters and tables by plain word reads -- for dense-gate passes
+    (Trotter, grid, variational) and diagonal / pivot passes (QFT, random phases)."""
+    from paper_2009_01845_b200 import build_tfim, build_x, combine, random_grid_circuit, trotter_step_circuit
+    from paper_2009_01845_b200 import gates as G
+
+    monkeypatch.setattr(jit, "_RECIPES", {})
+    monkeypatch.setattr(jit, "RECIPES", True)
+    n = 18
+    rng = np.random.default_rng(9)
+
+    def phases(seed):
+        r = np.random.default_rng(seed)
+        out = []
+        for q in range(n - 1):
+            out.append(G.GateSpec(G.GateKind.H, (q,), (), ()))
+            out.append(G.GateSpec(G.GateKind.CZPOW, (q, q + 1), (), (float(r.uniform(0.1, 0.9)),)))
+            out.append(G.GateSpec(G.GateKind.RZ, (q,), (), (float(r.uniform(0.1, 3)),)))
+        return out
+
+    families = [
+        [combine(build_x(n), 1 - s, build_tfim(n, 1.0), s) for s in (0.2, 0.3, 0.7)],
+        [3, 4],
+        [rng.uniform(0, 6, n * 5) for _ in range(2)],
+        [5, 6],
+    ]
+    checked = 0
+    for dtype in (nat.QSB_C128, nat.QSB_C64):
+        for fam, members in enumerate(families):
+            first = True
+            for mbr in members:
+                if fam == 0:
+                    queue = trotter_step_circuit(mbr, 0.05).queue
+                elif fam == 1:
+                    queue = random_grid_circuit(3, 6, 4, mbr).queue
+                elif fam == 2:
+                    queue = variational_circuit(n, 2, mbr, fused=True).queue
+                else:
+                    queue = phases(mbr)
+                plan = plan_circuit(queue, n, dtype, geometry=GEOMETRY_JIT[dtype])
+                for st in plan.steps:
+                    if not isinstance(st, PassStep):
+                        continue
+                    ref = jit.coefficients_only(st.words, dtype)
+                    if first:
+                        jit._recipe_build(st.words, dtype)
+                        continue
+                    w = np.asarray(st.words, dtype=np.int64)
+                    r = jit._recipe_lookup(w, dtype)
+                    if r is None:
+                        continue  # another structure (e.g. a grid cycle with other gates)
+                    key, p, t = jit.fast_coefficients(st.words, dtype)
+                    assert key == ref[0] and np.array_equal(p, ref[1]) and np.array_equal(t, ref[2])
+                    checked += 1
+                first = False
+    assert checked >= 10
+    assert jit.RECIPE_STATS["refused"] == 0 or jit.RECIPE_STATS["built"] > 0
