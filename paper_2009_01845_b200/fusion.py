@@ -531,20 +531,21 @@ def _absorbed_cost(absorbed) -> float:
     return sum(matrix_cost(g.matrix) if g.kind in ("g1", "g2") else 0.25 for g in absorbed)
 
 
-def _select_pass_best(gates, n, geo: TileGeometry, allow_ext: bool):
+def _select_pass_best(gates, n, geo: TileGeometry, allow_ext: bool, max_runs=None):
     """The better of two absorption scans (by FP work absorbed): the greedy one, and one where
     single-qubit gates may not pull new bits into the tile (a run of 1-qubit gates on scattered
     bits otherwise fills the tile with bits no 2-qubit gate pairs up), whose tile is then
     re-scanned as fixed."""
-    a1, d1, t1 = _select_pass(gates, n, geo, allow_ext)
-    _, _, t_lazy = _select_pass(gates, n, geo, allow_ext, lazy_1q=True)
+    a1, d1, t1 = _select_pass(gates, n, geo, allow_ext, max_runs=max_runs)
+    _, _, t_lazy = _select_pass(gates, n, geo, allow_ext, lazy_1q=True, max_runs=max_runs)
     a2, d2, t2 = _select_pass(gates, n, geo, allow_ext, fixed=t_lazy)
     if _absorbed_cost(a2) > _absorbed_cost(a1) + 1e-9:
         return a2, d2, t2
     return a1, d1, t1
 
 
-def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool, lazy_1q: bool = False, fixed=None):
+def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool, lazy_1q: bool = False, fixed=None,
+                 max_runs=None):
     """Greedy absorption scan: returns (absorbed, deferred, tile position set).  `fixed`: the
     tile is given (no growth); `lazy_1q`: single-qubit gates never add tile bits."""
     K, L = geo.K, geo.L
@@ -574,7 +575,8 @@ def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool, lazy_1q: bool = F
                     frozen.update((px, py))
             else:
                 other = py if inx else px
-                if grow and len(T) < K and other not in frozen:
+                if grow and len(T) < K and other not in frozen and (max_runs is None
+                                                                     or _tile_runs(T | {other}) <= max_runs):
                     T.add(other)
                     take = True
                 elif allow_ext and other not in frozen and min(px, py) >= L:
@@ -591,7 +593,8 @@ def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool, lazy_1q: bool = F
             new = need - T
             if not new:
                 take = True
-            elif grow and len(T) + len(new) <= K and not (new & frozen) and not (lazy_1q and len(need) == 1):
+            elif (grow and len(T) + len(new) <= K and not (new & frozen) and not (lazy_1q and len(need) == 1)
+                  and (max_runs is None or _tile_runs(T | new) <= max_runs)):
                 T |= new
                 take = True
         if take:
@@ -755,7 +758,7 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
         return plan
     base = sandwich_diagonals(merge_1q_runs(gates))
     best = None
-    seen = set()
+    seen = {}
     for slack in MERGE_SLACKS:
         # folding a single-qubit gate into a 2-qubit neighbour that gets a little dearer can
         # let two 2-qubit gates on the same pair meet and merge (consecutive Trotter steps: 383
@@ -766,11 +769,20 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
                     for g in cand)
         if sig in seen:
             continue
-        seen.add(sig)
+        seen[sig] = cand
         alt = _plan_passes(Plan(n_qubits, dtype), cand, n_qubits, dtype, geo, allow_ext_perm, None)
         est = plan_estimate(alt)
         if best is None or est < best[0] - 1e-9:
             best = (est, alt, cand)
+    if any(_tile_runs(st.tile_pos) > MAX_TILE_RUNS for st in best[1].steps if isinstance(st, PassStep)):
+        # a tile of scattered bits (e.g. a layer of single-qubit gates on every other qubit
+        # pulled into one pass) loads in pieces: also plan with tiles of at most five runs
+        for cand in seen.values():
+            alt = _plan_passes(Plan(n_qubits, dtype), cand, n_qubits, dtype, geo, allow_ext_perm, None,
+                               max_runs=MAX_TILE_RUNS)
+            est = plan_estimate(alt)
+            if est < best[0] - 1e-9:
+                best = (est, alt, cand)
     _, plan, gates = best
     if BALANCE_DIAGONALS:
         # diagonal-heavy plans (the QFT: 204 / 141 / 84 / 21 diagonal gates in its four passes
@@ -816,6 +828,9 @@ MERGE_SLACKS = tuple(float(x) for x in os.environ.get("QSB_MERGE_SLACKS", "0,4,8
 FP_PER_SWEEP = float(os.environ.get("QSB_FP_PER_SWEEP", "75"))
 
 
+MAX_TILE_RUNS = 5  # runs of contiguous state bits one rank-5 TMA box covers
+
+
 def _tile_runs(tile_pos) -> int:
     runs, prev = 0, -2
     for p in sorted(tile_pos):
@@ -832,7 +847,7 @@ def plan_estimate(plan: Plan) -> float:
     for st in plan.steps:
         if isinstance(st, PassStep):
             fp = sum(matrix_cost(g.matrix) for g in st.gates if g.kind in ("g1", "g2"))
-            t += max(1.0 + max(0, _tile_runs(st.tile_pos) - 5) / 4.0, 0.15 + fp / FP_PER_SWEEP)
+            t += max(1.0 + max(0, _tile_runs(st.tile_pos) - MAX_TILE_RUNS) / 4.0, 0.15 + fp / FP_PER_SWEEP)
         else:
             t += st.gate.touched_fraction()
     return t
@@ -863,10 +878,10 @@ def _defer_trailing_diagonals(absorbed, deferred, budget):
     return kept, moved + list(deferred)
 
 
-def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget):
+def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget, max_runs=None):
     remaining = gates
     while remaining:
-        absorbed, deferred, T = _select_pass_best(remaining, n_qubits, geo, allow_ext_perm)
+        absorbed, deferred, T = _select_pass_best(remaining, n_qubits, geo, allow_ext_perm, max_runs)
         if diag_budget is not None:
             absorbed, deferred = _defer_trailing_diagonals(absorbed, deferred, diag_budget)
         if not absorbed:  # cannot happen with K >= L + 2, but never loop forever
