@@ -734,26 +734,36 @@ __global__ void __launch_bounds__(kMT, 3) k_pieces2(const double* __restrict__ p
   bool seen = in.ser;              // a serial precedes the current element inside the block
   unsigned int slot = slot0;       // slot of the next serial; the current segment's is slot - 1
   const uint64_t bend = min((uint64_t)(blockIdx.x + 1) * kScanBlock, n);
-#pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    const uint64_t i = i0 + k;
-    if (i >= n) break;
-    if ((rc.serial >> k) & 1u) {
-      serial_idx[slot] = i;
-      ++slot;
-      seen = true;
-      V = piece_id();
-    } else {
-      V = piece_then(V, elem_piece(row[k], rc.e[k]));
-    }
-    bool end = (i + 1 == bend);
-    if (!end) {
-      // next element serial?  within the row use the bits, else the next thread's first bit
-      end = (k + 1 < kScanItems) ? ((rc.serial >> (k + 1)) & 1u) != 0 : false;
-    }
-    if (end) {
+  if (rc.serial == 0) {
+    // no serial in the row (nearly every row): the only segment end inside it is the block's
+    // last element, and the value there is the incoming segment composed with the whole row
+    V = piece_then(V, mine.v);
+    if (i0 < bend && bend - 1 - i0 < (uint64_t)kScanItems) {
       if (seen) after[slot - 1] = V;
       else head[blockIdx.x] = V;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const uint64_t i = i0 + k;
+      if (i >= n) break;
+      if ((rc.serial >> k) & 1u) {
+        serial_idx[slot] = i;
+        ++slot;
+        seen = true;
+        V = piece_id();
+      } else {
+        V = piece_then(V, elem_piece(row[k], rc.e[k]));
+      }
+      bool end = (i + 1 == bend);
+      if (!end) {
+        // next element serial?  within the row use the bits, else the next thread's first bit
+        end = (k + 1 < kScanItems) ? ((rc.serial >> (k + 1)) & 1u) != 0 : false;
+      }
+      if (end) {
+        if (seen) after[slot - 1] = V;
+        else head[blockIdx.x] = V;
+      }
     }
   }
   // the row's last element ends a segment when the next row starts with a serial
