@@ -531,21 +531,21 @@ def _absorbed_cost(absorbed) -> float:
     return sum(matrix_cost(g.matrix) if g.kind in ("g1", "g2") else 0.25 for g in absorbed)
 
 
-def _select_pass_best(gates, n, geo: TileGeometry, allow_ext: bool, max_runs=None):
+def _select_pass_best(gates, n, geo: TileGeometry, allow_ext: bool, max_runs=None, fp_budget=None):
     """The better of two absorption scans (by FP work absorbed): the greedy one, and one where
     single-qubit gates may not pull new bits into the tile (a run of 1-qubit gates on scattered
     bits otherwise fills the tile with bits no 2-qubit gate pairs up), whose tile is then
     re-scanned as fixed."""
-    a1, d1, t1 = _select_pass(gates, n, geo, allow_ext, max_runs=max_runs)
-    _, _, t_lazy = _select_pass(gates, n, geo, allow_ext, lazy_1q=True, max_runs=max_runs)
-    a2, d2, t2 = _select_pass(gates, n, geo, allow_ext, fixed=t_lazy)
+    a1, d1, t1 = _select_pass(gates, n, geo, allow_ext, max_runs=max_runs, fp_budget=fp_budget)
+    _, _, t_lazy = _select_pass(gates, n, geo, allow_ext, lazy_1q=True, max_runs=max_runs, fp_budget=fp_budget)
+    a2, d2, t2 = _select_pass(gates, n, geo, allow_ext, fixed=t_lazy, fp_budget=fp_budget)
     if _absorbed_cost(a2) > _absorbed_cost(a1) + 1e-9:
         return a2, d2, t2
     return a1, d1, t1
 
 
 def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool, lazy_1q: bool = False, fixed=None,
-                 max_runs=None):
+                 max_runs=None, fp_budget=None):
     """Greedy absorption scan: returns (absorbed, deferred, tile position set).  `fixed`: the
     tile is given (no growth); `lazy_1q`: single-qubit gates never add tile bits."""
     K, L = geo.K, geo.L
@@ -556,6 +556,7 @@ def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool, lazy_1q: bool = F
     blocked_support = 0
     blocked_targets = 0
     absorbed, deferred = [], []
+    fp_used = 0.0
     for g in gates:
         take = False
         if (g.tmask & blocked_support) or (g.smask & blocked_targets):
@@ -588,6 +589,8 @@ def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool, lazy_1q: bool = F
                     take = True
             if take:
                 loc[x], loc[y] = loc[y], loc[x]
+        elif fp_budget is not None and fp_used + matrix_cost(g.matrix) > fp_budget and fp_used > 0:
+            take = False  # the pass has its share of gate arithmetic: later passes take the rest
         else:
             need = {loc[t] for t in g.targets}
             new = need - T
@@ -598,6 +601,8 @@ def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool, lazy_1q: bool = F
                 T |= new
                 take = True
         if take:
+            if fp_budget is not None and g.kind in ("g1", "g2"):
+                fp_used += matrix_cost(g.matrix)
             absorbed.append(g)
         else:
             deferred.append(g)
@@ -653,7 +658,7 @@ def _entry_classes(m) -> np.ndarray:
 def _planner_switches():
     """Module switches the planner reads (part of a template's key: tests and experiments flip
     them at run time)."""
-    return (SNAP_TINY, MERGE_SLACKS, FP_PER_SWEEP, BALANCE_DIAGONALS, REORDER_GATES, SEED_GATES, MINIMAL_LAYOUT_CHANGES, TMA_STORE_LAYOUT, SPLIT_2Q,
+    return (SNAP_TINY, MERGE_SLACKS, FP_PER_SWEEP, FP_BUDGETS, BALANCE_DIAGONALS, REORDER_GATES, SEED_GATES, MINIMAL_LAYOUT_CHANGES, TMA_STORE_LAYOUT, SPLIT_2Q,
             SPLIT_MAX_CODE, MAX_2Q_CODE, X2_2Q, X2_BIG, X2_C64, id(GEOMETRY_JIT), id(GEOMETRY_JIT_2Q),
             id(GEOMETRY_JIT_2Q_SPLIT), id(GEOMETRY_JIT_2Q_X2))
 
@@ -770,10 +775,12 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
         if sig in seen:
             continue
         seen[sig] = cand
-        alt = _plan_passes(Plan(n_qubits, dtype), cand, n_qubits, dtype, geo, allow_ext_perm, None)
-        est = plan_estimate(alt)
-        if best is None or est < best[0] - 1e-9:
-            best = (est, alt, cand)
+        for budget in (None,) + FP_BUDGETS:
+            alt = _plan_passes(Plan(n_qubits, dtype), cand, n_qubits, dtype, geo, allow_ext_perm, None,
+                               fp_budget=budget)
+            est = plan_estimate(alt)
+            if best is None or est < best[0] - 1e-9:
+                best = (est, alt, cand)
     if any(_tile_runs(st.tile_pos) > MAX_TILE_RUNS for st in best[1].steps if isinstance(st, PassStep)):
         # a tile of scattered bits (e.g. a layer of single-qubit gates on every other qubit
         # pulled into one pass) loads in pieces: also plan with tiles of at most five runs
@@ -829,6 +836,12 @@ FP_PER_SWEEP = float(os.environ.get("QSB_FP_PER_SWEEP", "75"))
 
 
 MAX_TILE_RUNS = 5  # runs of contiguous state bits one rank-5 TMA box covers
+# per-pass FP work caps (FMAs per amplitude) tried besides the greedy absorption, kept when the
+# estimate prefers them (QSB_FP_BUDGETS, comma separated).  Measured (tools/budget_probe.py,
+# n = 30 c128): capping at 128 re-orders the grid's absorption into 34 passes instead of 36
+# (293 -> 288 ms); lower caps only add passes (variational 74 -> 78-81 ms, windowed Trotter
+# 130 -> 141-155 ms), so only 128 is tried
+FP_BUDGETS = tuple(float(x) for x in os.environ.get("QSB_FP_BUDGETS", "128").split(",") if x.strip())
 
 
 def _tile_runs(tile_pos) -> int:
@@ -878,10 +891,10 @@ def _defer_trailing_diagonals(absorbed, deferred, budget):
     return kept, moved + list(deferred)
 
 
-def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget, max_runs=None):
+def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget, max_runs=None, fp_budget=None):
     remaining = gates
     while remaining:
-        absorbed, deferred, T = _select_pass_best(remaining, n_qubits, geo, allow_ext_perm, max_runs)
+        absorbed, deferred, T = _select_pass_best(remaining, n_qubits, geo, allow_ext_perm, max_runs, fp_budget)
         if diag_budget is not None:
             absorbed, deferred = _defer_trailing_diagonals(absorbed, deferred, diag_budget)
         if not absorbed:  # cannot happen with K >= L + 2, but never loop forever
