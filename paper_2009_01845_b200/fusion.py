@@ -764,11 +764,21 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
     base = sandwich_diagonals(merge_1q_runs(gates))
     best = None
     seen = {}
+
+    def trial(cand, budget, runs):
+        nonlocal best
+        alt = _plan_passes(Plan(n_qubits, dtype), cand, n_qubits, dtype, geo, allow_ext_perm, None,
+                           max_runs=runs, fp_budget=budget, estimate_only=True)
+        est = plan_estimate(alt)
+        if best is None or est < best[0] - 1e-9:
+            best = (est, alt, cand, budget, runs)
+
     for slack in MERGE_SLACKS:
         # folding a single-qubit gate into a 2-qubit neighbour that gets a little dearer can
         # let two 2-qubit gates on the same pair meet and merge (consecutive Trotter steps: 383
-        # -> 315 FMAs per amplitude per step at n = 30), or just cost more: each variant is
-        # planned and the one with the lowest estimated time kept
+        # -> 315 FMAs per amplitude per step at n = 30), or just cost more; and capping the
+        # gate arithmetic a pass absorbs re-orders the greedy selection, sometimes into fewer
+        # passes: each variant is planned (tiles only) and the lowest estimate encoded
         cand = merge_2q_runs(merge_single_qubit(base, slack))
         sig = tuple((g.kind, g.targets, g.controls, round(matrix_cost(g.matrix), 6) if g.kind in ("g1", "g2") else 0)
                     for g in cand)
@@ -776,21 +786,15 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
             continue
         seen[sig] = cand
         for budget in (None,) + FP_BUDGETS:
-            alt = _plan_passes(Plan(n_qubits, dtype), cand, n_qubits, dtype, geo, allow_ext_perm, None,
-                               fp_budget=budget)
-            est = plan_estimate(alt)
-            if best is None or est < best[0] - 1e-9:
-                best = (est, alt, cand)
+            trial(cand, budget, None)
     if any(_tile_runs(st.tile_pos) > MAX_TILE_RUNS for st in best[1].steps if isinstance(st, PassStep)):
         # a tile of scattered bits (e.g. a layer of single-qubit gates on every other qubit
         # pulled into one pass) loads in pieces: also plan with tiles of at most five runs
         for cand in seen.values():
-            alt = _plan_passes(Plan(n_qubits, dtype), cand, n_qubits, dtype, geo, allow_ext_perm, None,
-                               max_runs=MAX_TILE_RUNS)
-            est = plan_estimate(alt)
-            if est < best[0] - 1e-9:
-                best = (est, alt, cand)
-    _, plan, gates = best
+            for budget in (None,) + FP_BUDGETS:
+                trial(cand, budget, MAX_TILE_RUNS)
+    _, _, gates, budget, runs = best
+    plan = _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, None, max_runs=runs, fp_budget=budget)
     if BALANCE_DIAGONALS:
         # diagonal-heavy plans (the QFT: 204 / 141 / 84 / 21 diagonal gates in its four passes
         # at n = 30) keep their early passes compute-bound; the trailing diagonals of a pass
@@ -838,10 +842,10 @@ FP_PER_SWEEP = float(os.environ.get("QSB_FP_PER_SWEEP", "75"))
 MAX_TILE_RUNS = 5  # runs of contiguous state bits one rank-5 TMA box covers
 # per-pass FP work caps (FMAs per amplitude) tried besides the greedy absorption, kept when the
 # estimate prefers them (QSB_FP_BUDGETS, comma separated).  Measured (tools/budget_probe.py,
-# n = 30 c128): capping at 128 re-orders the grid's absorption into 34 passes instead of 36
-# (293 -> 288 ms); lower caps only add passes (variational 74 -> 78-81 ms, windowed Trotter
-# 130 -> 141-155 ms), so only 128 is tried
-FP_BUDGETS = tuple(float(x) for x in os.environ.get("QSB_FP_BUDGETS", "128").split(",") if x.strip())
+# n = 30 c128): a cap re-orders the greedy absorption -- the grid 3x10 in 34 passes at 128 and
+# 32 at 192 instead of 36 (294 -> 291 / 279 ms), the windowed Trotter step in 13 passes at 192
+# (130 -> 126 ms); caps below ~100 only add passes (variational 74 -> 78-81 ms)
+FP_BUDGETS = tuple(float(x) for x in os.environ.get("QSB_FP_BUDGETS", "128,192").split(",") if x.strip())
 
 
 def _tile_runs(tile_pos) -> int:
@@ -891,7 +895,11 @@ def _defer_trailing_diagonals(absorbed, deferred, budget):
     return kept, moved + list(deferred)
 
 
-def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget, max_runs=None, fp_budget=None):
+def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget, max_runs=None, fp_budget=None,
+                 estimate_only=False):
+    """Greedy pass selection over `gates`.  estimate_only: passes carry their gates and tile but
+    no program (enough for plan_estimate; plan_circuit compares variants that way and encodes
+    only the one it keeps)."""
     remaining = gates
     while remaining:
         absorbed, deferred, T = _select_pass_best(remaining, n_qubits, geo, allow_ext_perm, max_runs, fp_budget)
@@ -906,6 +914,8 @@ def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget,
         if stand_alone < 1.0:
             # cheaper as sparse single-gate kernels than as a full sweep
             plan.steps.extend(GateStep(g) for g in absorbed)
+        elif estimate_only:
+            plan.steps.append(PassStep(None, absorbed, tuple(sorted(T)), False, 0, 0))
         else:
             pgeo = geo
             if geo == GEOMETRY_JIT[dtype] and dtype in GEOMETRY_JIT_2Q and any(g.kind == "g2" for g in absorbed):

@@ -20,15 +20,18 @@ cases = [("var c128", q.variational_circuit(n, 5, params, fused=True), q.Precisi
          ("var c64", q.variational_circuit(n, 5, params, fused=True), q.Precision.F32),
          ("grid c128", q.random_grid_circuit(3, 10, 20, 42), q.Precision.F64),
          ("trotter4 c128", q.Circuit(n).add([g for _ in range(4) for g in step.queue]), q.Precision.F64)]
+only = os.environ.get("ONLY")
 for name, circ, prec in cases:
+    if only and only not in name:
+        continue
     dt = prec.qsb_dtype
     geo = engine.default_geometry(dt)
     gates = [g for g in (fusion.normalize(s, n, i) for i, s in enumerate(circ.queue)) if g is not None]
     base = fusion.sandwich_diagonals(fusion.merge_1q_runs(gates))
     st = q.uniform_state(n, prec)
-    for slack in (0.0, 4.0):
+    for slack in [float(x) for x in os.environ.get("SLACKS", "0,4").split(",")]:
         cand = fusion.merge_2q_runs(fusion.merge_single_qubit(base, slack))
-        for budget in (None, 128, 96, 80, 72):
+        for budget in [None] + [float(x) for x in os.environ.get("BUDGETS", "128,96,80,72").split(",")]:
             plan = fusion._plan_passes(fusion.Plan(n, dt), cand, n, dt, geo, True, None, fp_budget=budget)
             steps = [s for s in plan.steps if isinstance(s, fusion.PassStep)]
             jit.precompile(steps, dt)
