@@ -130,6 +130,9 @@ X2_2Q = os.environ.get("QSB_X2_2Q", "1") != "0"
 # run 256 x 16 at two CTAs per SM instead of one CTA with two stages (20.4 / 23.4 -> 19.5 / 22.4 ms)
 X2_BIG = os.environ.get("QSB_X2_BIG", "1") != "0"
 X2_C64 = os.environ.get("QSB_X2_C64", "0") == "1"
+# complex64 passes of at least this much FP work per amplitude run 256 x 32 (0 disables)
+C64_WIDE_MIN_CODE = float(os.environ.get("QSB_C64_WIDE_MIN_CODE", "90"))
+C64_WIDE_MAX_CODE = 160.0
 SPLIT_MAX_CODE = float(os.environ.get("QSB_SPLIT_MAX_CODE", "100"))
 # ... unless the pass's straight-line gate code per thread (FP operations per amplitude x 32
 # amplitudes) would outgrow the instruction cache: measured on grid-30, the two passes of 16
@@ -659,7 +662,7 @@ def _planner_switches():
     """Module switches the planner reads (part of a template's key: tests and experiments flip
     them at run time)."""
     return (SNAP_TINY, MERGE_SLACKS, FP_PER_SWEEP, FP_BUDGETS, BALANCE_DIAGONALS, REORDER_GATES, SEED_GATES, MINIMAL_LAYOUT_CHANGES, TMA_STORE_LAYOUT, SPLIT_2Q,
-            SPLIT_MAX_CODE, MAX_2Q_CODE, X2_2Q, X2_BIG, X2_C64, id(GEOMETRY_JIT), id(GEOMETRY_JIT_2Q),
+            SPLIT_MAX_CODE, MAX_2Q_CODE, X2_2Q, X2_BIG, X2_C64, C64_WIDE_MIN_CODE, id(GEOMETRY_JIT), id(GEOMETRY_JIT_2Q),
             id(GEOMETRY_JIT_2Q_SPLIT), id(GEOMETRY_JIT_2Q_X2))
 
 
@@ -939,6 +942,19 @@ def _plan_passes(plan, gates, n_qubits, dtype, geo, allow_ext_perm, diag_budget,
                 if i3["transposes"] < info["transposes"] or (i3["transposes"] == info["transposes"]
                                                              and code > SPLIT_MAX_CODE):
                     words, info, used_geo = w3, i3, GEOMETRY_JIT_2Q_X2[dtype]
+            if pgeo is GEOMETRY_JIT_2Q.get(dtype) and dtype == nat.QSB_C64 and C64_WIDE_MIN_CODE > 0:
+                # complex64: the default 256 x 32 (one CTA, two stages) for the heavier passes or
+                # when it needs fewer layout changes (measured round 2, variational-30 c64: the
+                # 96 / 128 FMA/amp passes 5.00 / 6.23 -> 4.72 / 5.76 ms, a 56 FMA/amp pass with
+                # one layout change fewer 3.55 -> 3.21 ms; the 64 FMA/amp passes tie)
+                # -- but never for the very large passes of mid-size circuits, whose 32-amplitude
+                # straight-line kernels take ptxas minutes (the X2_C64 lesson)
+                code = sum(matrix_cost(g.matrix) for g in absorbed if g.kind in ("g1", "g2"))
+                if code <= C64_WIDE_MAX_CODE:
+                    w4, i4 = compile_pass(absorbed, T, n_qubits, dtype, geo, minimal=MINIMAL_LAYOUT_CHANGES)
+                    if i4["transposes"] < info["transposes"] or (code >= C64_WIDE_MIN_CODE
+                                                                 and i4["transposes"] <= info["transposes"]):
+                        words, info, used_geo = w4, i4, geo
             if pgeo is GEOMETRY_JIT_2Q.get(dtype) and dtype in GEOMETRY_JIT_2Q_SPLIT and SPLIT_2Q != "0":
                 code = sum(matrix_cost(g.matrix) for g in absorbed if g.kind in ("g1", "g2"))
                 chosen = False
