@@ -1,6 +1,6 @@
 """ncu target: the fused plan of one BASELINE workload, run twice (the first run compiles the
 specialised pass kernels; profile the second with -s <passes> -c ...).
-argv: workload (qft|variational|trotter|grid) n precision(f64|f32)."""
+argv: workload (qft|variational|trotter|trotter4|grid) n precision(f64|f32)."""
 import math
 import os
 import sys
@@ -24,6 +24,10 @@ def build(workload, n):
     if workload == "trotter":
         h = q.combine(q.build_x(n), 0.5, q.build_tfim(n, 1.0), 0.5)
         return q.trotter_step_circuit(h, 0.05)
+    if workload == "trotter4":  # four steps as one circuit, as evolve() plans them
+        h = q.combine(q.build_x(n), 0.5, q.build_tfim(n, 1.0), 0.5)
+        step = q.trotter_step_circuit(h, 0.05)
+        return q.Circuit(n).add([g for _ in range(4) for g in step.queue])
     if workload == "grid":
         rows = 3 if n % 3 == 0 else 2
         return q.random_grid_circuit(rows, n // rows, 20, 42)
