@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import os
 import struct
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -636,6 +637,7 @@ def _select_pass(gates, n, geo: TileGeometry, allow_ext: bool, lazy_1q: bool = F
 # ------------------------------------------------------------------------------------------
 PLAN_TEMPLATES = os.environ.get("QSB_PLAN_TEMPLATES", "1") != "0"
 _TEMPLATES: dict = {}
+_TEMPLATES_LOCK = threading.Lock()  # ranks planning concurrently (thread ranks, precompile pools)
 _TEMPLATES_MAX = 64
 _HH = 0.7071067811865475
 _GENERIC = 5
@@ -743,7 +745,9 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
                tuple((tuple(int(q) for q in spec.targets), tuple(int(q) for q in spec.controls), m.shape[0])
                      for spec, m in zip(specs, mats)))
         leaf = _entry_classes(np.concatenate([np.asarray(m, dtype=np.complex128).reshape(-1) for m in mats]))
-        for tpl in _TEMPLATES.get(key, ()):
+        with _TEMPLATES_LOCK:
+            tpls = list(_TEMPLATES.get(key, ()))
+        for tpl in tpls:
             if not _compatible(tpl.leaf_classes, leaf):
                 continue
             plan = tpl.instantiate(mats)
@@ -822,11 +826,13 @@ def plan_circuit(specs, n_qubits: int, dtype: int, allow_ext_perm: bool = True, 
                     best, best_max = alt, m
             plan = best
     if use_tpl:
-        if len(_TEMPLATES) >= _TEMPLATES_MAX and key not in _TEMPLATES:
-            _TEMPLATES.pop(next(iter(_TEMPLATES)))
-        # newest first; a few per gate layout (e.g. the first steps of an adiabatic schedule,
-        # where a zero coefficient makes gates exact identities)
-        _TEMPLATES[key] = [PlanTemplate(plan, leaf)] + _TEMPLATES.get(key, [])[:3]
+        tpl = PlanTemplate(plan, leaf)
+        with _TEMPLATES_LOCK:
+            if len(_TEMPLATES) >= _TEMPLATES_MAX and key not in _TEMPLATES:
+                _TEMPLATES.pop(next(iter(_TEMPLATES)))
+            # newest first; a few per gate layout (e.g. the first steps of an adiabatic
+            # schedule, where a zero coefficient makes gates exact identities)
+            _TEMPLATES[key] = [tpl] + _TEMPLATES.get(key, [])[:3]
     return plan
 
 
