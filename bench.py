@@ -481,7 +481,48 @@ def extra_workloads(q, engine, n, peak):
                      "roofline_frac": max(hbm_s, fp_s) / sec}
         del st, holder
         torch.cuda.empty_cache()
+    out.update(_api_workloads(q, n))
     out.update(_big_state_workloads(q, engine, n + 3, peak))
+    return out
+
+
+def _api_workloads(q, n):
+    """Whole API calls (device-synchronised wall time, warm): exact sampling of all n qubits of a
+    QFT state (1e5 shots; bit-identical to numpy's cumsum + searchsorted on the reference's
+    probabilities) and a 20-step adiabatic TFIM evolution (dt 0.05, T 1; the evolution API with
+    its windowed Trotter circuits, plan templates and host work included)."""
+    import time
+
+    import torch
+
+    out = {}
+    try:
+        st = q.qft_circuit(n).execute(q.basis_state(n, 12345))
+        q.sample(st, range(n), 100000, 42)
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(3):
+            t0 = time.perf_counter()
+            q.sample(st, range(n), 100000, 42)
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        out[f"sample_all_{n}_qubits_1e5_shots"] = {"seconds": best, "per": "call (wall, device-synchronised)"}
+        del st
+        torch.cuda.empty_cache()
+        cfg = q.EvolutionConfig(q.Solver.TROTTER, 0.05, 1.0)
+        q.adiabatic_evolve(q.build_x(n), q.build_tfim(n, 0.9), q.Schedule.linear(), cfg)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        psi = q.adiabatic_evolve(q.build_x(n), q.build_tfim(n, 1.0), q.Schedule.linear(), cfg)
+        torch.cuda.synchronize()
+        sec = time.perf_counter() - t0
+        out[f"adiabatic_tfim_{n}_20steps_c128"] = {"seconds": sec / 20, "per": "Trotter step (wall, device-synchronised)",
+                                                  "total_s": sec}
+        del psi
+        torch.cuda.empty_cache()
+    except Exception as exc:  # the headline stands; say why these are missing
+        torch.cuda.empty_cache()
+        out["api_workloads"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
     return out
 
 
