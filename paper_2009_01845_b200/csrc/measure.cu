@@ -245,31 +245,62 @@ __global__ void k_cumsum_serial(const double* __restrict__ p, uint64_t n, double
 constexpr int kScanItems = 16;                 // elements per thread
 constexpr int kScanBlock = kMT * kScanItems;   // 4096 elements per block
 
-// exclusive scan of the block sums (one block, sequential chunks per thread; approximate)
-__global__ void __launch_bounds__(1024) k_scan_top(double* __restrict__ v, uint64_t nb) {
-  __shared__ double sh[1024];
-  const uint64_t per = (nb + 1023) / 1024;
-  const uint64_t lo = threadIdx.x * per;
-  double acc = 0.0;
-  for (uint64_t i = lo; i < lo + per && i < nb; ++i) acc += v[i];
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double run = 0.0;
-    for (int t = 0; t < 1024; ++t) {
-      const double x = sh[t];
-      sh[t] = run;
-      run += x;
+// Exclusive scan of nb values by one CTA walking chunks of 1024 x 8 (each thread 8 consecutive
+// values, a block scan of the thread sums, a running carry): used for the block sums (approximate
+// doubles, classification only) and the serial-point counts (exact integers).  In place is fine
+// (every value is read before it is written, by the same thread).  Replaces a per-thread
+// sequential walk whose strided loads took 0.45 ms at 2^18 blocks.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_scan_chunked(const T* in, uint64_t nb, T* out, T* total) {
+  constexpr int kPer = 8;
+  __shared__ T wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  T carry = 0;
+  for (uint64_t b0 = 0; b0 < nb; b0 += 1024 * kPer) {
+    T x[kPer];
+    T sum = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const uint64_t i = b0 + (uint64_t)tid * kPer + k;
+      x[k] = i < nb ? in[i] : (T)0;
+      sum += x[k];
     }
+    T incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      const T t = wsum[lane];
+      T u = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const T y = __shfl_up_sync(0xffffffffu, u, o);
+        if (lane >= o) u += y;
+      }
+      wsum[lane] = u - t;  // exclusive over warps
+    }
+    __syncthreads();
+    T run = carry + wsum[w] + (incl - sum);
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const uint64_t i = b0 + (uint64_t)tid * kPer + k;
+      if (i < nb) out[i] = run;
+      run += x[k];
+    }
+    // chunk total: the last thread's inclusive value
+    __shared__ T chunk_total;
+    if (tid == 1023) chunk_total = run - carry;
+    __syncthreads();
+    carry += chunk_total;
+    __syncthreads();
   }
-  __syncthreads();
-  double run = sh[threadIdx.x];
-  for (uint64_t i = lo; i < lo + per && i < nb; ++i) {
-    const double x = v[i];
-    v[i] = run;
-    run += x;
-  }
+  if (total && tid == 0) *total = carry;
 }
+
 
 // Binade of an approximate prefix value: -100000 for zero.  "risky" when within `margin`
 // (relative) of a power of two or in the subnormal-adjacent range.  The strictly sequential
@@ -846,32 +877,6 @@ __global__ void __launch_bounds__(kMT, 3) k_materialize2(const double* __restric
   }
 }
 
-// exclusive scan of counts (single block), writes total to cnt_total
-__global__ void __launch_bounds__(1024) k_scan_counts(const unsigned int* __restrict__ cnt, uint64_t nb,
-                                                      unsigned int* __restrict__ base, unsigned int* total) {
-  __shared__ unsigned int sh[1024];
-  const uint64_t per = (nb + 1023) / 1024;
-  const uint64_t lo = threadIdx.x * per;
-  unsigned int acc = 0;
-  for (uint64_t i = lo; i < lo + per && i < nb; ++i) acc += cnt[i];
-  sh[threadIdx.x] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned int run = 0;
-    for (int t = 0; t < 1024; ++t) {
-      const unsigned int x = sh[t];
-      sh[t] = run;
-      run += x;
-    }
-    *total = run;
-  }
-  __syncthreads();
-  unsigned int run = sh[threadIdx.x];
-  for (uint64_t i = lo; i < lo + per && i < nb; ++i) {
-    base[i] = run;
-    run += cnt[i];
-  }
-}
 
 // total is read from a separate copy: c[n-1] itself is overwritten by the normalisation
 // ---- PCG64 ---------------------------------------------------------------------------------
@@ -1141,7 +1146,7 @@ static int cumsum_phases(const double* probs, uint64_t n, void* scratch, size_t 
 
   // A: approximate block sums and their exclusive scan (only used to classify)
   k_block_sums2<<<(int)nb, kMT, 0, st>>>(probs, n, bpre);
-  k_scan_top<<<1, 1024, 0, st>>>(bpre, nb);
+  k_scan_chunked<double><<<1, 1024, 0, st>>>(bpre, nb, bpre, nullptr);
   // B: serial points per block, their exclusive scan and total (read back to size the lists)
   k_count2<<<(int)nb, kMT, 0, st>>>(probs, n, margin, bpre, cnt);
   static unsigned int* h_total = nullptr;
@@ -1154,7 +1159,7 @@ static int cumsum_phases(const double* probs, uint64_t n, void* scratch, size_t 
     cudaError_t e = cudaMalloc(&d_tot, sizeof(double) * 2);
     if (e != cudaSuccess) return cuda_status(e, "device total");
   }
-  k_scan_counts<<<1, 1024, 0, st>>>(cnt, nb, base, d_tot);
+  k_scan_chunked<unsigned int><<<1, 1024, 0, st>>>(cnt, nb, base, d_tot);
   cudaError_t e = cudaMemcpyAsync(h_total, d_tot, sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return cuda_status(e, "serial count copy");
   e = cudaStreamSynchronize(st);
