@@ -196,11 +196,12 @@ int qsb_sample(const double* cum, uint64_t n, uint64_t state_hi, uint64_t state_
  * searchsorted index (sharded sampling). */
 int qsb_sample_counts(const double* cum, uint64_t n, uint64_t state_hi, uint64_t state_lo,
                       uint64_t inc_hi, uint64_t inc_lo, uint64_t n_shots, int64_t* counts, void* stream);
-/* qsb_cumsum_normalized + qsb_sample in one call without materialising the whole CDF: each
- * draw first finds its 4096-element block from the exact block boundaries of the scan, and only
- * the blocks that hold a draw get their cumulative values (written into `cum` at their
- * positions; other entries of `cum` are left unset).  Samples are bit-identical to the two-call
- * path.  `scratch`: qsb_sample_exact_scratch_bytes(n, n_shots) bytes; n_shots < 2^32. */
+/* qsb_cumsum_normalized + qsb_sample in one call without materialising the CDF: each draw
+ * finds its 4096-element block from the exact block boundaries of the scan; only the blocks
+ * that hold a draw get the exact cumulative value before each of their 16-element rows
+ * (written into `cum`, which needs ceil(n / 4096) * 256 doubles), and each draw walks its row
+ * with fl(c + p) from that value.  Samples are bit-identical to the two-call path.
+ * `scratch`: qsb_sample_exact_scratch_bytes(n, n_shots) bytes; n_shots < 2^32. */
 size_t qsb_sample_exact_scratch_bytes(uint64_t n, uint64_t n_shots);
 int qsb_sample_exact(const double* probs, uint64_t n, double* cum, void* scratch, size_t scratch_bytes,
                      uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t n_shots,

@@ -821,6 +821,40 @@ __global__ void k_total2(const Piece* __restrict__ head, const unsigned int* __r
 }
 
 // materialize + normalise: c_i / c_{n-1}, written coalesced through the padded shared row
+// Sparse sampling, pass E': the exact value before every row of 16 elements (the row start) of
+// the flagged blocks -- the materialise prologue without its per-element walk.  A draw then
+// finds its row by the row starts and walks at most 16 elements with fl(c + p) from the row's
+// exact start, which is the sequential cumsum itself (k_draw_rows).
+__global__ void __launch_bounds__(kMT, 3) k_row_starts(const double* __restrict__ p, uint64_t n, double margin,
+                                                    const double* __restrict__ block_prefix,
+                                                    const unsigned int* __restrict__ serial_base,
+                                                    const double* __restrict__ block_start,
+                                                    const double* __restrict__ serial_val,
+                                                    double* __restrict__ rs, const unsigned char* __restrict__ only) {
+  if (!only[blockIdx.x]) return;
+  __shared__ double sh[kMT * kRow];
+  __shared__ double wsum[kMT / 32];
+  __shared__ unsigned int usum[kMT / 32];
+  __shared__ RowSeg ssh[kMT];
+  RowClass rc;
+  uint64_t i0;
+  block_classify(p, n, margin, block_prefix, sh, wsum, rc, i0);
+  const double* row = sh + threadIdx.x * kRow;
+  RowSeg mine;
+  mine.v = piece_id();
+  mine.ser = rc.serial ? 1 : 0;
+  const int last_ser = rc.serial ? 31 - __clz(rc.serial) : -1;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (k > last_ser && i0 + k < n) mine.v = piece_then(mine.v, elem_piece(row[k], rc.e[k]));
+  const RowSeg in = block_excl_rowseg(mine, ssh);
+  const unsigned int slot0 = serial_base[blockIdx.x] + block_excl_count(__popc(rc.serial), usum);
+  // c before the row's first element: the incoming segment applied to its start value (the last
+  // serial before the row, or the block start)
+  const double c0 = in.ser ? serial_val[slot0 - 1] : block_start[blockIdx.x];
+  rs[(uint64_t)blockIdx.x * kMT + threadIdx.x] = piece_apply(in.v, c0);
+}
+
 __global__ void __launch_bounds__(kMT, 3) k_materialize2(const double* __restrict__ p, uint64_t n, double margin,
                                                       const double* __restrict__ block_prefix,
                                                       const unsigned int* __restrict__ serial_base,
@@ -1255,31 +1289,55 @@ __global__ void __launch_bounds__(kMT) k_draw_blocks(const double* __restrict__ 
   }
 }
 
-__global__ void __launch_bounds__(kMT) k_draw_final(const double* __restrict__ cum, uint64_t n, uint64_t s_hi,
-                                                    uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, uint64_t n_shots,
-                                                    const unsigned int* __restrict__ shot_block,
-                                                    long long* __restrict__ out, uint64_t clip_max) {
+// Sparse sampling, last pass: each draw searches its block's row ends (normalised like the CDF:
+// fl(c / c_{n-1})) for the first row ending above u, then walks that row with fl(c + p_i) from
+// its exact start -- the first element whose normalised value exceeds u, as searchsorted on the
+// full normalised cumsum gives.
+__global__ void __launch_bounds__(kMT) k_draw_rows(const double* __restrict__ p, uint64_t n,
+                                                   const double* __restrict__ rs, const double* __restrict__ bstart,
+                                                   uint64_t nb, const double* __restrict__ total, uint64_t s_hi,
+                                                   uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, uint64_t n_shots,
+                                                   const unsigned int* __restrict__ shot_block,
+                                                   long long* __restrict__ out) {
   const uint64_t t = (uint64_t)blockIdx.x * kMT + threadIdx.x;
   const uint64_t first = t * kShotsPerThread;
   if (first >= n_shots) return;
   const u128 inc = ((u128)i_hi << 64) | i_lo;
   u128 s = pcg_advance(((u128)s_hi << 64) | s_lo, inc, first);
   const u128 mult = pcg_mult();
+  const double tot = *total;
   for (int k = 0; k < kShotsPerThread; ++k) {
     const uint64_t shot = first + k;
     if (shot >= n_shots) break;
     s = s * mult + inc;
     const double u = (double)(pcg_out(s) >> 11) * (1.0 / 9007199254740992.0);
-    const uint64_t b0 = (uint64_t)shot_block[shot] * kScanBlock;
-    uint64_t lo = b0, hi = b0 + kScanBlock < n ? b0 + kScanBlock : n;
-    while (lo < hi) {  // every element before the block is <= u, the block's last one is not
+    const uint64_t b = shot_block[shot];
+    const uint64_t b0 = b * kScanBlock;
+    const uint64_t rows = min((uint64_t)kMT, (n - b0 + kScanItems - 1) / kScanItems);
+    const double* r_b = rs + b * kMT;
+    uint64_t lo = 0, hi = rows;  // first row whose end (the next row's start) exceeds u
+    while (lo < hi) {
       const uint64_t mid = lo + ((hi - lo) >> 1);
-      if (cum[mid] <= u)
+      const double end = (mid + 1 < rows) ? r_b[mid + 1] : (b + 1 < nb ? bstart[b + 1] : tot);
+      if (__ddiv_rn(end, tot) <= u)
         lo = mid + 1;
       else
         hi = mid;
     }
-    out[shot] = (long long)(lo > clip_max ? clip_max : lo);
+    const uint64_t r = lo < rows ? lo : rows - 1;
+    double c = r_b[r];
+    uint64_t res = n - 1;
+    const uint64_t i_first = b0 + r * kScanItems;
+    for (int q = 0; q < kScanItems; ++q) {
+      const uint64_t i = i_first + q;
+      if (i >= n) break;
+      c = __dadd_rn(c, p[i]);
+      if (__ddiv_rn(c, tot) > u) {
+        res = i;
+        break;
+      }
+    }
+    out[shot] = (long long)res;
   }
 }
 }  // namespace qsb
@@ -1320,10 +1378,10 @@ extern "C" int qsb_sample_exact(const double* probs, uint64_t n, double* cum, vo
   const uint64_t threads = (n_shots + kShotsPerThread - 1) / kShotsPerThread;
   const int grid = (int)((threads + kMT - 1) / kMT);
   k_draw_blocks<<<grid, kMT, 0, st>>>(ends, c.nb, s_hi, s_lo, i_hi, i_lo, n_shots, shot_block, flags);
-  k_materialize2<<<(int)c.nb, kMT, 0, st>>>(probs, n, c.margin, c.bpre, c.base, c.bstart, c.sval, c.d_total, cum, 1,
-                                            flags);
-  k_draw_final<<<grid, kMT, 0, st>>>(cum, n, s_hi, s_lo, i_hi, i_lo, n_shots, shot_block,
-                                      reinterpret_cast<long long*>(samples), n - 1);
+  // row starts of the flagged blocks in `cum` (nb x 256 doubles), then the row walks
+  k_row_starts<<<(int)c.nb, kMT, 0, st>>>(probs, n, c.margin, c.bpre, c.base, c.bstart, c.sval, cum, flags);
+  k_draw_rows<<<grid, kMT, 0, st>>>(probs, n, cum, c.bstart, c.nb, c.d_total, s_hi, s_lo, i_hi, i_lo, n_shots,
+                                    shot_block, reinterpret_cast<long long*>(samples));
   QSB_CHECK_LAUNCH("qsb_sample_exact");
   return QSB_OK;
 }

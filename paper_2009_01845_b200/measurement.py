@@ -184,12 +184,13 @@ SPARSE_CDF_MIN = 1 << 16
 
 def device_sample_exact(probs, n_shots: int, seed: int):
     """The draws of sample() straight from the probabilities: the exact scan's block
-    boundaries route every draw to its 4096-element block, and only those blocks are
-    materialised and searched (bit-identical to device_cdf + device_sample)."""
+    boundaries route every draw to its 4096-element block, the exact values before that block's
+    16-element rows route it to a row, and the row is walked with fl(c + p) (bit-identical to
+    device_cdf + device_sample)."""
     torch = nat.torch_mod()
     lib = nat.lib()
     n = probs.numel()
-    cum = torch.empty_like(probs)
+    cum = torch.empty(((n + 4095) // 4096) * 256, dtype=probs.dtype, device=probs.device)  # row starts
     nbytes = int(lib.qsb_sample_exact_scratch_bytes(n, int(n_shots)))
     scratch = torch.empty(nbytes, dtype=torch.uint8, device=probs.device)
     out = torch.empty(int(n_shots), dtype=torch.int64, device=probs.device)
