@@ -165,7 +165,7 @@ def sample(state, qubits, n_shots: int, seed: int, registers: dict | None = None
             raise ShapeError(f"register {name!r} references unmeasured qubits {sorted(missing)}")
         regs[name] = tuple(reg)
     probs = device_marginal(state, qubits)
-    if SPARSE_CDF and probs.numel() >= SPARSE_CDF_MIN and n_shots <= probs.numel() // 4096:
+    if SPARSE_CDF and probs.numel() >= SPARSE_CDF_MIN and n_shots < (1 << 32):
         samples = device_sample_exact(probs, n_shots, seed).cpu().numpy()
     else:
         cum = device_cdf(probs)
@@ -174,10 +174,10 @@ def sample(state, qubits, n_shots: int, seed: int, registers: dict | None = None
     return MeasurementResult(int(n_shots), qubits, samples, int(seed), regs)
 
 
-# sample() materialises only the CDF blocks that hold a draw (qsb_sample_exact) for marginals of
-# at least SPARSE_CDF_MIN outcomes and at most one shot per 4096-outcome block (measured at 2^30
-# outcomes: 1e5 shots 31.6 -> 24.2 ms; 1e6 shots touch nearly every block and are faster with
-# the full CDF, 32.2 vs 35.0 ms); QSB_SPARSE_CDF=0: always the full CDF
+# sample() draws through qsb_sample_exact (no CDF: row starts of the drawn blocks, a 16-element
+# walk per draw) for marginals of at least SPARSE_CDF_MIN outcomes.  Measured at 2^30 outcomes
+# (tools/sparse_vs_full.py): 1e5 / 3e5 / 1e6 / 3e6 shots 17.2 / 18.8 / 20.8 / 21.4 ms against
+# 27.1-28.5 ms through the full CDF; QSB_SPARSE_CDF=0: always the full CDF
 SPARSE_CDF = os.environ.get("QSB_SPARSE_CDF", "1") != "0"
 SPARSE_CDF_MIN = 1 << 16
 
