@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define QSB_ABI_VERSION 4
+#define QSB_ABI_VERSION 5
 
 typedef enum { QSB_C64 = 0, QSB_C128 = 1 } qsb_dtype;
 
@@ -206,6 +206,15 @@ size_t qsb_sample_exact_scratch_bytes(uint64_t n, uint64_t n_shots);
 int qsb_sample_exact(const double* probs, uint64_t n, double* cum, void* scratch, size_t scratch_bytes,
                      uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, uint64_t n_shots,
                      int64_t* samples, void* stream);
+/* The same with the approximate 4096-element block sums supplied (qsb_probabilities_block_sums
+ * computes them with the probabilities, in one read of the amplitudes). */
+int qsb_sample_exact_bsums(const double* probs, const double* block_sums, uint64_t n, double* cum, void* scratch,
+                           size_t scratch_bytes, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                           uint64_t inc_lo, uint64_t n_shots, int64_t* samples, void* stream);
+/* qsb_probabilities plus block_sums[b] = the sum of probs[4096 b .. 4096 b + 4095] in the order
+ * qsb_sample_exact forms it (ceil(n / 4096) doubles). */
+int qsb_probabilities_block_sums(const void* amps, uint64_t n, int dtype, double* probs, double* block_sums,
+                                 void* stream);
 
 /* ---- sharded execution helpers (sharding.py:53-111 partition / gather / _exchange_halves) - */
 /* dst[i'] = src[i] where bit b of i moves to bit dst_bit[b] of i' (moveaxis of partition /

@@ -86,6 +86,9 @@ SIGNATURES = {
     "qsb_sample_exact_scratch_bytes": (_c_size_t, [_c_u64, _c_u64]),
     "qsb_sample_exact": (_c_int, [_c_void_p, _c_u64, _c_void_p, _c_void_p, _c_size_t, _c_u64, _c_u64, _c_u64, _c_u64,
                                   _c_u64, _c_void_p, _c_void_p]),
+    "qsb_sample_exact_bsums": (_c_int, [_c_void_p, _c_void_p, _c_u64, _c_void_p, _c_void_p, _c_size_t, _c_u64, _c_u64,
+                                        _c_u64, _c_u64, _c_u64, _c_void_p, _c_void_p]),
+    "qsb_probabilities_block_sums": (_c_int, [_c_void_p, _c_u64, _c_int, _c_void_p, _c_void_p, _c_void_p]),
     "qsb_reduced_density": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_int, _c_void_p, _c_void_p,
                                      _c_void_p]),
     "qsb_pack_part": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_void_p, _c_u64, _c_u64, _c_u64, _c_void_p,

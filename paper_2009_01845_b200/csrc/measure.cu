@@ -620,6 +620,36 @@ __global__ void __launch_bounds__(kMT) k_block_sums2(const double* __restrict__ 
   }
 }
 
+// numpy |z|^2 of every amplitude (k_probs) and, per 4096-element block, the same approximate
+// sum k_block_sums2 forms (same per-thread order, same shuffle tree): the sampling pipeline's
+// first two passes in one read of the amplitudes
+template <typename R>
+__global__ void __launch_bounds__(kMT) k_probs_bsums(const cplx<R>* __restrict__ a, uint64_t n,
+                                                     double* __restrict__ p, double* __restrict__ block_sum) {
+  __shared__ double wsum[kMT / 32];
+  const uint64_t b0 = (uint64_t)blockIdx.x * kScanBlock;
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const uint64_t i = b0 + threadIdx.x + (uint64_t)k * kMT;
+    if (i < n) {
+      const cplx<R> v = a[i];
+      const double x = np_abs2((double)v.x, (double)v.y);
+      p[i] = x;
+      acc += x;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < kMT / 32; ++w) t += wsum[w];
+    block_sum[blockIdx.x] = t;
+  }
+}
+
 __global__ void __launch_bounds__(kMT, 3) k_count2(const double* __restrict__ p, uint64_t n, double margin,
                                                 const double* __restrict__ block_prefix,
                                                 unsigned int* __restrict__ cnt) {
@@ -1132,7 +1162,7 @@ struct CumsumCtx {
 };
 
 static int cumsum_phases(const double* probs, uint64_t n, void* scratch, size_t scratch_bytes, cudaStream_t st,
-                         CumsumCtx* ctx);
+                         CumsumCtx* ctx, const double* block_sums = nullptr);
 
 extern "C" int qsb_cumsum(const double* probs, uint64_t n, double* cum, void* scratch, size_t scratch_bytes,
                           int normalize, void* stream) {
@@ -1150,7 +1180,7 @@ extern "C" int qsb_cumsum(const double* probs, uint64_t n, double* cum, void* sc
 // phases A-D of the exact cumsum: block classification, serial points, block head pieces and
 // the stitch -- everything but the per-element values (k_materialize2)
 static int cumsum_phases(const double* probs, uint64_t n, void* scratch, size_t scratch_bytes, cudaStream_t st,
-                         CumsumCtx* ctx) {
+                         CumsumCtx* ctx, const double* block_sums) {
   if (scratch_bytes < qsb_cumsum_scratch_bytes(n)) {
     set_error("qsb_cumsum: scratch too small");
     return QSB_ERR_ARG;
@@ -1179,7 +1209,12 @@ static int cumsum_phases(const double* probs, uint64_t n, void* scratch, size_t 
   double* rstart = reinterpret_cast<double*>(w);
 
   // A: approximate block sums and their exclusive scan (only used to classify)
-  k_block_sums2<<<(int)nb, kMT, 0, st>>>(probs, n, bpre);
+  if (block_sums) {  // computed with the probabilities (qsb_probabilities_block_sums)
+    cudaError_t e = cudaMemcpyAsync(bpre, block_sums, nb * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return cuda_status(e, "block sums");
+  } else {
+    k_block_sums2<<<(int)nb, kMT, 0, st>>>(probs, n, bpre);
+  }
   k_scan_chunked<double><<<1, 1024, 0, st>>>(bpre, nb, bpre, nullptr);
   // B: serial points per block, their exclusive scan and total (read back to size the lists)
   k_count2<<<(int)nb, kMT, 0, st>>>(probs, n, margin, bpre, cnt);
@@ -1351,9 +1386,45 @@ extern "C" size_t qsb_sample_exact_scratch_bytes(uint64_t n, uint64_t n_shots) {
   return b;
 }
 
+extern "C" int qsb_probabilities_block_sums(const void* amps, uint64_t n, int dtype, double* probs,
+                                            double* block_sums, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  const uint64_t nb = (n + kScanBlock - 1) / kScanBlock;
+  if (n == 0) return QSB_OK;
+  if (dtype == QSB_C128)
+    k_probs_bsums<double><<<(int)nb, kMT, 0, st>>>(static_cast<const double2*>(amps), n, probs, block_sums);
+  else if (dtype == QSB_C64)
+    k_probs_bsums<float><<<(int)nb, kMT, 0, st>>>(static_cast<const float2*>(amps), n, probs, block_sums);
+  else {
+    set_error("unknown dtype %d", dtype);
+    return QSB_ERR_ARG;
+  }
+  QSB_CHECK_LAUNCH("qsb_probabilities_block_sums");
+  return QSB_OK;
+}
+
+static int sample_exact_impl(const double* probs, const double* block_sums, uint64_t n, double* cum, void* scratch,
+                             size_t scratch_bytes, uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo,
+                             uint64_t n_shots, int64_t* samples, void* stream);
+
 extern "C" int qsb_sample_exact(const double* probs, uint64_t n, double* cum, void* scratch, size_t scratch_bytes,
                                 uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo, uint64_t n_shots,
                                 int64_t* samples, void* stream) {
+  return sample_exact_impl(probs, nullptr, n, cum, scratch, scratch_bytes, s_hi, s_lo, i_hi, i_lo, n_shots, samples,
+                           stream);
+}
+
+extern "C" int qsb_sample_exact_bsums(const double* probs, const double* block_sums, uint64_t n, double* cum,
+                                      void* scratch, size_t scratch_bytes, uint64_t s_hi, uint64_t s_lo,
+                                      uint64_t i_hi, uint64_t i_lo, uint64_t n_shots, int64_t* samples,
+                                      void* stream) {
+  return sample_exact_impl(probs, block_sums, n, cum, scratch, scratch_bytes, s_hi, s_lo, i_hi, i_lo, n_shots,
+                           samples, stream);
+}
+
+static int sample_exact_impl(const double* probs, const double* block_sums, uint64_t n, double* cum, void* scratch,
+                             size_t scratch_bytes, uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo,
+                             uint64_t n_shots, int64_t* samples, void* stream) {
   cudaStream_t st = as_stream(stream);
   if (n == 0 || n_shots == 0) {
     set_error("qsb_sample_exact: empty distribution or no shots");
@@ -1365,7 +1436,7 @@ extern "C" int qsb_sample_exact(const double* probs, uint64_t n, double* cum, vo
   }
   const size_t cs = (qsb_cumsum_scratch_bytes(n) + 255) & ~(size_t)255;
   CumsumCtx c;
-  if (int rc = cumsum_phases(probs, n, scratch, cs, st, &c)) return rc;
+  if (int rc = cumsum_phases(probs, n, scratch, cs, st, &c, block_sums)) return rc;
   char* w = static_cast<char*>(scratch) + cs;
   double* ends = reinterpret_cast<double*>(w);
   w += (c.nb * sizeof(double) + 255) & ~(size_t)255;

@@ -164,6 +164,12 @@ def sample(state, qubits, n_shots: int, seed: int, registers: dict | None = None
         if missing:
             raise ShapeError(f"register {name!r} references unmeasured qubits {sorted(missing)}")
         regs[name] = tuple(reg)
+    n = state.n_qubits
+    if SPARSE_CDF and qubits == tuple(range(n)) and (1 << n) >= SPARSE_CDF_MIN and n_shots < (1 << 32):
+        # every qubit in order: the probabilities and the scan's block sums in one pass
+        probs, bsums = device_probabilities_block_sums(state)
+        samples = device_sample_exact(probs, n_shots, seed, bsums).cpu().numpy()
+        return MeasurementResult(int(n_shots), qubits, samples, int(seed), regs)
     probs = device_marginal(state, qubits)
     if SPARSE_CDF and probs.numel() >= SPARSE_CDF_MIN and n_shots < (1 << 32):
         samples = device_sample_exact(probs, n_shots, seed).cpu().numpy()
@@ -182,7 +188,17 @@ SPARSE_CDF = os.environ.get("QSB_SPARSE_CDF", "1") != "0"
 SPARSE_CDF_MIN = 1 << 16
 
 
-def device_sample_exact(probs, n_shots: int, seed: int):
+def device_probabilities_block_sums(state):
+    """(probabilities, approximate 4096-element block sums) of a state in one pass."""
+    n = state.n_amps
+    probs = _f64(n)
+    bsums = _f64((n + 4095) // 4096)
+    nat.check(nat.lib().qsb_probabilities_block_sums(state.data_ptr, n, state.precision.qsb_dtype, probs.data_ptr(),
+                                                     bsums.data_ptr(), nat.stream_ptr()), "probabilities")
+    return probs, bsums
+
+
+def device_sample_exact(probs, n_shots: int, seed: int, block_sums=None):
     """The draws of sample() straight from the probabilities: the exact scan's block
     boundaries route every draw to its 4096-element block, the exact values before that block's
     16-element rows route it to a row, and the row is walked with fl(c + p) (bit-identical to
@@ -195,6 +211,11 @@ def device_sample_exact(probs, n_shots: int, seed: int):
     scratch = torch.empty(nbytes, dtype=torch.uint8, device=probs.device)
     out = torch.empty(int(n_shots), dtype=torch.int64, device=probs.device)
     sh, sl, ih, il = pcg64_seed_state(seed)
+    if block_sums is not None:
+        nat.check(lib.qsb_sample_exact_bsums(probs.data_ptr(), block_sums.data_ptr(), n, cum.data_ptr(),
+                                             scratch.data_ptr(), nbytes, sh, sl, ih, il, int(n_shots), out.data_ptr(),
+                                             nat.stream_ptr()), "sample_exact")
+        return out
     nat.check(lib.qsb_sample_exact(probs.data_ptr(), n, cum.data_ptr(), scratch.data_ptr(), nbytes, sh, sl, ih, il,
                                    int(n_shots), out.data_ptr(), nat.stream_ptr()), "sample_exact")
     return out

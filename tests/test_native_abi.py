@@ -23,7 +23,7 @@ def test_library_exports_header_symbols():
     assert not missing, missing
     # the Python binding types every declared symbol
     assert set(syms) <= set(_native.SIGNATURES), set(syms) - set(_native.SIGNATURES)
-    assert lib.qsb_abi_version() == 4
+    assert lib.qsb_abi_version() == 5
 
 
 def test_pass_tile_geometry_matches_planner():
