@@ -650,26 +650,6 @@ __global__ void __launch_bounds__(kMT) k_probs_bsums(const cplx<R>* __restrict__
   }
 }
 
-__global__ void __launch_bounds__(kMT, 3) k_count2(const double* __restrict__ p, uint64_t n, double margin,
-                                                const double* __restrict__ block_prefix,
-                                                unsigned int* __restrict__ cnt) {
-  __shared__ double sh[kMT * kRow];
-  __shared__ double wsum[kMT / 32];
-  __shared__ unsigned int csum[kMT / 32];
-  RowClass rc;
-  uint64_t i0;
-  block_classify(p, n, margin, block_prefix, sh, wsum, rc, i0);
-  unsigned int c = __popc(rc.serial);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0) csum[threadIdx.x >> 5] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned int t = 0;
-    for (int w = 0; w < kMT / 32; ++w) t += csum[w];
-    cnt[blockIdx.x] = t;
-  }
-}
 
 // element segments: a serial element starts a new (empty) segment; V_i = composition of the
 // safe elements' pieces since the last serial (or the block start).  Thread rows are combined
@@ -766,11 +746,21 @@ __device__ __forceinline__ unsigned int block_excl_count(unsigned int c, unsigne
   return r;
 }
 
+// kLocal: the serial points' indices and after-pieces go to per-block lists of kSerCap entries
+// (block-local slots; cnt[b] = the block's serial count, *overflow set when a block has more) and
+// are compacted after the count scan -- the count pass then needs no classification of its own.
+// !kLocal: straight into the global lists at serial_base[b] + local slot (after a count pass).
+constexpr unsigned int kSerCap = 16;
+
+template <bool kLocal>
 __global__ void __launch_bounds__(kMT, 3) k_pieces2(const double* __restrict__ p, uint64_t n, double margin,
                                                  const double* __restrict__ block_prefix,
                                                  const unsigned int* __restrict__ serial_base,
                                                  Piece* __restrict__ head, Piece* __restrict__ after,
-                                                 unsigned long long* __restrict__ serial_idx) {
+                                                 unsigned long long* __restrict__ serial_idx,
+                                                 unsigned int* __restrict__ cnt, unsigned int* __restrict__ overflow) {
+  // !kLocal with cnt given: only the blocks whose serial points overflowed their local lists
+  if (!kLocal && cnt && cnt[blockIdx.x] <= kSerCap) return;
   __shared__ double sh[kMT * kRow];
   __shared__ double wsum[kMT / 32];
   __shared__ unsigned int usum[kMT / 32];
@@ -788,7 +778,13 @@ __global__ void __launch_bounds__(kMT, 3) k_pieces2(const double* __restrict__ p
   for (int k = 0; k < kScanItems; ++k)
     if (k > last_ser && i0 + k < n) mine.v = piece_then(mine.v, elem_piece(row[k], rc.e[k]));
   const RowSeg in = block_excl_rowseg(mine, ssh);
-  const unsigned int slot0 = serial_base[blockIdx.x] + block_excl_count(__popc(rc.serial), usum);
+  const unsigned int nser = __popc(rc.serial);
+  const unsigned int slot0 = (kLocal ? 0u : serial_base[blockIdx.x]) + block_excl_count(nser, usum);
+  if (kLocal && threadIdx.x == kMT - 1) {
+    cnt[blockIdx.x] = slot0 + nser;
+    if (slot0 + nser > kSerCap) atomicOr(overflow, 1u);
+  }
+  const uint64_t lbase = kLocal ? (uint64_t)blockIdx.x * kSerCap : 0;
   // walk the row: V = running segment value; at segment ends write head / after
   if (threadIdx.x == 0 && (rc.serial & 1u)) head[blockIdx.x] = piece_id();  // empty head segment
   Piece V = in.v;
@@ -800,7 +796,7 @@ __global__ void __launch_bounds__(kMT, 3) k_pieces2(const double* __restrict__ p
     // last element, and the value there is the incoming segment composed with the whole row
     V = piece_then(V, mine.v);
     if (i0 < bend && bend - 1 - i0 < (uint64_t)kScanItems) {
-      if (seen) after[slot - 1] = V;
+      if (seen) { if (!kLocal || slot - 1 < kSerCap) after[lbase + slot - 1] = V; }
       else head[blockIdx.x] = V;
     }
   } else {
@@ -809,7 +805,7 @@ __global__ void __launch_bounds__(kMT, 3) k_pieces2(const double* __restrict__ p
       const uint64_t i = i0 + k;
       if (i >= n) break;
       if ((rc.serial >> k) & 1u) {
-        serial_idx[slot] = i;
+        if (!kLocal || slot < kSerCap) serial_idx[lbase + slot] = i;
         ++slot;
         seen = true;
         V = piece_id();
@@ -822,7 +818,7 @@ __global__ void __launch_bounds__(kMT, 3) k_pieces2(const double* __restrict__ p
         end = (k + 1 < kScanItems) ? ((rc.serial >> (k + 1)) & 1u) != 0 : false;
       }
       if (end) {
-        if (seen) after[slot - 1] = V;
+        if (seen) { if (!kLocal || slot - 1 < kSerCap) after[lbase + slot - 1] = V; }
         else head[blockIdx.x] = V;
       }
     }
@@ -834,8 +830,24 @@ __global__ void __launch_bounds__(kMT, 3) k_pieces2(const double* __restrict__ p
   const bool next_ser = (threadIdx.x + 1 < kMT) ? first_bits[threadIdx.x + 1] != 0 : false;
   const uint64_t ilast = i0 + kScanItems - 1;
   if (next_ser && ilast < n && ilast + 1 != bend) {
-    if (seen) after[slot - 1] = V;
+    if (seen) { if (!kLocal || slot - 1 < kSerCap) after[lbase + slot - 1] = V; }
     else head[blockIdx.x] = V;
+  }
+}
+
+// per-block serial lists -> the global lists at the scanned bases (kLocal pieces pass)
+__global__ void __launch_bounds__(32) k_compact_serials(const unsigned int* __restrict__ cnt,
+                                                        const unsigned int* __restrict__ base,
+                                                        const Piece* __restrict__ loc_after,
+                                                        const unsigned long long* __restrict__ loc_idx,
+                                                        Piece* __restrict__ after,
+                                                        unsigned long long* __restrict__ serial_idx) {
+  const unsigned int c = cnt[blockIdx.x];
+  if (c > kSerCap) return;  // an overflowing block: its own pieces pass writes the global lists
+  const uint64_t lb = (uint64_t)blockIdx.x * kSerCap;
+  for (unsigned int j = threadIdx.x; j < c; j += 32) {
+    after[base[blockIdx.x] + j] = loc_after[lb + j];
+    serial_idx[base[blockIdx.x] + j] = loc_idx[lb + j];
   }
 }
 
@@ -1145,6 +1157,8 @@ extern "C" size_t qsb_cumsum_scratch_bytes(uint64_t n) {
 // dependent; they live in a separately grown buffer.
 static void* g_ser_buf = nullptr;
 static size_t g_ser_cap = 0;
+static void* g_loc_buf = nullptr;  // per-block serial lists (kLocal pieces pass)
+static size_t g_loc_cap = 0;
 
 extern "C" int qsb_cumsum_normalized(const double* probs, uint64_t n, double* cum, void* scratch,
                                      size_t scratch_bytes, void* stream) {
@@ -1216,8 +1230,8 @@ static int cumsum_phases(const double* probs, uint64_t n, void* scratch, size_t 
     k_block_sums2<<<(int)nb, kMT, 0, st>>>(probs, n, bpre);
   }
   k_scan_chunked<double><<<1, 1024, 0, st>>>(bpre, nb, bpre, nullptr);
-  // B: serial points per block, their exclusive scan and total (read back to size the lists)
-  k_count2<<<(int)nb, kMT, 0, st>>>(probs, n, margin, bpre, cnt);
+  // B+C: pieces, serial counts and block-local serial lists in one classifying pass; the counts'
+  // exclusive scan and total (read back to size the lists, with the overflow flag)
   static unsigned int* h_total = nullptr;
   if (!h_total) {
     cudaError_t e = cudaMallocHost(&h_total, sizeof(unsigned int) * 2);
@@ -1228,8 +1242,27 @@ static int cumsum_phases(const double* probs, uint64_t n, void* scratch, size_t 
     cudaError_t e = cudaMalloc(&d_tot, sizeof(double) * 2);
     if (e != cudaSuccess) return cuda_status(e, "device total");
   }
+  const size_t loc_need = nb * kSerCap * (sizeof(Piece) + sizeof(unsigned long long));
+  if (loc_need > g_loc_cap) {
+    if (g_loc_buf) cudaFree(g_loc_buf);
+    cudaError_t e = cudaMalloc(&g_loc_buf, loc_need);
+    if (e != cudaSuccess) {
+      g_loc_buf = nullptr;
+      g_loc_cap = 0;
+      return cuda_status(e, "block serial lists");
+    }
+    g_loc_cap = loc_need;
+  }
+  Piece* loc_after = static_cast<Piece*>(g_loc_buf);
+  unsigned long long* loc_idx = reinterpret_cast<unsigned long long*>(loc_after + nb * kSerCap);
+  {
+    cudaError_t e = cudaMemsetAsync(d_tot, 0, sizeof(unsigned int) * 2, st);
+    if (e != cudaSuccess) return cuda_status(e, "serial flags");
+  }
+  k_pieces2<true><<<(int)nb, kMT, 0, st>>>(probs, n, margin, bpre, nullptr, head, loc_after, loc_idx, cnt,
+                                           d_tot + 1);
   k_scan_chunked<unsigned int><<<1, 1024, 0, st>>>(cnt, nb, base, d_tot);
-  cudaError_t e = cudaMemcpyAsync(h_total, d_tot, sizeof(unsigned int), cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaMemcpyAsync(h_total, d_tot, sizeof(unsigned int) * 2, cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return cuda_status(e, "serial count copy");
   e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_status(e, "serial count sync");
@@ -1253,8 +1286,13 @@ static int cumsum_phases(const double* probs, uint64_t n, void* scratch, size_t 
   double* sval = reinterpret_cast<double*>(sb);
   double* d_total = reinterpret_cast<double*>(d_tot) + 1;
 
-  // C: block head pieces, serial indices and their after-pieces
-  k_pieces2<<<(int)nb, kMT, 0, st>>>(probs, n, margin, bpre, base, head, after, sidx);
+  // C: the serial indices and after-pieces into the global lists: compacted from the block
+  // lists, and for the blocks with more than kSerCap serial points (e.g. the first elements of a
+  // binade under a flat distribution) a second pieces pass over just those blocks writing them
+  // at the scanned bases
+  k_compact_serials<<<(int)nb, 32, 0, st>>>(cnt, base, loc_after, loc_idx, after, sidx);
+  if (h_total[1])
+    k_pieces2<false><<<(int)nb, kMT, 0, st>>>(probs, n, margin, bpre, base, head, after, sidx, cnt, nullptr);
   // D: stitch (segmented scan of heads, serial walk, block starts, total)
   k_seg_local<<<(int)na, kMT, 0, st>>>(head, cnt, nb, runp, agg);
   k_seg_top<<<1, kMT, 0, st>>>(agg, na);
