@@ -347,7 +347,7 @@ def run_gpu_arm(args, rank, world):
         w0 = time.perf_counter()
         st = circuit.execute(precision=prec)
         if pinned is not None:
-            pinned.copy_(st.tensor, non_blocking=True)
+            st.copy_to_host(pinned)  # chunked over four copy streams
         else:
             st.tensor[:1].cpu()
         torch.cuda.synchronize()
@@ -404,7 +404,7 @@ def run_gpu_arm(args, rank, world):
                      "traffic": traffic, "peak_kind": peak_kind, "kernel": "qsb_pass_<hash> (NVRTC-specialised fused pass)",
                      "bytes_per_launch": pass_bytes, "launches": len(launches)},
         "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "qft_circuit(n).execute() + state D2H (pinned)"},
+                "api": "qft_circuit(n).execute() + StateVector.copy_to_host(pinned)"},
         "workloads": others,
         "parity": parity,
         "gpu_launches": len(plan.steps) * args.steps,

@@ -59,3 +59,21 @@ def test_layout_follows_later_circuits_and_reads(cuda, no_scratch, monkeypatch):
     r1 = q.sample(d, range(n), 2000, seed=5)
     r2 = q.sample(c, range(n), 2000, seed=5)
     assert np.count_nonzero(r1.samples != r2.samples) <= 2
+
+
+def test_copy_to_host_chunked_equals_amplitudes(cuda):
+    """StateVector.copy_to_host: the chunked multi-stream readback into a pinned tensor equals
+    the amplitudes (single chunk below 2^20 amplitudes, four above)."""
+    import numpy as np
+    import torch
+
+    import paper_2009_01845_b200 as q
+
+    for n in (12, 22):
+        st = q.qft_circuit(n).execute(q.basis_state(n, 5))
+        out = torch.empty(1 << n, dtype=torch.complex128, pin_memory=True)
+        st.copy_to_host(out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.numpy(), st.amplitudes)
+    with pytest.raises(q.ShapeError):
+        st.copy_to_host(torch.empty(3, dtype=torch.complex128))
