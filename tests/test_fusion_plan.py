@@ -332,3 +332,49 @@ def test_plan_templates_reuse_structure_with_new_coefficients(dtype, tol, monkey
     plan = plan_circuit(spec_tuples_to_specs(gates), n, dtype, geometry=GEOMETRY_JIT[dtype])
     assert fusion.TEMPLATE_STATS["hits"] == before["hits"]
     assert max_abs(emulate_plan(plan, psi, npd), ov.run(gates, n, psi)) <= tol
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_plan_templates_on_mixed_random_structures(seed, monkeypatch):
+    """Random circuits of mixed gate kinds (dense 1- and 2-qubit unitaries, controlled
+    rotations, phase gates, SWAPs): the same structure with fresh parameters is planned from
+    the template and still equals the oracle."""
+    from paper_2009_01845_b200 import fusion
+    from paper_2009_01845_b200.fusion import GEOMETRY_JIT
+
+    monkeypatch.setattr(fusion, "_TEMPLATES", {})
+    n = 14
+    rng = np.random.default_rng(100 + seed)
+    layout = []
+    for _ in range(70):
+        a = int(rng.integers(n - 1))
+        layout.append((int(rng.integers(6)), a, int(rng.integers(n))))
+
+    def build(r):
+        out = []
+        for kind, a, c in layout:
+            if kind == 0:
+                u, _ = np.linalg.qr(r.standard_normal((4, 4)) + 1j * r.standard_normal((4, 4)))
+                out.append(ov.gate("Unitary", (a, a + 1), (), (), u))
+            elif kind == 1:
+                u, _ = np.linalg.qr(r.standard_normal((2, 2)) + 1j * r.standard_normal((2, 2)))
+                out.append(ov.gate("Unitary", (a,), (), (), u))
+            elif kind == 2 and c not in (a,):
+                out.append(ov.gate("RX", (a,), (c,), (float(r.uniform(0.1, 6)),)))
+            elif kind == 3:
+                out.append(ov.gate("CZPow", (a, a + 1), (), (float(r.uniform(0.1, 0.9)),)))
+            elif kind == 4:
+                out.append(ov.gate("SWAP", (a, (a + 3) % n)))
+            else:
+                out.append(ov.gate("RZ", (a,), (), (float(r.uniform(0.1, 6)),)))
+        return out
+
+    psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    psi /= np.linalg.norm(psi)
+    for k in range(3):
+        gates = build(np.random.default_rng(seed * 10 + k))
+        before = fusion.TEMPLATE_STATS["hits"]
+        plan = plan_circuit(spec_tuples_to_specs(gates), n, C128, geometry=GEOMETRY_JIT[C128])
+        if k > 0:
+            assert fusion.TEMPLATE_STATS["hits"] == before + 1
+        assert max_abs(emulate_plan(plan, psi), ov.run(gates, n, psi)) <= 1e-12
