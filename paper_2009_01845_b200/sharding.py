@@ -368,7 +368,8 @@ class CudaBackend:
 
         if not ngates:
             return shard
-        if engine.FIRST_RUN_BATCH and shard.numel() * shard.element_size() <= engine.GRID_BATCH_MAX_STATE_BYTES:
+        if (engine.FIRST_RUN_BATCH and engine.FUSION_DEFAULT
+                and shard.numel() * shard.element_size() <= engine.GRID_BATCH_MAX_STATE_BYTES):
             # small shards: one batched launch per 64 gates, no planning or kernel specialisation
             # (every step of an evolution brings new coefficients and often new layouts)
             engine._apply_gate_batch(shard.data_ptr(), n_local, self.dtype, engine.pack_gate_batch(ngates),
@@ -376,11 +377,12 @@ class CudaBackend:
             return shard
         # out-of-place passes (folded SWAPs) need one more shard-sized buffer
         allow_ext = engine.scratch_fits(shard.numel() * shard.element_size())
-        key = (allow_ext,) + tuple((g.kind, g.targets, g.controls, g.index,
-                                    None if g.matrix is None else g.matrix.tobytes()) for g in ngates)
+        fuse = engine.FUSION_DEFAULT
+        key = (allow_ext, fuse) + tuple((g.kind, g.targets, g.controls, g.index,
+                                          None if g.matrix is None else g.matrix.tobytes()) for g in ngates)
         plan_ = cache.get(key)
         if plan_ is None:
-            plan_ = plan_circuit(ngates, n_local, self.dtype, allow_ext_perm=allow_ext,
+            plan_ = plan_circuit(ngates, n_local, self.dtype, allow_ext_perm=allow_ext, fuse=fuse,
                                  geometry=engine.default_geometry(self.dtype))
             cache[key] = plan_
         holder = {}
