@@ -164,3 +164,37 @@ def test_evolve_step_windows_equal_single_steps(cuda, monkeypatch):
                    q.adiabatic_evolve(q.build_x(n), q.build_tfim(n, 1.0), q.Schedule.linear(), cfg).tensor)
     assert _device_max_abs_diff(outs[1][0], outs[4][0]) <= TOL64
     assert _device_max_abs_diff(outs[1][1], outs[4][1]) <= TOL64
+
+
+@pytest.mark.parametrize("prec,tol", [("f64", TOL64), ("f32", TOL32)])
+def test_template_and_recipe_plans_equal_per_gate_kernels(cuda, prec, tol, monkeypatch):
+    """Circuits of one structure with fresh angles (phase-heavy: H, CZPow, RZ, controlled RX, so
+    the passes hold pivots and diagonal terms, re-encoded from the template; and dense layers,
+    whose matrix words are patched) run on plans from the template with kernels reused through
+    coefficient recipes -- and still equal the per-gate kernels at n = 24."""
+    import paper_2009_01845_b200 as q
+    from paper_2009_01845_b200 import engine, fusion, jit
+
+    monkeypatch.setattr(engine, "FIRST_RUN_BATCH", False)  # planned passes from the first run
+    n = 24
+    precision = q.Precision(prec)
+
+    def build(seed):
+        r = np.random.default_rng(seed)
+        c = q.Circuit(n)
+        for layer in range(3):
+            for k in range(n):
+                c.add(q.H(k))
+                c.add(q.RZ(k, float(r.uniform(0.1, 3))))
+            for k in range(n - 1):
+                c.add(q.CZPow(k, k + 1, float(r.uniform(0.1, 0.9))))
+            for k in range(0, n - 2, 3):
+                c.add(q.RX(k + 2, float(r.uniform(0.1, 3)), controls=(k,)))
+        return c
+
+    hits0, rec0 = fusion.TEMPLATE_STATS["hits"], jit.RECIPE_STATS["hits"]
+    start = q.uniform_state(n, precision)
+    for seed in (1, 2, 3):
+        _fused_vs_per_gate(build(seed), n, precision, tol, initial=start)
+    assert fusion.TEMPLATE_STATS["hits"] >= hits0 + 2
+    assert jit.RECIPE_STATS["hits"] > rec0
