@@ -70,6 +70,9 @@ TMA_STORE = os.environ.get("QSB_TMA_STORE", "1") != "0"
 IMMEDIATE_C64 = os.environ.get("QSB_IMMEDIATE_C64", "1") == "1"
 IMMEDIATE_C128 = os.environ.get("QSB_IMMEDIATE_C128", "0") == "1"
 DYN_CHUNK = int(os.environ.get("QSB_DYN_CHUNK", "2"))
+# complex128 sign flips of a parity op as one three-input LOP3 per word (QSB_SIGN_LOP3=0: the
+# shared AND mask + XOR form)
+SIGN_LOP3 = os.environ.get("QSB_SIGN_LOP3", "1") != "0"
 
 
 def tiles_per_cta(ext_bits: int, consumers: int) -> int:
@@ -119,6 +122,12 @@ typedef unsigned int u32;
 typedef long long i64;
 struct __align__(64) TMap { u64 w[16]; };
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+// hi ^ (s & 0x80000000) as one LOP3 (the parity ops' sign flips)
+__device__ __forceinline__ u32 sgnx(u32 hi, u32 s) {
+  u32 d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x78;" : "=r"(d) : "r"(hi), "r"(s), "r"(0x80000000u));
+  return d;
+}
 __device__ __forceinline__ void mbar_init(u64* b, u32 c) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(b)), "r"(c)); }
 __device__ __forceinline__ void mbar_expect_tx(u64* b, u32 n) {
@@ -1026,12 +1035,17 @@ class _Gen:
         for sl in range(A):
             v = f"v{self.vm[sl]}"
             if self.dtype == nat.QSB_C128:
-                # flip the sign bits of both high words with a mask built from bit sl of W (no
-                # predicate, no select: three integer ops per amplitude)
+                # flip the sign bits of both high words with bit sl of W moved to bit 31: each word
+                # is one three-input LOP3, hi ^ (s & 0x80000000) (no predicate, no select)
                 sh = f"(W << {31 - sl})" if sl < 31 else "W"
-                self.emit(f"      {{ const int m = (int)({sh} & 0x80000000u); "
-                          f"{v}.x = __hiloint2double(__double2hiint({v}.x) ^ m, __double2loint({v}.x)); "
-                          f"{v}.y = __hiloint2double(__double2hiint({v}.y) ^ m, __double2loint({v}.y)); }}")
+                if SIGN_LOP3:
+                    self.emit(f"      {{ const unsigned s = {sh}; "
+                              f"{v}.x = __hiloint2double((int)sgnx((unsigned)__double2hiint({v}.x), s), __double2loint({v}.x)); "
+                              f"{v}.y = __hiloint2double((int)sgnx((unsigned)__double2hiint({v}.y), s), __double2loint({v}.y)); }}")
+                else:
+                    self.emit(f"      {{ const int m = (int)({sh} & 0x80000000u); "
+                              f"{v}.x = __hiloint2double(__double2hiint({v}.x) ^ m, __double2loint({v}.x)); "
+                              f"{v}.y = __hiloint2double(__double2hiint({v}.y) ^ m, __double2loint({v}.y)); }}")
             else:
                 self.emit(f"      if (W & {1 << sl}u) {{ {v}.x = -{v}.x; {v}.y = -{v}.y; }}")
         self.emit("    }")
