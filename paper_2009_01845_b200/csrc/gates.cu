@@ -423,10 +423,105 @@ static int launch_wide(cplx<R>* a, int n_qubits, const int* tbits, int nc, const
   return QSB_OK;
 }
 
+// 6-10 targets (the reference's apply_matrix takes any 2^t x 2^t matrix): one CTA of 2^t
+// threads per group of 2^t amplitudes, staged in shared memory; thread r forms row r of the
+// product, y_r = sum_c M[r][c] x_c in column order, reading the matrix transposed (coalesced
+// across the rows, L2-resident across the groups: at most 1024 x 1024 complex128 = 16 MB).
+// Diagonal and permutation matrices take the same dense body (exact zeros and ones change no
+// bits of a sum).  A drop-in completeness path, not a hot one.
+constexpr int kMaxDenseTargets = 10;
+
+template <typename R>
+__global__ void __launch_bounds__(1024) k_dense_big(cplx<R>* __restrict__ a, const double2* __restrict__ mt, int t,
+                                                    OccBits occ, uint64_t cmask, uint64_t n_groups,
+                                                    const int* __restrict__ tbits_dev) {
+  using C = cplx<R>;
+  extern __shared__ __align__(16) unsigned char big_raw[];
+  C* xs = reinterpret_cast<C*>(big_raw);
+  const int D = 1 << t;
+  const int r = threadIdx.x;
+  uint64_t off = 0;
+  for (int b = 0; b < t; ++b)
+    if ((r >> (t - 1 - b)) & 1) off |= 1ull << tbits_dev[b];
+  for (uint64_t g = blockIdx.x; g < n_groups; g += gridDim.x) {
+    const uint64_t base = insert_zero_bits(g, occ) | cmask;
+    xs[r] = a[base | off];
+    __syncthreads();
+    const double2 m0 = mt[r];
+    C m;
+    m.x = (R)m0.x;
+    m.y = (R)m0.y;
+    C y = cmul(m, xs[0]);
+    for (int c = 1; c < D; ++c) {
+      const double2 mc = mt[(uint64_t)c * D + r];
+      m.x = (R)mc.x;
+      m.y = (R)mc.y;
+      y = cmad(m, xs[c], y);
+    }
+    __syncthreads();
+    a[base | off] = y;
+  }
+}
+
+template <typename R>
+static int launch_dense_big(void* amps, int n_qubits, int t, const int* tbits, int nc, const int* cbits,
+                            const double* mat, cudaStream_t st) {
+  const int D = 1 << t;
+  OccBits occ;
+  int pos[64];
+  int np = 0;
+  for (int i = 0; i < t; ++i) pos[np++] = tbits[i];
+  for (int i = 0; i < nc; ++i) pos[np++] = cbits[i];
+  for (int i = 1; i < np; ++i)
+    for (int j = i; j > 0 && pos[j - 1] > pos[j]; --j) {
+      const int tmp = pos[j];
+      pos[j] = pos[j - 1];
+      pos[j - 1] = tmp;
+    }
+  occ.n = np;
+  for (int i = 0; i < np; ++i) occ.pos[i] = (uint8_t)pos[i];
+  uint64_t cmask = 0;
+  for (int i = 0; i < nc; ++i) cmask |= 1ull << cbits[i];
+  const uint64_t n_groups = 1ull << (n_qubits - np);
+  // the transposed matrix (mt[c][r] = M[r][c]) and the target bits on the device, freed in order
+  const size_t mbytes = (size_t)D * D * sizeof(double2);
+  double2* h = static_cast<double2*>(malloc(mbytes));
+  if (!h) {
+    set_error("apply_matrix: host staging of a %d x %d matrix", D, D);
+    return QSB_ERR_CAPACITY;
+  }
+  for (int r = 0; r < D; ++r)
+    for (int c = 0; c < D; ++c) h[(size_t)c * D + r] = make_double2(mat[2 * ((size_t)r * D + c)], mat[2 * ((size_t)r * D + c) + 1]);
+  void* dbuf = nullptr;
+  cudaError_t e = cudaMallocAsync(&dbuf, mbytes + 64 * sizeof(int), st);
+  if (e != cudaSuccess) {
+    free(h);
+    return cuda_status(e, "apply_matrix matrix buffer");
+  }
+  double2* mt = static_cast<double2*>(dbuf);
+  int* tb = reinterpret_cast<int*>(static_cast<char*>(dbuf) + mbytes);
+  e = cudaMemcpyAsync(mt, h, mbytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(tb, tbits, t * sizeof(int), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the pageable staging is reused below
+  free(h);
+  if (e != cudaSuccess) {
+    cudaFreeAsync(dbuf, st);
+    return cuda_status(e, "apply_matrix matrix upload");
+  }
+  const uint64_t grid = n_groups < 148ull * 4 ? n_groups : 148ull * 4;
+  k_dense_big<R><<<(int)grid, D, D * sizeof(cplx<R>), st>>>(static_cast<cplx<R>*>(amps), mt, t, occ, cmask, n_groups,
+                                                              tb);
+  e = cudaGetLastError();
+  cudaFreeAsync(dbuf, st);
+  if (e != cudaSuccess) return cuda_status(e, "qsb_apply_matrix(6-10 targets)");
+  return QSB_OK;
+}
+
 template <typename R>
 static int launch_gate(void* amps, int n_qubits, int t, const int* tbits, int nc, const int* cbits,
                        const double* mat, int kclass, cudaStream_t st) {
   cplx<R>* a = static_cast<cplx<R>*>(amps);
+  if (t > kMaxWideTargets) return launch_dense_big<R>(amps, n_qubits, t, tbits, nc, cbits, mat, st);
   switch (t) {
     case 3:
       return launch_wide<R, 3>(a, n_qubits, tbits, nc, cbits, mat, kclass, st);
@@ -1157,8 +1252,8 @@ int qsb_apply_matrix(void* amps, int n_qubits, int dtype, int n_targets, const i
                      int n_controls, const int* control_bits, const double* matrix, int kernel,
                      void* stream) {
   if (int s = check_dtype(dtype)) return s;
-  if (n_targets < 1 || n_targets > kMaxWideTargets) {
-    set_error("apply_matrix supports 1 to %d targets, got %d", kMaxWideTargets, n_targets);
+  if (n_targets < 1 || n_targets > kMaxDenseTargets) {
+    set_error("apply_matrix supports 1 to %d targets, got %d", kMaxDenseTargets, n_targets);
     return QSB_ERR_SHAPE;
   }
   if (n_qubits < 1 || n_qubits > 40 || n_controls < 0 || n_targets + n_controls > n_qubits) {

@@ -95,7 +95,32 @@ def test_apply_matrix_three_to_five_targets(cuda, t, prec):
         if mat is perm:
             assert np.array_equal(got.amplitudes, want)  # exact moves and +-1 / +-i phases
     with pytest.raises(q.ShapeError):
-        q.apply_matrix(q.zero_state(8), 8, list(range(6)), np.eye(64))
+        q.apply_matrix(q.zero_state(12), 12, list(range(11)), np.eye(2048))
+
+
+@pytest.mark.parametrize("t", [6, 8, 10])
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_apply_matrix_six_to_ten_targets(cuda, t, prec):
+    """apply_matrix with 6-10 targets (the dense shared-memory body), with a control and in
+    scattered target order, against the oracle restatement."""
+    import paper_2009_01845_b200 as q
+
+    n = 13
+    rng = np.random.default_rng(200 + t)
+    dtype = np.complex128 if prec == "f64" else np.complex64
+    tol = TOL64 if prec == "f64" else TOL32
+    d = 1 << t
+    unitary, _ = np.linalg.qr(rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d)))
+    diag = np.diag(np.exp(1j * rng.uniform(0, 2 * np.pi, d)))
+    for mat in (unitary, diag):
+        qubits = [int(x) for x in rng.permutation(n)[:t + 1]]
+        targets, controls = qubits[:t], qubits[t:]
+        psi = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)).astype(dtype)
+        want = psi.copy()
+        ov.apply_matrix(want, n, targets, mat, controls)
+        got = q.from_amplitudes(psi)
+        q.apply_matrix(got, n, targets, mat, controls)
+        assert max_abs(got.amplitudes, want) <= tol * (1 << (t - 5))  # sums of 2^t terms
 
 
 def test_control_leaves_unset_half_untouched(cuda):
