@@ -18,8 +18,9 @@ sweep = 2 * (1 << n) * 16
 st = q.uniform_state(n)
 _step = q.trotter_step_circuit(q.combine(q.build_x(n), 0.5, q.build_tfim(n, 1.0), 0.5), 0.05)
 # trotter4: four steps as one circuit, as evolve() plans them (evolution.STEP_WINDOW)
-circs = {"qft": q.qft_circuit(n), "trotter": _step, "trotter4": q.Circuit(n).add([g for _ in range(4) for g in _step.queue]),
-         "grid": q.random_grid_circuit(3, n // 3, 20, 42)}
+circs = {"qft": q.qft_circuit(n), "trotter": _step, "grid": q.random_grid_circuit(3, n // 3, 20, 42)}
+for _w in (2, 4, 6, 8):  # trotterK: K steps as one circuit
+    circs[f"trotter{_w}"] = q.Circuit(n).add([g for _ in range(_w) for g in _step.queue])
 for name in which:
     if name == "qft-api":
         # through Circuit.execute's engine.run_gates: no room for a scratch buffer, so the
@@ -54,7 +55,7 @@ for name in which:
     ps = [s for s in plan.steps if isinstance(s, PassStep)]
     gs = [s for s in plan.steps if isinstance(s, GateStep)]
     print(f"{name}-{n}: {ms:.1f} ms, {len(ps)} passes + {len(gs)} gate steps, sweeps {plan.state_sweeps():.1f}, "
-          f"eff {plan.state_sweeps() * sweep / ms / 1e6:.0f} GB/s" + (f", {ms / 4:.1f} ms per step" if name == "trotter4" else ""),
+          f"eff {plan.state_sweeps() * sweep / ms / 1e6:.0f} GB/s" + (f", {ms / int(name[7:]):.1f} ms per step" if name.startswith("trotter") and name[7:] else ""),
           flush=True)
     for x, s in zip([a_.elapsed_time(b_) for a_, b_ in evs], ps):
         print(f"   {x:8.2f} ms  {sweep / x / 1e6:6.0f} GB/s  gates={s.n_gates:3d} tr={s.n_transposes} ext={int(s.ext_perm)} "
