@@ -82,15 +82,6 @@ def _device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
-def _precision_of_torch(t) -> Precision:
-    torch = nat.torch_mod()
-    if t.dtype == torch.complex128:
-        return Precision.F64
-    if t.dtype == torch.complex64:
-        return Precision.F32
-    raise ShapeError(f"amplitude tensor dtype {t.dtype} is not complex64/complex128")
-
-
 def allocate(n_qubits: int, precision: Precision):
     """Uninitialised device buffer for 2**n amplitudes (the state allocator)."""
     torch = nat.torch_mod()
