@@ -17,6 +17,14 @@ name = sys.argv[1] if len(sys.argv) > 1 else "trotter4"
 if name == "trotter4":
     step = q.trotter_step_circuit(q.combine(q.build_x(n), 0.5, q.build_tfim(n, 1.0), 0.5), 0.05)
     circ = q.Circuit(n).add([g for _ in range(4) for g in step.queue])
+elif name == "var":
+    import math
+
+    import numpy as np
+
+    circ = q.variational_circuit(n, 5, np.random.default_rng(42).uniform(0, 2 * math.pi, n * 11), fused=True)
+elif name == "grid":
+    circ = q.random_grid_circuit(3, 10, 20, 42)
 else:
     circ = q.qft_circuit(n)
 st = q.uniform_state(n, q.Precision.F64)
