@@ -11,6 +11,10 @@ import paper_2009_01845_b200 as q
 from paper_2009_01845_b200 import engine, fusion, jit
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+if len(sys.argv) > 2:
+    from paper_2009_01845_b200 import evolution
+
+    evolution.STEP_WINDOW = int(sys.argv[2])
 orig = engine.run_plan
 records = []
 
@@ -23,7 +27,7 @@ def timed(state, plan, holder=None, stream=None, events=None):
 
 engine.run_plan = timed
 cfg = q.EvolutionConfig(q.Solver.TROTTER, 0.05, 1.0)
-for use in (True, False, True, False):
+for use in (True, True):
     fusion.PLAN_TEMPLATES = use
     jit.RECIPES = use
     q.adiabatic_evolve(q.build_x(n), q.build_tfim(n, 0.9), q.Schedule.linear(), cfg)
